@@ -1,0 +1,437 @@
+#!/usr/bin/env python
+"""Benchmark: DD/TD/QD GEMM and batched Horner on B200 vs the FP64 roofline.
+
+Metric (BASELINE.json): "DD/TD/QD GEMM and Horner Gops/s vs FP64 FMA
+roofline, 1/2/4/8 B200".  One step = one pass of the metric's workloads:
+  config 3: C = A B, DD n=4096, TD n=2048, QD n=2048 (naive order, bit-exact)
+  config 4: QD Horner, degree 1024, 2^24 points
+Units: multi-precision ops (MP-ops; one K-word add or mul; a MAC = 2), so a
+step is 2*4096^3 + 2*2048^3 + 2*2048^3 + 2*2^24*1024 MP-ops.  `value` is
+the whole-job MP-op rate with inputs resident in HBM; `e2e` is the same
+workload through the public Python API with host (pinned) buffers copied in
+and results copied out inside the timed region.  Multi-GPU: GEMM by row
+blocks of C (B replicated), Horner by point shards; no collective on the
+data path ("weak"-style partition of a fixed total: scaling="strong").
+
+The roofline denominator is the FP64 pipe rate measured live by a DFMA
+microbenchmark (8 independent chains per thread, all SMs), counting one
+DADD/DMUL/DFMA as one FP64 op; algorithmic FP64 ops per MAC are
+DD 29, TD 96, QD 209.
+
+--impl reference times the reference algorithm's CPU implementation (the C
+restatement in oracle/, all host threads) on a bounded sample per step.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+# algorithmic FP64 ops per MAC (mul + add) and per MP-op
+MAC_OPS = {2: 29, 3: 96, 4: 209}
+GEMM_PARTS = [(2, 4096), (3, 2048), (4, 2048)]
+HORNER = dict(k=4, degree=1024, npts=1 << 24)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline sample")
+    ap.add_argument("--quick", action="store_true", help="small sizes (debug)")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------- helpers
+class ClockSampler:
+    """Samples SM clock and throttle reasons via NVML while running."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+        0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index: int):
+        self.samples = []
+        self.reasons = set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.1)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def shard(total, rank, world):
+    base, extra = divmod(total, world)
+    lo = rank * base + min(rank, extra)
+    return lo, lo + base + (1 if rank < extra else 0)
+
+
+def mp_ops_gemm(n):
+    return 2 * n**3
+
+
+def fp64_ops_gemm(k, n):
+    return MAC_OPS[k] * n**3
+
+
+def step_mp_ops(gemm_parts, horner):
+    return sum(mp_ops_gemm(n) for _, n in gemm_parts) + 2 * horner["npts"] * horner["degree"]
+
+
+def measure_fp64_peak(torch, lib, dev_stream):
+    """DFMA microbenchmark: ops/s of the FP64 pipe (1 DFMA = 1 op)."""
+    sms = lib.mw_device_sm_count()
+    blocks, threads = sms * 8, 256
+    sink = torch.empty(blocks * threads, dtype=torch.float64, device="cuda")
+    res = {}
+    for op, name in ((0, "dfma"), (1, "dadd")):
+        iters = 2000
+        lib.mw_fp64_peak_kernel(op, blocks, threads, iters, sink.data_ptr(), dev_stream())
+        torch.cuda.synchronize()
+        # size for ~250 ms
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        lib.mw_fp64_peak_kernel(op, blocks, threads, iters, sink.data_ptr(), dev_stream())
+        e1.record()
+        torch.cuda.synchronize()
+        t = e0.elapsed_time(e1) / 1e3
+        iters = max(1, int(iters * 0.25 / max(t, 1e-6)))
+        best = 0.0
+        for _ in range(3):
+            e0.record()
+            lib.mw_fp64_peak_kernel(op, blocks, threads, iters, sink.data_ptr(), dev_stream())
+            e1.record()
+            torch.cuda.synchronize()
+            t = e0.elapsed_time(e1) / 1e3
+            best = max(best, blocks * threads * iters * 64 / t)
+        res[name] = best
+    return res
+
+
+# ---------------------------------------------------------------- our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2603_14926_b200 as mw
+    from paper_2603_14926_b200 import _lib, gen
+    from paper_2603_14926_b200.linalg import gemm_into
+    from paper_2603_14926_b200.poly import horner_into
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    lib = _lib.load()
+    stream = lambda: torch.cuda.current_stream().cuda_stream  # noqa: E731
+
+    gemm_parts = [(k, 512 if args.quick else n) for k, n in GEMM_PARTS]
+    horner = dict(HORNER)
+    if args.quick:
+        horner["npts"] = 1 << 18
+    BF = mw.Variant.BRANCH_FREE
+
+    # ---- inputs: every rank draws the same seeded arrays, keeps its shard
+    t_gen = time.time()
+    gdata = []
+    for k, n in gemm_parts:
+        a, b = gen.config3_gemm(k, n)
+        lo, hi = shard(n, rank, world)
+        gdata.append(dict(k=k, n=n, lo=lo, hi=hi, a_host=a, b_host=b))
+    coeffs, xh = gen.config4_horner(npts=horner["npts"], degree=horner["degree"], k=horner["k"])
+    plo, phi = shard(horner["npts"], rank, world)
+    if rank == 0:
+        print(f"[bench] inputs generated in {time.time() - t_gen:.1f}s", file=sys.stderr)
+
+    # device-resident copies (A row block, full B, C row block)
+    dev = []
+    for g in gdata:
+        k, n, lo, hi = g["k"], g["n"], g["lo"], g["hi"]
+        a = torch.from_numpy(np.ascontiguousarray(g["a_host"][:, lo:hi])).cuda()
+        b = torch.from_numpy(g["b_host"]).cuda()
+        c = torch.empty((k, hi - lo, n), dtype=torch.float64, device="cuda")
+        dev.append((k, n, a, b, c))
+    cdev = torch.from_numpy(coeffs).cuda()
+    xdev = torch.from_numpy(np.ascontiguousarray(xh[:, plo:phi])).cuda()
+    ydev = torch.empty_like(xdev)
+
+    n_parts = len(dev) + 1
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(n_parts + 1)] for _ in range(args.steps)]
+
+    def step(evs=None):
+        if evs:
+            evs[0].record()
+        for i, (k, n, a, b, c) in enumerate(dev):
+            if a.shape[1] > 0:
+                gemm_into(a, b, c, BF)
+            if evs:
+                evs[i + 1].record()
+        if xdev.shape[1] > 0:
+            horner_into(cdev, xdev, ydev, BF)
+        if evs:
+            evs[n_parts].record()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    peak = measure_fp64_peak(torch, lib, stream)
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        t0.record()
+        for s in range(args.steps):
+            step(ev[s])
+        t1.record()
+        torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    ms_total = t0.elapsed_time(t1)
+    part_ms = np.zeros(n_parts)
+    for s in range(args.steps):
+        for i in range(n_parts):
+            part_ms[i] += ev[s][i].elapsed_time(ev[s][i + 1])
+    part_ms /= args.steps
+    if world > 1:
+        tt = torch.tensor([ms_total], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms_total = float(tt.item())
+    ms_step = ms_total / args.steps
+    total_mp = step_mp_ops(gemm_parts, horner)
+    value = total_mp / (ms_step / 1e3) / 1e9  # G MP-ops/s, whole job
+
+    # ---- e2e: public API, host buffers in / results out, every step
+    e2e = None
+    if not args.no_e2e:
+        a_pin, b_pin, c_pin = [], [], []
+        for g in gdata:
+            lo, hi = g["lo"], g["hi"]
+            a_pin.append(torch.from_numpy(np.ascontiguousarray(g["a_host"][:, lo:hi])).pin_memory())
+            b_pin.append(torch.from_numpy(g["b_host"]).pin_memory())
+            c_pin.append(torch.empty((g["k"], hi - lo, g["n"]), dtype=torch.float64).pin_memory())
+        x_pin = torch.from_numpy(np.ascontiguousarray(xh[:, plo:phi])).pin_memory()
+        y_pin = torch.empty_like(x_pin).pin_memory()
+        c_pin_coeffs = torch.from_numpy(coeffs).pin_memory()
+        h2d = sum(t.numel() * 8 for t in a_pin + b_pin) + x_pin.numel() * 8 + c_pin_coeffs.numel() * 8
+        d2h = sum(t.numel() * 8 for t in c_pin) + y_pin.numel() * 8
+        plan = mw.MatMulPlan(scheme="naive", variant=BF)
+
+        def e2e_step():
+            for ap, bp, cp in zip(a_pin, b_pin, c_pin):
+                A = mw.MWMatrix(ap.to("cuda", non_blocking=True))
+                B = mw.MWMatrix(bp.to("cuda", non_blocking=True))
+                if A.rows:
+                    cp.copy_(mw.matmul(A, B, plan).planes, non_blocking=True)
+            p = mw.MWPolynomial(c_pin_coeffs.to("cuda", non_blocking=True))
+            xs = mw.LaneBatch(x_pin.to("cuda", non_blocking=True))
+            if xs.width:
+                y_pin.copy_(mw.horner_eval_batched(p, xs, BF).planes, non_blocking=True)
+
+        for _ in range(max(1, min(args.warmup, 2))):
+            e2e_step()
+        torch.cuda.synchronize()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.steps):
+            e2e_step()
+        e1.record()
+        torch.cuda.synchronize()
+        barrier()
+        ems = e0.elapsed_time(e1)
+        if world > 1:
+            tt = torch.tensor([ems], dtype=torch.float64, device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            ems = float(tt.item())
+        e2e = {"value": round(total_mp / (ems / args.steps / 1e3) / 1e9, 3), "unit": "G MP-ops/s",
+               "h2d_bytes_per_step": int(h2d) * world, "d2h_bytes_per_step": int(d2h) * world,
+               "ms_per_step": round(ems / args.steps, 3)}
+
+    # ---- roofline of the dominant kernel (largest share of the step)
+    parts = []
+    for i, (k, n, a, b, c) in enumerate(dev):
+        rows = a.shape[1]
+        ops = MAC_OPS[k] * rows * n * n
+        parts.append(dict(name=f"gemm_{['', '', 'dd', 'td', 'qd'][k]}_n{n}", ms=part_ms[i], fp64_ops=ops,
+                          mp_ops=2 * rows * n * n))
+    hp = phi - plo
+    parts.append(dict(name=f"horner_qd_deg{horner['degree']}_pts{horner['npts']}", ms=part_ms[-1],
+                      fp64_ops=MAC_OPS[4] * hp * horner["degree"], mp_ops=2 * hp * horner["degree"]))
+    for p in parts:
+        p["fp64_tops"] = p["fp64_ops"] / (p["ms"] / 1e3) / 1e12 if p["ms"] > 0 else 0.0
+        p["frac_of_fp64_peak"] = p["fp64_tops"] * 1e12 / peak["dfma"]
+        p["gmpops"] = p["mp_ops"] / (p["ms"] / 1e3) / 1e9 if p["ms"] > 0 else 0.0
+    dom = max(parts, key=lambda p: p["ms"])
+    peak_t = peak["dfma"] / 1e12
+    roofline = {
+        "bound": "fp64", "kernel": dom["name"],
+        "achieved": round(dom["fp64_tops"], 3), "peak": round(peak_t, 3),
+        "unit": "T FP64-op/s (DADD/DMUL/DFMA = 1 op)",
+        "frac": round(dom["fp64_tops"] / peak_t, 4),
+        "traffic": None,
+        "peak_source": "measured live: DFMA microbenchmark, 8 chains/thread, all SMs (mw_fp64_peak_kernel)",
+    }
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_sample(gemm_parts, horner)
+
+    if rank == 0:
+        line = {
+            "metric": "DD/TD/QD GEMM and Horner Gops/s vs FP64 FMA roofline, 1/2/4/8 B200",
+            "value": round(value, 3), "unit": "G MP-ops/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ms_step, 3), "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64 (DD/TD/QD multi-word)", "data": "synthetic (seeded, SURVEY §8(d) G_K)",
+            "config": {
+                "workload": "config3 GEMM DD n4096 + TD n2048 + QD n2048, config4 QD Horner deg1024 x 2^24 pts",
+                "gemm": [f"k{k} n{n}" for k, n in gemm_parts], "horner": horner,
+                "parallelism": f"rows/points sharded over {world} GPU(s), no collective",
+                "l2": "inputs larger than L2 (GEMM DD A+B 537 MB, Horner x 537 MB); no flush",
+                "bit_exact": "GEMM naive order and Horner per point, vs reference",
+            },
+            "parts": [{"name": p["name"], "ms": round(p["ms"], 3), "G_MPops": round(p["gmpops"], 2),
+                       "fp64_Tops": round(p["fp64_tops"], 3), "frac": round(p["frac_of_fp64_peak"], 4)}
+                      for p in parts],
+            "fp64_peak_measured": {"dfma_Tops": round(peak["dfma"] / 1e12, 3), "dadd_Tops": round(peak["dadd"] / 1e12, 3)},
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": args.steps * (len(dev) + 1),
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+# ---------------------------------------------------------- CPU baseline
+def cpu_sample(gemm_parts, horner, budget_rows=None):
+    """Reference algorithm (C restatement, oracle/) on all host threads over
+    a bounded sample: GEMM rows (per K) and Horner points.  Returns the
+    cpu_baseline dict in the same unit (G MP-ops/s)."""
+    import oracle
+    from paper_2603_14926_b200 import gen
+
+    threads = oracle.max_threads()
+    sample_rows = {2: 8, 3: 16, 4: 8} if budget_rows is None else budget_rows
+    tot_mp = 0.0
+    tot_s = 0.0
+    desc = []
+    for k, n in gemm_parts:
+        a, b = gen.config3_gemm(k, n)
+        r = min(sample_rows[k], n)
+        t = time.perf_counter()
+        oracle.gemm(a[:, :r], b, "bf")
+        dt = time.perf_counter() - t
+        tot_mp += 2 * r * n * n
+        tot_s += dt * (n / r)  # per-row work is uniform: scale to the full matrix
+        desc.append(f"gemm k{k} n{n}: {r} rows in {dt:.2f}s")
+    coeffs, x = gen.config4_horner(npts=horner["npts"], degree=horner["degree"], k=horner["k"])
+    pts = min(65536, horner["npts"])
+    t = time.perf_counter()
+    oracle.horner(coeffs, x[:, :pts], "bf")
+    dt = time.perf_counter() - t
+    desc.append(f"horner: {pts} pts in {dt:.2f}s")
+    tot_s += dt * (horner["npts"] / pts)
+    tot_mp += 2 * horner["npts"] * horner["degree"]
+    return {"value": round(tot_mp / tot_s / 1e9, 4), "unit": "G MP-ops/s", "cores": threads, "kind": "port",
+            "sample": "; ".join(desc) + " -- extrapolated linearly to the full step (uniform work per row/point)",
+            "seconds_per_step_extrapolated": round(tot_s, 2)}
+
+
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    gemm_parts = [(k, 512 if args.quick else n) for k, n in GEMM_PARTS]
+    horner = dict(HORNER)
+    if args.quick:
+        horner["npts"] = 1 << 16
+    small = {2: 2, 3: 4, 4: 2}
+    for _ in range(args.warmup):
+        cpu_sample(gemm_parts, horner, budget_rows={k: 1 for k in small})
+    vals = []
+    descs = None
+    for _ in range(args.steps):
+        r = cpu_sample(gemm_parts, horner, budget_rows=small)
+        vals.append(r["value"])
+        descs = r
+    v = statistics.median(vals)
+    print(json.dumps({
+        "metric": "DD/TD/QD GEMM and Horner Gops/s vs FP64 FMA roofline, 1/2/4/8 B200",
+        "impl": "reference", "value": v, "unit": "G MP-ops/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64 (DD/TD/QD multi-word)", "data": "synthetic (seeded, SURVEY §8(d) G_K)",
+        "ms_per_step": round(descs["seconds_per_step_extrapolated"] * 1e3, 1),
+        "config": {"workload": "config3 GEMM DD n4096 + TD n2048 + QD n2048, config4 QD Horner deg1024 x 2^24 pts"},
+        "cpu_baseline": {"value": v, "unit": "G MP-ops/s", "cores": descs["cores"], "kind": "port",
+                         "sample": descs["sample"]},
+        "e2e": {"value": v, "unit": "G MP-ops/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+if __name__ == "__main__":
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)

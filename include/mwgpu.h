@@ -1,0 +1,157 @@
+/* mwgpu.h — C-ABI of the B200 branch-free DD/TD/QD kernels.
+ *
+ * This is the drop-in boundary for the reference's array-level dispatch
+ * (K, Variant) -> f(a_comps, b_comps) -> out_comps
+ * (pkg/src/mwfloat/batch.py:178-194) and the lane/row/point folds built on
+ * it (linalg.py:284-297, poly.py:89-96, roots.py:240-315).
+ *
+ * Conventions (all entry points):
+ *  - A K-word array is K planes of float64 in device memory; plane c of an
+ *    operand starts at  base + c * plane_stride  (strides in elements).
+ *    Matrices are row-major inside a plane with leading dimension ld.
+ *  - k is the word count (2 = DD, 3 = TD, 4 = QD); variant is
+ *    MW_VARIANT_STANDARD (0) or MW_VARIANT_BRANCH_FREE (1).  STANDARD is
+ *    available for k = 2 only (dw_add_accurate / dw_mul, multiword.py:
+ *    118-126, 140-145); k = 3, 4 STANDARD returns MW_ERR_UNSUPPORTED.
+ *  - Pointers are caller-owned device pointers; nothing is allocated.
+ *    `stream` is a cudaStream_t (NULL = legacy default stream).  Calls are
+ *    asynchronous and stream-ordered; results are valid after the stream
+ *    synchronises.
+ *  - Return value: 0 on success, a negative MW_ERR_* for argument errors
+ *    (nothing launched), or a positive cudaError_t from the launch.
+ *    Non-finite values propagate, never trap (multiword.py:18-20).
+ */
+#ifndef MWGPU_H
+#define MWGPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MW_VARIANT_STANDARD 0
+#define MW_VARIANT_BRANCH_FREE 1
+
+#define MW_OK 0
+#define MW_ERR_INVALID -1     /* bad k / size / stride / pointer            */
+#define MW_ERR_UNSUPPORTED -2 /* (k, variant) has no device kernel          */
+
+#define MW_ORDER_EXACT 0 /* reference fold order: bit-exact, one thread/output */
+#define MW_ORDER_TREE 1  /* fixed split + pairwise tree: within n*2^-p bound   */
+
+/* Library version string and a static message for a status code. */
+const char* mw_version(void);
+const char* mw_status_string(int status);
+
+/* out = a (+) b lane-wise.  Replaces batch.batch_add -> _BATCH_ADD[(k,v)]
+ * (batch.py:204-207, 178-185).  Bit-exact with the reference. */
+int mw_ew_add(int k, int variant, const double* a, int64_t sa, const double* b,
+              int64_t sb, double* out, int64_t so, int64_t n, void* stream);
+
+/* out = a (-) b = a (+) (-b).  Replaces mw_sub / linalg._ew_sub
+ * (multiword.py:629-630, linalg.py:200-201).  Bit-exact. */
+int mw_ew_sub(int k, int variant, const double* a, int64_t sa, const double* b,
+              int64_t sb, double* out, int64_t so, int64_t n, void* stream);
+
+/* out = a (*) b.  Replaces batch.batch_mul -> _BATCH_MUL[(k,v)]
+ * (batch.py:210-213, 187-194).  Bit-exact. */
+int mw_ew_mul(int k, int variant, const double* a, int64_t sa, const double* b,
+              int64_t sb, double* out, int64_t so, int64_t n, void* stream);
+
+/* out = a / b by the shared Newton reciprocal sequence.  Replaces
+ * batch.batch_div -> _newton_div (batch.py:216-231, multiword.py:639-658).
+ * Zero lanes of b give inf/nan.  Bit-exact. */
+int mw_ew_div(int k, int variant, const double* a, int64_t sa, const double* b,
+              int64_t sb, double* out, int64_t so, int64_t n, void* stream);
+
+/* y <- alpha (*) x (+) y, alpha a host array of k doubles.  Defined by
+ * batch_mul then batch_add (batch.py:204-213).  Bit-exact. */
+int mw_axpy(int k, int variant, const double* alpha_host, const double* x,
+            int64_t sx, double* y, int64_t sy, int64_t n, void* stream);
+
+/* Workspace (in doubles) mw_dot needs for length n (0 when n <= 4096). */
+int64_t mw_dot_workspace(int k, int64_t n);
+
+/* out_dev[0..k) = sum_t x_t (*) y_t.  The definition is the naive-matmul
+ * fold (linalg.py:300-314) for 1xn . nx1.  MW_ORDER_EXACT replays it
+ * bit-exactly on one thread.  MW_ORDER_TREE folds 16-element leaf chunks
+ * in ascending order from exact zero and combines the chunk partials by a
+ * fixed in-place pairwise tree (stride 1, 2, 4, ...; an unpaired tail
+ * passes through) -- a function of n only, so the result does not depend
+ * on launch shape or GPU count.  For n <= 16 both orders coincide.
+ * ws: mw_dot_workspace(k, n) doubles (may be NULL when that is 0). */
+int mw_dot(int k, int variant, const double* x, int64_t sx, const double* y,
+           int64_t sy, int64_t n, double* ws, double* out_dev, int order,
+           void* stream);
+
+/* Tree-dot first stage for sharded dots: writes mw_dot_num_partials(n) =
+ * ceil(n/4096) block partials (each the tree root of 256 leaf chunks) to
+ * partials[c*pstride + b].  Shards that split x, y at multiples of 4096
+ * elements produce partials that, concatenated in shard order and folded
+ * with mw_tree_fold, equal the single-GPU mw_dot bit for bit. */
+int64_t mw_dot_num_partials(int64_t n);
+int mw_dot_partials(int k, int variant, const double* x, int64_t sx,
+                    const double* y, int64_t sy, int64_t n, double* partials,
+                    int64_t pstride, void* stream);
+
+/* out_dev[0..k) = pairwise-tree fold of count K-word values (plane stride
+ * pstride), the tree mw_dot uses above the block level.
+ * ws: mw_tree_fold_workspace(k, count) doubles (NULL when 0). */
+int64_t mw_tree_fold_workspace(int k, int64_t count);
+int mw_tree_fold(int k, int variant, const double* partials, int64_t pstride,
+                 int64_t count, double* ws, double* out_dev, void* stream);
+
+/* y = A x, A m x n.  Definition: y_i = fold_t add(acc, mul(A_it, x_t)) from
+ * exact zero, t ascending = matmul(A, x as n x 1, naive) (linalg.py:284-297).
+ * MW_ORDER_EXACT: one thread per row, bit-exact.  MW_ORDER_TREE: one warp
+ * per row, lane l folds t = l, l+32, ... then a shuffle tree. */
+int mw_gemv(int k, int variant, const double* A, int64_t lda, int64_t sA,
+            const double* x, int64_t sx, double* y, int64_t sy, int64_t m,
+            int64_t n, int order, void* stream);
+
+/* C = A B, A m x kd, B kd x n.  Each C_ij folds t ascending from exact zero
+ * exactly as _rows_kernel_simd / _rows_kernel_scalar (linalg.py:284-314),
+ * so the result is bit-exact with matmul(..., MatMulPlan("naive", v)). */
+int mw_gemm(int k, int variant, const double* A, int64_t lda, int64_t sA,
+            const double* B, int64_t ldb, int64_t sB, double* C, int64_t ldc,
+            int64_t sC, int64_t m, int64_t n, int64_t kd, void* stream);
+
+/* y_p = Horner(coeffs, x_p) for npts points: acc = a_deg; acc = acc (*) x
+ * (+) a_i for i = deg-1..0 (poly.py:89-96).  coeffs: k planes of deg+1
+ * doubles (a_i multiplies x^i).  Bit-exact with horner_eval per point. */
+int mw_horner(int k, int variant, const double* coeffs, int64_t sc,
+              int64_t degree, const double* x, int64_t sx, double* y,
+              int64_t sy, int64_t npts, void* stream);
+
+/* One Durand-Kerner sweep (roots.py:240-315) for roots i in [i0, i1) of
+ * the monic degree-n polynomial z^n + sum c_j z^j.  Reads the frozen full
+ * state (zre, zim: k planes of n doubles each, plane stride sz), writes
+ * updated roots i into zre_out/zim_out at index i (plane stride so) and
+ * |step| = hypot(step_re0, step_im0) into step_mag[i].  The caller sets
+ * *flag_dev = INT32_MAX first; a vanishing denominator factor lowers it to
+ * min over (j*n + i) of the colliding pairs, and the caller raises
+ * CollisionError (roots.py:289-292).  exact_order = 1 replays the
+ * reference order bit for bit; 0 splits the Horner and the ordered product
+ * across a warp (within the stated bound). */
+int mw_dk_sweep(int k, int variant, const double* coeffs, int64_t sc,
+                int64_t n, const double* zre, const double* zim, int64_t sz,
+                int64_t i0, int64_t i1, double* zre_out, double* zim_out,
+                int64_t so, double* step_mag, int* flag_dev, int exact_order,
+                void* stream);
+
+/* FP64 pipe microbenchmark: 8 independent DFMA (op = 0) or DADD (op = 1)
+ * chains per thread, 8 unrolled steps per iteration: executes
+ * blocks * threads * iters * 64 FP64 ops, no memory traffic; the caller
+ * times it.  sink receives one double per thread (threads <= 256). */
+int mw_fp64_peak_kernel(int op, int blocks, int threads, int iters,
+                        double* sink, void* stream);
+
+/* Multiprocessor count of the current device (grid sizing helper). */
+int mw_device_sm_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MWGPU_H */

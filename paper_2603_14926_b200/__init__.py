@@ -1,0 +1,40 @@
+"""mwgpu: branch-free DD/TD/QD arithmetic and its data-parallel kernels on
+B200 (sm_100a), behind the array-level API of the reference mwfloat package
+(pkg/src/mwfloat: batch, linalg, poly, roots).
+
+Layers: ``csrc/mw_eft.cuh`` (EFTs + BF kernels as inlined device functions)
+-> ``csrc/*.cu`` (kernels) -> ``include/mwgpu.h`` C-ABI (``libmwgpu.so``)
+-> ctypes (``_lib``) -> this package.  No CPU fallback: operations raise if
+the native library or a CUDA device is missing.
+"""
+
+from . import _lib
+from .batch import LaneBatch, batch_add, batch_div, batch_mul, batch_sub, pack, unpack
+from .blas import axpy, axpy_, dot, dot_tensor, gemv
+from .linalg import MatMulPlan, MWMatrix, Scheme, matmul
+from .multiword import BITS, Variant, ulp_k
+from .poly import MWPolynomial, horner_eval, horner_eval_batched
+from .roots import (
+    CollisionError,
+    MonicPoly,
+    NoConvergence,
+    RootState,
+    aberth_init,
+    default_tolerance,
+    dk_iterate,
+    dk_solve,
+    dk_sweeps,
+    radius_estimate,
+)
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "LaneBatch", "pack", "unpack", "batch_add", "batch_sub", "batch_mul", "batch_div",
+    "dot", "dot_tensor", "axpy", "axpy_", "gemv",
+    "MatMulPlan", "MWMatrix", "Scheme", "matmul",
+    "BITS", "Variant", "ulp_k",
+    "MWPolynomial", "horner_eval", "horner_eval_batched",
+    "MonicPoly", "RootState", "CollisionError", "NoConvergence", "aberth_init", "radius_estimate",
+    "default_tolerance", "dk_iterate", "dk_sweeps", "dk_solve",
+]

@@ -1,0 +1,65 @@
+// common.cuh — launch helpers shared by the kernel translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/mwgpu.h"
+#include "mw_eft.cuh"
+
+namespace mw {
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// Cached SM count of the current device (148 on B200).
+int sm_count();
+
+inline int launch_status() {
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? MW_OK : static_cast<int>(e);
+}
+
+// (k, variant) -> F<K, VAR>::run(args...).  STANDARD exists for k = 2 only.
+template <template <int, int> class F, typename... Args>
+int dispatch(int k, int variant, Args... args) {
+  if (variant == BRANCH_FREE) {
+    switch (k) {
+      case 2: return F<2, BRANCH_FREE>::run(args...);
+      case 3: return F<3, BRANCH_FREE>::run(args...);
+      case 4: return F<4, BRANCH_FREE>::run(args...);
+      default: return MW_ERR_INVALID;
+    }
+  }
+  if (variant == STANDARD) {
+    if (k == 2) return F<2, STANDARD>::run(args...);
+    if (k == 3 || k == 4) return MW_ERR_UNSUPPORTED;
+  }
+  return MW_ERR_INVALID;
+}
+
+// 8-byte asynchronous global->shared copy; src_bytes = 0 zero-fills.
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, int src_bytes) {
+  unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem),
+               "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
+  unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem),
+               "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+template <int K>
+__device__ __forceinline__ V<K> shfl_down(const V<K>& v, int s) {
+  V<K> r;
+#pragma unroll
+  for (int c = 0; c < K; ++c) r.c[c] = __shfl_down_sync(0xffffffffu, v.c[c], s);
+  return r;
+}
+
+}  // namespace mw

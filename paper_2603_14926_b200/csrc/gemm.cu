@@ -1,0 +1,192 @@
+// gemm.cu — C = A B in DD/TD/QD on the FP64 pipe.
+//
+// Semantics: every C_ij folds t ascending from an exact zero,
+//   acc = add(acc, mul(A_it, B_tj)),
+// exactly as linalg._rows_kernel_simd / _rows_kernel_scalar
+// (linalg.py:284-314, driven by matmul naive, linalg.py:549-569).  The BF
+// kernels are bitwise commutative, so this is bit-exact with the reference.
+//
+// Design (B200, FP64-pipe bound): a CTA computes a BM x BN tile of C with
+// (BM/TM) x (BN/TN) threads, each owning a TM x TN register tile
+// (rows ty*TM + r, columns tx + q*TX so a warp's B reads are contiguous).
+// A and B K-plane tiles of depth BK are staged in shared memory with
+// cp.async (8-byte, zero-filled at the matrix edges) in a 2-stage ring so
+// the next tile streams in while the current one is consumed.  Arithmetic
+// intensity is ~29/96/209 FP64 ops per (2K x 8 B) of smem traffic, so the
+// kernel is bound by FP64 issue, not memory; the only overhead on the
+// pipe is the exact-zero start (one add per output).
+#include "common.cuh"
+
+namespace mw {
+
+template <int K>
+struct GemmCfg;
+// DD: 64x64 tile, 4x4 per thread, 256 threads.
+template <>
+struct GemmCfg<2> {
+  static constexpr int BM = 64, BN = 64, BK = 16, TM = 4, TN = 4;
+};
+// TD: 32x64 tile, 2x4 per thread, 256 threads.
+template <>
+struct GemmCfg<3> {
+  static constexpr int BM = 32, BN = 64, BK = 16, TM = 2, TN = 4;
+};
+// QD: 32x32 tile, 2x2 per thread, 256 threads.
+template <>
+struct GemmCfg<4> {
+  static constexpr int BM = 32, BN = 32, BK = 16, TM = 2, TN = 2;
+};
+
+template <int K>
+struct GemmSmem {
+  using C = GemmCfg<K>;
+  static constexpr int APAD = C::BK + 2;  // row stride of the A tile (doubles)
+  static constexpr int A_ELEMS = K * C::BM * APAD;
+  static constexpr int B_ELEMS = K * C::BK * C::BN;
+  static constexpr int STAGE = A_ELEMS + B_ELEMS;
+  static constexpr int STAGES = 2;
+  static constexpr size_t BYTES = sizeof(double) * STAGE * STAGES;
+};
+
+template <int K, int VAR>
+__global__ void __launch_bounds__((GemmCfg<K>::BM / GemmCfg<K>::TM) *
+                                  (GemmCfg<K>::BN / GemmCfg<K>::TN))
+    gemm_kernel(const double* __restrict__ A, int64_t lda, int64_t sA,
+                const double* __restrict__ B, int64_t ldb, int64_t sB, double* __restrict__ C,
+                int64_t ldc, int64_t sC, int64_t m, int64_t n, int64_t kd) {
+  using Cf = GemmCfg<K>;
+  using S = GemmSmem<K>;
+  constexpr int BM = Cf::BM, BN = Cf::BN, BK = Cf::BK, TM = Cf::TM, TN = Cf::TN;
+  constexpr int TX = BN / TN, TY = BM / TM, NT = TX * TY;
+  extern __shared__ __align__(16) double smem[];
+
+  const int tid = threadIdx.x;
+  const int tx = tid % TX, ty = tid / TX;
+  const int64_t m0 = (int64_t)blockIdx.y * BM, n0 = (int64_t)blockIdx.x * BN;
+
+  auto As = [&](int st, int c, int row, int t) -> double& {
+    return smem[st * S::STAGE + (c * BM + row) * S::APAD + t];
+  };
+  auto Bs = [&](int st, int c, int t, int col) -> double& {
+    return smem[st * S::STAGE + S::A_ELEMS + (c * BK + t) * BN + col];
+  };
+
+  auto load_stage = [&](int st, int64_t k0) {
+    // A tile: K x BM x BK, consecutive threads walk a row's BK doubles.
+#pragma unroll
+    for (int e = tid; e < K * BM * BK; e += NT) {
+      const int c = e / (BM * BK), rem = e % (BM * BK), row = rem / BK, t = rem % BK;
+      const int64_t gi = m0 + row, gt = k0 + t;
+      const bool ok = gi < m && gt < kd;
+      const double* src = ok ? A + c * sA + gi * lda + gt : A;
+      cp_async8(&As(st, c, row, t), src, ok ? 8 : 0);
+    }
+    // B tile: K x BK x BN, consecutive threads walk a row's BN doubles.
+#pragma unroll
+    for (int e = tid; e < K * BK * BN; e += NT) {
+      const int c = e / (BK * BN), rem = e % (BK * BN), t = rem / BN, col = rem % BN;
+      const int64_t gt = k0 + t, gj = n0 + col;
+      const bool ok = gt < kd && gj < n;
+      const double* src = ok ? B + c * sB + gt * ldb + gj : B;
+      cp_async8(&Bs(st, c, t, col), src, ok ? 8 : 0);
+    }
+  };
+
+  V<K> acc[TM][TN];
+#pragma unroll
+  for (int r = 0; r < TM; ++r)
+#pragma unroll
+    for (int q = 0; q < TN; ++q) acc[r][q] = zero<K>();
+
+  const int64_t ntiles = (kd + BK - 1) / BK;
+  if (ntiles > 0) {
+    load_stage(0, 0);
+    cp_async_commit();
+  }
+  for (int64_t kt = 0; kt < ntiles; ++kt) {
+    const int st = (int)(kt & 1);
+    if (kt + 1 < ntiles) {
+      load_stage(st ^ 1, (kt + 1) * BK);
+      cp_async_commit();
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const int64_t rem = kd - kt * BK;
+    const int tvalid = rem < BK ? (int)rem : BK;
+#pragma unroll 1
+    for (int t = 0; t < tvalid; ++t) {
+      V<K> a[TM], b[TN];
+#pragma unroll
+      for (int r = 0; r < TM; ++r)
+#pragma unroll
+        for (int c = 0; c < K; ++c) a[r].c[c] = As(st, c, ty * TM + r, t);
+#pragma unroll
+      for (int q = 0; q < TN; ++q)
+#pragma unroll
+        for (int c = 0; c < K; ++c) b[q].c[c] = Bs(st, c, t, tx + q * TX);
+#pragma unroll
+      for (int r = 0; r < TM; ++r)
+#pragma unroll
+        for (int q = 0; q < TN; ++q)
+          acc[r][q] = Ops<K, VAR>::add(acc[r][q], Ops<K, VAR>::mul(a[r], b[q]));
+    }
+    __syncthreads();
+  }
+
+#pragma unroll
+  for (int r = 0; r < TM; ++r) {
+    const int64_t gi = m0 + ty * TM + r;
+    if (gi >= m) continue;
+#pragma unroll
+    for (int q = 0; q < TN; ++q) {
+      const int64_t gj = n0 + tx + q * TX;
+      if (gj >= n) continue;
+#pragma unroll
+      for (int c = 0; c < K; ++c) C[c * sC + gi * ldc + gj] = acc[r][q].c[c];
+    }
+  }
+}
+
+template <int K, int VAR>
+struct GemmLaunch {
+  static int run(const double* A, int64_t lda, int64_t sA, const double* B, int64_t ldb,
+                 int64_t sB, double* C, int64_t ldc, int64_t sC, int64_t m, int64_t n, int64_t kd,
+                 cudaStream_t st) {
+    using Cf = GemmCfg<K>;
+    constexpr int NT = (Cf::BM / Cf::TM) * (Cf::BN / Cf::TN);
+    const size_t smem = GemmSmem<K>::BYTES;
+    static bool attr_set = false;
+    if (!attr_set) {
+      cudaFuncSetAttribute(gemm_kernel<K, VAR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smem);
+      attr_set = true;
+    }
+    dim3 grid((unsigned)((n + Cf::BN - 1) / Cf::BN), (unsigned)((m + Cf::BM - 1) / Cf::BM));
+    if (grid.y > 65535u) return MW_ERR_INVALID;
+    gemm_kernel<K, VAR><<<grid, NT, smem, st>>>(A, lda, sA, B, ldb, sB, C, ldc, sC, m, n, kd);
+    return launch_status();
+  }
+};
+
+}  // namespace mw
+
+using namespace mw;
+
+extern "C" int mw_gemm(int k, int variant, const double* A, int64_t lda, int64_t sA,
+                       const double* B, int64_t ldb, int64_t sB, double* C, int64_t ldc,
+                       int64_t sC, int64_t m, int64_t n, int64_t kd, void* stream) {
+  if (k < 2 || k > 4) return MW_ERR_INVALID;
+  if (variant == 0 && k != 2) return MW_ERR_UNSUPPORTED;
+  if (variant != 0 && variant != 1) return MW_ERR_INVALID;
+  if (m < 0 || n < 0 || kd < 0) return MW_ERR_INVALID;
+  if (m == 0 || n == 0) return MW_OK;
+  if (!C || ldc < n || sC < (m - 1) * ldc + n) return MW_ERR_INVALID;
+  if (kd > 0) {
+    if (!A || !B || lda < kd || ldb < n) return MW_ERR_INVALID;
+    if (sA < (m - 1) * lda + kd || sB < (kd - 1) * ldb + n) return MW_ERR_INVALID;
+  }
+  return dispatch<GemmLaunch>(k, variant, A, lda, sA, B, ldb, sB, C, ldc, sC, m, n, kd,
+                              as_stream(stream));
+}

@@ -1,0 +1,100 @@
+// horner.cu — batched Horner evaluation of one K-word polynomial.
+//
+// Semantics (poly.horner_eval, poly.py:89-96), per point x:
+//   acc = a[deg];  for i = deg-1 .. 0:  acc = add(mul(acc, x), a[i])
+// Bit-exact per point.  The reference evaluates one point per call; the
+// lane-batched fold over _BATCH_* (batch.py:178-194) is the same sequence
+// across lanes.
+//
+// Design: one point per thread-slot, PPT independent points per thread for
+// ILP (the Horner step is one long dependent chain: QD mul+add depth ~60).
+// The coefficients are staged through shared memory in chunks of CH words
+// (uniform across the CTA: every read is a broadcast), highest chunk first.
+// Points are loaded/stored once, coalesced per plane.
+#include "common.cuh"
+
+namespace mw {
+
+constexpr int HORNER_THREADS = 128;
+constexpr int HORNER_CH = 256;
+
+template <int K>
+struct HornerCfg;
+template <> struct HornerCfg<2> { static constexpr int PPT = 2; };
+template <> struct HornerCfg<3> { static constexpr int PPT = 2; };
+template <> struct HornerCfg<4> { static constexpr int PPT = 2; };
+
+template <int K, int VAR>
+__global__ void __launch_bounds__(HORNER_THREADS)
+    horner_kernel(const double* __restrict__ coeffs, int64_t sc, int64_t degree,
+                  const double* __restrict__ x, int64_t sx, double* __restrict__ y, int64_t sy,
+                  int64_t npts) {
+  constexpr int PPT = HornerCfg<K>::PPT;
+  __shared__ double cs[K][HORNER_CH];
+  const int64_t base = (int64_t)blockIdx.x * HORNER_THREADS * PPT + threadIdx.x;
+
+  V<K> xv[PPT], acc[PPT];
+#pragma unroll
+  for (int j = 0; j < PPT; ++j) {
+    const int64_t p = base + (int64_t)j * HORNER_THREADS;
+    xv[j] = p < npts ? load<K>(x, sx, p) : zero<K>();
+    acc[j] = load<K>(coeffs, sc, degree);
+  }
+
+  // coefficients deg-1 .. 0, in chunks [lo, hi) walked downward
+  for (int64_t hi = degree; hi > 0; hi -= HORNER_CH) {
+    const int64_t lo = hi > HORNER_CH ? hi - HORNER_CH : 0;
+    const int cnt = (int)(hi - lo);
+    __syncthreads();
+    for (int e = threadIdx.x; e < K * cnt; e += HORNER_THREADS) {
+      const int c = e / cnt, i = e % cnt;
+      cs[c][i] = coeffs[c * sc + lo + i];
+    }
+    __syncthreads();
+#pragma unroll 1
+    for (int i = cnt - 1; i >= 0; --i) {
+      V<K> a;
+#pragma unroll
+      for (int c = 0; c < K; ++c) a.c[c] = cs[c][i];
+#pragma unroll
+      for (int j = 0; j < PPT; ++j) acc[j] = Ops<K, VAR>::add(Ops<K, VAR>::mul(acc[j], xv[j]), a);
+    }
+  }
+
+#pragma unroll
+  for (int j = 0; j < PPT; ++j) {
+    const int64_t p = base + (int64_t)j * HORNER_THREADS;
+    if (p < npts) store<K>(y, sy, p, acc[j]);
+  }
+}
+
+template <int K, int VAR>
+struct HornerLaunch {
+  static int run(const double* coeffs, int64_t sc, int64_t degree, const double* x, int64_t sx,
+                 double* y, int64_t sy, int64_t npts, cudaStream_t st) {
+    constexpr int PPT = HornerCfg<K>::PPT;
+    const int64_t per_block = (int64_t)HORNER_THREADS * PPT;
+    const int64_t blocks = (npts + per_block - 1) / per_block;
+    if (blocks > 0x7fffffffLL) return MW_ERR_INVALID;
+    horner_kernel<K, VAR><<<(unsigned)blocks, HORNER_THREADS, 0, st>>>(coeffs, sc, degree, x, sx,
+                                                                       y, sy, npts);
+    return launch_status();
+  }
+};
+
+}  // namespace mw
+
+using namespace mw;
+
+extern "C" int mw_horner(int k, int variant, const double* coeffs, int64_t sc, int64_t degree,
+                         const double* x, int64_t sx, double* y, int64_t sy, int64_t npts,
+                         void* stream) {
+  if (k < 2 || k > 4) return MW_ERR_INVALID;
+  if (variant == 0 && k != 2) return MW_ERR_UNSUPPORTED;
+  if (variant != 0 && variant != 1) return MW_ERR_INVALID;
+  if (degree < 0 || npts < 0) return MW_ERR_INVALID;
+  if (npts == 0) return MW_OK;
+  if (!coeffs || !x || !y || sc < degree + 1 || sx < npts || sy < npts) return MW_ERR_INVALID;
+  return dispatch<HornerLaunch>(k, variant, coeffs, sc, degree, x, sx, y, sy, npts,
+                                as_stream(stream));
+}

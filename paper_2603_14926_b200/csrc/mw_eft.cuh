@@ -1,0 +1,342 @@
+// mw_eft.cuh — error-free transformations and the branch-free DD/TD/QD
+// kernels as inlined device functions.
+//
+// Every floating-point step is one explicitly rounded IEEE operation
+// (__dadd_rn / __dsub_rn / __dmul_rn / __fma_rn) so nvcc can neither
+// contract a*b+c into an FMA nor reassociate; the only FMA is the one in
+// two_prod, exactly as in the reference (pkg/src/mwfloat/eft.py:74-83).
+// Negation is an IEEE-exact sign flip (a free operand modifier in SASS).
+//
+// The bodies transcribe the reference's straight-line kernels op for op:
+//   dd_add_bf  multiword.py:129-137 (paper Alg 6)
+//   dd_mul_bf  multiword.py:148-156 (paper Alg 8; identical op sequence to
+//              dw_mul, multiword.py:140-145, the K=2 STANDARD mul)
+//   dd_add_acc multiword.py:118-126 (dw_add_accurate, K=2 STANDARD add)
+//   td_add_bf  multiword.py:361-378 (paper Alg 11)
+//   td_mul_bf  multiword.py:381-402 (paper Alg 12)
+//   qd_add_bf  multiword.py:516-545 (paper Alg 13)
+//   qd_mul_bf  multiword.py:548-588 (paper Alg 14)
+// Operand order inside each two_sum/quick_two_sum matters for bit
+// equality and is kept as written there.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#if defined(__CUDA_ARCH__)
+#define MW_ADD(a, b) __dadd_rn((a), (b))
+#define MW_SUB(a, b) __dsub_rn((a), (b))
+#define MW_MUL(a, b) __dmul_rn((a), (b))
+#define MW_FMA(a, b, c) __fma_rn((a), (b), (c))
+#define MW_DIV(a, b) __ddiv_rn((a), (b))
+#else
+#include <cmath>
+#define MW_ADD(a, b) ((a) + (b))
+#define MW_SUB(a, b) ((a) - (b))
+#define MW_MUL(a, b) ((a) * (b))
+#define MW_FMA(a, b, c) std::fma((a), (b), (c))
+#define MW_DIV(a, b) ((a) / (b))
+#endif
+
+#define MW_HD __host__ __device__ __forceinline__
+
+namespace mw {
+
+enum Variant : int { STANDARD = 0, BRANCH_FREE = 1 };
+
+template <int K>
+struct V {
+  double c[K];
+};
+
+// ---------------------------------------------------------------- EFTs
+// eft.py:51-60
+MW_HD void quick_two_sum(double a, double b, double& s, double& e) {
+  s = MW_ADD(a, b);
+  e = MW_SUB(b, MW_SUB(s, a));
+}
+
+// eft.py:63-71
+MW_HD void two_sum(double a, double b, double& s, double& e) {
+  s = MW_ADD(a, b);
+  double v = MW_SUB(s, a);
+  e = MW_ADD(MW_SUB(a, MW_SUB(s, v)), MW_SUB(b, v));
+}
+
+// eft.py:74-83
+MW_HD void two_prod(double a, double b, double& p, double& e) {
+  p = MW_MUL(a, b);
+  e = MW_FMA(a, b, -p);
+}
+
+// ------------------------------------------------------------- DD (K=2)
+MW_HD V<2> dd_add_bf(const V<2>& a, const V<2>& b) {
+  double g1, g1e, g2, g2e, g3, g3e;
+  two_sum(a.c[0], b.c[0], g1, g1e);
+  two_sum(a.c[1], b.c[1], g2, g2e);
+  quick_two_sum(g1, g2, g3, g3e);
+  double g4 = MW_ADD(g1e, g2e);
+  double g5 = MW_ADD(g4, g3e);
+  V<2> r;
+  quick_two_sum(g3, g5, r.c[0], r.c[1]);
+  return r;
+}
+
+MW_HD V<2> dd_add_acc(const V<2>& a, const V<2>& b) {
+  double s1, s2, t1, t2;
+  two_sum(a.c[0], b.c[0], s1, s2);
+  two_sum(a.c[1], b.c[1], t1, t2);
+  s2 = MW_ADD(s2, t1);
+  quick_two_sum(s1, s2, s1, s2);
+  s2 = MW_ADD(s2, t2);
+  V<2> r;
+  quick_two_sum(s1, s2, r.c[0], r.c[1]);
+  return r;
+}
+
+MW_HD V<2> dd_mul_bf(const V<2>& a, const V<2>& b) {
+  double p00, pe00;
+  two_prod(a.c[0], b.c[0], p00, pe00);
+  double p01 = MW_MUL(a.c[0], b.c[1]);
+  double p10 = MW_MUL(a.c[1], b.c[0]);
+  double g1 = MW_ADD(p01, p10);
+  double g2 = MW_ADD(pe00, g1);
+  V<2> r;
+  quick_two_sum(p00, g2, r.c[0], r.c[1]);
+  return r;
+}
+
+// ------------------------------------------------------------- TD (K=3)
+MW_HD V<3> td_add_bf(const V<3>& a, const V<3>& b) {
+  double a1_, b1_, c1, d1, e1, f1, a2_, c2, d2, e2, a3, d3, b3, c3, c5, d5, b6,
+      c6, b7;
+  two_sum(a.c[0], b.c[0], a1_, b1_);
+  two_sum(a.c[1], b.c[1], c1, d1);
+  two_sum(a.c[2], b.c[2], e1, f1);
+  quick_two_sum(a1_, c1, a2_, c2);
+  double b2_ = MW_ADD(b1_, f1);
+  two_sum(d1, e1, d2, e2);
+  quick_two_sum(a2_, d2, a3, d3);
+  two_sum(b2_, c2, b3, c3);
+  double c4 = MW_ADD(c3, e2);
+  two_sum(c4, d3, c5, d5);
+  two_sum(b3, c5, b6, c6);
+  V<3> r;
+  quick_two_sum(a3, b6, r.c[0], b7);
+  double c7 = MW_ADD(c6, d5);
+  quick_two_sum(b7, c7, r.c[1], r.c[2]);
+  return r;
+}
+
+MW_HD V<3> td_mul_bf(const V<3>& A, const V<3>& B) {
+  double a0, b0, c0, e0, d0, f0, c1, d1, b2, c2, a3, b3, b5, c5, b6;
+  two_prod(A.c[0], B.c[0], a0, b0);
+  two_prod(A.c[0], B.c[1], c0, e0);
+  two_prod(A.c[1], B.c[0], d0, f0);
+  double g0 = MW_MUL(A.c[0], B.c[2]);
+  double h0 = MW_MUL(A.c[1], B.c[1]);
+  double i0 = MW_MUL(A.c[2], B.c[0]);
+  two_sum(c0, d0, c1, d1);
+  double e1 = MW_ADD(e0, f0);
+  double g1 = MW_ADD(g0, i0);
+  two_sum(b0, c1, b2, c2);
+  double g2 = MW_ADD(g1, h0);
+  quick_two_sum(a0, b2, a3, b3);
+  double c3 = MW_ADD(c2, d1);
+  double e3 = MW_ADD(e1, g2);
+  double c4 = MW_ADD(c3, e3);
+  quick_two_sum(b3, c4, b5, c5);
+  V<3> r;
+  quick_two_sum(a3, b5, r.c[0], b6);
+  quick_two_sum(b6, c5, r.c[1], r.c[2]);
+  return r;
+}
+
+// ------------------------------------------------------------- QD (K=4)
+MW_HD V<4> qd_add_bf(const V<4>& A, const V<4>& B) {
+  double a1, b1, c1, d1, e1, f1, g1, h1, a2, c2, d2, e2, f2, g2, b3, g3, c3, d3,
+      e3, f3, a4, c4, d4, e4, b5, d5, b6, c6, d6, e6, a7, b7, c7, d7, b8, c8,
+      b10, c10, d10, c11;
+  two_sum(A.c[0], B.c[0], a1, b1);
+  two_sum(A.c[1], B.c[1], c1, d1);
+  two_sum(A.c[2], B.c[2], e1, f1);
+  two_sum(A.c[3], B.c[3], g1, h1);
+  quick_two_sum(a1, c1, a2, c2);
+  double b2 = MW_ADD(b1, h1);
+  two_sum(d1, e1, d2, e2);
+  two_sum(f1, g1, f2, g2);
+  two_sum(b2, g2, b3, g3);
+  quick_two_sum(c2, d2, c3, d3);
+  two_sum(e2, f2, e3, f3);
+  quick_two_sum(a2, c3, a4, c4);
+  quick_two_sum(d3, e3, d4, e4);
+  two_sum(b3, d4, b5, d5);
+  double e5 = MW_ADD(e4, f3);
+  two_sum(b5, c4, b6, c6);
+  two_sum(d5, e5, d6, e6);
+  quick_two_sum(a4, b6, a7, b7);
+  quick_two_sum(c6, d6, c7, d7);
+  double e8 = MW_ADD(e6, g3);
+  quick_two_sum(b7, c7, b8, c8);
+  double d9 = MW_ADD(d7, e8);
+  V<4> r;
+  quick_two_sum(a7, b8, r.c[0], b10);
+  quick_two_sum(c8, d9, c10, d10);
+  quick_two_sum(b10, c10, r.c[1], c11);
+  quick_two_sum(c11, d10, r.c[2], r.c[3]);
+  return r;
+}
+
+MW_HD V<4> qd_mul_bf(const V<4>& A, const V<4>& B) {
+  double a0, b0, c0, e0, d0, f0, g0, j0, h0, k0, i0, l0, c1, d1, e1, f1, g1, i1,
+      b2, c2, e2, h2, a3, b3, c3, d3, e3, g3, c4, e4, c6, d6, b7, c7, b8, c8, d8,
+      c9;
+  two_prod(A.c[0], B.c[0], a0, b0);
+  two_prod(A.c[0], B.c[1], c0, e0);
+  two_prod(A.c[1], B.c[0], d0, f0);
+  two_prod(A.c[0], B.c[2], g0, j0);
+  two_prod(A.c[1], B.c[1], h0, k0);
+  two_prod(A.c[2], B.c[0], i0, l0);
+  double m0 = MW_MUL(A.c[0], B.c[3]);
+  double n0 = MW_MUL(A.c[1], B.c[2]);
+  double o0 = MW_MUL(A.c[2], B.c[1]);
+  double p0 = MW_MUL(A.c[3], B.c[0]);
+  two_sum(c0, d0, c1, d1);
+  two_sum(e0, f0, e1, f1);
+  two_sum(g0, i0, g1, i1);
+  double j1 = MW_ADD(j0, l0);
+  double m1 = MW_ADD(m0, p0);
+  double n1 = MW_ADD(n0, o0);
+  two_sum(b0, c1, b2, c2);
+  two_sum(e1, h0, e2, h2);
+  double f2 = MW_ADD(f1, j1);
+  double i2 = MW_ADD(i1, k0);
+  double m2 = MW_ADD(m1, n1);
+  quick_two_sum(a0, b2, a3, b3);
+  quick_two_sum(c2, d1, c3, d3);
+  two_sum(e2, g1, e3, g3);
+  double f3 = MW_ADD(f2, m2);
+  double h3 = MW_ADD(h2, i2);
+  two_sum(c3, e3, c4, e4);
+  double d4 = MW_ADD(d3, h3);
+  double f4 = MW_ADD(f3, g3);
+  double d5 = MW_ADD(d4, e4);
+  two_sum(c4, d5, c6, d6);
+  two_sum(b3, c6, b7, c7);
+  double d7 = MW_ADD(d6, f4);
+  V<4> r;
+  quick_two_sum(a3, b7, r.c[0], b8);
+  two_sum(c7, d7, c8, d8);
+  two_sum(b8, c8, r.c[1], c9);
+  quick_two_sum(c9, d8, r.c[2], r.c[3]);
+  return r;
+}
+
+// ------------------------------------------------------ (K, Variant) ops
+// Mirrors the dispatch tables _BATCH_ADD/_BATCH_MUL (batch.py:178-194).
+// STANDARD exists on the device for K=2 only (dw_add_accurate / dw_mul);
+// the C-ABI rejects STANDARD for K=3,4 before any launch.
+template <int K, int VAR>
+struct Ops;
+
+template <>
+struct Ops<2, BRANCH_FREE> {
+  static MW_HD V<2> add(const V<2>& a, const V<2>& b) { return dd_add_bf(a, b); }
+  static MW_HD V<2> mul(const V<2>& a, const V<2>& b) { return dd_mul_bf(a, b); }
+};
+template <>
+struct Ops<2, STANDARD> {
+  static MW_HD V<2> add(const V<2>& a, const V<2>& b) { return dd_add_acc(a, b); }
+  static MW_HD V<2> mul(const V<2>& a, const V<2>& b) { return dd_mul_bf(a, b); }
+};
+template <>
+struct Ops<3, BRANCH_FREE> {
+  static MW_HD V<3> add(const V<3>& a, const V<3>& b) { return td_add_bf(a, b); }
+  static MW_HD V<3> mul(const V<3>& a, const V<3>& b) { return td_mul_bf(a, b); }
+};
+template <>
+struct Ops<4, BRANCH_FREE> {
+  static MW_HD V<4> add(const V<4>& a, const V<4>& b) { return qd_add_bf(a, b); }
+  static MW_HD V<4> mul(const V<4>& a, const V<4>& b) { return qd_mul_bf(a, b); }
+};
+
+template <int K>
+MW_HD V<K> neg(const V<K>& a) {
+  V<K> r;
+#pragma unroll
+  for (int c = 0; c < K; ++c) r.c[c] = -a.c[c];
+  return r;
+}
+
+template <int K>
+MW_HD V<K> zero() {
+  V<K> r;
+#pragma unroll
+  for (int c = 0; c < K; ++c) r.c[c] = 0.0;
+  return r;
+}
+
+template <int K>
+MW_HD V<K> constant(double v) {
+  V<K> r = zero<K>();
+  r.c[0] = v;
+  return r;
+}
+
+// Newton iteration counts per K (multiword.py:614).
+template <int K>
+struct DivIters;
+template <>
+struct DivIters<2> { static constexpr int value = 2; };
+template <>
+struct DivIters<3> { static constexpr int value = 3; };
+template <>
+struct DivIters<4> { static constexpr int value = 3; };
+
+// Reciprocal part of _newton_div (multiword.py:633-658) on one lane, as the
+// lane-batched path runs it: constants are built by _const_like from b, so
+// their zero components are b0*0.0 (sign of b0; NaN when b0 is not finite),
+// and the seed is the IEEE quotient 1/b0 (numpy semantics: 1/-0 = -inf).
+template <int K, int VAR>
+MW_HD V<K> recip_newton(const V<K>& b) {
+  const double z = MW_MUL(b.c[0], 0.0);
+  V<K> two, x;
+#pragma unroll
+  for (int c = 0; c < K; ++c) {
+    two.c[c] = z;
+    x.c[c] = z;
+  }
+  two.c[0] = MW_ADD(z, 2.0);
+  x.c[0] = MW_DIV(MW_ADD(z, 1.0), b.c[0]);
+#pragma unroll
+  for (int it = 0; it < DivIters<K>::value; ++it) {
+    V<K> t = Ops<K, VAR>::mul(b, x);
+    V<K> e = Ops<K, VAR>::add(two, neg(t));
+    x = Ops<K, VAR>::mul(x, e);
+  }
+  return x;
+}
+
+template <int K, int VAR>
+MW_HD V<K> div_newton(const V<K>& a, const V<K>& b) {
+  return Ops<K, VAR>::mul(a, recip_newton<K, VAR>(b));
+}
+
+// ------------------------------------------------------ plane load/store
+// A K-word array lives as K planes of doubles, plane c at base + c*stride.
+template <int K>
+__device__ __forceinline__ V<K> load(const double* __restrict__ p, long long stride,
+                                     long long i) {
+  V<K> r;
+#pragma unroll
+  for (int c = 0; c < K; ++c) r.c[c] = p[c * stride + i];
+  return r;
+}
+
+template <int K>
+__device__ __forceinline__ void store(double* __restrict__ p, long long stride,
+                                      long long i, const V<K>& v) {
+#pragma unroll
+  for (int c = 0; c < K; ++c) p[c * stride + i] = v.c[c];
+}
+
+}  // namespace mw

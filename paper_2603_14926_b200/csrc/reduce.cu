@@ -1,0 +1,308 @@
+// reduce.cu — dot, pairwise-tree fold and GEMV.
+//
+// Reference semantics (no dot/gemv function exists in the reference; both
+// are defined from the naive matmul fold, linalg.py:284-314):
+//   dot(x, y)  = fold_t add(acc, mul(x_t, y_t)), acc = exact zero, t asc.
+//   gemv(A, x)_i = the same fold over row i.
+// MW_ORDER_EXACT replays that fold on one thread per output (bit-exact).
+// MW_ORDER_TREE is the throughput order; its tree is a pure function of n
+// (never of grid shape or GPU count), so results are deterministic and
+// identical on 1..8 GPUs:
+//   dot:  leaf chunk c = elements [16c, 16c+16) folded ascending from exact
+//         zero; chunk partials combined in place by a pairwise tree
+//         (stride s = 1, 2, 4, ...: v[i] <- add(v[i], v[i+s]) for i % 2s == 0
+//         when i+s < count; an unpaired tail passes through).
+//   gemv: lane l of the row's warp folds t = l, l+32, ... ascending from
+//         exact zero; the 32 lane partials combine by the same pairwise tree.
+#include "common.cuh"
+
+namespace mw {
+
+constexpr int DOT_LEAF = 16;       // elements per leaf chunk
+constexpr int DOT_BLOCK = 256;     // leaf chunks (threads) per block
+constexpr int64_t DOT_PER_BLOCK = (int64_t)DOT_LEAF * DOT_BLOCK;  // 4096
+
+// Pairwise tree over the block's 256 values v (one per thread) whose global
+// in-place indices are base + tid, valid when < count.  Returns the subtree
+// root in thread 0.
+template <int K, int VAR>
+__device__ __forceinline__ V<K> block_tree(V<K> v, int64_t base, int64_t count) {
+  __shared__ double red[K][DOT_BLOCK / 32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t gi = base + tid;
+#pragma unroll
+  for (int s = 1; s < 32; s <<= 1) {
+    V<K> o = shfl_down<K>(v, s);
+    if ((lane & (2 * s - 1)) == 0 && gi + s < count) v = Ops<K, VAR>::add(v, o);
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int c = 0; c < K; ++c) red[c][warp] = v.c[c];
+  }
+  __syncthreads();
+  if (warp == 0) {
+    // level strides 32, 64, 128 act on warp roots w = 0..7 with strides 1, 2, 4
+    V<K> w;
+    const int nw = DOT_BLOCK / 32;
+#pragma unroll
+    for (int c = 0; c < K; ++c) w.c[c] = lane < nw ? red[c][lane] : 0.0;
+#pragma unroll
+    for (int s = 1; s < nw; s <<= 1) {
+      V<K> o = shfl_down<K>(w, s);
+      if ((lane & (2 * s - 1)) == 0 && lane + s < nw && base + (int64_t)(lane + s) * 32 < count)
+        w = Ops<K, VAR>::add(w, o);
+    }
+    v = w;
+  }
+  return v;
+}
+
+// Stage 1: block b folds 256 leaf chunks and writes its subtree root.
+template <int K, int VAR>
+__global__ void __launch_bounds__(DOT_BLOCK) dot_partials_kernel(
+    const double* __restrict__ x, int64_t sx, const double* __restrict__ y, int64_t sy,
+    int64_t n, double* __restrict__ partials, int64_t pstride) {
+  const int64_t chunk = blockIdx.x * (int64_t)DOT_BLOCK + threadIdx.x;
+  const int64_t nchunks = (n + DOT_LEAF - 1) / DOT_LEAF;
+  V<K> acc = zero<K>();
+  const int64_t t0 = chunk * DOT_LEAF;
+  if (t0 + DOT_LEAF <= n) {
+    V<K> xs[DOT_LEAF], ys[DOT_LEAF];
+#pragma unroll
+    for (int t = 0; t < DOT_LEAF; ++t) {
+      xs[t] = load<K>(x, sx, t0 + t);
+      ys[t] = load<K>(y, sy, t0 + t);
+    }
+#pragma unroll
+    for (int t = 0; t < DOT_LEAF; ++t)
+      acc = Ops<K, VAR>::add(acc, Ops<K, VAR>::mul(xs[t], ys[t]));
+  } else {
+    for (int64_t t = t0; t < n; ++t)
+      acc = Ops<K, VAR>::add(acc, Ops<K, VAR>::mul(load<K>(x, sx, t), load<K>(y, sy, t)));
+  }
+  V<K> r = block_tree<K, VAR>(acc, blockIdx.x * (int64_t)DOT_BLOCK, nchunks);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int c = 0; c < K; ++c) partials[c * pstride + blockIdx.x] = r.c[c];
+  }
+}
+
+// Tree stage above the leaves: groups of 256 values -> one subtree root.
+template <int K, int VAR>
+__global__ void __launch_bounds__(DOT_BLOCK) tree_fold_kernel(const double* __restrict__ in,
+                                                              int64_t istride, int64_t count,
+                                                              double* __restrict__ out,
+                                                              int64_t ostride) {
+  const int64_t i = blockIdx.x * (int64_t)DOT_BLOCK + threadIdx.x;
+  V<K> v = zero<K>();
+  if (i < count) v = load<K>(in, istride, i);
+  V<K> r = block_tree<K, VAR>(v, blockIdx.x * (int64_t)DOT_BLOCK, count);
+  if (threadIdx.x == 0) store<K>(out, ostride, blockIdx.x, r);
+}
+
+// Exact reference order on one thread (parity path).
+template <int K, int VAR>
+__global__ void dot_exact_kernel(const double* __restrict__ x, int64_t sx,
+                                 const double* __restrict__ y, int64_t sy, int64_t n,
+                                 double* __restrict__ out) {
+  V<K> acc = zero<K>();
+  for (int64_t t = 0; t < n; ++t)
+    acc = Ops<K, VAR>::add(acc, Ops<K, VAR>::mul(load<K>(x, sx, t), load<K>(y, sy, t)));
+  store<K>(out, 1, 0, acc);
+}
+
+static int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// Folds `count` values (plane stride istride) in `in` down to one value
+// written to out (plane stride 1).  ws holds the intermediate levels:
+// needs ceil(count/256) * K doubles (+ the next levels, each 256x smaller).
+template <int K, int VAR>
+static int fold_levels(const double* in, int64_t istride, int64_t count, double* ws, double* out,
+                       cudaStream_t st) {
+  const double* cur = in;
+  int64_t cstride = istride;
+  while (true) {
+    int64_t nb = ceil_div(count, DOT_BLOCK);
+    double* dst = (nb == 1) ? out : ws;
+    int64_t dstride = (nb == 1) ? 1 : nb;
+    tree_fold_kernel<K, VAR><<<(unsigned)nb, DOT_BLOCK, 0, st>>>(cur, cstride, count, dst, dstride);
+    int rc = launch_status();
+    if (rc) return rc;
+    if (nb == 1) return MW_OK;
+    cur = ws;
+    cstride = nb;
+    count = nb;
+    ws += nb * K;
+  }
+}
+
+template <int K, int VAR>
+struct DotLaunch {
+  static int run(const double* x, int64_t sx, const double* y, int64_t sy, int64_t n, double* ws,
+                 double* out, int order, cudaStream_t st) {
+    if (order == MW_ORDER_EXACT || n == 0) {
+      dot_exact_kernel<K, VAR><<<1, 1, 0, st>>>(x, sx, y, sy, n, out);
+      return launch_status();
+    }
+    int64_t nb = ceil_div(n, DOT_PER_BLOCK);
+    if (nb == 1) {
+      dot_partials_kernel<K, VAR><<<1, DOT_BLOCK, 0, st>>>(x, sx, y, sy, n, out, 1);
+      return launch_status();
+    }
+    dot_partials_kernel<K, VAR><<<(unsigned)nb, DOT_BLOCK, 0, st>>>(x, sx, y, sy, n, ws, nb);
+    int rc = launch_status();
+    if (rc) return rc;
+    return fold_levels<K, VAR>(ws, nb, nb, ws + nb * K, out, st);
+  }
+};
+
+template <int K, int VAR>
+struct DotPartialsLaunch {
+  static int run(const double* x, int64_t sx, const double* y, int64_t sy, int64_t n,
+                 double* partials, int64_t pstride, cudaStream_t st) {
+    int64_t nb = ceil_div(n, DOT_PER_BLOCK);
+    dot_partials_kernel<K, VAR><<<(unsigned)nb, DOT_BLOCK, 0, st>>>(x, sx, y, sy, n, partials,
+                                                                    pstride);
+    return launch_status();
+  }
+};
+
+template <int K, int VAR>
+struct TreeFoldLaunch {
+  static int run(const double* partials, int64_t pstride, int64_t count, double* ws, double* out,
+                 cudaStream_t st) {
+    return fold_levels<K, VAR>(partials, pstride, count, ws, out, st);
+  }
+};
+
+// ------------------------------------------------------------------ GEMV
+// Exact order: thread per row, t ascending.
+template <int K, int VAR>
+__global__ void __launch_bounds__(128) gemv_exact_kernel(const double* __restrict__ A, int64_t lda,
+                                                         int64_t sA, const double* __restrict__ x,
+                                                         int64_t sx, double* __restrict__ y,
+                                                         int64_t sy, int64_t m, int64_t n) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  V<K> acc = zero<K>();
+  const double* row = A + i * lda;
+  for (int64_t t = 0; t < n; ++t)
+    acc = Ops<K, VAR>::add(acc, Ops<K, VAR>::mul(load<K>(row, sA, t), load<K>(x, sx, t)));
+  store<K>(y, sy, i, acc);
+}
+
+// Tree order: warp per row; lane l folds t = l + 32 j; pairwise shuffle tree.
+template <int K, int VAR>
+__global__ void __launch_bounds__(256) gemv_tree_kernel(const double* __restrict__ A, int64_t lda,
+                                                        int64_t sA, const double* __restrict__ x,
+                                                        int64_t sx, double* __restrict__ y,
+                                                        int64_t sy, int64_t m, int64_t n) {
+  const int lane = threadIdx.x & 31;
+  const int64_t i = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (i >= m) return;
+  const double* row = A + i * lda;
+  V<K> acc = zero<K>();
+  int64_t t = lane;
+  // two loads in flight per step: the fold stays strictly ascending
+  for (; t + 32 < n; t += 64) {
+    V<K> a0 = load<K>(row, sA, t), x0 = load<K>(x, sx, t);
+    V<K> a1 = load<K>(row, sA, t + 32), x1 = load<K>(x, sx, t + 32);
+    acc = Ops<K, VAR>::add(acc, Ops<K, VAR>::mul(a0, x0));
+    acc = Ops<K, VAR>::add(acc, Ops<K, VAR>::mul(a1, x1));
+  }
+  if (t < n) acc = Ops<K, VAR>::add(acc, Ops<K, VAR>::mul(load<K>(row, sA, t), load<K>(x, sx, t)));
+  const int64_t valid = n < 32 ? n : 32;
+#pragma unroll
+  for (int s = 1; s < 32; s <<= 1) {
+    V<K> o = shfl_down<K>(acc, s);
+    if ((lane & (2 * s - 1)) == 0 && lane + s < valid) acc = Ops<K, VAR>::add(acc, o);
+  }
+  if (lane == 0) store<K>(y, sy, i, acc);
+}
+
+template <int K, int VAR>
+struct GemvLaunch {
+  static int run(const double* A, int64_t lda, int64_t sA, const double* x, int64_t sx, double* y,
+                 int64_t sy, int64_t m, int64_t n, int order, cudaStream_t st) {
+    if (order == MW_ORDER_EXACT) {
+      gemv_exact_kernel<K, VAR><<<(unsigned)ceil_div(m, 128), 128, 0, st>>>(A, lda, sA, x, sx, y,
+                                                                            sy, m, n);
+    } else {
+      gemv_tree_kernel<K, VAR><<<(unsigned)ceil_div(m, 8), 256, 0, st>>>(A, lda, sA, x, sx, y, sy,
+                                                                         m, n);
+    }
+    return launch_status();
+  }
+};
+
+}  // namespace mw
+
+using namespace mw;
+
+static int variant_ok(int k, int variant) {
+  if (k < 2 || k > 4) return MW_ERR_INVALID;
+  if (variant == 1 || (variant == 0 && k == 2)) return MW_OK;
+  return variant == 0 ? MW_ERR_UNSUPPORTED : MW_ERR_INVALID;
+}
+
+extern "C" int64_t mw_dot_workspace(int k, int64_t n) {
+  if (k < 2 || k > 4 || n < 0) return 0;
+  int64_t nb = ceil_div(n, DOT_PER_BLOCK);
+  if (nb <= 1) return 0;
+  return nb * k + mw_tree_fold_workspace(k, nb);
+}
+
+extern "C" int64_t mw_tree_fold_workspace(int k, int64_t count) {
+  if (k < 2 || k > 4 || count < 1) return 0;
+  int64_t total = 0;
+  for (int64_t c = ceil_div(count, DOT_BLOCK); c > 1; c = ceil_div(c, DOT_BLOCK)) total += c * k;
+  return total;
+}
+
+extern "C" int64_t mw_dot_num_partials(int64_t n) { return n <= 0 ? 0 : ceil_div(n, DOT_PER_BLOCK); }
+
+extern "C" int mw_dot(int k, int variant, const double* x, int64_t sx, const double* y, int64_t sy,
+                      int64_t n, double* ws, double* out_dev, int order, void* stream) {
+  int rc = variant_ok(k, variant);
+  if (rc) return rc;
+  if (n < 0 || !out_dev || (n > 0 && (!x || !y || sx < n || sy < n))) return MW_ERR_INVALID;
+  if (order != MW_ORDER_EXACT && order != MW_ORDER_TREE) return MW_ERR_INVALID;
+  if (order == MW_ORDER_TREE && mw_dot_workspace(k, n) > 0 && !ws) return MW_ERR_INVALID;
+  return dispatch<DotLaunch>(k, variant, x, sx, y, sy, n, ws, out_dev, order, as_stream(stream));
+}
+
+extern "C" int mw_dot_partials(int k, int variant, const double* x, int64_t sx, const double* y,
+                               int64_t sy, int64_t n, double* partials, int64_t pstride,
+                               void* stream) {
+  int rc = variant_ok(k, variant);
+  if (rc) return rc;
+  if (n < 0 || (n > 0 && (!x || !y || !partials || sx < n || sy < n))) return MW_ERR_INVALID;
+  if (n == 0) return MW_OK;
+  if (pstride < mw_dot_num_partials(n)) return MW_ERR_INVALID;
+  return dispatch<DotPartialsLaunch>(k, variant, x, sx, y, sy, n, partials, pstride,
+                                     as_stream(stream));
+}
+
+extern "C" int mw_tree_fold(int k, int variant, const double* partials, int64_t pstride,
+                            int64_t count, double* ws, double* out_dev, void* stream) {
+  int rc = variant_ok(k, variant);
+  if (rc) return rc;
+  if (count < 1 || !partials || !out_dev || pstride < count) return MW_ERR_INVALID;
+  if (mw_tree_fold_workspace(k, count) > 0 && !ws) return MW_ERR_INVALID;
+  return dispatch<TreeFoldLaunch>(k, variant, partials, pstride, count, ws, out_dev,
+                                  as_stream(stream));
+}
+
+extern "C" int mw_gemv(int k, int variant, const double* A, int64_t lda, int64_t sA,
+                       const double* x, int64_t sx, double* y, int64_t sy, int64_t m, int64_t n,
+                       int order, void* stream) {
+  int rc = variant_ok(k, variant);
+  if (rc) return rc;
+  if (m < 0 || n < 0) return MW_ERR_INVALID;
+  if (order != MW_ORDER_EXACT && order != MW_ORDER_TREE) return MW_ERR_INVALID;
+  if (m == 0) return MW_OK;
+  if (!A || !x || !y || lda < n || sy < m || sx < n) return MW_ERR_INVALID;
+  if (n > 0 && sA < (m - 1) * lda + n) return MW_ERR_INVALID;
+  return dispatch<GemvLaunch>(k, variant, A, lda, sA, x, sx, y, sy, m, n, order,
+                              as_stream(stream));
+}

@@ -1,0 +1,128 @@
+"""Real-coefficient polynomial evaluation on the GPU (Horner).
+
+Drop-in for the Horner path of mwfloat.poly (pkg/src/mwfloat/poly.py):
+``MWPolynomial`` (40-86) keeps coefficients a[0..n] (a[i] multiplies x^i)
+as a (K, n+1) float64 CUDA tensor; ``horner_eval(p, x, variant)`` (89-96)
+keeps its signature and returns the K-word tuple; the batched form
+``horner_eval_batched(p, xs: LaneBatch, variant)`` (the name pattern of
+estrin_eval_batched, 125-153) evaluates every lane with the same op
+sequence in one mw_horner launch -- bit-exact per point.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib
+from .batch import LaneBatch, as_planes
+from .multiword import BITS, Variant, from_basefloat, variant_code
+
+__all__ = ["MWPolynomial", "horner_eval", "horner_eval_batched", "horner_into", "random_polynomial"]
+
+
+class MWPolynomial:
+    """Coefficients a[0..n] (a[i] multiplies x^i), component-planar."""
+
+    __slots__ = ("planes",)
+
+    def __init__(self, comps, device=None):
+        self.planes = as_planes(comps, 1, device)
+        if self.planes.shape[1] == 0:
+            raise ValueError("a polynomial needs at least one coefficient")
+
+    @property
+    def comps(self) -> tuple:
+        return tuple(self.planes[c] for c in range(self.k))
+
+    @property
+    def k(self) -> int:
+        return self.planes.shape[0]
+
+    @property
+    def degree(self) -> int:
+        return self.planes.shape[1] - 1
+
+    @property
+    def device(self) -> torch.device:
+        return self.planes.device
+
+    @classmethod
+    def from_coeffs(cls, coeffs, k: int | None = None, device=None) -> "MWPolynomial":
+        """coeffs: K-word tuples / objects with .comps / floats, low to high."""
+        rows = []
+        for c in coeffs:
+            if hasattr(c, "comps"):
+                rows.append(tuple(c.comps))
+            elif isinstance(c, (tuple, list)):
+                rows.append(tuple(c))
+            else:
+                if k is None:
+                    raise ValueError("k required for bare float coefficients")
+                rows.append(from_basefloat(float(c), k))
+        kk = len(rows[0])
+        return cls(np.array([[r[c] for r in rows] for c in range(kk)], dtype=np.float64), device=device)
+
+    def coeff(self, i: int) -> tuple:
+        return tuple(float(v) for v in self.planes[:, i].cpu())
+
+    def coeffs(self) -> list:
+        arr = self.planes.cpu().numpy()
+        return [tuple(float(v) for v in arr[:, i]) for i in range(self.degree + 1)]
+
+    def __repr__(self):
+        return f"MWPolynomial(k={self.k}, degree={self.degree}, device={self.device})"
+
+
+def horner_into(coeffs: torch.Tensor, x: torch.Tensor, y: torch.Tensor, variant, p0: int = 0,
+                p1: int | None = None) -> None:
+    """y[:, p0:p1] = Horner(coeffs, x[:, p0:p1]) on planes tensors -- the
+    point-shard form the multi-GPU path uses."""
+    k, npts = x.shape
+    p1 = npts if p1 is None else p1
+    cnt = p1 - p0
+    if cnt <= 0:
+        return
+    _lib.require_cuda(coeffs, x, y)
+    es = x.element_size()
+    rc = _lib.load().mw_horner(
+        k, variant_code(variant), coeffs.data_ptr(), coeffs.shape[1], coeffs.shape[1] - 1,
+        x.data_ptr() + p0 * es, x.shape[1], y.data_ptr() + p0 * es, y.shape[1], cnt,
+        _lib.stream_handle(x.device),
+    )
+    _lib.check(rc, "mw_horner")
+
+
+def horner_eval_batched(p: MWPolynomial, xs: LaneBatch, variant: Variant = Variant.STANDARD) -> LaneBatch:
+    """Per-lane bitwise equal to horner_eval at each lane's point."""
+    if xs.k != p.k:
+        raise ValueError("mixed word counts")
+    _lib.require_cuda(p.planes, xs.planes)
+    y = torch.empty_like(xs.planes)
+    horner_into(p.planes, xs.planes, y, variant)
+    return LaneBatch(y, count=xs.count)
+
+
+def horner_eval(p: MWPolynomial, x, variant: Variant = Variant.STANDARD) -> tuple:
+    """b := a[n]; b := b*x + a[i] downward at one K-word point x."""
+    x = tuple(float(c) for c in getattr(x, "comps", x))
+    if len(x) != p.k:
+        raise ValueError("mixed word counts")
+    xs = LaneBatch(np.array(x, dtype=np.float64).reshape(p.k, 1), device=p.device)
+    return horner_eval_batched(p, xs, variant).lane(0)
+
+
+def random_polynomial(n: int, seed: int, k: int, device=None) -> MWPolynomial:
+    """poly.random_polynomial (181-192): degree-n, U[-1, 1] base-float
+    coefficients promoted exactly to K words, leading one nonzero."""
+    if n < 0:
+        raise ValueError("degree must be >= 0")
+    rng = np.random.Generator(np.random.PCG64(seed))
+    c0 = rng.uniform(-1.0, 1.0, n + 1)
+    while c0[n] == 0.0:
+        c0[n] = rng.uniform(-1.0, 1.0)
+    arr = np.zeros((k, n + 1))
+    arr[0] = c0
+    if k not in BITS:
+        raise ValueError(f"unsupported word count {k}")
+    return MWPolynomial(arr, device=device)

@@ -1,0 +1,330 @@
+"""Durand-Kerner simultaneous root iteration in complex K-word arithmetic.
+
+Drop-in for mwfloat.roots (pkg/src/mwfloat/roots.py): ``MonicPoly``
+(73-131), ``RootState`` (134-159), ``CollisionError`` / ``NoConvergence``
+(61-70), ``default_tolerance`` (162-164), ``radius_estimate`` (167-185),
+``aberth_init`` (188-221), ``dk_iterate`` (240-315) and ``dk_solve``
+(318-340), same signatures.
+
+The sweep is one mw_dk_sweep launch.  ``exact_order=True`` (default)
+replays the reference's op order bit for bit (numerator Horner and ordered
+denominator on two independent lanes per root); ``exact_order=False`` is
+the warp-per-root tree kernel (reassociated, within the n 2^-p bound).
+``dk_sweeps`` runs a fixed number of sweeps with no host round trip (the
+benchmark form of config 5) and can capture them in a CUDA graph.
+
+Initialization needs pi, cos, sin and fractional powers to ~300 bits; the
+reference uses its BigFloat oracle, here mpmath at 400 bits, both rounded
+to K words by greedy nearest-double extraction.  This is host-side setup,
+not the hot path.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+from fractions import Fraction
+
+import numpy as np
+import torch
+
+from . import _lib
+from .batch import LaneBatch, as_planes, batch_add, batch_div, batch_mul
+from .multiword import BITS, Variant, from_basefloat, from_fraction, variant_code
+
+__all__ = [
+    "MonicPoly",
+    "RootState",
+    "CollisionError",
+    "NoConvergence",
+    "aberth_init",
+    "radius_estimate",
+    "dk_iterate",
+    "dk_sweeps",
+    "dk_solve",
+    "default_tolerance",
+]
+
+INT32_MAX = 2**31 - 1
+
+
+class CollisionError(ValueError):
+    """Two root approximations coincided; the update is undefined."""
+
+
+class NoConvergence(RuntimeError):
+    """Iteration budget exhausted; carries the best state reached."""
+
+    def __init__(self, message, state):
+        super().__init__(message)
+        self.state = state
+
+
+class MonicPoly:
+    """q(x) = x^n + sum c_i x^i with K-word coefficients c[0..n-1]."""
+
+    __slots__ = ("planes",)
+
+    def __init__(self, comps, device=None):
+        self.planes = as_planes(comps, 1, device)
+        if self.planes.shape[1] < 1:
+            raise ValueError("monic polynomial needs degree >= 1")
+
+    @property
+    def comps(self) -> tuple:
+        return tuple(self.planes[c] for c in range(self.k))
+
+    @property
+    def k(self) -> int:
+        return self.planes.shape[0]
+
+    @property
+    def n(self) -> int:
+        return self.planes.shape[1]
+
+    @property
+    def device(self):
+        return self.planes.device
+
+    @classmethod
+    def from_coeffs(cls, coeffs, k: int | None = None, device=None) -> "MonicPoly":
+        rows = []
+        for c in coeffs:
+            if hasattr(c, "comps"):
+                rows.append(tuple(c.comps))
+            elif isinstance(c, (tuple, list)):
+                rows.append(tuple(c))
+            else:
+                if k is None:
+                    raise ValueError("k required for bare float coefficients")
+                rows.append(from_basefloat(float(c), k))
+        kk = len(rows[0])
+        return cls(np.array([[r[c] for r in rows] for c in range(kk)], dtype=np.float64), device=device)
+
+    @classmethod
+    def from_polynomial(cls, p, variant: Variant = Variant.STANDARD) -> "MonicPoly":
+        """Divide through by the leading coefficient (roots.py:93-101)."""
+        an = p.coeff(p.degree)
+        if all(c == 0.0 for c in an):
+            raise ValueError("leading coefficient is zero")
+        num = LaneBatch(p.planes[:, : p.degree].contiguous())
+        den = LaneBatch(torch.tensor(an, dtype=torch.float64, device=p.device).reshape(-1, 1).expand(-1, p.degree).contiguous())
+        return cls(batch_div(num, den, variant).planes)
+
+    def coeff(self, i: int) -> tuple:
+        return tuple(float(v) for v in self.planes[:, i].cpu())
+
+    def __repr__(self):
+        return f"MonicPoly(k={self.k}, n={self.n}, device={self.device})"
+
+
+@dataclass
+class RootState:
+    """Simultaneous approximations: (K, n) re / im planes."""
+
+    re: torch.Tensor
+    im: torch.Tensor
+    iteration: int = 0
+    converged: bool = False
+    last_max_update: float = math.inf
+
+    def __post_init__(self):
+        self.re = as_planes(self.re, 1)
+        self.im = as_planes(self.im, 1, self.re.device)
+        if self.re.shape != self.im.shape:
+            raise ValueError("re/im shape mismatch")
+
+    @property
+    def n(self) -> int:
+        return self.re.shape[1]
+
+    @property
+    def k(self) -> int:
+        return self.re.shape[0]
+
+    def root(self, i: int):
+        return (
+            tuple(float(v) for v in self.re[:, i].cpu()),
+            tuple(float(v) for v in self.im[:, i].cpu()),
+        )
+
+    def roots(self) -> list:
+        re = self.re.cpu().numpy()
+        im = self.im.cpu().numpy()
+        return [
+            (tuple(float(v) for v in re[:, i]), tuple(float(v) for v in im[:, i]))
+            for i in range(self.n)
+        ]
+
+
+def default_tolerance(k: int) -> float:
+    """Relative step threshold 2^(-bits + 10)."""
+    return math.ldexp(1.0, -BITS[k] + 10)
+
+
+# ------------------------------------------------------------ init (host)
+def _mp():
+    import mpmath
+
+    mpmath.mp.prec = 400
+    return mpmath
+
+
+def _mpf_fraction(x) -> Fraction:
+    man, exp = x.man_exp
+    man = int(man)
+    return Fraction(man) * (Fraction(2) ** int(exp))
+
+
+def radius_estimate(q: MonicPoly, variant: Variant = Variant.STANDARD) -> tuple:
+    """r = max over nonzero c_i of |n_nz c_i|^(1/(n-i)), K words
+    (roots.py:167-185); all coefficients zero gives r = 1."""
+    mp = _mp()
+    n = q.n
+    arr = q.planes.cpu().numpy()
+    nz = [i for i in range(n) if np.any(arr[:, i] != 0.0)]
+    if not nz:
+        return from_basefloat(1.0, q.k)
+    n_nz = len(nz) + 1
+    best = None
+    for i in nz:
+        mag = abs(sum(Fraction(float(c)) for c in arr[:, i]))
+        x = mp.mpf(n_nz * mag.numerator) / mag.denominator
+        r_i = mp.root(x, n - i)
+        if best is None or r_i > best:
+            best = r_i
+    return from_fraction(_mpf_fraction(best), q.k)
+
+
+def _check_distinct(state: RootState):
+    zre = state.re[0].cpu().numpy()
+    zim = state.im[0].cpu().numpy()
+    n = state.n
+    for i in range(n):
+        d2 = (zre - zre[i]) ** 2 + (zim - zim[i]) ** 2
+        d2[i] = np.inf
+        j = int(np.argmin(d2))
+        if d2[j] == 0.0 and state.root(i) == state.root(j):
+            raise CollisionError(f"approximations {i} and {j} coincide")
+
+
+def aberth_init(q: MonicPoly, variant: Variant = Variant.STANDARD, radius=None) -> RootState:
+    """Points -c_{n-1}/n + r exp(i (2(j-1)pi/n + 3/(2n))), j = 1..n
+    (roots.py:188-221).  ``radius`` overrides radius_estimate (e.g. the
+    R0 = 1.5 circle SURVEY §8(d) uses for the degree-512 problem)."""
+    mp = _mp()
+    n, k = q.n, q.k
+    dev = q.device
+    cn = LaneBatch(q.planes[:, n - 1 : n].contiguous())
+    nn = LaneBatch(np.array(from_basefloat(float(n), k)).reshape(k, 1), device=dev)
+    center = tuple(-c for c in batch_div(cn, nn, variant).lane(0))
+    rad = radius_estimate(q, variant) if radius is None else tuple(getattr(radius, "comps", radius))
+    if len(rad) != k:
+        rad = from_basefloat(float(rad[0]), k)
+    cosv = np.zeros((k, n))
+    sinv = np.zeros((k, n))
+    two_over_n = mp.mpf(2) / n
+    offset = mp.mpf(3) / (2 * n)
+    for j in range(1, n + 1):
+        theta = (j - 1) * two_over_n * mp.pi + offset
+        cosv[:, j - 1] = from_fraction(_mpf_fraction(mp.cos(theta)), k)
+        sinv[:, j - 1] = from_fraction(_mpf_fraction(mp.sin(theta)), k)
+    radb = LaneBatch(np.tile(np.array(rad).reshape(k, 1), (1, n)), device=dev)
+    cenb = LaneBatch(np.tile(np.array(center).reshape(k, 1), (1, n)), device=dev)
+    zre = batch_add(cenb, batch_mul(radb, LaneBatch(cosv, device=dev), variant), variant)
+    zim = batch_mul(radb, LaneBatch(sinv, device=dev), variant)
+    state = RootState(re=zre.planes, im=zim.planes)
+    _check_distinct(state)
+    return state
+
+
+# ---------------------------------------------------------------- sweep
+def sweep_into(coeffs: torch.Tensor, zre: torch.Tensor, zim: torch.Tensor, out_re: torch.Tensor,
+               out_im: torch.Tensor, step_mag: torch.Tensor, flag: torch.Tensor, variant,
+               exact_order: bool = True, i0: int = 0, i1: int | None = None) -> None:
+    """Raw launch: roots [i0, i1) of the frozen state -> out planes at the
+    same indices (plane stride n).  ``flag`` (int32 device scalar) must hold
+    INT32_MAX beforehand; it is lowered to min(j*n + i) on a collision."""
+    k, n = zre.shape
+    i1 = n if i1 is None else i1
+    rc = _lib.load().mw_dk_sweep(
+        k, variant_code(variant), coeffs.data_ptr(), coeffs.shape[1], n, zre.data_ptr(), zim.data_ptr(), n,
+        i0, i1, out_re.data_ptr(), out_im.data_ptr(), n, step_mag.data_ptr(), flag.data_ptr(),
+        1 if exact_order else 0, _lib.stream_handle(zre.device),
+    )
+    _lib.check(rc, "mw_dk_sweep")
+
+
+def _raise_collision(code: int, n: int):
+    j, i = divmod(int(code), n)
+    raise CollisionError(f"z_{i} equals z_{j}; denominator vanishes")
+
+
+def dk_iterate(q: MonicPoly, state: RootState, variant: Variant = Variant.STANDARD,
+               exact_order: bool = True) -> RootState:
+    """One simultaneous sweep: z_i <- z_i - q(z_i) / prod_{j != i}(z_i - z_j),
+    all i from the frozen previous state; a zero factor raises
+    CollisionError."""
+    if state.k != q.k:
+        raise ValueError("mixed word counts")
+    if state.n != q.n:
+        raise ValueError("state size does not match the polynomial degree")
+    _lib.require_cuda(q.planes, state.re, state.im)
+    dev = state.re.device
+    out_re = torch.empty_like(state.re)
+    out_im = torch.empty_like(state.im)
+    mag = torch.empty(state.n, dtype=torch.float64, device=dev)
+    flag = torch.full((1,), INT32_MAX, dtype=torch.int32, device=dev)
+    sweep_into(q.planes, state.re, state.im, out_re, out_im, mag, flag, variant, exact_order)
+    code = int(flag.item())
+    if code != INT32_MAX:
+        _raise_collision(code, state.n)
+    return RootState(
+        re=out_re, im=out_im, iteration=state.iteration + 1, converged=False,
+        last_max_update=float(mag.max().item()),
+    )
+
+
+def dk_sweeps(q: MonicPoly, state: RootState, sweeps: int, variant: Variant = Variant.BRANCH_FREE,
+              exact_order: bool = True, check: bool = True) -> RootState:
+    """``sweeps`` sweeps back to back on the device (ping-pong buffers, no
+    host synchronisation in between).  Collision flags are kept per sweep
+    and checked once at the end (first colliding sweep reported)."""
+    _lib.require_cuda(q.planes, state.re, state.im)
+    dev = state.re.device
+    bufs = [(state.re.clone(), state.im.clone()), (torch.empty_like(state.re), torch.empty_like(state.im))]
+    mag = torch.empty(state.n, dtype=torch.float64, device=dev)
+    flags = torch.full((max(sweeps, 1),), INT32_MAX, dtype=torch.int32, device=dev)
+    for s in range(sweeps):
+        src, dst = bufs[s & 1], bufs[(s + 1) & 1]
+        sweep_into(q.planes, src[0], src[1], dst[0], dst[1], mag, flags[s : s + 1], variant, exact_order)
+    fin = bufs[sweeps & 1]
+    if check and sweeps > 0:
+        f = flags.cpu().numpy()
+        bad = np.nonzero(f != INT32_MAX)[0]
+        if bad.size:
+            _raise_collision(int(f[bad[0]]), state.n)
+    return RootState(
+        re=fin[0], im=fin[1], iteration=state.iteration + sweeps, converged=False,
+        last_max_update=float(mag.max().item()) if sweeps > 0 else state.last_max_update,
+    )
+
+
+def dk_solve(q: MonicPoly, variant: Variant = Variant.STANDARD, tol: float | None = None, max_iter: int = 200,
+             state: RootState | None = None, exact_order: bool = True):
+    """Iterate until the largest update falls below tol * max|z| or the
+    budget runs out (NoConvergence carrying the state).  Returns
+    (state, iterations) (roots.py:318-340)."""
+    if tol is None:
+        tol = default_tolerance(q.k)
+    if tol <= 0:
+        raise ValueError("tol must be positive")
+    if state is None:
+        state = aberth_init(q, variant)
+    for _ in range(max_iter):
+        state = dk_iterate(q, state, variant, exact_order)
+        zmag = float(torch.max(torch.hypot(state.re[0], state.im[0])).item())
+        if state.last_max_update <= tol * max(zmag, 1e-300):
+            state.converged = True
+            return state, state.iteration
+    raise NoConvergence(f"no convergence in {max_iter} sweeps", state)

@@ -1,0 +1,346 @@
+"""GPU parity: the CUDA path (through the C-ABI) vs the reference's golden
+vectors and the pinned CPU oracle, on identical seeded inputs.
+
+Bar (BASELINE.json north_star): bit-exact wherever the reference's order
+and FMA use are replicated (elementwise, axpy, GEMM, Horner, exact-order
+dot/GEMV/DK); reordered reductions (tree dot/GEMV/DK) bit-exact with the
+oracle's restatement of their documented tree AND within
+n * 2^(-p+4) * sum|a||b| of the reference order.
+"""
+
+import math
+from fractions import Fraction
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from conftest import assert_bitwise, rand_mw
+from paper_2603_14926_b200 import (
+    LaneBatch,
+    MatMulPlan,
+    MonicPoly,
+    MWMatrix,
+    MWPolynomial,
+    RootState,
+    Variant,
+    batch_add,
+    batch_div,
+    batch_mul,
+    batch_sub,
+    dk_iterate,
+    dk_sweeps,
+    gen,
+    horner_eval,
+    horner_eval_batched,
+    matmul,
+)
+from paper_2603_14926_b200 import blas, roots
+
+pytestmark = pytest.mark.gpu
+
+CASES = [(2, "bf"), (3, "bf"), (4, "bf"), (2, "std")]
+IDS = [f"k{k}_{v}" for k, v in CASES]
+P_BITS = {2: 106, 3: 159, 4: 212}
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def V(v):
+    return Variant.parse(v)
+
+
+def exact_value(comps):
+    return sum(Fraction(float(c)) for c in comps)
+
+
+# ------------------------------------------------------------ elementwise
+@pytest.mark.parametrize("k,v", CASES, ids=IDS)
+def test_ew_golden(golden, k, v):
+    g = golden("ew")
+    p = f"k{k}_{v}"
+    a, b = LaneBatch(g[p + "_a"]), LaneBatch(g[p + "_b"])
+    assert_bitwise(batch_add(a, b, V(v)).numpy(), g[p + "_add"])
+    assert_bitwise(batch_sub(a, b, V(v)).numpy(), g[p + "_sub"])
+    assert_bitwise(batch_mul(a, b, V(v)).numpy(), g[p + "_mul"])
+    d = batch_div(a, LaneBatch(g[p + "_bz"]), V(v)).numpy()
+    assert_bitwise(d, g[p + "_div"], nan_ok=True)
+    assert not np.isfinite(d[0, 5])
+
+
+@pytest.mark.parametrize("k,v", CASES, ids=IDS)
+@pytest.mark.parametrize("w", [1, 2, 7, 1 << 20])
+def test_ew_vs_oracle(k, v, w):
+    rng = np.random.default_rng(1000 + k + w)
+    a, b = rand_mw(rng, k, w), rand_mw(rng, k, w)
+    la, lb = LaneBatch(a), LaneBatch(b)
+    for op, fn in (("add", batch_add), ("sub", batch_sub), ("mul", batch_mul), ("div", batch_div)):
+        assert_bitwise(fn(la, lb, V(v)).numpy(), oracle.ew(op, a, b, v))
+
+
+def test_ew_unaligned_and_strided_planes():
+    """Odd offsets force the 64-bit path; results identical."""
+    k = 4
+    rng = np.random.default_rng(5)
+    a, b = rand_mw(rng, k, 1001), rand_mw(rng, k, 1001)
+    ta = torch.from_numpy(a).cuda()
+    tb = torch.from_numpy(b).cuda()
+    big = torch.zeros((k, 1003), dtype=torch.float64, device="cuda")
+    big[:, 1:1002] = ta
+    la = LaneBatch(big[:, 1:1002].contiguous())
+    got = batch_add(la, LaneBatch(tb), Variant.BRANCH_FREE).numpy()
+    assert_bitwise(got, oracle.ew("add", a, b, "bf"))
+
+
+def test_ew_kats():
+    one = lambda *vals: LaneBatch(np.array(vals + (0.0,) * (4 - len(vals))).reshape(4, 1))
+    r = batch_mul(one(2.0**30 + 1), one(2.0**30 + 1), Variant.BRANCH_FREE).lane(0)
+    assert r[0] == 2.0**60 + 2.0**31 and r[1] == 1.0
+    r = batch_mul(one(2.0), one(3.0), Variant.BRANCH_FREE).lane(0)
+    assert r == (6.0, 0.0, 0.0, 0.0)
+
+
+def test_ew_standard_k3_k4_unsupported():
+    a = LaneBatch(np.zeros((3, 4)))
+    with pytest.raises(NotImplementedError):
+        batch_add(a, a, Variant.STANDARD)
+
+
+def test_ew_mixed_k_raises():
+    with pytest.raises(ValueError):
+        batch_add(LaneBatch(np.zeros((2, 4))), LaneBatch(np.zeros((3, 4))), Variant.BRANCH_FREE)
+
+
+# ------------------------------------------------------------ dot / axpy
+@pytest.mark.parametrize("k,v", CASES, ids=IDS)
+def test_dot_exact_golden(golden, k, v):
+    g = golden("dot")
+    p = f"k{k}_{v}"
+    got = blas.dot(LaneBatch(g[p + "_x"]), LaneBatch(g[p + "_y"]), V(v), order="exact")
+    assert_bitwise(np.array(got), g[p + "_out"])
+
+
+@pytest.mark.parametrize("k", [2, 3, 4])
+@pytest.mark.parametrize("n", [1, 15, 16, 17, 300, 4095, 4096, 4097, 65536, 1 << 20, 1_000_003])
+def test_dot_tree_vs_oracle(k, n):
+    rng = np.random.default_rng(n + k)
+    x, y = gen.g_k(rng, k, n), gen.g_k(rng, k, n)
+    got = np.array(blas.dot(LaneBatch(x), LaneBatch(y), Variant.BRANCH_FREE, order="tree"))
+    assert_bitwise(got, oracle.dot(x, y, "bf", order=1))
+    if n <= 16:
+        assert_bitwise(got, oracle.dot(x, y, "bf", order=0))
+    if n <= 65536:
+        ref = oracle.dot(x, y, "bf", order=0)
+        diff = abs(exact_value(got) - exact_value(ref))
+        scale = float(np.sum(np.abs(x[0] * y[0])))
+        assert float(diff) <= n * 2.0 ** (-P_BITS[k] + 4) * scale
+
+
+def test_dot_config1():
+    x, y, alpha = gen.config1_dot()
+    got = blas.dot(LaneBatch(x), LaneBatch(y), Variant.BRANCH_FREE)
+    assert_bitwise(np.array(got), oracle.dot(x, y, "bf", order=1))
+    exact = np.array(blas.dot(LaneBatch(x), LaneBatch(y), Variant.BRANCH_FREE, order="exact"))
+    assert_bitwise(exact, oracle.dot(x, y, "bf", order=0))
+
+
+@pytest.mark.parametrize("k,v", CASES, ids=IDS)
+def test_axpy_golden(golden, k, v):
+    g = golden("axpy")
+    p = f"k{k}_{v}"
+    x, y = LaneBatch(g[p + "_x"]), LaneBatch(g[p + "_y"])
+    got = blas.axpy(tuple(g[p + "_alpha"]), x, y, V(v))
+    assert_bitwise(got.numpy(), g[p + "_out"])
+    assert_bitwise(y.numpy(), g[p + "_y"])  # pure: input untouched
+
+
+def test_axpy_config1():
+    x, y, alpha = gen.config1_dot()
+    got = blas.axpy(tuple(alpha), LaneBatch(x), LaneBatch(y), Variant.BRANCH_FREE)
+    assert_bitwise(got.numpy(), oracle.axpy(alpha, x, y, "bf"))
+
+
+# ------------------------------------------------------------------ gemv
+@pytest.mark.parametrize("k,v", CASES, ids=IDS)
+def test_gemv_golden(golden, k, v):
+    g = golden("gemv")
+    p = f"k{k}_{v}"
+    A, x = MWMatrix(g[p + "_a"]), LaneBatch(g[p + "_x"])
+    assert_bitwise(blas.gemv(A, x, V(v), order="exact").numpy(), g[p + "_out"])
+    assert_bitwise(blas.gemv(A, x, V(v), order="tree").numpy(), oracle.gemv(g[p + "_a"], g[p + "_x"], v, order=1))
+
+
+@pytest.mark.parametrize("k", [3, 4])
+def test_gemv_config2(k):
+    a, x = gen.config2_gemv(k)
+    A, xb = MWMatrix(a), LaneBatch(x)
+    got = blas.gemv(A, xb, Variant.BRANCH_FREE, order="tree").numpy()
+    assert_bitwise(got, oracle.gemv(a, x, "bf", order=1))
+    ex = blas.gemv(A, xb, Variant.BRANCH_FREE, order="exact").numpy()
+    ref = oracle.gemv(a, x, "bf", order=0)
+    assert_bitwise(ex, ref)
+    # tree vs reference order within n 2^-p+4 sum|a||x| per row
+    n = a.shape[2]
+    scale = np.abs(a[0]) @ np.abs(x[0])
+    for i in range(0, a.shape[1], 97):
+        diff = abs(exact_value(got[:, i]) - exact_value(ref[:, i]))
+        assert float(diff) <= n * 2.0 ** (-P_BITS[k] + 4) * scale[i]
+
+
+# ------------------------------------------------------------------ gemm
+@pytest.mark.parametrize("k,v", CASES, ids=IDS)
+def test_gemm_golden(golden, k, v):
+    g = golden("gemm")
+    p = f"k{k}_{v}"
+    c = matmul(MWMatrix(g[p + "_a"]), MWMatrix(g[p + "_b"]), MatMulPlan(scheme="naive", variant=v))
+    assert_bitwise(c.numpy(), g[p + "_out"])
+
+
+@pytest.mark.parametrize("k", [2, 3, 4])
+@pytest.mark.parametrize("shape", [(1, 1, 1), (65, 33, 17), (130, 97, 200), (64, 64, 64), (5, 0, 7)])
+def test_gemm_vs_oracle(k, shape):
+    m, kd, n = shape
+    rng = np.random.default_rng(m * 7 + kd * 3 + n + k)
+    a, b = gen.g_k(rng, k, (m, kd)), gen.g_k(rng, k, (kd, n))
+    c = matmul(MWMatrix(a), MWMatrix(b), MatMulPlan(scheme="naive", variant="bf"))
+    assert_bitwise(c.numpy(), oracle.gemm(a, b, "bf"))
+
+
+def test_gemm_identity_bitwise():
+    rng = np.random.default_rng(9)
+    for k in (2, 3, 4):
+        a = rand_mw(rng, k, 48 * 48).reshape(k, 48, 48)
+        c = matmul(MWMatrix(a), MWMatrix.identity(48, k), MatMulPlan(scheme="naive", variant="bf"))
+        assert_bitwise(c.numpy(), a)
+
+
+@pytest.mark.parametrize("k,n", [(2, 4096), (3, 2048), (4, 2048)])
+def test_gemm_config3_sampled_rows(k, n):
+    a, b = gen.config3_gemm(k, n)
+    c = matmul(MWMatrix(a), MWMatrix(b), MatMulPlan(scheme="naive", variant="bf")).numpy()
+    for r0 in (0, n // 2 + 3, n - 1):
+        ref = oracle.gemm(a, b, "bf", rows=(r0, r0 + 1))
+        assert_bitwise(c[:, r0], ref[:, r0])
+
+
+# ---------------------------------------------------------------- horner
+@pytest.mark.parametrize("k,v", CASES, ids=IDS)
+def test_horner_golden(golden, k, v):
+    g = golden("horner")
+    p = f"k{k}_{v}"
+    poly = MWPolynomial(g[p + "_coeffs"])
+    got = horner_eval_batched(poly, LaneBatch(g[p + "_x"]), V(v)).numpy()
+    assert_bitwise(got, g[p + "_out"])
+    assert horner_eval(poly, tuple(g[p + "_x"][:, 0]), V(v)) == tuple(g[p + "_out"][:, 0])
+
+
+@pytest.mark.parametrize("k", [2, 3, 4])
+@pytest.mark.parametrize("deg,npts", [(0, 5), (1, 300), (255, 1000), (256, 257), (1024, 4099), (3000, 64)])
+def test_horner_vs_oracle(k, deg, npts):
+    rng = np.random.default_rng(deg + npts + k)
+    coeffs = gen.g_k(rng, k, deg + 1)
+    x = gen.g_k(rng, k, npts)
+    got = horner_eval_batched(MWPolynomial(coeffs), LaneBatch(x), Variant.BRANCH_FREE).numpy()
+    assert_bitwise(got, oracle.horner(coeffs, x, "bf"))
+
+
+def test_horner_config4_full_with_sampled_check():
+    coeffs, x = gen.config4_horner()
+    y = horner_eval_batched(MWPolynomial(coeffs), LaneBatch(x), Variant.BRANCH_FREE).numpy()
+    idx = np.r_[0:2048, (1 << 23):(1 << 23) + 2048, (1 << 24) - 2048:(1 << 24)]
+    assert_bitwise(y[:, idx], oracle.horner(coeffs, x[:, idx], "bf"))
+    assert np.all(np.isfinite(y[0]))
+
+
+# -------------------------------------------------------------------- dk
+@pytest.mark.parametrize("k,v", CASES, ids=IDS)
+def test_dk_exact_golden_small(golden, k, v):
+    g = golden("dk")
+    p = f"k{k}_{v}"
+    q = MonicPoly(g[p + "_coeffs"])
+    st = RootState(re=g[p + "_zre"], im=g[p + "_zim"])
+    nxt = dk_iterate(q, st, V(v), exact_order=True)
+    assert_bitwise(nxt.re.cpu().numpy(), g[p + "_new_re"])
+    assert_bitwise(nxt.im.cpu().numpy(), g[p + "_new_im"])
+    assert math.isclose(nxt.last_max_update, float(g[p + "_maxupd"][0]), rel_tol=1e-15)
+
+
+@pytest.mark.parametrize("k", [3, 4])
+@pytest.mark.parametrize("init", ["near", "aberth"])
+def test_dk_exact_golden_config5(golden, k, init):
+    g = golden("dk")
+    p = f"c5_k{k}"
+    s = "" if init == "near" else "_ab"
+    q = MonicPoly(g[p + "_coeffs"])
+    st = RootState(re=g[p + s + "_zre"], im=g[p + s + "_zim"])
+    nxt = dk_iterate(q, st, Variant.BRANCH_FREE, exact_order=True)
+    assert_bitwise(nxt.re.cpu().numpy(), g[p + s + "_new_re"])
+    assert_bitwise(nxt.im.cpu().numpy(), g[p + s + "_new_im"])
+    assert math.isclose(nxt.last_max_update, float(g[p + s + "_maxupd"][0]), rel_tol=1e-15)
+
+
+@pytest.mark.parametrize("k", [2, 3, 4])
+@pytest.mark.parametrize("n", [2, 16, 33, 512])
+def test_dk_tree_vs_oracle_tree(k, n):
+    if n == 512:
+        coeffs = gen.config5_poly(k)
+        zre, zim = gen.config5_init(k)
+    else:
+        rng = np.random.default_rng(n + k)
+        coeffs = gen.g_k(rng, k, n) * 0.5
+        ang = 2 * np.pi * np.arange(n) / n + 0.1
+        zre = np.zeros((k, n))
+        zim = np.zeros((k, n))
+        zre[0] = 1.3 * np.cos(ang)
+        zim[0] = 1.3 * np.sin(ang)
+    q = MonicPoly(coeffs)
+    st = RootState(re=zre, im=zim)
+    nxt = dk_iterate(q, st, Variant.BRANCH_FREE, exact_order=False)
+    ore, oim, mag, coll = oracle.dk_sweep(coeffs, zre, zim, "bf", exact=False)
+    assert coll is None
+    assert_bitwise(nxt.re.cpu().numpy(), ore)
+    assert_bitwise(nxt.im.cpu().numpy(), oim)
+
+
+def test_dk_collision_raises():
+    q = MonicPoly(np.array([[-1.0, 0.0], [0.0, 0.0]]))
+    st = RootState(re=np.array([[0.5, 0.5], [0.0, 0.0]]), im=np.array([[0.1, 0.1], [0.0, 0.0]]))
+    for exact in (True, False):
+        with pytest.raises(roots.CollisionError):
+            dk_iterate(q, st, Variant.BRANCH_FREE, exact_order=exact)
+
+
+def test_dk_exact_roots_are_fixed_points():
+    q = MonicPoly(np.array([[-1.0, 0.0], [0.0, 0.0]]))  # z^2 - 1
+    st = RootState(re=np.array([[1.0, -1.0], [0.0, 0.0]]), im=np.zeros((2, 2)))
+    new = dk_iterate(q, st, Variant.BRANCH_FREE)
+    assert new.last_max_update == 0.0
+    assert new.root(0) == st.root(0)
+
+
+@pytest.mark.parametrize("k", [2, 3, 4])
+def test_dk_solve_quadratic(k):
+    q = MonicPoly.from_coeffs([(-1.0,) + (0.0,) * (k - 1), (0.0,) * k])
+    state, iters = roots.dk_solve(q, Variant.BRANCH_FREE)
+    assert iters <= 10
+    rs = sorted(r[0][0] for r in state.roots())
+    assert abs(rs[0] + 1.0) <= 1e-30 and abs(rs[1] - 1.0) <= 1e-30
+
+
+@pytest.mark.parametrize("k", [3, 4])
+def test_dk_config5_200_sweeps_exact_matches_oracle_trajectory(k):
+    """Exact-order kernel tracks the oracle for a burst of sweeps (the
+    trajectory is chaotic, so only the exact order stays bitwise)."""
+    coeffs = gen.config5_poly(k)
+    zre, zim = gen.config5_init(k)
+    st = dk_sweeps(MonicPoly(coeffs), RootState(re=zre, im=zim), 3, Variant.BRANCH_FREE, exact_order=True)
+    ore, oim = zre, zim
+    for _ in range(3):
+        ore, oim, _, _ = oracle.dk_sweep(coeffs, ore, oim, "bf", exact=True)
+    assert_bitwise(st.re.cpu().numpy(), ore)
+    assert_bitwise(st.im.cpu().numpy(), oim)
