@@ -52,6 +52,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline sample")
     ap.add_argument("--quick", action="store_true", help="small sizes (debug)")
+    ap.add_argument("--no-secondary", action="store_true", help="skip configs 1, 2 and 5")
     return ap.parse_args()
 
 
@@ -157,6 +158,19 @@ def measure_fp64_peak(torch, lib, dev_stream):
             best = max(best, blocks * threads * iters * 64 / t)
         res[name] = best
     return res
+
+
+def ncu_traffic(kernel):
+    """DRAM bytes (read + write) per launch of `kernel` from the committed
+    ncu --set full capture summary (profiles/ncu_summary.json), or None."""
+    path = os.path.join(REPO, "profiles", "ncu_summary.json")
+    try:
+        ent = json.load(open(path)).get(kernel)
+        if ent is None:
+            return None, None
+        return int(ent["dram_bytes_per_launch"]), f"profiles/ncu_summary.json ({ent['round']}, {ent['report']})"
+    except (OSError, ValueError, KeyError):
+        return None, None
 
 
 # ---------------------------------------------------------------- our arm
@@ -309,15 +323,20 @@ def run_ours(args):
     for i, (k, n, a, b, c) in enumerate(dev):
         rows = a.shape[1]
         ops = MAC_OPS[k] * rows * n * n
-        parts.append(dict(name=f"gemm_{['', '', 'dd', 'td', 'qd'][k]}_n{n}", ms=part_ms[i], fp64_ops=ops,
+        parts.append(dict(name=f"gemm_{['', '', 'dd', 'td', 'qd'][k]}_n{n}", kernel=f"gemm_kernel<{k},1>",
+                          ms=part_ms[i], fp64_ops=ops,
                           mp_ops=2 * rows * n * n))
     hp = phi - plo
-    parts.append(dict(name=f"horner_qd_deg{horner['degree']}_pts{horner['npts']}", ms=part_ms[-1],
+    parts.append(dict(name=f"horner_qd_deg{horner['degree']}_pts{horner['npts']}", kernel="horner_kernel<4,1>",
+                      ms=part_ms[-1],
                       fp64_ops=MAC_OPS[4] * hp * horner["degree"], mp_ops=2 * hp * horner["degree"]))
     for p in parts:
         p["fp64_tops"] = p["fp64_ops"] / (p["ms"] / 1e3) / 1e12 if p["ms"] > 0 else 0.0
         p["frac_of_fp64_peak"] = p["fp64_tops"] * 1e12 / peak["dfma"]
         p["gmpops"] = p["mp_ops"] / (p["ms"] / 1e3) / 1e9 if p["ms"] > 0 else 0.0
+    for p, (k, n, a, b, c) in zip(parts, dev):
+        p["alg_bytes"] = (a.numel() + b.numel() + c.numel()) * 8
+    parts[-1]["alg_bytes"] = (xdev.numel() + ydev.numel() + cdev.numel()) * 8
     dom = max(parts, key=lambda p: p["ms"])
     peak_t = peak["dfma"] / 1e12
     roofline = {
@@ -325,9 +344,16 @@ def run_ours(args):
         "achieved": round(dom["fp64_tops"], 3), "peak": round(peak_t, 3),
         "unit": "T FP64-op/s (DADD/DMUL/DFMA = 1 op)",
         "frac": round(dom["fp64_tops"] / peak_t, 4),
-        "traffic": None,
+        "traffic": ncu_traffic(dom["kernel"])[0],
+        "traffic_unit": "DRAM bytes per launch (ncu dram__bytes_read.sum + dram__bytes_write.sum)",
+        "traffic_source": ncu_traffic(dom["kernel"])[1],
+        "algorithmic_bytes": dom["alg_bytes"],
         "peak_source": "measured live: DFMA microbenchmark, 8 chains/thread, all SMs (mw_fp64_peak_kernel)",
     }
+
+    sec = None
+    if not args.no_secondary:
+        sec = secondary(args, torch, dist, mw, world, rank, peak)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -356,14 +382,118 @@ def run_ours(args):
             "e2e": e2e,
             "gpu_launches": args.steps * (len(dev) + 1),
             "clocks": clk.summary(),
+            "secondary": sec,
         }
         print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()
 
 
+# ------------------------------------------------ secondary configs 1, 2, 5
+ADD_OPS = {2: 20, 3: 57, 4: 103}
+MUL_OPS = {2: 9, 3: 39, 4: 106}
+
+
+def secondary(args, torch, dist, mw, world, rank, peak):
+    """The other §8 rows, measured on the same run (not the headline):
+    config 1 dot/axpy (DD n=65536), config 2 GEMV (TD/QD 2048^2),
+    config 5 DK (TD/QD n=512, 200 sweeps; roots sharded + one all-gather
+    per sweep when N > 1).  Device time via CUDA events, max over ranks."""
+    from paper_2603_14926_b200 import blas, gen
+    from paper_2603_14926_b200 import dist as mwdist
+    from paper_2603_14926_b200.roots import INT32_MAX, sweep_into
+
+    BF = mw.Variant.BRANCH_FREE
+    hbm = 6538.9e9
+    try:
+        hbm = json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json")))["hbm_gbs"] * 1e9
+    except (OSError, ValueError, KeyError):
+        pass
+    out = {}
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > L2 (126 MB)
+
+    def timed(fn, reps, flush_l2=False):
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+        for _ in range(2):
+            fn()
+        torch.cuda.synchronize()
+        for e0, e1 in evs:
+            if flush_l2:
+                flush.fill_(1)
+            e0.record()
+            fn()
+            e1.record()
+        torch.cuda.synchronize()
+        ms = statistics.median(e0.elapsed_time(e1) for e0, e1 in evs)
+        if world > 1:
+            t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
+
+    # ---- config 1: dot and axpy, DD n = 65536 (2 MiB: L2-resident, launch-bound)
+    x, y, alpha = gen.config1_dot()
+    n1 = x.shape[1]
+    lo, hi = mwdist.aligned_shard_range(n1, rank, world, mwdist.DOT_PARTIAL_SPAN)
+    X, Y = mw.LaneBatch(x), mw.LaneBatch(y)
+    if world == 1:
+        dres = torch.empty(2, dtype=torch.float64, device="cuda")
+        ms_dot = timed(lambda: blas.dot_tensor(X, Y, BF, out=dres), 200)
+    else:
+        be = mwdist.gpu_dot_backend(BF)
+        ms_dot = timed(lambda: mwdist.dot_allgather(X.planes, Y.planes, be), 50)
+    Xs, Ys = mw.LaneBatch(x[:, lo:hi]), mw.LaneBatch(y[:, lo:hi])
+    ms_axpy = timed(lambda: blas.axpy_(tuple(alpha), Xs, Ys, BF), 200)
+    out["config1_dot_dd_n65536"] = {
+        "us_per_call": round(ms_dot * 1e3, 2), "G_MPops": round(2 * n1 / (ms_dot / 1e3) / 1e9, 3),
+        "hbm_frac": round(2 * 2 * n1 * 8 / (ms_dot / 1e3) / hbm, 4),
+        "order": "tree (16-leaf chunks + pairwise tree)" + (", all-gather-then-sum over ranks" if world > 1 else ""),
+        "note": "2 MiB input is L2-resident and launch-bound; hbm_frac is bytes/time vs HBM copy peak"}
+    out["config1_axpy_dd_n65536"] = {
+        "us_per_call": round(ms_axpy * 1e3, 2), "G_MPops": round(2 * n1 / (ms_axpy / 1e3) / 1e9, 3),
+        "hbm_frac": round(3 * 2 * (hi - lo) * 8 * world / (ms_axpy / 1e3) / hbm, 4)}
+
+    # ---- config 2: GEMV TD / QD 2048 x 2048, row blocks per rank, L2 flushed
+    for k in (3, 4):
+        a, xv = gen.config2_gemv(k)
+        m = a.shape[1]
+        rlo, rhi = mwdist.shard_range(m, rank, world)
+        A, XV = mw.MWMatrix(a), mw.LaneBatch(xv)
+        yb = torch.empty((k, rhi - rlo), dtype=torch.float64, device="cuda")
+        ms = timed(lambda: blas.gemv(A, XV, BF, "tree", rlo, rhi, out=yb), 20, flush_l2=True)
+        fp = MAC_OPS[k] * m * m
+        out[f"config2_gemv_{'td' if k == 3 else 'qd'}_n2048"] = {
+            "ms": round(ms, 4), "G_MPops": round(2 * m * m / (ms / 1e3) / 1e9, 2),
+            "fp64_frac": round(fp / (ms / 1e3) / peak["dfma"], 4),
+            "hbm_GBps": round(k * m * m * 8 / (ms / 1e3) / 1e9, 1), "order": "tree (warp per row)",
+            "l2": "flushed before each call"}
+        del A
+
+    # ---- config 5: DK, n = 512, 200 sweeps (near-root init, SURVEY §8(d) (ii))
+    for k in (3, 4):
+        coeffs = torch.from_numpy(gen.config5_poly(k)).cuda()
+        zre0, zim0 = (torch.from_numpy(t).cuda() for t in gen.config5_init(k))
+        n5 = zre0.shape[1]
+        mp_sweep = n5 * (20 * n5 + 31)
+        fp_sweep = n5 * (n5 * (6 * MUL_OPS[k] + 14 * ADD_OPS[k]) + 20 * MUL_OPS[k] + 11 * ADD_OPS[k])
+        for exact in (False, True):
+            sweeps = 200
+            if world == 1:
+                q = mw.MonicPoly(coeffs)
+                st = mw.RootState(re=zre0, im=zim0)
+                ms = timed(lambda: mw.dk_sweeps(q, st, sweeps, BF, exact_order=exact, check=False), 2)
+            else:
+                ms = timed(lambda: mwdist.dk_sweeps_sharded(coeffs, zre0, zim0, sweeps, BF, exact_order=exact), 2)
+            out[f"config5_dk_{'td' if k == 3 else 'qd'}_n512_{'exact' if exact else 'tree'}"] = {
+                "ms_200_sweeps": round(ms, 3), "us_per_sweep": round(ms * 1e3 / sweeps, 2),
+                "G_MPops": round(mp_sweep * sweeps / (ms / 1e3) / 1e9, 3),
+                "fp64_frac": round(fp_sweep * sweeps / (ms / 1e3) / peak["dfma"] / world, 4),
+                "collective": "all_gather of (re, im) K-planes per sweep" if world > 1 else None}
+    return out
+
+
 # ---------------------------------------------------------- CPU baseline
-def cpu_sample(gemm_parts, horner, budget_rows=None):
+def cpu_sample(gemm_parts, horner, budget_rows=None, horner_pts=1 << 19):
     """Reference algorithm (C restatement, oracle/) on all host threads over
     a bounded sample: GEMM rows (per K) and Horner points.  Returns the
     cpu_baseline dict in the same unit (G MP-ops/s)."""
@@ -371,7 +501,7 @@ def cpu_sample(gemm_parts, horner, budget_rows=None):
     from paper_2603_14926_b200 import gen
 
     threads = oracle.max_threads()
-    sample_rows = {2: 8, 3: 16, 4: 8} if budget_rows is None else budget_rows
+    sample_rows = {2: 64, 3: 64, 4: 32} if budget_rows is None else budget_rows
     tot_mp = 0.0
     tot_s = 0.0
     desc = []
@@ -381,11 +511,11 @@ def cpu_sample(gemm_parts, horner, budget_rows=None):
         t = time.perf_counter()
         oracle.gemm(a[:, :r], b, "bf")
         dt = time.perf_counter() - t
-        tot_mp += 2 * r * n * n
+        tot_mp += 2 * n**3
         tot_s += dt * (n / r)  # per-row work is uniform: scale to the full matrix
         desc.append(f"gemm k{k} n{n}: {r} rows in {dt:.2f}s")
     coeffs, x = gen.config4_horner(npts=horner["npts"], degree=horner["degree"], k=horner["k"])
-    pts = min(65536, horner["npts"])
+    pts = min(horner_pts, horner["npts"])
     t = time.perf_counter()
     oracle.horner(coeffs, x[:, :pts], "bf")
     dt = time.perf_counter() - t
@@ -406,13 +536,13 @@ def run_reference(args):
     horner = dict(HORNER)
     if args.quick:
         horner["npts"] = 1 << 16
-    small = {2: 2, 3: 4, 4: 2}
+    small = {2: 16, 3: 16, 4: 8}
     for _ in range(args.warmup):
-        cpu_sample(gemm_parts, horner, budget_rows={k: 1 for k in small})
+        cpu_sample(gemm_parts, horner, budget_rows={k: 1 for k in small}, horner_pts=4096)
     vals = []
     descs = None
     for _ in range(args.steps):
-        r = cpu_sample(gemm_parts, horner, budget_rows=small)
+        r = cpu_sample(gemm_parts, horner, budget_rows=small, horner_pts=1 << 18)
         vals.append(r["value"])
         descs = r
     v = statistics.median(vals)

@@ -104,8 +104,9 @@ int mw_tree_fold(int k, int variant, const double* partials, int64_t pstride,
 
 /* y = A x, A m x n.  Definition: y_i = fold_t add(acc, mul(A_it, x_t)) from
  * exact zero, t ascending = matmul(A, x as n x 1, naive) (linalg.py:284-297).
- * MW_ORDER_EXACT: one thread per row, bit-exact.  MW_ORDER_TREE: one warp
- * per row, lane l folds t = l, l+32, ... then a shuffle tree. */
+ * MW_ORDER_EXACT: one thread per row, bit-exact.  MW_ORDER_TREE: 128
+ * partials per row (four warps); partial u folds t = u, u+128, ... from
+ * exact zero, then an in-place pairwise tree over min(n, 128) partials. */
 int mw_gemv(int k, int variant, const double* A, int64_t lda, int64_t sA,
             const double* x, int64_t sx, double* y, int64_t sy, int64_t m,
             int64_t n, int order, void* stream);

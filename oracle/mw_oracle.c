@@ -392,8 +392,8 @@ int mwo_tree_fold(int k, int variant, const double* v, int64_t sv, int64_t count
 }
 
 /* gemv: order 0 = reference fold per row (= matmul(A, x as n x 1, naive),
- * linalg.py:284-297); order 1 = TREE (lane l of 32 folds t = l, l+32, ...,
- * then the pairwise tree over the min(n, 32) lane partials). */
+ * linalg.py:284-297); order 1 = TREE (partial u of 128 folds t = u, u+128,
+ * ... from zero, then the pairwise tree over the min(n, 128) partials). */
 int mwo_gemv(int k, int variant, const double* A, int64_t lda, int64_t sA, const double* x,
              int64_t sx, double* y, int64_t sy, int64_t m, int64_t n, int order) {
   mw_binop add, mul;
@@ -406,9 +406,9 @@ int mwo_gemv(int k, int variant, const double* A, int64_t lda, int64_t sA, const
     if (order == 0) {
       r = fold_range(row, sA, 1, x, sx, 1, 0, n, 1, k, add, mul);
     } else {
-      mwv lanes[32];
-      int64_t valid = n < 32 ? n : 32;
-      for (int l = 0; l < valid; ++l) lanes[l] = fold_range(row, sA, 1, x, sx, 1, l, n, 32, k, add, mul);
+      mwv lanes[128];
+      int64_t valid = n < 128 ? n : 128;
+      for (int l = 0; l < valid; ++l) lanes[l] = fold_range(row, sA, 1, x, sx, 1, l, n, 128, k, add, mul);
       r = valid > 0 ? pairwise_tree(lanes, valid, add) : mzero();
     }
     st(y, sy, i, k, &r);

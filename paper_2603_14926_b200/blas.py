@@ -15,7 +15,8 @@ from its primitives, and these definitions are what the kernels compute:
   reference; ``axpy_`` updates y in place.
 * ``gemv(A, x)`` = y_i folded like dot over row i; bit-exact with
   matmul(A, x as n x 1, naive) for ``order="exact"``; ``order="tree"``
-  splits each row over a warp (lane l folds t = l, l+32, ...).
+  splits each row over 128 partials (four warps; partial u folds
+  t = u, u+128, ...) combined by the pairwise tree.
 """
 
 from __future__ import annotations

@@ -19,6 +19,8 @@
 
 namespace mw {
 
+constexpr int GEMM_GROUP_M = 16;
+
 template <int K>
 struct GemmCfg;
 // DD: 64x64 tile, 4x4 per thread, 256 threads.
@@ -62,7 +64,16 @@ __global__ void __launch_bounds__((GemmCfg<K>::BM / GemmCfg<K>::TM) *
 
   const int tid = threadIdx.x;
   const int tx = tid % TX, ty = tid / TX;
-  const int64_t m0 = (int64_t)blockIdx.y * BM, n0 = (int64_t)blockIdx.x * BN;
+  // Grouped raster: consecutive CTAs walk GROUP_M tile-rows of one
+  // tile-column band, so the ~300 co-resident CTAs share A and B panels in
+  // L2 and B is streamed from HBM ~grid_m/GROUP_M times instead of grid_m.
+  const int64_t grid_m = (m + BM - 1) / BM, grid_n = (n + BN - 1) / BN;
+  const int64_t pid = blockIdx.x;
+  const int64_t per_group = (int64_t)GEMM_GROUP_M * grid_n;
+  const int64_t first_m = (pid / per_group) * GEMM_GROUP_M;
+  const int64_t gsize = (grid_m - first_m) < GEMM_GROUP_M ? (grid_m - first_m) : GEMM_GROUP_M;
+  const int64_t in_group = pid % per_group;
+  const int64_t m0 = (first_m + in_group % gsize) * BM, n0 = (in_group / gsize) * BN;
 
   auto As = [&](int st, int c, int row, int t) -> double& {
     return smem[st * S::STAGE + (c * BM + row) * S::APAD + t];
@@ -163,9 +174,9 @@ struct GemmLaunch {
                            (int)smem);
       attr_set = true;
     }
-    dim3 grid((unsigned)((n + Cf::BN - 1) / Cf::BN), (unsigned)((m + Cf::BM - 1) / Cf::BM));
-    if (grid.y > 65535u) return MW_ERR_INVALID;
-    gemm_kernel<K, VAR><<<grid, NT, smem, st>>>(A, lda, sA, B, ldb, sB, C, ldc, sC, m, n, kd);
+    const int64_t tiles = ((n + Cf::BN - 1) / Cf::BN) * ((m + Cf::BM - 1) / Cf::BM);
+    if (tiles > 0x7fffffffLL) return MW_ERR_INVALID;
+    gemm_kernel<K, VAR><<<(unsigned)tiles, NT, smem, st>>>(A, lda, sA, B, ldb, sB, C, ldc, sC, m, n, kd);
     return launch_status();
   }
 };

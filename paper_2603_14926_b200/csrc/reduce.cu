@@ -12,8 +12,8 @@
 //         zero; chunk partials combined in place by a pairwise tree
 //         (stride s = 1, 2, 4, ...: v[i] <- add(v[i], v[i+s]) for i % 2s == 0
 //         when i+s < count; an unpaired tail passes through).
-//   gemv: lane l of the row's warp folds t = l, l+32, ... ascending from
-//         exact zero; the 32 lane partials combine by the same pairwise tree.
+//   gemv: 128 partials per row; partial u folds t = u, u+128, ... ascending
+//         from exact zero; the partials combine by the same pairwise tree.
 #include "common.cuh"
 
 namespace mw {
@@ -191,33 +191,68 @@ __global__ void __launch_bounds__(128) gemv_exact_kernel(const double* __restric
   store<K>(y, sy, i, acc);
 }
 
-// Tree order: warp per row; lane l folds t = l + 32 j; pairwise shuffle tree.
+// Tree order: GEMV_P = 128 partials per row, four warps per row.  Partial u
+// (lane l of warp w, u = 32w + l) folds t = u, u+128, u+256, ... ascending
+// from exact zero; the partials combine by the in-place pairwise tree
+// (strides 1..64, pairs valid while the partner index < min(n, 128)).
+// Four elements are loaded ahead of their arithmetic so HBM latency
+// overlaps the FP64 chain.
+constexpr int GEMV_WARPS = 4;
+constexpr int GEMV_P = 32 * GEMV_WARPS;
+constexpr int GEMV_ROWS_PER_CTA = 2;
+
 template <int K, int VAR>
-__global__ void __launch_bounds__(256) gemv_tree_kernel(const double* __restrict__ A, int64_t lda,
-                                                        int64_t sA, const double* __restrict__ x,
-                                                        int64_t sx, double* __restrict__ y,
-                                                        int64_t sy, int64_t m, int64_t n) {
+__global__ void __launch_bounds__(32 * GEMV_WARPS * GEMV_ROWS_PER_CTA)
+    gemv_tree_kernel(const double* __restrict__ A, int64_t lda, int64_t sA,
+                     const double* __restrict__ x, int64_t sx, double* __restrict__ y, int64_t sy,
+                     int64_t m, int64_t n) {
+  __shared__ double red[GEMV_ROWS_PER_CTA][K][GEMV_WARPS];
   const int lane = threadIdx.x & 31;
-  const int64_t i = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (i >= m) return;
-  const double* row = A + i * lda;
+  const int warp = (threadIdx.x >> 5) % GEMV_WARPS;
+  const int slot = (threadIdx.x >> 5) / GEMV_WARPS;
+  const int64_t i = blockIdx.x * (int64_t)GEMV_ROWS_PER_CTA + slot;
+  const bool live = i < m;
+  const double* row = A + (live ? i : 0) * lda;
+  const int u = warp * 32 + lane;
   V<K> acc = zero<K>();
-  int64_t t = lane;
-  // two loads in flight per step: the fold stays strictly ascending
-  for (; t + 32 < n; t += 64) {
-    V<K> a0 = load<K>(row, sA, t), x0 = load<K>(x, sx, t);
-    V<K> a1 = load<K>(row, sA, t + 32), x1 = load<K>(x, sx, t + 32);
-    acc = Ops<K, VAR>::add(acc, Ops<K, VAR>::mul(a0, x0));
-    acc = Ops<K, VAR>::add(acc, Ops<K, VAR>::mul(a1, x1));
+  int64_t t = u;
+  constexpr int D = 4;
+  for (; t + (D - 1) * GEMV_P < n; t += D * GEMV_P) {
+    V<K> a[D], xv[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      a[d] = load<K>(row, sA, t + d * GEMV_P);
+      xv[d] = load<K>(x, sx, t + d * GEMV_P);
+    }
+#pragma unroll
+    for (int d = 0; d < D; ++d) acc = Ops<K, VAR>::add(acc, Ops<K, VAR>::mul(a[d], xv[d]));
   }
-  if (t < n) acc = Ops<K, VAR>::add(acc, Ops<K, VAR>::mul(load<K>(row, sA, t), load<K>(x, sx, t)));
-  const int64_t valid = n < 32 ? n : 32;
+  for (; t < n; t += GEMV_P)
+    acc = Ops<K, VAR>::add(acc, Ops<K, VAR>::mul(load<K>(row, sA, t), load<K>(x, sx, t)));
+  const int64_t valid = n < GEMV_P ? n : GEMV_P;
 #pragma unroll
   for (int s = 1; s < 32; s <<= 1) {
     V<K> o = shfl_down<K>(acc, s);
-    if ((lane & (2 * s - 1)) == 0 && lane + s < valid) acc = Ops<K, VAR>::add(acc, o);
+    if ((lane & (2 * s - 1)) == 0 && u + s < valid) acc = Ops<K, VAR>::add(acc, o);
   }
-  if (lane == 0) store<K>(y, sy, i, acc);
+  if (lane == 0) {
+#pragma unroll
+    for (int c = 0; c < K; ++c) red[slot][c][warp] = acc.c[c];
+  }
+  __syncthreads();
+  if (warp == 0 && lane == 0 && live) {
+    V<K> r[GEMV_WARPS];
+#pragma unroll
+    for (int w = 0; w < GEMV_WARPS; ++w)
+#pragma unroll
+      for (int c = 0; c < K; ++c) r[w].c[c] = red[slot][c][w];
+#pragma unroll
+    for (int s = 1; s < GEMV_WARPS; s <<= 1)
+#pragma unroll
+      for (int w = 0; w + s < GEMV_WARPS; w += 2 * s)
+        if (32 * (w + s) < valid) r[w] = Ops<K, VAR>::add(r[w], r[w + s]);
+    store<K>(y, sy, i, r[0]);
+  }
 }
 
 template <int K, int VAR>
@@ -228,8 +263,9 @@ struct GemvLaunch {
       gemv_exact_kernel<K, VAR><<<(unsigned)ceil_div(m, 128), 128, 0, st>>>(A, lda, sA, x, sx, y,
                                                                             sy, m, n);
     } else {
-      gemv_tree_kernel<K, VAR><<<(unsigned)ceil_div(m, 8), 256, 0, st>>>(A, lda, sA, x, sx, y, sy,
-                                                                         m, n);
+      gemv_tree_kernel<K, VAR><<<(unsigned)ceil_div(m, GEMV_ROWS_PER_CTA),
+                                 32 * GEMV_WARPS * GEMV_ROWS_PER_CTA, 0, st>>>(A, lda, sA, x, sx, y,
+                                                                               sy, m, n);
     }
     return launch_status();
   }

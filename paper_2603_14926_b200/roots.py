@@ -171,9 +171,10 @@ def _mp():
 
 
 def _mpf_fraction(x) -> Fraction:
-    man, exp = x.man_exp
-    man = int(man)
-    return Fraction(man) * (Fraction(2) ** int(exp))
+    """Exact value of a finite mpmath mpf."""
+    sign, man, exp, _ = x._mpf_
+    v = Fraction(int(man)) * (Fraction(2) ** int(exp))
+    return -v if sign else v
 
 
 def radius_estimate(q: MonicPoly, variant: Variant = Variant.STANDARD) -> tuple:

@@ -1,0 +1,90 @@
+"""The C-ABI library: loads without a GPU, exports every symbol the header
+declares, and rejects bad arguments before launching anything."""
+
+import ctypes
+import os
+import re
+
+import pytest
+
+from paper_2603_14926_b200 import _lib
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(REPO, "include", "mwgpu.h")
+
+
+def declared_symbols():
+    text = open(HEADER).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(mw_\w+)\s*\(", text)))
+
+
+def test_library_loads_on_cpu():
+    lib = _lib.load()
+    assert _lib.version().startswith("mwgpu")
+    assert lib is _lib.load()
+
+
+def test_every_declared_symbol_is_exported():
+    syms = declared_symbols()
+    assert len(syms) >= 17
+    lib = ctypes.CDLL(_lib.LIB_PATH)
+    missing = [s for s in syms if not hasattr(lib, s)]
+    assert missing == []
+
+
+def test_binding_covers_the_header():
+    assert set(declared_symbols()) == set(_lib.EXPORTS)
+
+
+def test_status_strings():
+    lib = _lib.load()
+    assert lib.mw_status_string(0) == b"ok"
+    assert b"invalid" in lib.mw_status_string(-1)
+    assert b"variant" in lib.mw_status_string(-2)
+
+
+@pytest.mark.parametrize("fn", ["mw_ew_add", "mw_ew_sub", "mw_ew_mul", "mw_ew_div"])
+def test_ew_argument_checks(fn):
+    f = getattr(_lib.load(), fn)
+    p = 0x1000  # never dereferenced: every call below returns before a launch
+    assert f(5, 1, p, 8, p, 8, p, 8, 8, None) == _lib.MW_ERR_INVALID  # bad k
+    assert f(3, 0, p, 8, p, 8, p, 8, 8, None) == _lib.MW_ERR_UNSUPPORTED  # TD STANDARD
+    assert f(4, 0, p, 8, p, 8, p, 8, 8, None) == _lib.MW_ERR_UNSUPPORTED
+    assert f(2, 7, p, 8, p, 8, p, 8, 8, None) == _lib.MW_ERR_INVALID  # bad variant
+    assert f(2, 1, p, 4, p, 8, p, 8, 8, None) == _lib.MW_ERR_INVALID  # stride < n
+    assert f(2, 1, None, 8, p, 8, p, 8, 8, None) == _lib.MW_ERR_INVALID  # null
+    assert f(2, 1, p, 8, p, 8, p, 8, -1, None) == _lib.MW_ERR_INVALID
+    assert f(2, 1, None, 0, None, 0, None, 0, 0, None) == _lib.MW_OK  # empty
+
+
+def test_gemm_argument_checks():
+    f = _lib.load().mw_gemm
+    p = 0x1000
+    assert f(3, 0, p, 4, 16, p, 4, 16, p, 4, 16, 4, 4, 4, None) == _lib.MW_ERR_UNSUPPORTED
+    assert f(2, 1, p, 3, 16, p, 4, 16, p, 4, 16, 4, 4, 4, None) == _lib.MW_ERR_INVALID  # lda < kd
+    assert f(2, 1, p, 4, 15, p, 4, 16, p, 4, 16, 4, 4, 4, None) == _lib.MW_ERR_INVALID  # plane stride
+    assert f(2, 1, p, 4, 16, p, 4, 16, p, 4, 16, 0, 4, 4, None) == _lib.MW_OK  # m = 0
+
+
+def test_other_entry_checks():
+    lib = _lib.load()
+    p = 0x1000
+    assert lib.mw_horner(2, 1, p, 3, 5, p, 8, p, 8, 8, None) == _lib.MW_ERR_INVALID  # sc < deg+1
+    assert lib.mw_horner(4, 0, p, 8, 5, p, 8, p, 8, 8, None) == _lib.MW_ERR_UNSUPPORTED
+    assert lib.mw_gemv(2, 1, p, 8, 64, p, 8, p, 8, 8, 8, 3, None) == _lib.MW_ERR_INVALID  # order
+    assert lib.mw_dot(2, 1, p, 8, p, 8, 8, None, p, 9, None) == _lib.MW_ERR_INVALID
+    assert lib.mw_dk_sweep(3, 1, p, 8, 8, p, p, 8, 4, 2, p, p, 8, p, p, 1, None) == _lib.MW_ERR_INVALID  # i1 < i0
+    assert lib.mw_fp64_peak_kernel(0, 1, 512, 1, p, None) == _lib.MW_ERR_INVALID
+
+
+def test_workspace_sizes():
+    lib = _lib.load()
+    assert lib.mw_dot_workspace(2, 4096) == 0
+    assert lib.mw_dot_num_partials(4097) == 2
+    assert lib.mw_dot_workspace(2, 4097) == 2 * 2
+    assert lib.mw_dot_workspace(4, 65536) == 16 * 4
+    # 2^28 elements: 65536 partials, then 256 level-2 values
+    assert lib.mw_dot_workspace(2, 1 << 28) == 65536 * 2 + 256 * 2
+    assert lib.mw_tree_fold_workspace(3, 256) == 0
+    assert lib.mw_tree_fold_workspace(3, 257) == 2 * 3

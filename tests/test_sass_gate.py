@@ -1,0 +1,116 @@
+"""SASS gate -- the device analogue of the reference's branch-free checks
+(bytecode has no JUMP opcodes, pkg/tests/test_eft.py:120-127; BF kernels
+have zero comparisons, test_multiword.py:498-518) and of its
+no-contraction assumption (README.md:48-54).
+
+Reads the compiled sm_100a machine code of libmwgpu.so with cuobjdump
+(no GPU needed) and checks, per lane-wise kernel:
+  * the FP64 instruction mix equals the algorithm's op count exactly:
+    DFMA only from two_prod (DD/TD/QD mul: 1/3/6, add: 0), DMUL 3/6/10,
+    DADD 20/57/103 for add and 5/30/90 for mul -- so nvcc contracted or
+    dropped nothing;
+  * the branch-free bodies contain no branches beyond the grid-stride
+    loop's control flow, and no FP64 comparisons (DSETP).
+"""
+
+import re
+import shutil
+import subprocess
+
+import pytest
+
+from paper_2603_14926_b200 import _lib
+
+CUOBJDUMP = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+
+# per lane: (DADD, DMUL, DFMA)
+ADD_MIX = {2: (20, 0, 0), 3: (57, 0, 0), 4: (103, 0, 0)}
+MUL_MIX = {2: (5, 3, 1), 3: (30, 6, 3), 4: (90, 10, 6)}
+
+
+@pytest.fixture(scope="module")
+def sass():
+    if not shutil.which(CUOBJDUMP) and not __import__("os").path.exists(CUOBJDUMP):
+        pytest.skip("cuobjdump not available")
+    out = subprocess.run([CUOBJDUMP, "-sass", _lib.LIB_PATH], capture_output=True, text=True, check=True).stdout
+    funcs = {}
+    cur = None
+    for line in out.splitlines():
+        m = re.search(r"Function : (\S+)", line)
+        if m:
+            cur = m.group(1)
+            funcs[cur] = []
+        elif cur is not None:
+            m = re.match(r"\s+/\*[0-9a-f]+\*/\s+(.*?);", line)
+            if m:
+                funcs[cur].append(m.group(1))
+    return funcs
+
+
+def opcode(ins):
+    toks = ins.split()
+    if toks and toks[0].startswith("@"):
+        toks = toks[1:]
+    return toks[0] if toks else ""
+
+
+def mix(body):
+    ops = [opcode(i) for i in body]
+    count = lambda p: sum(1 for o in ops if o == p or o.startswith(p + "."))  # noqa: E731
+    return count("DADD"), count("DMUL"), count("DFMA"), count("BRA"), count("DSETP")
+
+
+def find(funcs, name, k, var, op):
+    key = f"_ZN2mw{len(name)}{name}ILi{k}ELi{var}ELi{op}EEEv"
+    hits = [f for f in funcs if f.startswith(key)]
+    assert len(hits) == 1, (key, hits)
+    return funcs[hits[0]]
+
+
+def lane_bodies(a, m, f, table_entry):
+    """Number of lane bodies the kernel contains (nvcc may unroll the
+    grid-stride loop); the FP64 mix must be exactly that many copies of
+    the per-lane algorithm."""
+    dadd, dmul, dfma = table_entry
+    assert a % dadd == 0, (a, dadd)
+    u = a // dadd
+    assert (a, m, f) == (u * dadd, u * dmul, u * dfma)
+    return u
+
+
+@pytest.mark.parametrize("k", [2, 3, 4])
+@pytest.mark.parametrize("op,table", [(0, ADD_MIX), (2, MUL_MIX)], ids=["add", "mul"])
+def test_fp64_mix_equals_algorithm(sass, k, op, table):
+    # ew_kernel_v1: one lane per body
+    a, m, f, _, _ = mix(find(sass, "ew_kernel_v1", k, 1, op))
+    assert lane_bodies(a, m, f, table[k]) >= 1
+    # ew_kernel_v2: two lanes per body (128-bit path)
+    a, m, f, _, _ = mix(find(sass, "ew_kernel_v2", k, 1, op))
+    assert lane_bodies(a, m, f, table[k]) % 2 == 0
+
+
+@pytest.mark.parametrize("k", [2, 3, 4])
+@pytest.mark.parametrize("op,table", [(0, ADD_MIX), (1, ADD_MIX), (2, MUL_MIX)], ids=["add", "sub", "mul"])
+def test_bf_bodies_branch_free(sass, k, op, table):
+    for name in ("ew_kernel_v1", "ew_kernel_v2"):
+        a, m, f, bra, dsetp = mix(find(sass, name, k, 1, op))
+        assert dsetp == 0, "FP64 comparison in a branch-free body"
+        u = lane_bodies(a, m, f, table[k])
+        # only loop control: per unrolled trip a bound check, plus entry/exit
+        assert bra <= u + 4, f"{name} k={k} op={op}: {bra} branches for {u} lane bodies"
+
+
+def test_dd_standard_add_is_accurate_add(sass):
+    # dw_add_accurate (multiword.py:118-126): 2 two_sum + 2 adds + 2 qts = 20
+    a, m, f, _, dsetp = mix(find(sass, "ew_kernel_v1", 2, 0, 0))
+    assert dsetp == 0
+    assert lane_bodies(a, m, f, (20, 0, 0)) >= 1
+
+
+def test_gemm_inner_loop_has_no_contraction(sass):
+    """DD GEMM: the MAC body issues exactly one DFMA per product."""
+    hits = [f for f in sass if f.startswith("_ZN2mw11gemm_kernelILi2ELi1E")]
+    assert len(hits) == 1
+    a, m, f, _, _ = mix(sass[hits[0]])
+    # 4x4 register tile per t step: 16 MACs -> 16 DFMA, 48 DMUL, 16*25 DADD
+    assert (a, m, f) == (400, 48, 16)
