@@ -75,18 +75,19 @@ int64_t mw_dot_workspace(int k, int64_t n);
 
 /* out_dev[0..k) = sum_t x_t (*) y_t.  The definition is the naive-matmul
  * fold (linalg.py:300-314) for 1xn . nx1.  MW_ORDER_EXACT replays it
- * bit-exactly on one thread.  MW_ORDER_TREE folds 16-element leaf chunks
- * in ascending order from exact zero and combines the chunk partials by a
- * fixed in-place pairwise tree (stride 1, 2, 4, ...; an unpaired tail
- * passes through) -- a function of n only, so the result does not depend
- * on launch shape or GPU count.  For n <= 16 both orders coincide.
+ * bit-exactly on one thread.  MW_ORDER_TREE: block b covers elements
+ * [4096b, 4096b+4096); its partial p (p < 256) folds elements
+ * 4096b + p + 256j (j = 0..15) ascending from exact zero (and exists iff
+ * 4096b + p < n); all partials combine by a fixed in-place pairwise tree
+ * (stride 1, 2, 4, ...; an unpaired tail passes through) -- a function of n
+ * only, so the result does not depend on launch shape or GPU count.
  * ws: mw_dot_workspace(k, n) doubles (may be NULL when that is 0). */
 int mw_dot(int k, int variant, const double* x, int64_t sx, const double* y,
            int64_t sy, int64_t n, double* ws, double* out_dev, int order,
            void* stream);
 
 /* Tree-dot first stage for sharded dots: writes mw_dot_num_partials(n) =
- * ceil(n/4096) block partials (each the tree root of 256 leaf chunks) to
+ * ceil(n/4096) block partials (each the tree root of its 256 partials) to
  * partials[c*pstride + b].  Shards that split x, y at multiples of 4096
  * elements produce partials that, concatenated in shard order and folded
  * with mw_tree_fold, equal the single-GPU mw_dot bit for bit. */

@@ -120,7 +120,7 @@ def dot(x, y, variant=BRANCH_FREE, order: int = 0) -> np.ndarray:
     y = _planes(y)
     k, n = x.shape
     out = np.zeros(k)
-    scratch = np.zeros(max(1, (n + 15) // 16) * 4)
+    scratch = np.zeros(max(1, n) * 4)
     _check(lib().mwo_dot(k, _variant(variant), _ptr(x), n, _ptr(y), n, n, order, _ptr(out), _ptr(scratch)))
     return out
 

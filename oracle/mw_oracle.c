@@ -353,9 +353,11 @@ static mwv pairwise_tree(mwv* v, int64_t count, mw_binop add) {
   return v[0];
 }
 
-/* dot: order 0 = reference fold; order 1 = TREE (16-element leaf chunks
- * folded ascending from zero, then pairwise tree over chunk partials).
- * scratch: ceil(n/16) mwv slots (caller-provided, only for order 1). */
+/* dot: order 0 = reference fold; order 1 = TREE: block b covers elements
+ * [4096b, 4096b+4096); partial 256b + p (p < 256) folds elements
+ * 4096b + p + 256j (j = 0..15) ascending from zero and exists iff
+ * 4096b + p < n; then the pairwise tree over all partials.
+ * scratch: room for the partial count (<= n) mwv slots (order 1 only). */
 int mwo_dot(int k, int variant, const double* x, int64_t sx, const double* y, int64_t sy,
             int64_t n, int order, double* out, void* scratch) {
   mw_binop add, mul;
@@ -365,14 +367,17 @@ int mwo_dot(int k, int variant, const double* x, int64_t sx, const double* y, in
   if (order == 0 || n == 0) {
     r = fold_range(x, sx, 1, y, sy, 1, 0, n, 1, k, add, mul);
   } else {
-    int64_t nch = (n + 15) / 16;
+    int64_t nb = (n + 4095) / 4096;
+    int64_t last = n - (nb - 1) * 4096;
+    int64_t np = (nb - 1) * 256 + (last < 256 ? last : 256);
     mwv* v = (mwv*)scratch;
 #pragma omp parallel for schedule(static)
-    for (int64_t c = 0; c < nch; ++c) {
-      int64_t t1 = (c + 1) * 16 < n ? (c + 1) * 16 : n;
-      v[c] = fold_range(x, sx, 1, y, sy, 1, c * 16, t1, 1, k, add, mul);
+    for (int64_t q = 0; q < np; ++q) {
+      int64_t b = q / 256, p = q % 256;
+      int64_t t1 = (b + 1) * 4096 < n ? (b + 1) * 4096 : n;
+      v[q] = fold_range(x, sx, 1, y, sy, 1, b * 4096 + p, t1, 256, k, add, mul);
     }
-    r = pairwise_tree(v, nch, add);
+    r = pairwise_tree(v, np, add);
   }
   st(out, 1, 0, k, &r);
   return 0;
@@ -544,12 +549,13 @@ int mwo_dk_sweep(int k, int variant, const double* coeffs, int64_t sc, int64_t n
         den = c_mul(&den, &f, k, add, mul);
       }
     } else {
-      /* TREE: lane products over j = l, l+32, ... then pairwise tree */
-      cmw dl[32], tl[32];
-      int64_t nl = n < 32 ? n : 32;
-      for (int l = 0; l < nl; ++l) {
-        dl[l] = c_one();
-        for (int64_t j = l; j < n; j += 32) {
+      /* TREE (the GPU kernel's documented order, P = 64 partials) */
+      enum { P = 64 };
+      cmw dl[P], tl[P];
+      int64_t nl = n < P ? n : P;
+      for (int u = 0; u < nl; ++u) {
+        dl[u] = c_one();
+        for (int64_t j = u; j < n; j += P) {
           cmw f;
           mwv zjr = ld(zre, sz, j, k), zji = ld(zim, sz, j, k);
           mwv nzr = mneg(&zjr, k), nzi = mneg(&zji, k);
@@ -560,22 +566,31 @@ int mwo_dk_sweep(int k, int variant, const double* coeffs, int64_t sc, int64_t n
             int64_t key = j * n + i;
             if (my_coll < 0 || key < my_coll) my_coll = key;
           }
-          dl[l] = c_mul(&dl[l], &f, k, add, mul);
+          dl[u] = c_mul(&dl[u], &f, k, add, mul);
         }
       }
       for (int64_t s = 1; s < nl; s <<= 1)
-        for (int64_t l = 0; l + s < nl; l += 2 * s) dl[l] = c_mul(&dl[l], &dl[l + s], k, add, mul);
+        for (int64_t u = 0; u + s < nl; u += 2 * s) dl[u] = c_mul(&dl[u], &dl[u + s], k, add, mul);
       den = dl[0];
-      /* numerator: monic a_0..a_n, blocks of B, lane scale (z^B)^l */
-      int64_t B = (n + 1 + 31) / 32;
+      /* numerator: monic a_0..a_n, blocks of B, scale w^u */
+      int64_t B = (n + 1 + P - 1) / P;
       int64_t nb = (n + 1 + B - 1) / B;
       cmw w = c_one(), sq = z;
       for (int64_t e = B; e > 0; e >>= 1) {
         if (e & 1) w = c_mul(&w, &sq, k, add, mul);
         if (e > 1) sq = c_mul(&sq, &sq, k, add, mul);
       }
-      for (int l = 0; l < nb; ++l) {
-        int64_t lo = l * B, hi = lo + B < n + 1 ? lo + B : n + 1;
+      /* Hillis-Steele product scan over 32 lanes: x_0 = 1, x_l = w */
+      cmw xs[32], nx[32];
+      for (int l = 0; l < 32; ++l) xs[l] = l == 0 ? c_one() : w;
+      for (int s = 1; s < 32; s <<= 1) {
+        for (int l = 0; l < 32; ++l) nx[l] = l >= s ? c_mul(&xs[l], &xs[l - s], k, add, mul) : xs[l];
+        memcpy(xs, nx, sizeof(xs));
+      }
+      cmw w32 = w;
+      for (int r = 0; r < 5; ++r) w32 = c_mul(&w32, &w32, k, add, mul);
+      for (int u = 0; u < nb; ++u) {
+        int64_t lo = u * B, hi = lo + B < n + 1 ? lo + B : n + 1;
         cmw p;
         p.re = (hi - 1 == n) ? mconst(1.0) : ld(coeffs, sc, hi - 1, k);
         p.im = mzero();
@@ -585,17 +600,14 @@ int mwo_dk_sweep(int k, int variant, const double* coeffs, int64_t sc, int64_t n
           p.re = add(&p.re, &cc);
           p.im = add(&p.im, &zz);
         }
-        cmw scale = c_one(), wp = w;
-        for (int e = l; e > 0; e >>= 1) {
-          if (e & 1) scale = c_mul(&scale, &wp, k, add, mul);
-          if (e > 1) wp = c_mul(&wp, &wp, k, add, mul);
-        }
-        tl[l] = c_mul(&p, &scale, k, add, mul);
+        cmw scale = xs[u % 32];
+        if (u >= 32) scale = c_mul(&scale, &w32, k, add, mul);
+        tl[u] = c_mul(&p, &scale, k, add, mul);
       }
       for (int64_t s = 1; s < nb; s <<= 1)
-        for (int64_t l = 0; l + s < nb; l += 2 * s) {
-          tl[l].re = add(&tl[l].re, &tl[l + s].re);
-          tl[l].im = add(&tl[l].im, &tl[l + s].im);
+        for (int64_t u = 0; u + s < nb; u += 2 * s) {
+          tl[u].re = add(&tl[u].re, &tl[u + s].re);
+          tl[u].im = add(&tl[u].im, &tl[u + s].im);
         }
       acc = tl[0];
     }

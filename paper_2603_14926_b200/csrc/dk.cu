@@ -17,11 +17,10 @@
 // exact.  The reciprocal of mag is computed once and applied to both
 // parts, which is the identical op sequence the reference runs twice.
 //
-// exact_order = 0 (tree): a warp per root.  Lane l owns factors
-// j = l, l+32, ... (ascending, from (1,0)) and the coefficient block
-// [l*B, (l+1)*B) of the monic polynomial, evaluated by Horner and scaled by
-// (z^B)^l; lane results combine in a pairwise shuffle tree.  Same
-// arithmetic per term, reassociated: within the n*2^-p relative bound.
+// exact_order = 0 (tree): four warps per root (definition below): 64
+// strided partial products for the denominator, 64 Horner blocks for the
+// numerator scaled by powers of z^B, pairwise trees.  Same arithmetic per
+// term, reassociated: within the n*2^-p relative bound.
 #include <climits>
 
 #include "common.cuh"
@@ -43,6 +42,15 @@ __device__ __forceinline__ Cx<K, VAR> c_mul(const Cx<K, VAR>& a, const Cx<K, VAR
   r.re = O::add(p1, neg(p2));
   r.im = O::add(O::add(p3, neg(p1)), neg(p2));
   return r;
+}
+
+// Out-of-line copy for the tree kernel: its many call sites (chains, trees,
+// scans, powers) would otherwise inline ~30 copies of a 400-1000
+// instruction body and thrash the instruction cache (ncu: stall
+// "no_instructions" dominated).  Same ops, same bits.
+template <int K, int VAR>
+__device__ __noinline__ Cx<K, VAR> c_mul_ol(const Cx<K, VAR> a, const Cx<K, VAR> b) {
+  return c_mul<K, VAR>(a, b);
 }
 
 template <int K, int VAR>
@@ -154,93 +162,170 @@ __global__ void __launch_bounds__(2 * DK_EXACT_ROOTS)
 }
 
 // ----------------------------------------------------------- tree order
-constexpr int DK_TREE_WARPS = 4;  // roots per CTA
+// DK_P = 64 partials per role.
+//  denominator: partial u (u < 64) folds the factors
+//    j = u, u+64, ... ascending from (1, 0) (j == i pinned to (1, 0));
+//    partials combine by the in-place pairwise product tree (strides
+//    1..32, pair valid while the partner index < min(n, 64)).
+//  numerator: the monic coefficients a_0..a_n (a_n = 1) split
+//    into blocks of B = ceil((n+1)/64); block u = [uB, (u+1)B) is evaluated
+//    by Horner from its top coefficient, scaled by w^u with w = z^B, and the
+//    terms combine by the pairwise sum tree (valid while < #blocks).
+//    w = z^B by right-to-left square-and-multiply; w^u for u < 32 by a
+//    Hillis-Steele product scan over the warp (x_l <- x_l * x_{l-s} for
+//    s = 1, 2, 4, 8, 16 from x_0 = 1, x_l = w), and for u >= 32 as
+//    (the same scan) * w^32, w^32 = five squarings of w.
+constexpr int DK_P = 64;
 
 template <int K, int VAR>
-__device__ __forceinline__ Cx<K, VAR> shfl_down_cx(const Cx<K, VAR>& v, int s) {
+__device__ __forceinline__ Cx<K, VAR> shfl_cx(const Cx<K, VAR>& v, int s, bool up) {
   Cx<K, VAR> r;
-  r.re = shfl_down<K>(v.re, s);
-  r.im = shfl_down<K>(v.im, s);
+#pragma unroll
+  for (int c = 0; c < K; ++c) {
+    r.re.c[c] = up ? __shfl_up_sync(0xffffffffu, v.re.c[c], s) : __shfl_down_sync(0xffffffffu, v.re.c[c], s);
+    r.im.c[c] = up ? __shfl_up_sync(0xffffffffu, v.im.c[c], s) : __shfl_down_sync(0xffffffffu, v.im.c[c], s);
+  }
   return r;
 }
 
+// Mapping: one CTA of two warps per root.  Warp 0 owns the 64 denominator
+// partials (lane l: u = l and u = l + 32, two independent product chains);
+// warp 1 owns the 64 numerator blocks (lane l: blocks l and l + 32, two
+// Horner chains, plus the power chain).  Four independent dependency
+// chains per lane pair keep the FP64 pipe fed with ~3.5 roots per SM.
 template <int K, int VAR>
-__global__ void __launch_bounds__(32 * DK_TREE_WARPS)
+__global__ void __launch_bounds__(64)
     dk_tree_kernel(const double* __restrict__ coeffs, int64_t sc, int64_t n,
                    const double* __restrict__ zre, const double* __restrict__ zim, int64_t sz,
                    int64_t i0, int64_t i1, double* __restrict__ zre_out,
                    double* __restrict__ zim_out, int64_t so, double* __restrict__ step_mag,
                    int* __restrict__ flag) {
   using O = Ops<K, VAR>;
+  __shared__ double part[2][K];
   const int lane = threadIdx.x & 31;
-  const int64_t i = i0 + (int64_t)blockIdx.x * DK_TREE_WARPS + (threadIdx.x >> 5);
-  if (i >= i1) return;
+  const int warp = threadIdx.x >> 5;
+  const int64_t i = i0 + blockIdx.x;
   Cx<K, VAR> z;
   z.re = load<K>(zre, sz, i);
   z.im = load<K>(zim, sz, i);
-
-  // ---- denominator: lane l folds j = l, l+32, ... ascending
-  Cx<K, VAR> den = c_one<K, VAR>();
-  for (int64_t j = lane; j < n; j += 32) {
-    Cx<K, VAR> f;
-    f.re = O::add(z.re, neg(load<K>(zre, sz, j)));
-    f.im = O::add(z.im, neg(load<K>(zim, sz, j)));
-    if (j == i) f = c_one<K, VAR>();
-    if (fabs(f.re.c[0]) + fabs(f.im.c[0]) == 0.0) {
-      const long long key = (long long)j * n + i;
-      atomicMin(flag, key > INT_MAX ? INT_MAX : (int)key);
-    }
-    den = c_mul(den, f);
-  }
-
-  // ---- numerator: monic coefficients a_0..a_n (a_n = 1), block size B
-  const int64_t B = (n + 1 + 31) / 32;
-  const int64_t lo = lane * B;
-  const int64_t hi = (lo + B < n + 1) ? lo + B : n + 1;  // [lo, hi)
-  Cx<K, VAR> p;
-  p.re = zero<K>();
-  p.im = zero<K>();
-  if (lo < hi) {
-    // Horner over the block: p = a_{hi-1}; p = p*z + a_c for c = hi-2..lo
-    Cx<K, VAR> a;
-    a.re = (hi - 1 == n) ? constant<K>(1.0) : load<K>(coeffs, sc, hi - 1);
-    a.im = zero<K>();
-    p = a;
-    for (int64_t c = hi - 2; c >= lo; --c) {
-      p = c_mul(p, z);
-      p.re = O::add(p.re, load<K>(coeffs, sc, c));
-      p.im = O::add(p.im, zero<K>());
-    }
-  }
-  // w = z^B by square-and-multiply, then the lane's scale (z^B)^lane
-  Cx<K, VAR> w = c_one<K, VAR>(), sq = z;
-  for (int64_t e = B; e > 0; e >>= 1) {
-    if (e & 1) w = c_mul(w, sq);
-    if (e > 1) sq = c_mul(sq, sq);
-  }
-  Cx<K, VAR> scale = c_one<K, VAR>(), wp = w;
-  for (int e = lane; e > 0; e >>= 1) {
-    if (e & 1) scale = c_mul(scale, wp);
-    if (e > 1) wp = c_mul(wp, wp);
-  }
-  Cx<K, VAR> term = c_mul(p, scale);
-  const bool has_block = lo < hi;
-  const int nblocks = (int)((n + 1 + B - 1) / B);
-
-  // ---- pairwise shuffle trees (product for den, sum for the numerator)
+  Cx<K, VAR> num;
+  if (warp == 0) {
+    // ---- denominator partials u = lane (lo) and u = lane + 32 (hi)
+    Cx<K, VAR> v[2] = {c_one<K, VAR>(), c_one<K, VAR>()};
+    for (int64_t j0 = lane; j0 < n; j0 += DK_P) {
 #pragma unroll
-  for (int s = 1; s < 32; s <<= 1) {
-    Cx<K, VAR> od = shfl_down_cx(den, s);
-    Cx<K, VAR> ot = shfl_down_cx(term, s);
-    if ((lane & (2 * s - 1)) == 0) {
-      if (lane + s < 32 && lane + s < n) den = c_mul(den, od);
-      if (has_block && lane + s < nblocks) {
-        term.re = O::add(term.re, ot.re);
-        term.im = O::add(term.im, ot.im);
+      for (int h = 0; h < 2; ++h) {
+        const int64_t j = j0 + 32 * h;
+        if (j < n) {
+          Cx<K, VAR> f;
+          f.re = O::add(z.re, neg(load<K>(zre, sz, j)));
+          f.im = O::add(z.im, neg(load<K>(zim, sz, j)));
+          if (j == i) f = c_one<K, VAR>();
+          if (fabs(f.re.c[0]) + fabs(f.im.c[0]) == 0.0) {
+            const long long key = (long long)j * n + i;
+            atomicMin(flag, key > INT_MAX ? INT_MAX : (int)key);
+          }
+          v[h] = c_mul_ol(v[h], f);
+        }
       }
     }
+    const int64_t valid = n < DK_P ? n : DK_P;
+#pragma unroll
+    for (int s = 1; s < 32; s <<= 1) {
+      Cx<K, VAR> o0 = shfl_cx(v[0], s, false), o1 = shfl_cx(v[1], s, false);
+      if ((lane & (2 * s - 1)) == 0) {
+        if (lane + s < valid) v[0] = c_mul_ol(v[0], o0);
+        if (lane + 32 + s < valid) v[1] = c_mul_ol(v[1], o1);
+      }
+    }
+    if (lane == 0) {
+      Cx<K, VAR> den = (32 < valid) ? c_mul_ol(v[0], v[1]) : v[0];
+#pragma unroll
+      for (int c = 0; c < K; ++c) {
+        part[0][c] = den.re.c[c];
+        part[1][c] = den.im.c[c];
+      }
+    }
+  } else {
+    // ---- numerator blocks u = lane (lo) and u = lane + 32 (hi)
+    const int64_t B = (n + 1 + DK_P - 1) / DK_P;
+    const int64_t nblocks = (n + 1 + B - 1) / B;
+    Cx<K, VAR> p[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int64_t lo = (lane + 32 * h) * B;
+      const int64_t hi = (lo + B < n + 1) ? lo + B : n + 1;
+      p[h].re = zero<K>();
+      p[h].im = zero<K>();
+      if (lo < hi) p[h].re = (hi - 1 == n) ? constant<K>(1.0) : load<K>(coeffs, sc, hi - 1);
+    }
+    // the two Horner chains advance together (same trip count except at the tail)
+    const int64_t lo0 = lane * B, lo1 = (lane + 32) * B;
+    const int64_t hi0 = (lo0 + B < n + 1) ? lo0 + B : n + 1;
+    const int64_t hi1 = (lo1 + B < n + 1) ? lo1 + B : n + 1;
+    for (int64_t d = 2; d <= B; ++d) {
+      const int64_t c0 = hi0 - d, c1 = hi1 - d;
+      if (c0 >= lo0) {
+        p[0] = c_mul_ol(p[0], z);
+        p[0].re = O::add(p[0].re, load<K>(coeffs, sc, c0));
+        p[0].im = O::add(p[0].im, zero<K>());
+      }
+      if (c1 >= lo1) {
+        p[1] = c_mul_ol(p[1], z);
+        p[1].re = O::add(p[1].re, load<K>(coeffs, sc, c1));
+        p[1].im = O::add(p[1].im, zero<K>());
+      }
+    }
+    // w = z^B (right-to-left square-and-multiply; uniform across lanes)
+    Cx<K, VAR> w = c_one<K, VAR>(), sq = z;
+    for (int64_t e = B; e > 0; e >>= 1) {
+      if (e & 1) w = c_mul_ol(w, sq);
+      if (e > 1) sq = c_mul_ol(sq, sq);
+    }
+    Cx<K, VAR> w32 = w;
+#pragma unroll
+    for (int r = 0; r < 5; ++r) w32 = c_mul_ol(w32, w32);
+    // x_lane = w^lane by a Hillis-Steele product scan
+    Cx<K, VAR> x = lane == 0 ? c_one<K, VAR>() : w;
+#pragma unroll
+    for (int s = 1; s < 32; s <<= 1) {
+      Cx<K, VAR> o = shfl_cx(x, s, true);
+      if (lane >= s) x = c_mul_ol(x, o);
+    }
+    Cx<K, VAR> t[2];
+    t[0] = c_mul_ol(p[0], x);
+    Cx<K, VAR> xh = c_mul_ol(x, w32);
+    t[1] = c_mul_ol(p[1], xh);
+#pragma unroll
+    for (int s = 1; s < 32; s <<= 1) {
+      Cx<K, VAR> o0 = shfl_cx(t[0], s, false), o1 = shfl_cx(t[1], s, false);
+      if ((lane & (2 * s - 1)) == 0) {
+        if (lane + s < nblocks) {
+          t[0].re = O::add(t[0].re, o0.re);
+          t[0].im = O::add(t[0].im, o0.im);
+        }
+        if (lane + 32 + s < nblocks) {
+          t[1].re = O::add(t[1].re, o1.re);
+          t[1].im = O::add(t[1].im, o1.im);
+        }
+      }
+    }
+    num = t[0];
+    if (32 < nblocks) {
+      num.re = O::add(t[0].re, t[1].re);
+      num.im = O::add(t[0].im, t[1].im);
+    }
   }
-  if (lane == 0) dk_tail<K, VAR>(term, den, z, zre_out, zim_out, so, step_mag, i);
+  __syncthreads();
+  if (warp == 1 && lane == 0) {
+    Cx<K, VAR> den;
+#pragma unroll
+    for (int c = 0; c < K; ++c) {
+      den.re.c[c] = part[0][c];
+      den.im.c[c] = part[1][c];
+    }
+    dk_tail<K, VAR>(num, den, z, zre_out, zim_out, so, step_mag, i);
+  }
 }
 
 template <int K, int VAR>
@@ -255,8 +340,7 @@ struct DkLaunch {
       dk_exact_kernel<K, VAR><<<(unsigned)blocks, 2 * DK_EXACT_ROOTS, 0, st>>>(
           coeffs, sc, n, zre, zim, sz, i0, i1, zre_out, zim_out, so, step_mag, flag);
     } else {
-      const int64_t blocks = (cnt + DK_TREE_WARPS - 1) / DK_TREE_WARPS;
-      dk_tree_kernel<K, VAR><<<(unsigned)blocks, 32 * DK_TREE_WARPS, 0, st>>>(
+      dk_tree_kernel<K, VAR><<<(unsigned)cnt, 64, 0, st>>>(
           coeffs, sc, n, zre, zim, sz, i0, i1, zre_out, zim_out, so, step_mag, flag);
     }
     return launch_status();

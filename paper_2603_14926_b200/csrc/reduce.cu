@@ -8,18 +8,21 @@
 // MW_ORDER_TREE is the throughput order; its tree is a pure function of n
 // (never of grid shape or GPU count), so results are deterministic and
 // identical on 1..8 GPUs:
-//   dot:  leaf chunk c = elements [16c, 16c+16) folded ascending from exact
-//         zero; chunk partials combined in place by a pairwise tree
-//         (stride s = 1, 2, 4, ...: v[i] <- add(v[i], v[i+s]) for i % 2s == 0
-//         when i+s < count; an unpaired tail passes through).
+//   dot:  block b covers elements [4096b, 4096b+4096); its partial p
+//         (p = 0..255, global partial index 256b + p) folds the elements
+//         4096b + p + 256j, j = 0..15, ascending from exact zero (coalesced:
+//         consecutive lanes read consecutive elements).  Partial 256b + p
+//         exists iff 4096b + p < n.  Partials combine by the in-place
+//         pairwise tree (stride s = 1, 2, 4, ...: v[i] <- add(v[i], v[i+s])
+//         for i % 2s == 0 when i+s < count; an unpaired tail passes through).
 //   gemv: 128 partials per row; partial u folds t = u, u+128, ... ascending
 //         from exact zero; the partials combine by the same pairwise tree.
 #include "common.cuh"
 
 namespace mw {
 
-constexpr int DOT_LEAF = 16;       // elements per leaf chunk
-constexpr int DOT_BLOCK = 256;     // leaf chunks (threads) per block
+constexpr int DOT_LEAF = 16;       // elements per partial
+constexpr int DOT_BLOCK = 256;     // partials (threads) per block
 constexpr int64_t DOT_PER_BLOCK = (int64_t)DOT_LEAF * DOT_BLOCK;  // 4096
 
 // Pairwise tree over the block's 256 values v (one per thread) whose global
@@ -57,30 +60,36 @@ __device__ __forceinline__ V<K> block_tree(V<K> v, int64_t base, int64_t count) 
   return v;
 }
 
-// Stage 1: block b folds 256 leaf chunks and writes its subtree root.
+// Number of dot partials for length n (see the order definition above).
+__host__ __device__ __forceinline__ int64_t dot_partial_count(int64_t n) {
+  if (n <= 0) return 0;
+  const int64_t nb = (n + DOT_PER_BLOCK - 1) / DOT_PER_BLOCK;
+  const int64_t last = n - (nb - 1) * DOT_PER_BLOCK;
+  return (nb - 1) * DOT_BLOCK + (last < DOT_BLOCK ? last : DOT_BLOCK);
+}
+
+// Stage 1: block b folds its 256 strided partials and writes their tree root.
 template <int K, int VAR>
 __global__ void __launch_bounds__(DOT_BLOCK) dot_partials_kernel(
     const double* __restrict__ x, int64_t sx, const double* __restrict__ y, int64_t sy,
     int64_t n, double* __restrict__ partials, int64_t pstride) {
-  const int64_t chunk = blockIdx.x * (int64_t)DOT_BLOCK + threadIdx.x;
-  const int64_t nchunks = (n + DOT_LEAF - 1) / DOT_LEAF;
+  const int64_t base = blockIdx.x * DOT_PER_BLOCK + threadIdx.x;
   V<K> acc = zero<K>();
-  const int64_t t0 = chunk * DOT_LEAF;
-  if (t0 + DOT_LEAF <= n) {
+  if (blockIdx.x * DOT_PER_BLOCK + DOT_PER_BLOCK <= n) {
     V<K> xs[DOT_LEAF], ys[DOT_LEAF];
 #pragma unroll
-    for (int t = 0; t < DOT_LEAF; ++t) {
-      xs[t] = load<K>(x, sx, t0 + t);
-      ys[t] = load<K>(y, sy, t0 + t);
+    for (int j = 0; j < DOT_LEAF; ++j) {
+      xs[j] = load<K>(x, sx, base + j * DOT_BLOCK);
+      ys[j] = load<K>(y, sy, base + j * DOT_BLOCK);
     }
 #pragma unroll
-    for (int t = 0; t < DOT_LEAF; ++t)
-      acc = Ops<K, VAR>::add(acc, Ops<K, VAR>::mul(xs[t], ys[t]));
+    for (int j = 0; j < DOT_LEAF; ++j)
+      acc = Ops<K, VAR>::add(acc, Ops<K, VAR>::mul(xs[j], ys[j]));
   } else {
-    for (int64_t t = t0; t < n; ++t)
+    for (int64_t t = base; t < n; t += DOT_BLOCK)
       acc = Ops<K, VAR>::add(acc, Ops<K, VAR>::mul(load<K>(x, sx, t), load<K>(y, sy, t)));
   }
-  V<K> r = block_tree<K, VAR>(acc, blockIdx.x * (int64_t)DOT_BLOCK, nchunks);
+  V<K> r = block_tree<K, VAR>(acc, blockIdx.x * (int64_t)DOT_BLOCK, dot_partial_count(n));
   if (threadIdx.x == 0) {
 #pragma unroll
     for (int c = 0; c < K; ++c) partials[c * pstride + blockIdx.x] = r.c[c];

@@ -41,6 +41,7 @@ __all__ = [
     "radius_estimate",
     "dk_iterate",
     "dk_sweeps",
+    "DKSweepGraph",
     "dk_solve",
     "default_tolerance",
 ]
@@ -309,6 +310,66 @@ def dk_sweeps(q: MonicPoly, state: RootState, sweeps: int, variant: Variant = Va
         re=fin[0], im=fin[1], iteration=state.iteration + sweeps, converged=False,
         last_max_update=float(mag.max().item()) if sweeps > 0 else state.last_max_update,
     )
+
+
+class DKSweepGraph:
+    """``sweeps`` DK sweeps captured once into a CUDA graph (state reset,
+    flag reset and every sweep launch), so a fixed-sweep run costs one
+    graph launch instead of ``sweeps`` host round trips.
+
+        g = DKSweepGraph(q, state, 200, Variant.BRANCH_FREE)
+        g.replay()              # rerun from `state` (or g.load(new_state))
+        final = g.result()      # RootState; raises CollisionError
+    """
+
+    def __init__(self, q: MonicPoly, state: RootState, sweeps: int, variant: Variant = Variant.BRANCH_FREE,
+                 exact_order: bool = True):
+        _lib.require_cuda(q.planes, state.re, state.im)
+        if sweeps < 1:
+            raise ValueError("sweeps must be >= 1")
+        self.q, self.n, self.sweeps = q, state.n, sweeps
+        self.iteration0 = state.iteration
+        dev = state.re.device
+        self.src = (state.re.clone(), state.im.clone())
+        self.bufs = [(torch.empty_like(state.re), torch.empty_like(state.im)) for _ in range(2)]
+        self.mag = torch.empty(state.n, dtype=torch.float64, device=dev)
+        self.flags = torch.empty(sweeps, dtype=torch.int32, device=dev)
+
+        def body():
+            self.bufs[0][0].copy_(self.src[0])
+            self.bufs[0][1].copy_(self.src[1])
+            self.flags.fill_(INT32_MAX)
+            for s_ in range(sweeps):
+                a, b = self.bufs[s_ & 1], self.bufs[(s_ + 1) & 1]
+                sweep_into(q.planes, a[0], a[1], b[0], b[1], self.mag, self.flags[s_ : s_ + 1], variant,
+                           exact_order)
+
+        side = torch.cuda.Stream(device=dev)
+        side.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(side):
+            body()  # warm-up outside capture (lazy init of kernels / attributes)
+        torch.cuda.current_stream(dev).wait_stream(side)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            body()
+
+    def load(self, state: RootState):
+        self.src[0].copy_(state.re)
+        self.src[1].copy_(state.im)
+        self.iteration0 = state.iteration
+
+    def replay(self):
+        self.graph.replay()
+
+    def result(self, check: bool = True) -> RootState:
+        if check:
+            f = self.flags.cpu().numpy()
+            bad = np.nonzero(f != INT32_MAX)[0]
+            if bad.size:
+                _raise_collision(int(f[bad[0]]), self.n)
+        fin = self.bufs[self.sweeps & 1]
+        return RootState(re=fin[0].clone(), im=fin[1].clone(), iteration=self.iteration0 + self.sweeps,
+                         converged=False, last_max_update=float(self.mag.max().item()))
 
 
 def dk_solve(q: MonicPoly, variant: Variant = Variant.STANDARD, tol: float | None = None, max_iter: int = 200,

@@ -126,13 +126,13 @@ def test_dot_exact_golden(golden, k, v):
 
 
 @pytest.mark.parametrize("k", [2, 3, 4])
-@pytest.mark.parametrize("n", [1, 15, 16, 17, 300, 4095, 4096, 4097, 65536, 1 << 20, 1_000_003])
+@pytest.mark.parametrize("n", [1, 15, 16, 17, 255, 256, 257, 300, 4095, 4096, 4097, 65536, 1 << 20, 1_000_003])
 def test_dot_tree_vs_oracle(k, n):
     rng = np.random.default_rng(n + k)
     x, y = gen.g_k(rng, k, n), gen.g_k(rng, k, n)
     got = np.array(blas.dot(LaneBatch(x), LaneBatch(y), Variant.BRANCH_FREE, order="tree"))
     assert_bitwise(got, oracle.dot(x, y, "bf", order=1))
-    if n <= 16:
+    if n == 1:
         assert_bitwise(got, oracle.dot(x, y, "bf", order=0))
     if n <= 65536:
         ref = oracle.dot(x, y, "bf", order=0)
@@ -344,3 +344,19 @@ def test_dk_config5_200_sweeps_exact_matches_oracle_trajectory(k):
         ore, oim, _, _ = oracle.dk_sweep(coeffs, ore, oim, "bf", exact=True)
     assert_bitwise(st.re.cpu().numpy(), ore)
     assert_bitwise(st.im.cpu().numpy(), oim)
+
+
+@pytest.mark.parametrize("exact", [True, False])
+def test_dk_sweep_graph_matches_eager(exact):
+    k = 3
+    coeffs = gen.config5_poly(k)
+    zre, zim = gen.config5_init(k)
+    q, st = MonicPoly(coeffs), RootState(re=zre, im=zim)
+    eager = dk_sweeps(q, st, 5, Variant.BRANCH_FREE, exact_order=exact)
+    g = roots.DKSweepGraph(q, st, 5, Variant.BRANCH_FREE, exact_order=exact)
+    g.replay()
+    g.replay()  # replays are idempotent (state reset inside the graph)
+    r = g.result()
+    assert_bitwise(r.re.cpu().numpy(), eager.re.cpu().numpy())
+    assert_bitwise(r.im.cpu().numpy(), eager.im.cpu().numpy())
+    assert r.iteration == 5
