@@ -569,8 +569,11 @@ int mwo_dk_sweep(int k, int variant, const double* coeffs, int64_t sc, int64_t n
           dl[u] = c_mul(&dl[u], &f, k, add, mul);
         }
       }
-      for (int64_t s = 1; s < nl; s <<= 1)
-        for (int64_t u = 0; u + s < nl; u += 2 * s) dl[u] = c_mul(&dl[u], &dl[u + s], k, add, mul);
+      /* (u, u+32) first, then the pairwise tree over the low 32 */
+      for (int u = 0; u < 32 && u + 32 < nl; ++u) dl[u] = c_mul(&dl[u], &dl[u + 32], k, add, mul);
+      int64_t n32 = nl < 32 ? nl : 32;
+      for (int64_t s = 1; s < n32; s <<= 1)
+        for (int64_t u = 0; u + s < n32; u += 2 * s) dl[u] = c_mul(&dl[u], &dl[u + s], k, add, mul);
       den = dl[0];
       /* numerator: monic a_0..a_n, blocks of B, scale w^u */
       int64_t B = (n + 1 + P - 1) / P;
@@ -604,8 +607,13 @@ int mwo_dk_sweep(int k, int variant, const double* coeffs, int64_t sc, int64_t n
         if (u >= 32) scale = c_mul(&scale, &w32, k, add, mul);
         tl[u] = c_mul(&p, &scale, k, add, mul);
       }
-      for (int64_t s = 1; s < nb; s <<= 1)
-        for (int64_t u = 0; u + s < nb; u += 2 * s) {
+      for (int u = 0; u < 32 && u + 32 < nb; ++u) {
+        tl[u].re = add(&tl[u].re, &tl[u + 32].re);
+        tl[u].im = add(&tl[u].im, &tl[u + 32].im);
+      }
+      int64_t b32 = nb < 32 ? nb : 32;
+      for (int64_t s = 1; s < b32; s <<= 1)
+        for (int64_t u = 0; u + s < b32; u += 2 * s) {
           tl[u].re = add(&tl[u].re, &tl[u + s].re);
           tl[u].im = add(&tl[u].im, &tl[u + s].im);
         }

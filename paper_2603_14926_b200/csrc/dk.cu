@@ -165,12 +165,14 @@ __global__ void __launch_bounds__(2 * DK_EXACT_ROOTS)
 // DK_P = 64 partials per role.
 //  denominator: partial u (u < 64) folds the factors
 //    j = u, u+64, ... ascending from (1, 0) (j == i pinned to (1, 0));
-//    partials combine by the in-place pairwise product tree (strides
-//    1..32, pair valid while the partner index < min(n, 64)).
+//    with V = min(n, 64) partials: first v_l <- v_l * v_{l+32} (l < 32,
+//    l + 32 < V), then the in-place pairwise tree over v_0..v_31 (strides
+//    1..16, pair valid while the partner index < min(V, 32)).
 //  numerator: the monic coefficients a_0..a_n (a_n = 1) split
 //    into blocks of B = ceil((n+1)/64); block u = [uB, (u+1)B) is evaluated
-//    by Horner from its top coefficient, scaled by w^u with w = z^B, and the
-//    terms combine by the pairwise sum tree (valid while < #blocks).
+//    by Horner from its top coefficient, scaled by w^u with w = z^B; the
+//    terms combine like the denominator (t_l + t_{l+32} first, then the
+//    pairwise tree over 32, validity against the number of blocks).
 //    w = z^B by right-to-left square-and-multiply; w^u for u < 32 by a
 //    Hillis-Steele product scan over the warp (x_l <- x_l * x_{l-s} for
 //    s = 1, 2, 4, 8, 16 from x_0 = 1, x_l = w), and for u >= 32 as
@@ -188,29 +190,33 @@ __device__ __forceinline__ Cx<K, VAR> shfl_cx(const Cx<K, VAR>& v, int s, bool u
   return r;
 }
 
-// Mapping: one CTA of two warps per root.  Warp 0 owns the 64 denominator
-// partials (lane l: u = l and u = l + 32, two independent product chains);
-// warp 1 owns the 64 numerator blocks (lane l: blocks l and l + 32, two
-// Horner chains, plus the power chain).  Four independent dependency
-// chains per lane pair keep the FP64 pipe fed with ~3.5 roots per SM.
+// Mapping: one CTA of three warps per root, one role each, so the three
+// dependency chains run on different schedulers:
+//   warp 0  denominator: lane l owns partials l and l+32 (two product chains)
+//   warp 1  numerator:   lane l owns blocks l and l+32 (two Horner chains)
+//   warp 2  powers:      w = z^B, w^32, the scan x_l = w^l and x_l * w^32,
+//                        handed to warp 1 through shared memory.
 template <int K, int VAR>
-__global__ void __launch_bounds__(64)
+__global__ void __launch_bounds__(96)
     dk_tree_kernel(const double* __restrict__ coeffs, int64_t sc, int64_t n,
                    const double* __restrict__ zre, const double* __restrict__ zim, int64_t sz,
                    int64_t i0, int64_t i1, double* __restrict__ zre_out,
                    double* __restrict__ zim_out, int64_t so, double* __restrict__ step_mag,
                    int* __restrict__ flag) {
   using O = Ops<K, VAR>;
-  __shared__ double part[2][K];
+  __shared__ double den_s[2][K];
+  __shared__ double pw[2][2][K][32];  // [lo/hi][re/im][c][lane]
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int64_t i = i0 + blockIdx.x;
+  const int64_t B = (n + 1 + DK_P - 1) / DK_P;
+  const int64_t nblocks = (n + 1 + B - 1) / B;
   Cx<K, VAR> z;
   z.re = load<K>(zre, sz, i);
   z.im = load<K>(zim, sz, i);
-  Cx<K, VAR> num;
+  Cx<K, VAR> p[2];
   if (warp == 0) {
-    // ---- denominator partials u = lane (lo) and u = lane + 32 (hi)
+    // ---- denominator partials u = lane and u = lane + 32
     Cx<K, VAR> v[2] = {c_one<K, VAR>(), c_one<K, VAR>()};
     for (int64_t j0 = lane; j0 < n; j0 += DK_P) {
 #pragma unroll
@@ -230,39 +236,32 @@ __global__ void __launch_bounds__(64)
       }
     }
     const int64_t valid = n < DK_P ? n : DK_P;
-#pragma unroll
+    if (lane + 32 < valid) v[0] = c_mul_ol(v[0], v[1]);
+    const int64_t v32 = valid < 32 ? valid : 32;
+#pragma unroll 1
     for (int s = 1; s < 32; s <<= 1) {
-      Cx<K, VAR> o0 = shfl_cx(v[0], s, false), o1 = shfl_cx(v[1], s, false);
-      if ((lane & (2 * s - 1)) == 0) {
-        if (lane + s < valid) v[0] = c_mul_ol(v[0], o0);
-        if (lane + 32 + s < valid) v[1] = c_mul_ol(v[1], o1);
-      }
+      Cx<K, VAR> o = shfl_cx(v[0], s, false);
+      if ((lane & (2 * s - 1)) == 0 && lane + s < v32) v[0] = c_mul_ol(v[0], o);
     }
     if (lane == 0) {
-      Cx<K, VAR> den = (32 < valid) ? c_mul_ol(v[0], v[1]) : v[0];
 #pragma unroll
       for (int c = 0; c < K; ++c) {
-        part[0][c] = den.re.c[c];
-        part[1][c] = den.im.c[c];
+        den_s[0][c] = v[0].re.c[c];
+        den_s[1][c] = v[0].im.c[c];
       }
     }
-  } else {
-    // ---- numerator blocks u = lane (lo) and u = lane + 32 (hi)
-    const int64_t B = (n + 1 + DK_P - 1) / DK_P;
-    const int64_t nblocks = (n + 1 + B - 1) / B;
-    Cx<K, VAR> p[2];
+  } else if (warp == 1) {
+    // ---- numerator blocks u = lane and u = lane + 32 (two Horner chains)
+    const int64_t lo0 = lane * B, lo1 = (lane + 32) * B;
+    const int64_t hi0 = (lo0 + B < n + 1) ? lo0 + B : n + 1;
+    const int64_t hi1 = (lo1 + B < n + 1) ? lo1 + B : n + 1;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      const int64_t lo = (lane + 32 * h) * B;
-      const int64_t hi = (lo + B < n + 1) ? lo + B : n + 1;
+      const int64_t lo = h ? lo1 : lo0, hi = h ? hi1 : hi0;
       p[h].re = zero<K>();
       p[h].im = zero<K>();
       if (lo < hi) p[h].re = (hi - 1 == n) ? constant<K>(1.0) : load<K>(coeffs, sc, hi - 1);
     }
-    // the two Horner chains advance together (same trip count except at the tail)
-    const int64_t lo0 = lane * B, lo1 = (lane + 32) * B;
-    const int64_t hi0 = (lo0 + B < n + 1) ? lo0 + B : n + 1;
-    const int64_t hi1 = (lo1 + B < n + 1) ? lo1 + B : n + 1;
     for (int64_t d = 2; d <= B; ++d) {
       const int64_t c0 = hi0 - d, c1 = hi1 - d;
       if (c0 >= lo0) {
@@ -276,55 +275,65 @@ __global__ void __launch_bounds__(64)
         p[1].im = O::add(p[1].im, zero<K>());
       }
     }
-    // w = z^B (right-to-left square-and-multiply; uniform across lanes)
+  } else {
+    // ---- powers: w = z^B, w^32, x_l = w^l (scan), x_l * w^32
     Cx<K, VAR> w = c_one<K, VAR>(), sq = z;
     for (int64_t e = B; e > 0; e >>= 1) {
       if (e & 1) w = c_mul_ol(w, sq);
       if (e > 1) sq = c_mul_ol(sq, sq);
     }
     Cx<K, VAR> w32 = w;
-#pragma unroll
+#pragma unroll 1
     for (int r = 0; r < 5; ++r) w32 = c_mul_ol(w32, w32);
-    // x_lane = w^lane by a Hillis-Steele product scan
     Cx<K, VAR> x = lane == 0 ? c_one<K, VAR>() : w;
-#pragma unroll
+#pragma unroll 1
     for (int s = 1; s < 32; s <<= 1) {
       Cx<K, VAR> o = shfl_cx(x, s, true);
       if (lane >= s) x = c_mul_ol(x, o);
     }
-    Cx<K, VAR> t[2];
-    t[0] = c_mul_ol(p[0], x);
     Cx<K, VAR> xh = c_mul_ol(x, w32);
-    t[1] = c_mul_ol(p[1], xh);
 #pragma unroll
-    for (int s = 1; s < 32; s <<= 1) {
-      Cx<K, VAR> o0 = shfl_cx(t[0], s, false), o1 = shfl_cx(t[1], s, false);
-      if ((lane & (2 * s - 1)) == 0) {
-        if (lane + s < nblocks) {
-          t[0].re = O::add(t[0].re, o0.re);
-          t[0].im = O::add(t[0].im, o0.im);
-        }
-        if (lane + 32 + s < nblocks) {
-          t[1].re = O::add(t[1].re, o1.re);
-          t[1].im = O::add(t[1].im, o1.im);
-        }
-      }
-    }
-    num = t[0];
-    if (32 < nblocks) {
-      num.re = O::add(t[0].re, t[1].re);
-      num.im = O::add(t[0].im, t[1].im);
+    for (int c = 0; c < K; ++c) {
+      pw[0][0][c][lane] = x.re.c[c];
+      pw[0][1][c][lane] = x.im.c[c];
+      pw[1][0][c][lane] = xh.re.c[c];
+      pw[1][1][c][lane] = xh.im.c[c];
     }
   }
   __syncthreads();
-  if (warp == 1 && lane == 0) {
+  if (warp != 1) return;
+  Cx<K, VAR> t[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    Cx<K, VAR> x;
+#pragma unroll
+    for (int c = 0; c < K; ++c) {
+      x.re.c[c] = pw[h][0][c][lane];
+      x.im.c[c] = pw[h][1][c][lane];
+    }
+    t[h] = c_mul_ol(p[h], x);
+  }
+  if (lane + 32 < nblocks) {
+    t[0].re = O::add(t[0].re, t[1].re);
+    t[0].im = O::add(t[0].im, t[1].im);
+  }
+  const int64_t b32 = nblocks < 32 ? nblocks : 32;
+#pragma unroll
+  for (int s = 1; s < 32; s <<= 1) {
+    Cx<K, VAR> o = shfl_cx(t[0], s, false);
+    if ((lane & (2 * s - 1)) == 0 && lane + s < b32) {
+      t[0].re = O::add(t[0].re, o.re);
+      t[0].im = O::add(t[0].im, o.im);
+    }
+  }
+  if (lane == 0) {
     Cx<K, VAR> den;
 #pragma unroll
     for (int c = 0; c < K; ++c) {
-      den.re.c[c] = part[0][c];
-      den.im.c[c] = part[1][c];
+      den.re.c[c] = den_s[0][c];
+      den.im.c[c] = den_s[1][c];
     }
-    dk_tail<K, VAR>(num, den, z, zre_out, zim_out, so, step_mag, i);
+    dk_tail<K, VAR>(t[0], den, z, zre_out, zim_out, so, step_mag, i);
   }
 }
 
@@ -340,7 +349,7 @@ struct DkLaunch {
       dk_exact_kernel<K, VAR><<<(unsigned)blocks, 2 * DK_EXACT_ROOTS, 0, st>>>(
           coeffs, sc, n, zre, zim, sz, i0, i1, zre_out, zim_out, so, step_mag, flag);
     } else {
-      dk_tree_kernel<K, VAR><<<(unsigned)cnt, 64, 0, st>>>(
+      dk_tree_kernel<K, VAR><<<(unsigned)cnt, 96, 0, st>>>(
           coeffs, sc, n, zre, zim, sz, i0, i1, zre_out, zim_out, so, step_mag, flag);
     }
     return launch_status();
