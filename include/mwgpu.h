@@ -10,9 +10,10 @@
  *    operand starts at  base + c * plane_stride  (strides in elements).
  *    Matrices are row-major inside a plane with leading dimension ld.
  *  - k is the word count (2 = DD, 3 = TD, 4 = QD); variant is
- *    MW_VARIANT_STANDARD (0) or MW_VARIANT_BRANCH_FREE (1).  STANDARD is
- *    available for k = 2 only (dw_add_accurate / dw_mul, multiword.py:
- *    118-126, 140-145); k = 3, 4 STANDARD returns MW_ERR_UNSUPPORTED.
+ *    MW_VARIANT_STANDARD (0, the reference's default: dw_add_accurate /
+ *    dw_mul and the renormalising tw_/qw_ add/mul, multiword.py:118-145,
+ *    164-513) or MW_VARIANT_BRANCH_FREE (1, multiword.py:129-156,
+ *    361-402, 516-588).  Both exist for every k.
  *  - Pointers are caller-owned device pointers; nothing is allocated.
  *    `stream` is a cudaStream_t (NULL = legacy default stream).  Calls are
  *    asynchronous and stream-ordered; results are valid after the stream
@@ -35,7 +36,7 @@ extern "C" {
 
 #define MW_OK 0
 #define MW_ERR_INVALID -1     /* bad k / size / stride / pointer            */
-#define MW_ERR_UNSUPPORTED -2 /* (k, variant) has no device kernel          */
+#define MW_ERR_UNSUPPORTED -2 /* reserved: (k, variant) without a kernel     */
 
 #define MW_ORDER_EXACT 0 /* reference fold order: bit-exact, one thread/output */
 #define MW_ORDER_TREE 1  /* fixed split + pairwise tree: within n*2^-p bound   */
@@ -125,6 +126,18 @@ int mw_gemm(int k, int variant, const double* A, int64_t lda, int64_t sA,
 int mw_horner(int k, int variant, const double* coeffs, int64_t sc,
               int64_t degree, const double* x, int64_t sx, double* y,
               int64_t sy, int64_t npts, void* stream);
+
+/* Batched polynomial evaluation, one point per thread:
+ * method 0 = Horner, 1 = Estrin (coefficients zero-padded to a power of
+ * two, level-by-level pairwise combine, x squared between levels;
+ * poly.estrin_eval / estrin_eval_batched, poly.py:106-153).  xim == NULL:
+ * real points x (k planes, stride sx) -> y; xim != NULL: complex points
+ * (xre, xim) -> (yre, yim) with the 3M product and (a_i, 0) coefficients
+ * (poly.eval_complex, poly.py:156-178).  Bit-exact per point. */
+int mw_poly_eval(int k, int variant, const double* coeffs, int64_t sc,
+                 int64_t degree, const double* xre, const double* xim,
+                 int64_t sx, double* yre, double* yim, int64_t sy,
+                 int64_t npts, int method, void* stream);
 
 /* One Durand-Kerner sweep (roots.py:240-315) for roots i in [i0, i1) of
  * the monic degree-n polynomial z^n + sum c_j z^j.  Reads the frozen full

@@ -53,6 +53,7 @@ def lib():
         L.mwo_gemv.argtypes = [I, I, P, I64, I64, P, I64, P, I64, I64, I64, I]
         L.mwo_gemm_rows.argtypes = [I, I, P, I64, I64, P, I64, I64, P, I64, I64, I64, I64, I64, I64]
         L.mwo_horner.argtypes = [I, I, P, I64, I64, P, I64, P, I64, I64]
+        L.mwo_poly_eval.argtypes = [I, I, P, I64, I64, P, P, I64, P, P, I64, I64, I, P, I64]
         L.mwo_dk_sweep.argtypes = [I, I, P, I64, I64, P, P, I64, I64, I64, P, P, I64, P, P, I]
         L.mwo_set_threads.argtypes = [I]
         L.mwo_max_threads.restype = I
@@ -168,6 +169,33 @@ def horner(coeffs, x, variant=BRANCH_FREE) -> np.ndarray:
     y = np.zeros((k, npts))
     _check(lib().mwo_horner(k, _variant(variant), _ptr(coeffs), nc, nc - 1, _ptr(x), npts, _ptr(y), npts, npts))
     return y
+
+
+def poly_eval(coeffs, xre, xim=None, variant=BRANCH_FREE, method: str = "estrin"):
+    """Batched Horner / Estrin (poly.py:89-178) at real points (xim None)
+    or complex points; returns y or (yre, yim)."""
+    coeffs = _planes(coeffs)
+    xre = _planes(xre)
+    k, npts = xre.shape
+    deg = coeffs.shape[1] - 1
+    length = 1
+    while length < deg + 1:
+        length *= 2
+    nt = max_threads()
+    scratch = np.zeros(nt * length * 8 * 2 + 8)
+    yre = np.zeros((k, npts))
+    yim = None
+    xp = None
+    if xim is not None:
+        xim = _planes(xim)
+        yim = np.zeros((k, npts))
+        xp = _ptr(xim)
+    _check(
+        lib().mwo_poly_eval(k, _variant(variant), _ptr(coeffs), coeffs.shape[1], deg, _ptr(xre), xp, npts,
+                            _ptr(yre), None if yim is None else _ptr(yim), npts, npts,
+                            {"horner": 0, "estrin": 1}[method], _ptr(scratch), length * 2)
+    )
+    return yre if xim is None else (yre, yim)
 
 
 def dk_sweep(coeffs, zre, zim, variant=BRANCH_FREE, exact: bool = True, rows=None):

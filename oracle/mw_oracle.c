@@ -221,8 +221,187 @@ static mwv qw_mul_bf(const mwv* A, const mwv* B) {
   return r;
 }
 
+/* ------------------------- Standard TD/QD (branchy renormalisation) */
+/* multiword.py:164-188 _renorm4 */
+static void renorm4(double c0, double c1, double c2, double c3, double* r) {
+  if (isinf(c0)) {
+    r[0] = c0; r[1] = c1; r[2] = c2; r[3] = c3;
+    return;
+  }
+  double s0, s1, s2, s3;
+  quick_two_sum(c2, c3, &s0, &c3);
+  quick_two_sum(c1, s0, &s0, &c2);
+  quick_two_sum(c0, s0, &c0, &c1);
+  s0 = c0; s1 = c1; s2 = 0.0; s3 = 0.0;
+  if (s1 != 0.0) {
+    quick_two_sum(s1, c2, &s1, &s2);
+    if (s2 != 0.0) quick_two_sum(s2, c3, &s2, &s3);
+    else quick_two_sum(s1, c3, &s1, &s2);
+  } else {
+    quick_two_sum(s0, c2, &s0, &s1);
+    if (s1 != 0.0) quick_two_sum(s1, c3, &s1, &s2);
+    else quick_two_sum(s0, c3, &s0, &s1);
+  }
+  r[0] = s0; r[1] = s1; r[2] = s2; r[3] = s3;
+}
+/* multiword.py:191-194 */
+static mwv tw_renorm(double s0, double s1, double s2, double t0) {
+  double r[4];
+  renorm4(s0, s1, s2, t0, r);
+  mwv v = {{r[0], r[1], r[2], 0.0}};
+  return v;
+}
+/* multiword.py:197-241 */
+static mwv qw_renorm(double x0, double x1, double x2, double x3, double x4) {
+  mwv v;
+  if (isinf(x0)) {
+    v.c[0] = x0; v.c[1] = x1; v.c[2] = x2; v.c[3] = x3;
+    return v;
+  }
+  double s0, s1, s2, s3;
+  quick_two_sum(x3, x4, &s0, &x4);
+  quick_two_sum(x2, s0, &s0, &x3);
+  quick_two_sum(x1, s0, &s0, &x2);
+  quick_two_sum(x0, s0, &x0, &x1);
+  s0 = x0; s1 = x1; s2 = 0.0; s3 = 0.0;
+  if (s1 != 0.0) {
+    quick_two_sum(s1, x2, &s1, &s2);
+    if (s2 != 0.0) {
+      quick_two_sum(s2, x3, &s2, &s3);
+      if (s3 != 0.0) s3 = s3 + x4;
+      else quick_two_sum(s2, x4, &s2, &s3);
+    } else {
+      quick_two_sum(s1, x3, &s1, &s2);
+      if (s2 != 0.0) quick_two_sum(s2, x4, &s2, &s3);
+      else quick_two_sum(s1, x4, &s1, &s2);
+    }
+  } else {
+    quick_two_sum(s0, x2, &s0, &s1);
+    if (s1 != 0.0) {
+      quick_two_sum(s1, x3, &s1, &s2);
+      if (s2 != 0.0) quick_two_sum(s2, x4, &s2, &s3);
+      else quick_two_sum(s1, x4, &s1, &s2);
+    } else {
+      quick_two_sum(s0, x3, &s0, &s1);
+      if (s1 != 0.0) quick_two_sum(s1, x4, &s1, &s2);
+      else quick_two_sum(s0, x4, &s0, &s1);
+    }
+  }
+  v.c[0] = s0; v.c[1] = s1; v.c[2] = s2; v.c[3] = s3;
+  return v;
+}
+/* multiword.py:249-280 tw_add */
+static mwv tw_add_std(const mwv* a, const mwv* b) {
+  double s0 = a->c[0] + b->c[0], s1 = a->c[1] + b->c[1], s2 = a->c[2] + b->c[2];
+  double v0 = s0 - a->c[0], v1 = s1 - a->c[1], v2 = s2 - a->c[2];
+  double u0 = s0 - v0, u1 = s1 - v1, u2 = s2 - v2;
+  double w0 = a->c[0] - u0, w1 = a->c[1] - u1, w2 = a->c[2] - u2;
+  u0 = b->c[0] - v0; u1 = b->c[1] - v1; u2 = b->c[2] - v2;
+  double t0 = w0 + u0, t1 = w1 + u1, t2 = w2 + u2, i1, i2, i3;
+  two_sum(s1, t0, &s1, &t0);
+  two_sum(s2, t0, &i1, &i2);
+  two_sum(t1, i1, &s2, &i3);
+  two_sum(i2, i3, &t0, &t1);
+  t0 = t0 + t1 + t2;
+  return tw_renorm(s0, s1, s2, t0);
+}
+/* multiword.py:283-322 tw_mul (literal, incl. the overwritten chain) */
+static mwv tw_mul_std(const mwv* a, const mwv* b) {
+  double p0, q0, p1, q1, p2, q2, p3, q3, p4, q4, p5, q5, i1, i2, i3, s0, t0, s1, t1, s2;
+  two_prod(a->c[0], b->c[0], &p0, &q0);
+  two_prod(a->c[0], b->c[1], &p1, &q1);
+  two_prod(a->c[1], b->c[0], &p2, &q2);
+  two_prod(a->c[0], b->c[2], &p3, &q3);
+  two_prod(a->c[1], b->c[1], &p4, &q4);
+  two_prod(a->c[2], b->c[0], &p5, &q5);
+  two_sum(p1, p2, &i1, &i2);
+  two_sum(q0, i1, &p1, &i3);
+  two_sum(i2, i3, &p2, &q0);
+  two_sum(p2, q1, &i1, &i2);
+  two_sum(q2, i1, &p2, &i3);
+  two_sum(i2, i3, &q1, &q2);
+  two_sum(p3, p4, &i1, &i2);
+  two_sum(p5, i1, &p3, &i3);
+  two_sum(i2, i3, &p4, &p5);
+  two_sum(p2, p3, &s0, &t0);
+  two_sum(q1, p4, &s1, &t1);
+  s2 = q2 + p5;
+  two_sum(s1, t0, &s1, &t0);
+  s2 = s2 + (t0 + t1);
+  two_sum(q0, q3, &q0, &q3);
+  two_sum(q4, q5, &q4, &q5);
+  two_sum(q0, q4, &t0, &t1);
+  t1 = t1 + (q3 + q5);
+  two_sum(q3, s1, &t0, &t1);
+  (void)s2;
+  return tw_renorm(p0, p1, s0, t0);
+}
+/* multiword.py:410-415 _three_sum */
+static void three_sum(double* a, double* b, double* c) {
+  double t1, t2, t3;
+  two_sum(*a, *b, &t1, &t2);
+  two_sum(*c, t1, a, &t3);
+  two_sum(t2, t3, b, c);
+}
+/* multiword.py:442-487 qw_add (merge with _quick_three_accum 425-439) */
+static mwv qw_add_std(const mwv* A, const mwv* B) {
+  const double* a = A->c;
+  const double* b = B->c;
+  int i = 0, j = 0;
+  double u, v;
+  if (fabs(a[0]) > fabs(b[0])) { u = a[0]; i = 1; } else { u = b[0]; j = 1; }
+  if (fabs(a[i]) > fabs(b[j])) { v = a[i]; i++; } else { v = b[j]; j++; }
+  quick_two_sum(u, v, &u, &v);
+  double x[4] = {0.0, 0.0, 0.0, 0.0};
+  int k = 0;
+  while (k < 4) {
+    if (i >= 4 && j >= 4) {
+      x[k] = u;
+      if (k < 3) x[k + 1] = v;
+      break;
+    }
+    double t;
+    if (i >= 4) t = b[j++];
+    else if (j >= 4 || fabs(a[i]) > fabs(b[j])) t = a[i++];
+    else t = b[j++];
+    /* _quick_three_accum(u, v, t) */
+    double s, uu, vv;
+    two_sum(v, t, &s, &vv);
+    two_sum(u, s, &s, &uu);
+    int za = uu != 0.0, zb = vv != 0.0;
+    if (za && zb) { u = uu; v = vv; x[k++] = s; }
+    else if (!zb) { u = s; v = uu; }
+    else { u = s; v = vv; }
+  }
+  for (int m = i; m < 4; ++m) x[3] = x[3] + a[m];
+  for (int m = j; m < 4; ++m) x[3] = x[3] + b[m];
+  return qw_renorm(x[0], x[1], x[2], x[3], 0.0);
+}
+/* multiword.py:490-513 qw_mul */
+static mwv qw_mul_std(const mwv* A, const mwv* B) {
+  const double* a = A->c;
+  const double* b = B->c;
+  double p0, q0, p1, q1, p2, q2, p3, q3, p4, q4, p5, q5, s0, t0, s1, t1, s2;
+  two_prod(a[0], b[0], &p0, &q0);
+  two_prod(a[0], b[1], &p1, &q1);
+  two_prod(a[1], b[0], &p2, &q2);
+  two_prod(a[0], b[2], &p3, &q3);
+  two_prod(a[1], b[1], &p4, &q4);
+  two_prod(a[2], b[0], &p5, &q5);
+  three_sum(&p1, &p2, &q0);
+  three_sum(&p2, &q1, &q2);
+  three_sum(&p3, &p4, &p5);
+  two_sum(p2, p3, &s0, &t0);
+  two_sum(q1, p4, &s1, &t1);
+  s2 = q2 + p5;
+  two_sum(s1, t0, &s1, &t0);
+  s2 = s2 + (t0 + t1);
+  s1 = s1 + (a[0] * b[3] + a[1] * b[2] + a[2] * b[1] + a[3] * b[0] + q0 + q3 + q4 + q5);
+  return qw_renorm(p0, p1, s0, s1, s2);
+}
+
 /* --------------------------------------- dispatch (multiword.py:595-611,
- * batch.py:178-194).  STANDARD is restated for K=2 only. */
+ * batch.py:178-194). */
 static int pick(int k, int variant, mw_binop* add, mw_binop* mul) {
   if (variant == 1) {
     if (k == 2) { *add = dw_add_bf; *mul = dw_mul_bf; return 0; }
@@ -231,7 +410,9 @@ static int pick(int k, int variant, mw_binop* add, mw_binop* mul) {
     return -1;
   }
   if (variant == 0 && k == 2) { *add = dw_add_accurate; *mul = dw_mul_std; return 0; }
-  return variant == 0 && (k == 3 || k == 4) ? -2 : -1;
+  if (variant == 0 && k == 3) { *add = tw_add_std; *mul = tw_mul_std; return 0; }
+  if (variant == 0 && k == 4) { *add = qw_add_std; *mul = qw_mul_std; return 0; }
+  return -1;
 }
 
 static inline mwv ld(const double* p, int64_t s, int64_t i, int k) {
@@ -461,6 +642,108 @@ int mwo_horner(int k, int variant, const double* coeffs, int64_t sc, int64_t deg
       acc = add(&t, &a);
     }
     st(y, sy, p, k, &acc);
+  }
+  return 0;
+}
+
+/* --------------------------------------------------- poly.py:106-178 */
+/* multiword.cmul (683-692) / cadd (675-676) on (re, im) pairs */
+typedef struct {
+  mwv re, im;
+} cpair;
+
+static cpair p_cmul(const cpair* a, const cpair* b, int k, mw_binop add, mw_binop mul) {
+  mwv p1 = mul(&a->re, &b->re);
+  mwv p2 = mul(&a->im, &b->im);
+  mwv sa = add(&a->re, &a->im), sb = add(&b->re, &b->im);
+  mwv p3 = mul(&sa, &sb);
+  mwv np1 = mneg(&p1, k), np2 = mneg(&p2, k);
+  cpair r;
+  r.re = add(&p1, &np2);
+  mwv t = add(&p3, &np1);
+  r.im = add(&t, &np2);
+  return r;
+}
+static cpair p_cadd(const cpair* a, const cpair* b, mw_binop add) {
+  cpair r;
+  r.re = add(&a->re, &b->re);
+  r.im = add(&a->im, &b->im);
+  return r;
+}
+
+/* method 0: Horner (poly.py:89-96 real; 166-170 complex); method 1:
+ * Estrin level by level on the zero-padded power-of-two array
+ * (poly.py:106-122, 171-177).  xim == NULL: real points.
+ * scratch: padded length cpair slots. */
+int mwo_poly_eval(int k, int variant, const double* coeffs, int64_t sc, int64_t degree,
+                  const double* xre, const double* xim, int64_t sx, double* yre, double* yim,
+                  int64_t sy, int64_t npts, int method, void* scratch_all, int64_t scratch_per_thread) {
+  mw_binop add, mul;
+  int rc = pick(k, variant, &add, &mul);
+  if (rc) return rc;
+  int cplx = xim != 0;
+  int64_t length = 1;
+  while (length < degree + 1) length *= 2;
+#pragma omp parallel for schedule(static)
+  for (int64_t p = 0; p < npts; ++p) {
+#ifdef _OPENMP
+    cpair* level = (cpair*)scratch_all + (int64_t)omp_get_thread_num() * scratch_per_thread;
+#else
+    cpair* level = (cpair*)scratch_all;
+#endif
+    cpair z;
+    z.re = ld(xre, sx, p, k);
+    z.im = cplx ? ld(xim, sx, p, k) : mzero();
+    cpair r;
+    if (method == 0) {
+      if (!cplx) {
+        mwv acc = ld(coeffs, sc, degree, k);
+        for (int64_t i = degree - 1; i >= 0; --i) {
+          mwv t = mul(&acc, &z.re);
+          mwv a = ld(coeffs, sc, i, k);
+          acc = add(&t, &a);
+        }
+        r.re = acc;
+        r.im = mzero();
+      } else {
+        r.re = ld(coeffs, sc, degree, k);
+        r.im = mzero();
+        for (int64_t i = degree - 1; i >= 0; --i) {
+          cpair t = p_cmul(&r, &z, k, add, mul);
+          cpair a;
+          a.re = ld(coeffs, sc, i, k);
+          a.im = mzero();
+          r = p_cadd(&t, &a, add);
+        }
+      }
+    } else {
+      for (int64_t i = 0; i < length; ++i) {
+        level[i].re = i <= degree ? ld(coeffs, sc, i, k) : mzero();
+        level[i].im = mzero();
+      }
+      int64_t len = length;
+      while (len > 1) {
+        for (int64_t i = 0; i < len; i += 2) {
+          if (!cplx) {
+            mwv t = mul(&level[i + 1].re, &z.re);
+            level[i / 2].re = add(&level[i].re, &t);
+          } else {
+            cpair t = p_cmul(&level[i + 1], &z, k, add, mul);
+            level[i / 2] = p_cadd(&level[i], &t, add);
+          }
+        }
+        len /= 2;
+        if (len > 1) {
+          if (!cplx)
+            z.re = mul(&z.re, &z.re);
+          else
+            z = p_cmul(&z, &z, k, add, mul);
+        }
+      }
+      r = level[0];
+    }
+    st(yre, sy, p, k, &r.re);
+    if (cplx) st(yim, sy, p, k, &r.im);
   }
   return 0;
 }

@@ -11,9 +11,17 @@ the native library or a CUDA device is missing.
 from . import _lib
 from .batch import LaneBatch, batch_add, batch_div, batch_mul, batch_sub, pack, unpack
 from .blas import axpy, axpy_, dot, dot_tensor, gemv
-from .linalg import MatMulPlan, MWMatrix, Scheme, matmul
+from .linalg import CMWMatrix, MatMulPlan, MWMatrix, Scheme, cmatmul, gen_complex_test_matrices, matmul
 from .multiword import BITS, Variant, ulp_k
-from .poly import MWPolynomial, horner_eval, horner_eval_batched
+from .poly import (
+    MWPolynomial,
+    estrin_eval,
+    estrin_eval_batched,
+    eval_complex,
+    eval_complex_batched,
+    horner_eval,
+    horner_eval_batched,
+)
 from .roots import (
     CollisionError,
     MonicPoly,
@@ -32,9 +40,10 @@ __version__ = "0.1.0"
 __all__ = [
     "LaneBatch", "pack", "unpack", "batch_add", "batch_sub", "batch_mul", "batch_div",
     "dot", "dot_tensor", "axpy", "axpy_", "gemv",
-    "MatMulPlan", "MWMatrix", "Scheme", "matmul",
+    "MatMulPlan", "MWMatrix", "CMWMatrix", "Scheme", "matmul", "cmatmul", "gen_complex_test_matrices",
     "BITS", "Variant", "ulp_k",
-    "MWPolynomial", "horner_eval", "horner_eval_batched",
+    "MWPolynomial", "horner_eval", "horner_eval_batched", "estrin_eval", "estrin_eval_batched",
+    "eval_complex", "eval_complex_batched",
     "MonicPoly", "RootState", "CollisionError", "NoConvergence", "aberth_init", "radius_estimate",
     "default_tolerance", "dk_iterate", "dk_sweeps", "dk_solve",
 ]

@@ -47,6 +47,7 @@ _SIGS = {
     "mw_gemv": ([I, I, P, I64, I64, P, I64, P, I64, I64, I64, I, P], I),
     "mw_gemm": ([I, I, P, I64, I64, P, I64, I64, P, I64, I64, I64, I64, I64, P], I),
     "mw_horner": ([I, I, P, I64, I64, P, I64, P, I64, I64, P], I),
+    "mw_poly_eval": ([I, I, P, I64, I64, P, P, I64, P, P, I64, I64, I, P], I),
     "mw_dk_sweep": ([I, I, P, I64, I64, P, P, I64, I64, I64, P, P, I64, P, P, I, P], I),
     "mw_fp64_peak_kernel": ([I, I, I, I, P, P], I),
     "mw_device_sm_count": ([], I),
@@ -89,8 +90,7 @@ def check(rc: int, what: str):
         return
     if rc == MW_ERR_UNSUPPORTED:
         raise NotImplementedError(
-            f"{what}: no device kernel for this (k, variant); the B200 path implements "
-            "BRANCH_FREE for K=2,3,4 and STANDARD for K=2 (no CPU fallback)"
+            f"{what}: no device kernel for this (k, variant) (no CPU fallback)"
         )
     if rc == MW_ERR_INVALID:
         raise ValueError(f"{what}: invalid arguments")

@@ -19,7 +19,7 @@ inline int launch_status() {
   return e == cudaSuccess ? MW_OK : static_cast<int>(e);
 }
 
-// (k, variant) -> F<K, VAR>::run(args...).  STANDARD exists for k = 2 only.
+// (k, variant) -> F<K, VAR>::run(args...) for k = 2, 3, 4 and both variants.
 template <template <int, int> class F, typename... Args>
 int dispatch(int k, int variant, Args... args) {
   if (variant == BRANCH_FREE) {
@@ -31,8 +31,12 @@ int dispatch(int k, int variant, Args... args) {
     }
   }
   if (variant == STANDARD) {
-    if (k == 2) return F<2, STANDARD>::run(args...);
-    if (k == 3 || k == 4) return MW_ERR_UNSUPPORTED;
+    switch (k) {
+      case 2: return F<2, STANDARD>::run(args...);
+      case 3: return F<3, STANDARD>::run(args...);
+      case 4: return F<4, STANDARD>::run(args...);
+      default: return MW_ERR_INVALID;
+    }
   }
   return MW_ERR_INVALID;
 }

@@ -365,7 +365,6 @@ extern "C" int mw_dk_sweep(int k, int variant, const double* coeffs, int64_t sc,
                            int64_t i1, double* zre_out, double* zim_out, int64_t so,
                            double* step_mag, int* flag_dev, int exact_order, void* stream) {
   if (k < 2 || k > 4) return MW_ERR_INVALID;
-  if (variant == 0 && k != 2) return MW_ERR_UNSUPPORTED;
   if (variant != 0 && variant != 1) return MW_ERR_INVALID;
   if (n < 1 || i0 < 0 || i1 < i0 || i1 > n) return MW_ERR_INVALID;
   if (i1 == i0) return MW_OK;

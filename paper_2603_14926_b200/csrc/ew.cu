@@ -125,8 +125,7 @@ using namespace mw;
                       int64_t sb, double* out, int64_t so, int64_t n, void* stream) {     \
     int chk = ew_check(k, a, sa, b, sb, out, so, n);                                       \
     if (chk <= 0) {                                                                        \
-      if (chk == MW_OK && (variant == 1 || (variant == 0 && k == 2))) return MW_OK;        \
-      if (chk == MW_OK) return (variant == 0) ? MW_ERR_UNSUPPORTED : MW_ERR_INVALID;       \
+      if (chk == MW_OK) return (variant == 0 || variant == 1) ? MW_OK : MW_ERR_INVALID;    \
       return chk;                                                                          \
     }                                                                                      \
     return dispatch<FUNCTOR>(k, variant, a, sa, b, sb, out, so, n, (const double*)nullptr, \
@@ -142,8 +141,7 @@ extern "C" int mw_axpy(int k, int variant, const double* alpha_host, const doubl
                        int64_t sx, double* y, int64_t sy, int64_t n, void* stream) {
   int chk = ew_check(k, x, sx, y, sy, y, sy, n);
   if (chk <= 0) {
-    if (chk == MW_OK && (variant == 1 || (variant == 0 && k == 2))) return MW_OK;
-    if (chk == MW_OK) return (variant == 0) ? MW_ERR_UNSUPPORTED : MW_ERR_INVALID;
+    if (chk == MW_OK) return (variant == 0 || variant == 1) ? MW_OK : MW_ERR_INVALID;
     return chk;
   }
   if (!alpha_host) return MW_ERR_INVALID;

@@ -189,7 +189,6 @@ extern "C" int mw_gemm(int k, int variant, const double* A, int64_t lda, int64_t
                        const double* B, int64_t ldb, int64_t sB, double* C, int64_t ldc,
                        int64_t sC, int64_t m, int64_t n, int64_t kd, void* stream) {
   if (k < 2 || k > 4) return MW_ERR_INVALID;
-  if (variant == 0 && k != 2) return MW_ERR_UNSUPPORTED;
   if (variant != 0 && variant != 1) return MW_ERR_INVALID;
   if (m < 0 || n < 0 || kd < 0) return MW_ERR_INVALID;
   if (m == 0 || n == 0) return MW_OK;

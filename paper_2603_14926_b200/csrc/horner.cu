@@ -90,7 +90,6 @@ extern "C" int mw_horner(int k, int variant, const double* coeffs, int64_t sc, i
                          const double* x, int64_t sx, double* y, int64_t sy, int64_t npts,
                          void* stream) {
   if (k < 2 || k > 4) return MW_ERR_INVALID;
-  if (variant == 0 && k != 2) return MW_ERR_UNSUPPORTED;
   if (variant != 0 && variant != 1) return MW_ERR_INVALID;
   if (degree < 0 || npts < 0) return MW_ERR_INVALID;
   if (npts == 0) return MW_OK;

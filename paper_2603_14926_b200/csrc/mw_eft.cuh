@@ -16,6 +16,8 @@
 //   td_mul_bf  multiword.py:381-402 (paper Alg 12)
 //   qd_add_bf  multiword.py:516-545 (paper Alg 13)
 //   qd_mul_bf  multiword.py:548-588 (paper Alg 14)
+// and the conventional (Standard) TD/QD kernels with their branchy
+// renormalisation (multiword.py:164-241, 249-322, 410-513).
 // Operand order inside each two_sum/quick_two_sum matters for bit
 // equality and is kept as written there.
 #pragma once
@@ -231,10 +233,272 @@ MW_HD V<4> qd_mul_bf(const V<4>& A, const V<4>& B) {
   return r;
 }
 
+// ------------------------------------------- Standard (renormalising) TD/QD
+// The reference's conventional kernels, branches and all: a branch-free
+// core followed by a value-dependent renormalisation (multiword.py:
+// 164-241 _renorm4 / tw_renormalize / qw_renormalize, 249-322 tw_add /
+// tw_mul, 410-513 qw_add / qw_mul).  On the GPU each lane simply takes its
+// own path (warp divergence is the cost the branch-free variants remove).
+MW_HD bool mw_isinf(double x) {
+#if defined(__CUDA_ARCH__)
+  return isinf(x);
+#else
+  return std::isinf(x);
+#endif
+}
+
+// multiword.py:164-188
+MW_HD void renorm4(double c0, double c1, double c2, double c3, double& s0, double& s1, double& s2,
+                   double& s3) {
+  if (mw_isinf(c0)) {
+    s0 = c0;
+    s1 = c1;
+    s2 = c2;
+    s3 = c3;
+    return;
+  }
+  double t;
+  quick_two_sum(c2, c3, t, c3);
+  quick_two_sum(c1, t, t, c2);
+  quick_two_sum(c0, t, c0, c1);
+  s0 = c0;
+  s1 = c1;
+  s2 = 0.0;
+  s3 = 0.0;
+  if (s1 != 0.0) {
+    quick_two_sum(s1, c2, s1, s2);
+    if (s2 != 0.0)
+      quick_two_sum(s2, c3, s2, s3);
+    else
+      quick_two_sum(s1, c3, s1, s2);
+  } else {
+    quick_two_sum(s0, c2, s0, s1);
+    if (s1 != 0.0)
+      quick_two_sum(s1, c3, s1, s2);
+    else
+      quick_two_sum(s0, c3, s0, s1);
+  }
+}
+
+// multiword.py:191-194
+MW_HD V<3> tw_renormalize(double s0, double s1, double s2, double t0) {
+  V<3> r;
+  double unused;
+  renorm4(s0, s1, s2, t0, r.c[0], r.c[1], r.c[2], unused);
+  return r;
+}
+
+// multiword.py:197-241
+MW_HD V<4> qw_renormalize(double x0, double x1, double x2, double x3, double x4) {
+  V<4> r;
+  if (mw_isinf(x0)) {
+    r.c[0] = x0;
+    r.c[1] = x1;
+    r.c[2] = x2;
+    r.c[3] = x3;
+    return r;
+  }
+  double s0, s1, s2, s3;
+  quick_two_sum(x3, x4, s0, x4);
+  quick_two_sum(x2, s0, s0, x3);
+  quick_two_sum(x1, s0, s0, x2);
+  quick_two_sum(x0, s0, x0, x1);
+  s0 = x0;
+  s1 = x1;
+  s2 = 0.0;
+  s3 = 0.0;
+  if (s1 != 0.0) {
+    quick_two_sum(s1, x2, s1, s2);
+    if (s2 != 0.0) {
+      quick_two_sum(s2, x3, s2, s3);
+      if (s3 != 0.0)
+        s3 = MW_ADD(s3, x4);
+      else
+        quick_two_sum(s2, x4, s2, s3);
+    } else {
+      quick_two_sum(s1, x3, s1, s2);
+      if (s2 != 0.0)
+        quick_two_sum(s2, x4, s2, s3);
+      else
+        quick_two_sum(s1, x4, s1, s2);
+    }
+  } else {
+    quick_two_sum(s0, x2, s0, s1);
+    if (s1 != 0.0) {
+      quick_two_sum(s1, x3, s1, s2);
+      if (s2 != 0.0)
+        quick_two_sum(s2, x4, s2, s3);
+      else
+        quick_two_sum(s1, x4, s1, s2);
+    } else {
+      quick_two_sum(s0, x3, s0, s1);
+      if (s1 != 0.0)
+        quick_two_sum(s1, x4, s1, s2);
+      else
+        quick_two_sum(s0, x4, s0, s1);
+    }
+  }
+  r.c[0] = s0;
+  r.c[1] = s1;
+  r.c[2] = s2;
+  r.c[3] = s3;
+  return r;
+}
+
+// multiword.py:249-280 tw_add = tw_renormalize(_tw_add_core)
+MW_HD V<3> tw_add_std(const V<3>& a, const V<3>& b) {
+  double s0 = MW_ADD(a.c[0], b.c[0]), s1 = MW_ADD(a.c[1], b.c[1]), s2 = MW_ADD(a.c[2], b.c[2]);
+  double v0 = MW_SUB(s0, a.c[0]), v1 = MW_SUB(s1, a.c[1]), v2 = MW_SUB(s2, a.c[2]);
+  double u0 = MW_SUB(s0, v0), u1 = MW_SUB(s1, v1), u2 = MW_SUB(s2, v2);
+  double w0 = MW_SUB(a.c[0], u0), w1 = MW_SUB(a.c[1], u1), w2 = MW_SUB(a.c[2], u2);
+  u0 = MW_SUB(b.c[0], v0);
+  u1 = MW_SUB(b.c[1], v1);
+  u2 = MW_SUB(b.c[2], v2);
+  double t0 = MW_ADD(w0, u0), t1 = MW_ADD(w1, u1), t2 = MW_ADD(w2, u2);
+  double i1, i2, i3;
+  two_sum(s1, t0, s1, t0);
+  two_sum(s2, t0, i1, i2);
+  two_sum(t1, i1, s2, i3);
+  two_sum(i2, i3, t0, t1);
+  t0 = MW_ADD(MW_ADD(t0, t1), t2);
+  return tw_renormalize(s0, s1, s2, t0);
+}
+
+// multiword.py:283-322 tw_mul = tw_renormalize(_tw_mul_core), literal
+// transcription including the overwritten error chain.
+MW_HD V<3> tw_mul_std(const V<3>& a, const V<3>& b) {
+  double p0, q0, p1, q1, p2, q2, p3, q3, p4, q4, p5, q5, i1, i2, i3, s0, t0, s1, t1;
+  two_prod(a.c[0], b.c[0], p0, q0);
+  two_prod(a.c[0], b.c[1], p1, q1);
+  two_prod(a.c[1], b.c[0], p2, q2);
+  two_prod(a.c[0], b.c[2], p3, q3);
+  two_prod(a.c[1], b.c[1], p4, q4);
+  two_prod(a.c[2], b.c[0], p5, q5);
+  two_sum(p1, p2, i1, i2);
+  two_sum(q0, i1, p1, i3);
+  two_sum(i2, i3, p2, q0);
+  two_sum(p2, q1, i1, i2);
+  two_sum(q2, i1, p2, i3);
+  two_sum(i2, i3, q1, q2);
+  two_sum(p3, p4, i1, i2);
+  two_sum(p5, i1, p3, i3);
+  two_sum(i2, i3, p4, p5);
+  two_sum(p2, p3, s0, t0);
+  two_sum(q1, p4, s1, t1);
+  double s2 = MW_ADD(q2, p5);
+  two_sum(s1, t0, s1, t0);
+  s2 = MW_ADD(s2, MW_ADD(t0, t1));
+  two_sum(q0, q3, q0, q3);
+  two_sum(q4, q5, q4, q5);
+  two_sum(q0, q4, t0, t1);
+  t1 = MW_ADD(t1, MW_ADD(q3, q5));
+  two_sum(q3, s1, t0, t1);
+  (void)s2;
+  return tw_renormalize(p0, p1, s0, t0);
+}
+
+// multiword.py:410-415 _three_sum
+MW_HD void three_sum(double& a, double& b, double& c) {
+  double t1, t2, t3;
+  two_sum(a, b, t1, t2);
+  two_sum(c, t1, a, t3);
+  two_sum(t2, t3, b, c);
+}
+
+// multiword.py:425-439 _quick_three_accum; returns true when s is emitted
+MW_HD bool quick_three_accum(double& u, double& v, double t, double& s) {
+  two_sum(v, t, s, v);
+  two_sum(u, s, s, u);
+  const bool za = u != 0.0, zb = v != 0.0;
+  if (za && zb) return true;
+  if (!zb) {
+    v = u;
+    u = s;
+    return false;
+  }
+  u = s;
+  return false;
+}
+
+// multiword.py:442-487 qw_add (magnitude merge) + qw_renormalize
+MW_HD V<4> qw_add_std(const V<4>& a, const V<4>& b) {
+  int i = 0, j = 0;
+  double u, v;
+  if (fabs(a.c[0]) > fabs(b.c[0])) {
+    u = a.c[0];
+    i = 1;
+  } else {
+    u = b.c[0];
+    j = 1;
+  }
+  if (fabs(a.c[i]) > fabs(b.c[j])) {
+    v = a.c[i];
+    ++i;
+  } else {
+    v = b.c[j];
+    ++j;
+  }
+  quick_two_sum(u, v, u, v);
+  double x[4] = {0.0, 0.0, 0.0, 0.0};
+  int k = 0;
+  while (k < 4) {
+    if (i >= 4 && j >= 4) {
+      x[k] = u;
+      if (k < 3) x[k + 1] = v;
+      break;
+    }
+    double t;
+    if (i >= 4) {
+      t = b.c[j];
+      ++j;
+    } else if (j >= 4 || fabs(a.c[i]) > fabs(b.c[j])) {
+      t = a.c[i];
+      ++i;
+    } else {
+      t = b.c[j];
+      ++j;
+    }
+    double s;
+    if (quick_three_accum(u, v, t, s)) {
+      x[k] = s;
+      ++k;
+    }
+  }
+  for (int m = i; m < 4; ++m) x[3] = MW_ADD(x[3], a.c[m]);
+  for (int m = j; m < 4; ++m) x[3] = MW_ADD(x[3], b.c[m]);
+  return qw_renormalize(x[0], x[1], x[2], x[3], 0.0);
+}
+
+// multiword.py:490-513 qw_mul = qw_renormalize(_qw_mul_core)
+MW_HD V<4> qw_mul_std(const V<4>& a, const V<4>& b) {
+  double p0, q0, p1, q1, p2, q2, p3, q3, p4, q4, p5, q5, s0, t0, s1, t1;
+  two_prod(a.c[0], b.c[0], p0, q0);
+  two_prod(a.c[0], b.c[1], p1, q1);
+  two_prod(a.c[1], b.c[0], p2, q2);
+  two_prod(a.c[0], b.c[2], p3, q3);
+  two_prod(a.c[1], b.c[1], p4, q4);
+  two_prod(a.c[2], b.c[0], p5, q5);
+  three_sum(p1, p2, q0);
+  three_sum(p2, q1, q2);
+  three_sum(p3, p4, p5);
+  two_sum(p2, p3, s0, t0);
+  two_sum(q1, p4, s1, t1);
+  double s2 = MW_ADD(q2, p5);
+  two_sum(s1, t0, s1, t0);
+  s2 = MW_ADD(s2, MW_ADD(t0, t1));
+  double acc = MW_ADD(MW_MUL(a.c[0], b.c[3]), MW_MUL(a.c[1], b.c[2]));
+  acc = MW_ADD(acc, MW_MUL(a.c[2], b.c[1]));
+  acc = MW_ADD(acc, MW_MUL(a.c[3], b.c[0]));
+  acc = MW_ADD(acc, q0);
+  acc = MW_ADD(acc, q3);
+  acc = MW_ADD(acc, q4);
+  acc = MW_ADD(acc, q5);
+  s1 = MW_ADD(s1, acc);
+  return qw_renormalize(p0, p1, s0, s1, s2);
+}
+
 // ------------------------------------------------------ (K, Variant) ops
 // Mirrors the dispatch tables _BATCH_ADD/_BATCH_MUL (batch.py:178-194).
-// STANDARD exists on the device for K=2 only (dw_add_accurate / dw_mul);
-// the C-ABI rejects STANDARD for K=3,4 before any launch.
 template <int K, int VAR>
 struct Ops;
 
@@ -252,6 +516,16 @@ template <>
 struct Ops<3, BRANCH_FREE> {
   static MW_HD V<3> add(const V<3>& a, const V<3>& b) { return td_add_bf(a, b); }
   static MW_HD V<3> mul(const V<3>& a, const V<3>& b) { return td_mul_bf(a, b); }
+};
+template <>
+struct Ops<3, STANDARD> {
+  static MW_HD V<3> add(const V<3>& a, const V<3>& b) { return tw_add_std(a, b); }
+  static MW_HD V<3> mul(const V<3>& a, const V<3>& b) { return tw_mul_std(a, b); }
+};
+template <>
+struct Ops<4, STANDARD> {
+  static MW_HD V<4> add(const V<4>& a, const V<4>& b) { return qw_add_std(a, b); }
+  static MW_HD V<4> mul(const V<4>& a, const V<4>& b) { return qw_mul_std(a, b); }
 };
 template <>
 struct Ops<4, BRANCH_FREE> {

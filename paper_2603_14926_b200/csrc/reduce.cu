@@ -286,8 +286,7 @@ using namespace mw;
 
 static int variant_ok(int k, int variant) {
   if (k < 2 || k > 4) return MW_ERR_INVALID;
-  if (variant == 1 || (variant == 0 && k == 2)) return MW_OK;
-  return variant == 0 ? MW_ERR_UNSUPPORTED : MW_ERR_INVALID;
+  return (variant == 0 || variant == 1) ? MW_OK : MW_ERR_INVALID;
 }
 
 extern "C" int64_t mw_dot_workspace(int k, int64_t n) {

@@ -28,7 +28,8 @@ from . import _lib
 from .batch import LaneBatch, as_planes
 from .multiword import BITS, Variant, variant_code
 
-__all__ = ["Scheme", "MatMulPlan", "MWMatrix", "matmul", "gemv"]
+__all__ = ["Scheme", "MatMulPlan", "MWMatrix", "CMWMatrix", "matmul", "cmatmul", "gemv",
+           "gen_complex_test_matrices"]
 
 
 class Scheme(enum.Enum):
@@ -123,6 +124,100 @@ class MWMatrix:
 
     def __repr__(self):
         return f"MWMatrix(k={self.k}, rows={self.rows}, cols={self.cols}, device={self.device})"
+
+
+class CMWMatrix:
+    """Complex matrix as a (re, im) pair of equally shaped MWMatrix
+    (linalg.py:161-193)."""
+
+    __slots__ = ("re", "im")
+
+    def __init__(self, re: MWMatrix, im: MWMatrix):
+        if (re.rows, re.cols, re.k) != (im.rows, im.cols, im.k):
+            raise ValueError("re/im shape mismatch")
+        self.re = re
+        self.im = im
+
+    @property
+    def rows(self):
+        return self.re.rows
+
+    @property
+    def cols(self):
+        return self.re.cols
+
+    @property
+    def k(self):
+        return self.re.k
+
+    def bitwise_equal(self, other: "CMWMatrix") -> bool:
+        return self.re.bitwise_equal(other.re) and self.im.bitwise_equal(other.im)
+
+    def __repr__(self):
+        return f"CMWMatrix(k={self.k}, rows={self.rows}, cols={self.cols})"
+
+
+def gen_complex_test_matrices(n: int, seed: int, k: int, device=None):
+    """The reference's random complex pair (linalg.py:247-276): per matrix
+    u1, u2 ~ U[0,1) (n^2 each) for Box-Muller normals r = sqrt(-2 ln(1-u1))
+    (cos, sin)(2 pi u2), then U[0,1) factors for re and im; entries
+    exp(r) (u - 1/2) promoted exactly to K words.  Host numpy, seeded
+    PCG64, identical draws to the reference."""
+    if n < 1:
+        raise ValueError("n must be >= 1")
+    rng = np.random.Generator(np.random.PCG64(seed))
+
+    def one_matrix():
+        u1 = rng.random((n, n))
+        u2 = rng.random((n, n))
+        radial = np.sqrt(-2.0 * np.log1p(-u1))
+        rn_re = radial * np.cos(2.0 * np.pi * u2)
+        rn_im = radial * np.sin(2.0 * np.pi * u2)
+        ure = rng.random((n, n))
+        uim = rng.random((n, n))
+        re0 = np.exp(rn_re) * (ure - 0.5)
+        im0 = np.exp(rn_im) * (uim - 0.5)
+        re = np.zeros((k, n, n))
+        im = np.zeros((k, n, n))
+        re[0] = re0
+        im[0] = im0
+        return CMWMatrix(MWMatrix(re, device=device), MWMatrix(im, device=device))
+
+    return one_matrix(), one_matrix()
+
+
+def _ew(name: str, a: torch.Tensor, b: torch.Tensor, variant) -> torch.Tensor:
+    """Lane-wise K-word op over two equally shaped planes tensors."""
+    k = a.shape[0]
+    n = a[0].numel()
+    out = torch.empty_like(a)
+    rc = getattr(_lib.load(), name)(k, variant_code(variant), a.data_ptr(), n, b.data_ptr(), n, out.data_ptr(), n, n,
+                                    _lib.stream_handle(a.device))
+    _lib.check(rc, name)
+    return out
+
+
+def cmatmul(a: CMWMatrix, b: CMWMatrix, plan: MatMulPlan | None = None) -> CMWMatrix:
+    """Complex product via three real multiplications (linalg.py:572-590):
+    P1 = Re(a) Re(b), P2 = Im(a) Im(b), P3 = (Re+Im)(a) (Re+Im)(b);
+    Re = P1 - P2, Im = (P3 - P1) - P2 -- the same kernels and order as the
+    reference, so bit-exact with cmatmul(..., naive)."""
+    if plan is None:
+        plan = MatMulPlan()
+    if a.cols != b.rows:
+        raise ValueError("shape mismatch")
+    if a.k != b.k:
+        raise ValueError("mixed word counts")
+    v = plan.variant
+    _lib.require_cuda(a.re.planes, b.re.planes)
+    sum_a = MWMatrix(_ew("mw_ew_add", a.re.planes, a.im.planes, v))
+    sum_b = MWMatrix(_ew("mw_ew_add", b.re.planes, b.im.planes, v))
+    p1 = matmul(a.re, b.re, plan).planes
+    p2 = matmul(a.im, b.im, plan).planes
+    p3 = matmul(sum_a, sum_b, plan).planes
+    re = _ew("mw_ew_sub", p1, p2, v)
+    im = _ew("mw_ew_sub", _ew("mw_ew_sub", p3, p1, v), p2, v)
+    return CMWMatrix(MWMatrix(re), MWMatrix(im))
 
 
 def gemm_into(a: torch.Tensor, b: torch.Tensor, c: torch.Tensor, variant, row0: int = 0,

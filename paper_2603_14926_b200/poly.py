@@ -1,4 +1,5 @@
-"""Real-coefficient polynomial evaluation on the GPU (Horner).
+"""Real-coefficient polynomial evaluation on the GPU (Horner, Estrin,
+complex points).
 
 Drop-in for the Horner path of mwfloat.poly (pkg/src/mwfloat/poly.py):
 ``MWPolynomial`` (40-86) keeps coefficients a[0..n] (a[i] multiplies x^i)
@@ -6,7 +7,10 @@ as a (K, n+1) float64 CUDA tensor; ``horner_eval(p, x, variant)`` (89-96)
 keeps its signature and returns the K-word tuple; the batched form
 ``horner_eval_batched(p, xs: LaneBatch, variant)`` (the name pattern of
 estrin_eval_batched, 125-153) evaluates every lane with the same op
-sequence in one mw_horner launch -- bit-exact per point.
+sequence in one mw_horner launch -- bit-exact per point.  ``estrin_eval``
+/ ``estrin_eval_batched`` (106-153) and ``eval_complex`` (156-178, Horner
+or Estrin with the 3M complex product) run through mw_poly_eval, also
+bit-exact per point; ``eval_complex_batched`` is the lane-batched form.
 """
 
 from __future__ import annotations
@@ -18,7 +22,19 @@ from . import _lib
 from .batch import LaneBatch, as_planes
 from .multiword import BITS, Variant, from_basefloat, variant_code
 
-__all__ = ["MWPolynomial", "horner_eval", "horner_eval_batched", "horner_into", "random_polynomial"]
+__all__ = [
+    "MWPolynomial",
+    "horner_eval",
+    "horner_eval_batched",
+    "horner_into",
+    "estrin_eval",
+    "estrin_eval_batched",
+    "eval_complex",
+    "eval_complex_batched",
+    "random_polynomial",
+]
+
+_METHODS = {"horner": 0, "estrin": 1}
 
 
 class MWPolynomial:
@@ -110,6 +126,65 @@ def horner_eval(p: MWPolynomial, x, variant: Variant = Variant.STANDARD) -> tupl
         raise ValueError("mixed word counts")
     xs = LaneBatch(np.array(x, dtype=np.float64).reshape(p.k, 1), device=p.device)
     return horner_eval_batched(p, xs, variant).lane(0)
+
+
+def _poly_eval(p: MWPolynomial, xre: torch.Tensor, xim, variant, method: str):
+    if method not in _METHODS:
+        raise ValueError(f"unknown method {method!r}")
+    _lib.require_cuda(p.planes, xre)
+    k, npts = xre.shape
+    yre = torch.empty_like(xre)
+    yim = torch.empty_like(xim) if xim is not None else None
+    rc = _lib.load().mw_poly_eval(
+        k, variant_code(variant), p.planes.data_ptr(), p.planes.shape[1], p.degree,
+        xre.data_ptr(), None if xim is None else xim.data_ptr(), npts,
+        yre.data_ptr(), None if yim is None else yim.data_ptr(), npts, npts, _METHODS[method],
+        _lib.stream_handle(xre.device),
+    )
+    _lib.check(rc, "mw_poly_eval")
+    return yre, yim
+
+
+def estrin_eval_batched(p: MWPolynomial, xs: LaneBatch, variant: Variant = Variant.STANDARD) -> LaneBatch:
+    """Per-lane bitwise equal to estrin_eval at each lane's point
+    (poly.py:125-153)."""
+    if xs.k != p.k:
+        raise ValueError("mixed word counts")
+    y, _ = _poly_eval(p, xs.planes, None, variant, "estrin")
+    return LaneBatch(y, count=xs.count)
+
+
+def estrin_eval(p: MWPolynomial, x, variant: Variant = Variant.STANDARD) -> tuple:
+    """Pairwise combine a[2i] + a[2i+1] * x, square x, repeat (poly.py:106-122)."""
+    x = tuple(float(c) for c in getattr(x, "comps", x))
+    if len(x) != p.k:
+        raise ValueError("mixed word counts")
+    xs = LaneBatch(np.array(x, dtype=np.float64).reshape(p.k, 1), device=p.device)
+    return estrin_eval_batched(p, xs, variant).lane(0)
+
+
+def eval_complex_batched(p: MWPolynomial, zre: LaneBatch, zim: LaneBatch, method: str = "horner",
+                         variant: Variant = Variant.STANDARD):
+    """Evaluate at complex points (zre + i zim) lane-wise with the 3M
+    complex product; returns (re, im) batches (poly.py:156-178 per lane)."""
+    if zre.k != p.k or zim.k != p.k:
+        raise ValueError("mixed word counts")
+    if zre.width != zim.width:
+        raise ValueError("mixed lane widths")
+    yre, yim = _poly_eval(p, zre.planes, zim.planes, variant, method)
+    return LaneBatch(yre, count=zre.count), LaneBatch(yim, count=zre.count)
+
+
+def eval_complex(p: MWPolynomial, z, method: str = "horner", variant: Variant = Variant.STANDARD):
+    """Evaluate at one complex point z = (re, im) of K-word tuples."""
+    re = tuple(float(c) for c in z[0])
+    im = tuple(float(c) for c in z[1])
+    if len(re) != p.k or len(im) != p.k:
+        raise ValueError("mixed word counts")
+    a = LaneBatch(np.array(re).reshape(p.k, 1), device=p.device)
+    b = LaneBatch(np.array(im).reshape(p.k, 1), device=p.device)
+    yr, yi = eval_complex_batched(p, a, b, method, variant)
+    return yr.lane(0), yi.lane(0)
 
 
 def random_polynomial(n: int, seed: int, k: int, device=None) -> MWPolynomial:

@@ -20,6 +20,9 @@ public functions on small seeded cases:
               degree-512 problem expanded with Fractions +
               from_oracle, one sweep from the near-root start and one from
               the R0 = 1.5 Aberth circle                     (roots.py:188-315)
+  cgemm.npz   cmatmul (3M) on gen_complex_test_matrices     (linalg.py:247-276, 572-590)
+  polyx.npz   estrin_eval per point (== estrin_eval_batched) and
+              eval_complex Horner / Estrin                   (poly.py:106-178)
 
 Every array is stored component-planar (K x ...).  The fixtures are small
 (< 1 MB total) and committed; tests/test_oracle_golden.py pins the C
@@ -71,6 +74,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--ref", default=None, help="path containing the built mwfloat package")
     ap.add_argument("--skip-dk512", action="store_true")
+    ap.add_argument("--only", default="", help="comma list of fixture names to (re)generate")
     args = ap.parse_args()
     sys.path.insert(0, args.ref or build_reference())
     import mwfloat
@@ -79,9 +83,14 @@ def main():
     from mwfloat.oracle import BigFloat, oracle_cos, oracle_pi, oracle_sin
 
     BF, STD = Variant.BRANCH_FREE, Variant.STANDARD
-    cases = [(2, BF), (3, BF), (4, BF), (2, STD)]
+    cases = [(2, BF), (3, BF), (4, BF), (2, STD), (3, STD), (4, STD)]
     tag = {BF: "bf", STD: "std"}
     t0 = time.time()
+
+    only = set(filter(None, args.only.split(",")))
+
+    def want(name):
+        return not only or name in only
 
     # ------------------------------------------------------------- ew
     out = {}
@@ -113,7 +122,8 @@ def main():
             sb = tuple(float(c) for c in b[:, lane])
             assert multiword.mw_add(sa, sb, v) == tuple(out[p + "_add"][:, lane])
             assert multiword.mw_mul(sa, sb, v) == tuple(out[p + "_mul"][:, lane])
-    np.savez_compressed(os.path.join(HERE, "ew.npz"), **out)
+    if want("ew"):
+        np.savez_compressed(os.path.join(HERE, "ew.npz"), **out)
     print(f"ew done {time.time() - t0:.1f}s")
 
     # ------------------------------------------------------------- dot
@@ -136,7 +146,8 @@ def main():
         out[p + "_x"] = x
         out[p + "_y"] = y
         out[p + "_out"] = np.array(acc)
-    np.savez_compressed(os.path.join(HERE, "dot.npz"), **out)
+    if want("dot"):
+        np.savez_compressed(os.path.join(HERE, "dot.npz"), **out)
 
     # ------------------------------------------------------------- axpy
     out = {}
@@ -154,7 +165,8 @@ def main():
         out[p + "_x"] = x
         out[p + "_y"] = y
         out[p + "_out"] = np.stack(r.comps)
-    np.savez_compressed(os.path.join(HERE, "axpy.npz"), **out)
+    if want("axpy"):
+        np.savez_compressed(os.path.join(HERE, "axpy.npz"), **out)
     print(f"dot/axpy done {time.time() - t0:.1f}s")
 
     # ------------------------------------------------------------- gemv
@@ -173,7 +185,8 @@ def main():
         out[p + "_a"] = a
         out[p + "_x"] = x
         out[p + "_out"] = np.stack([c[:, 0] for c in r.comps])
-    np.savez_compressed(os.path.join(HERE, "gemv.npz"), **out)
+    if want("gemv"):
+        np.savez_compressed(os.path.join(HERE, "gemv.npz"), **out)
 
     # ------------------------------------------------------------- gemm
     out = {}
@@ -190,12 +203,14 @@ def main():
         out[p + "_a"] = a
         out[p + "_b"] = b
         out[p + "_out"] = np.stack(r.comps)
-    np.savez_compressed(os.path.join(HERE, "gemm.npz"), **out)
+    if want("gemm"):
+        np.savez_compressed(os.path.join(HERE, "gemm.npz"), **out)
     print(f"gemv/gemm done {time.time() - t0:.1f}s")
 
     # ------------------------------------------------------------- horner
     out = {}
-    for k, v, deg, npts in [(4, BF, 1024, 24), (3, BF, 100, 40), (2, BF, 100, 40), (2, STD, 100, 40)]:
+    for k, v, deg, npts in [(4, BF, 1024, 24), (3, BF, 100, 40), (2, BF, 100, 40), (2, STD, 100, 40),
+                            (3, STD, 100, 40), (4, STD, 200, 24)]:
         coeffs, x = gen.config4_horner(npts=npts, degree=deg, k=k, seed=500 + k)
         # half the points carry full K-word values
         rng = np.random.default_rng(550 + k)
@@ -208,7 +223,8 @@ def main():
         out[p + "_coeffs"] = coeffs
         out[p + "_x"] = x
         out[p + "_out"] = y
-    np.savez_compressed(os.path.join(HERE, "horner.npz"), **out)
+    if want("horner"):
+        np.savez_compressed(os.path.join(HERE, "horner.npz"), **out)
     print(f"horner done {time.time() - t0:.1f}s")
 
     # ------------------------------------------------------------- dk
@@ -224,7 +240,7 @@ def main():
         out[p + "_new_re"] = np.stack(nxt.re)
         out[p + "_new_im"] = np.stack(nxt.im)
         out[p + "_maxupd"] = np.array([nxt.last_max_update])
-    if not args.skip_dk512:
+    if not args.skip_dk512 and want("dk"):
         n = 512
         r = gen.config5_roots(n, 0)
         for k in (3, 4):
@@ -275,7 +291,57 @@ def main():
             out[p + "_ab_new_im"] = np.stack(nxt2.im)
             out[p + "_ab_maxupd"] = np.array([nxt2.last_max_update])
             print(f"dk512 k={k} done {time.time() - t0:.1f}s")
-    np.savez_compressed(os.path.join(HERE, "dk.npz"), **out)
+    if want("dk"):
+        np.savez_compressed(os.path.join(HERE, "dk.npz"), **out)
+    # ------------------------------------------------------------- estrin / complex eval
+    out = {}
+    for k, v, deg, npts in [(4, BF, 1024, 16), (3, BF, 100, 33), (2, BF, 37, 33), (2, STD, 37, 33), (4, BF, 0, 3),
+                            (3, BF, 1, 5), (3, STD, 20, 9), (4, STD, 20, 9)]:
+        rng = np.random.default_rng(700 + k + deg)
+        coeffs = gen.g_k(rng, k, deg + 1)
+        x = gen.g_k(rng, k, npts) * 1.1
+        zr = gen.g_k(rng, k, npts) * 0.9
+        zi = gen.g_k(rng, k, npts) * 0.9
+        p_ = poly.MWPolynomial(tuple(coeffs))
+        est = np.zeros((k, npts))
+        hre = np.zeros((k, npts)); him = np.zeros((k, npts))
+        ere = np.zeros((k, npts)); eim = np.zeros((k, npts))
+        for i in range(npts):
+            est[:, i] = poly.estrin_eval(p_, tuple(float(c) for c in x[:, i]), v)
+            z = (tuple(float(c) for c in zr[:, i]), tuple(float(c) for c in zi[:, i]))
+            r = poly.eval_complex(p_, z, "horner", v)
+            hre[:, i], him[:, i] = r[0], r[1]
+            r = poly.eval_complex(p_, z, "estrin", v)
+            ere[:, i], eim[:, i] = r[0], r[1]
+        bat = np.stack(poly.estrin_eval_batched(p_, batch.LaneBatch(tuple(x)), v).comps)
+        assert np.array_equal(bat.view(np.int64), est.view(np.int64))
+        p = f"k{k}_{tag[v]}_d{deg}"
+        out[p + "_coeffs"] = coeffs
+        out[p + "_x"] = x
+        out[p + "_estrin"] = est
+        out[p + "_zre"] = zr
+        out[p + "_zim"] = zi
+        out[p + "_ch_re"] = hre
+        out[p + "_ch_im"] = him
+        out[p + "_ce_re"] = ere
+        out[p + "_ce_im"] = eim
+    if want("polyx"):
+        np.savez_compressed(os.path.join(HERE, "polyx.npz"), **out)
+    print(f"polyx done {time.time() - t0:.1f}s")
+
+    # ------------------------------------------------------------- 3M complex GEMM
+    out = {}
+    for k, v, n in [(2, BF, 24), (3, BF, 17), (4, BF, 16), (2, STD, 24), (3, STD, 12), (4, STD, 10)]:
+        a, b = linalg.gen_complex_test_matrices(n, 20240806 + k, k)
+        c = linalg.cmatmul(a, b, linalg.MatMulPlan(scheme="naive", variant=v))
+        p = f"k{k}_{tag[v]}"
+        for nm, m in (("a", a), ("b", b), ("c", c)):
+            out[f"{p}_{nm}_re"] = np.stack(m.re.comps)
+            out[f"{p}_{nm}_im"] = np.stack(m.im.comps)
+    if want("cgemm"):
+        np.savez_compressed(os.path.join(HERE, "cgemm.npz"), **out)
+    print(f"cgemm done {time.time() - t0:.1f}s")
+
     print(f"all done {time.time() - t0:.1f}s  (mwfloat {getattr(mwfloat, '__version__', '?')})")
 
 

@@ -49,8 +49,7 @@ def test_ew_argument_checks(fn):
     f = getattr(_lib.load(), fn)
     p = 0x1000  # never dereferenced: every call below returns before a launch
     assert f(5, 1, p, 8, p, 8, p, 8, 8, None) == _lib.MW_ERR_INVALID  # bad k
-    assert f(3, 0, p, 8, p, 8, p, 8, 8, None) == _lib.MW_ERR_UNSUPPORTED  # TD STANDARD
-    assert f(4, 0, p, 8, p, 8, p, 8, 8, None) == _lib.MW_ERR_UNSUPPORTED
+    assert f(3, 0, p, 4, p, 8, p, 8, 8, None) == _lib.MW_ERR_INVALID  # TD STANDARD, bad stride
     assert f(2, 7, p, 8, p, 8, p, 8, 8, None) == _lib.MW_ERR_INVALID  # bad variant
     assert f(2, 1, p, 4, p, 8, p, 8, 8, None) == _lib.MW_ERR_INVALID  # stride < n
     assert f(2, 1, None, 8, p, 8, p, 8, 8, None) == _lib.MW_ERR_INVALID  # null
@@ -61,7 +60,7 @@ def test_ew_argument_checks(fn):
 def test_gemm_argument_checks():
     f = _lib.load().mw_gemm
     p = 0x1000
-    assert f(3, 0, p, 4, 16, p, 4, 16, p, 4, 16, 4, 4, 4, None) == _lib.MW_ERR_UNSUPPORTED
+    assert f(3, 2, p, 4, 16, p, 4, 16, p, 4, 16, 4, 4, 4, None) == _lib.MW_ERR_INVALID  # variant
     assert f(2, 1, p, 3, 16, p, 4, 16, p, 4, 16, 4, 4, 4, None) == _lib.MW_ERR_INVALID  # lda < kd
     assert f(2, 1, p, 4, 15, p, 4, 16, p, 4, 16, 4, 4, 4, None) == _lib.MW_ERR_INVALID  # plane stride
     assert f(2, 1, p, 4, 16, p, 4, 16, p, 4, 16, 0, 4, 4, None) == _lib.MW_OK  # m = 0
@@ -71,7 +70,7 @@ def test_other_entry_checks():
     lib = _lib.load()
     p = 0x1000
     assert lib.mw_horner(2, 1, p, 3, 5, p, 8, p, 8, 8, None) == _lib.MW_ERR_INVALID  # sc < deg+1
-    assert lib.mw_horner(4, 0, p, 8, 5, p, 8, p, 8, 8, None) == _lib.MW_ERR_UNSUPPORTED
+    assert lib.mw_horner(4, 5, p, 8, 5, p, 8, p, 8, 8, None) == _lib.MW_ERR_INVALID
     assert lib.mw_gemv(2, 1, p, 8, 64, p, 8, p, 8, 8, 8, 3, None) == _lib.MW_ERR_INVALID  # order
     assert lib.mw_dot(2, 1, p, 8, p, 8, 8, None, p, 9, None) == _lib.MW_ERR_INVALID
     assert lib.mw_dk_sweep(3, 1, p, 8, 8, p, p, 8, 4, 2, p, p, 8, p, p, 1, None) == _lib.MW_ERR_INVALID  # i1 < i0

@@ -36,11 +36,11 @@ from paper_2603_14926_b200 import (
     horner_eval_batched,
     matmul,
 )
-from paper_2603_14926_b200 import blas, roots
+from paper_2603_14926_b200 import blas, poly as mwpoly, roots
 
 pytestmark = pytest.mark.gpu
 
-CASES = [(2, "bf"), (3, "bf"), (4, "bf"), (2, "std")]
+CASES = [(2, "bf"), (3, "bf"), (4, "bf"), (2, "std"), (3, "std"), (4, "std")]
 IDS = [f"k{k}_{v}" for k, v in CASES]
 P_BITS = {2: 106, 3: 159, 4: 212}
 
@@ -105,10 +105,19 @@ def test_ew_kats():
     assert r == (6.0, 0.0, 0.0, 0.0)
 
 
-def test_ew_standard_k3_k4_unsupported():
-    a = LaneBatch(np.zeros((3, 4)))
-    with pytest.raises(NotImplementedError):
-        batch_add(a, a, Variant.STANDARD)
+@pytest.mark.parametrize("k", [3, 4])
+def test_ew_standard_renormalising_vs_oracle(k):
+    """Standard TD/QD (branchy renormalisation, multiword.py:164-513) on
+    wide-exponent inputs, zeros, cancellations and infinities."""
+    rng = np.random.default_rng(77 + k)
+    a, b = rand_mw(rng, k, 50000), rand_mw(rng, k, 50000)
+    a[:, :100] = -b[:, :100]          # exact cancellation
+    b[:, 100:200] = 0.0               # zero operand
+    a[1:, 200:300] = 0.0              # short expansions
+    a[0, 300] = np.inf
+    la, lb = LaneBatch(a), LaneBatch(b)
+    for op, fn in (("add", batch_add), ("sub", batch_sub), ("mul", batch_mul)):
+        assert_bitwise(fn(la, lb, Variant.STANDARD).numpy(), oracle.ew(op, a, b, "std"), nan_ok=True)
 
 
 def test_ew_mixed_k_raises():
@@ -360,3 +369,55 @@ def test_dk_sweep_graph_matches_eager(exact):
     assert_bitwise(r.re.cpu().numpy(), eager.re.cpu().numpy())
     assert_bitwise(r.im.cpu().numpy(), eager.im.cpu().numpy())
     assert r.iteration == 5
+
+
+# ------------------------------------------------- Estrin / complex eval
+POLYX = [(4, "bf", 1024), (3, "bf", 100), (2, "bf", 37), (2, "std", 37), (4, "bf", 0), (3, "bf", 1),
+         (3, "std", 20), (4, "std", 20)]
+
+
+@pytest.mark.parametrize("k,v,deg", POLYX, ids=[f"k{k}_{v}_d{d}" for k, v, d in POLYX])
+def test_estrin_complex_golden(golden, k, v, deg):
+    g = golden("polyx")
+    p = f"k{k}_{v}_d{deg}"
+    P = MWPolynomial(g[p + "_coeffs"])
+    assert_bitwise(mwpoly.estrin_eval_batched(P, LaneBatch(g[p + "_x"]), V(v)).numpy(), g[p + "_estrin"])
+    assert mwpoly.estrin_eval(P, tuple(g[p + "_x"][:, 0]), V(v)) == tuple(g[p + "_estrin"][:, 0])
+    for method, tag in (("horner", "ch"), ("estrin", "ce")):
+        re, im = mwpoly.eval_complex_batched(P, LaneBatch(g[p + "_zre"]), LaneBatch(g[p + "_zim"]), method, V(v))
+        assert_bitwise(re.numpy(), g[f"{p}_{tag}_re"])
+        assert_bitwise(im.numpy(), g[f"{p}_{tag}_im"])
+    z0 = (tuple(g[p + "_zre"][:, 0]), tuple(g[p + "_zim"][:, 0]))
+    r = mwpoly.eval_complex(P, z0, "estrin", V(v))
+    assert r == (tuple(g[p + "_ce_re"][:, 0]), tuple(g[p + "_ce_im"][:, 0]))
+
+
+@pytest.mark.parametrize("k", [2, 3, 4])
+@pytest.mark.parametrize("deg,npts", [(2, 100), (255, 1000), (256, 513), (1024, 4096)])
+def test_estrin_complex_vs_oracle(k, deg, npts):
+    rng = np.random.default_rng(deg * 3 + npts + k)
+    coeffs = gen.g_k(rng, k, deg + 1)
+    x = gen.g_k(rng, k, npts)
+    zi = gen.g_k(rng, k, npts)
+    P = MWPolynomial(coeffs)
+    assert_bitwise(mwpoly.estrin_eval_batched(P, LaneBatch(x), Variant.BRANCH_FREE).numpy(),
+                   oracle.poly_eval(coeffs, x, None, "bf", "estrin"))
+    for method in ("horner", "estrin"):
+        re, im = mwpoly.eval_complex_batched(P, LaneBatch(x), LaneBatch(zi), method, Variant.BRANCH_FREE)
+        ore, oim = oracle.poly_eval(coeffs, x, zi, "bf", method)
+        assert_bitwise(re.numpy(), ore)
+        assert_bitwise(im.numpy(), oim)
+
+
+# ------------------------------------------------------- 3M complex GEMM
+@pytest.mark.parametrize("k,v", CASES, ids=IDS)
+def test_cmatmul_golden(golden, k, v):
+    from paper_2603_14926_b200 import CMWMatrix, cmatmul
+
+    g = golden("cgemm")
+    p = f"k{k}_{v}"
+    a = CMWMatrix(MWMatrix(g[p + "_a_re"]), MWMatrix(g[p + "_a_im"]))
+    b = CMWMatrix(MWMatrix(g[p + "_b_re"]), MWMatrix(g[p + "_b_im"]))
+    c = cmatmul(a, b, MatMulPlan(scheme="naive", variant=v))
+    assert_bitwise(c.re.numpy(), g[p + "_c_re"])
+    assert_bitwise(c.im.numpy(), g[p + "_c_im"])

@@ -148,7 +148,7 @@ def _oracle_batch(monkeypatch):
     monkeypatch.setattr(roots, "batch_div", mk("div"))
 
 
-@pytest.mark.parametrize("k,v", [(2, "bf"), (3, "bf"), (4, "bf"), (2, "std")])
+@pytest.mark.parametrize("k,v", [(2, "bf"), (3, "bf"), (4, "bf"), (2, "std"), (3, "std"), (4, "std")])
 def test_aberth_init_host_logic_matches_reference(golden, monkeypatch, k, v):
     """radius_estimate (mpmath) + angles + lane ops reproduce the
     reference's aberth_init state bit for bit (roots.py:188-221)."""
@@ -178,3 +178,16 @@ def test_generators_are_seeded_and_normalised():
     assert x.shape == (2, 1024) and alpha.shape == (2,)
     coeffs, pts = gen.config4_horner(npts=100, degree=8)
     assert coeffs.shape == (4, 9) and not pts[1:].any()
+
+
+@pytest.mark.parametrize("k,n", [(2, 24), (3, 17), (4, 16)])
+def test_gen_complex_test_matrices_match_reference(golden, k, n):
+    from paper_2603_14926_b200.linalg import gen_complex_test_matrices
+
+    g = golden("cgemm")
+    a, b = gen_complex_test_matrices(n, 20240806 + k, k, device="cpu")
+    p = f"k{k}_bf"
+    assert_bitwise(a.re.numpy(), g[p + "_a_re"])
+    assert_bitwise(a.im.numpy(), g[p + "_a_im"])
+    assert_bitwise(b.re.numpy(), g[p + "_b_re"])
+    assert_bitwise(b.im.numpy(), g[p + "_b_im"])
