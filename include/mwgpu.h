@@ -120,6 +120,19 @@ int mw_gemm(int k, int variant, const double* A, int64_t lda, int64_t sA,
             const double* B, int64_t ldb, int64_t sB, double* C, int64_t ldc,
             int64_t sC, int64_t m, int64_t n, int64_t kd, void* stream);
 
+/* Batched / accumulating form of mw_gemm: for b < batch,
+ *   C_b = Cin_b + A_b B_b   (every C_ij folds t ascending starting from
+ *                            Cin_ij, or from exact zero when Cin == NULL),
+ * operand b at base + b * bs (elements), planes at + c * s.  The Strassen
+ * scheme (linalg.py:390-546) runs its 7^L leaf products and its odd-size
+ * peel folds (which start from a product, linalg.py:470-500) through it. */
+int mw_gemm_batched(int k, int variant, const double* A, int64_t lda,
+                    int64_t sA, int64_t bsA, const double* B, int64_t ldb,
+                    int64_t sB, int64_t bsB, double* C, int64_t ldc,
+                    int64_t sC, int64_t bsC, const double* Cin, int64_t ldci,
+                    int64_t sCi, int64_t bsCi, int64_t m, int64_t n,
+                    int64_t kd, int64_t batch, void* stream);
+
 /* y_p = Horner(coeffs, x_p) for npts points: acc = a_deg; acc = acc (*) x
  * (+) a_i for i = deg-1..0 (poly.py:89-96).  coeffs: k planes of deg+1
  * doubles (a_i multiplies x^i).  Bit-exact with horner_eval per point. */

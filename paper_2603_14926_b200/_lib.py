@@ -46,6 +46,8 @@ _SIGS = {
     "mw_tree_fold": ([I, I, P, I64, I64, P, P, P], I),
     "mw_gemv": ([I, I, P, I64, I64, P, I64, P, I64, I64, I64, I, P], I),
     "mw_gemm": ([I, I, P, I64, I64, P, I64, I64, P, I64, I64, I64, I64, I64, P], I),
+    "mw_gemm_batched": ([I, I, P, I64, I64, I64, P, I64, I64, I64, P, I64, I64, I64, P, I64, I64, I64, I64, I64,
+                         I64, I64, P], I),
     "mw_horner": ([I, I, P, I64, I64, P, I64, P, I64, I64, P], I),
     "mw_poly_eval": ([I, I, P, I64, I64, P, P, I64, P, P, I64, I64, I, P], I),
     "mw_dk_sweep": ([I, I, P, I64, I64, P, P, I64, I64, I64, P, P, I64, P, P, I, P], I),

@@ -50,12 +50,17 @@ struct GemmSmem {
   static constexpr size_t BYTES = sizeof(double) * STAGE * STAGES;
 };
 
-template <int K, int VAR>
+// EXT = false: one product from an exact zero (the hot path); EXT = true:
+// a batch of products (blockIdx.y strides the batch) with an optional
+// initial accumulator Cin, used by the Strassen scheme.
+template <int K, int VAR, bool EXT>
 __global__ void __launch_bounds__((GemmCfg<K>::BM / GemmCfg<K>::TM) *
                                   (GemmCfg<K>::BN / GemmCfg<K>::TN))
-    gemm_kernel(const double* __restrict__ A, int64_t lda, int64_t sA,
-                const double* __restrict__ B, int64_t ldb, int64_t sB, double* __restrict__ C,
-                int64_t ldc, int64_t sC, int64_t m, int64_t n, int64_t kd) {
+    gemm_kernel(const double* __restrict__ A0, int64_t lda, int64_t sA,
+                const double* __restrict__ B0, int64_t ldb, int64_t sB, double* __restrict__ C0,
+                int64_t ldc, int64_t sC, int64_t m, int64_t n, int64_t kd,
+                const double* __restrict__ Cin0, int64_t ldci, int64_t sCi, int64_t batch,
+                int64_t bsA, int64_t bsB, int64_t bsC, int64_t bsCi) {
   using Cf = GemmCfg<K>;
   using S = GemmSmem<K>;
   constexpr int BM = Cf::BM, BN = Cf::BN, BK = Cf::BK, TM = Cf::TM, TN = Cf::TN;
@@ -82,7 +87,8 @@ __global__ void __launch_bounds__((GemmCfg<K>::BM / GemmCfg<K>::TM) *
     return smem[st * S::STAGE + S::A_ELEMS + (c * BK + t) * BN + col];
   };
 
-  auto load_stage = [&](int st, int64_t k0) {
+  auto load_stage = [&](const double* __restrict__ A, const double* __restrict__ B, int st,
+                        int64_t k0) {
     // A tile: K x BM x BK, consecutive threads walk a row's BK doubles.
 #pragma unroll
     for (int e = tid; e < K * BM * BK; e += NT) {
@@ -103,21 +109,34 @@ __global__ void __launch_bounds__((GemmCfg<K>::BM / GemmCfg<K>::TM) *
     }
   };
 
+  const int64_t nbatch = EXT ? batch : 1;
+  for (int64_t bi = EXT ? blockIdx.y : 0; bi < nbatch; bi += EXT ? gridDim.y : 1) {
+  if (EXT && bi != blockIdx.y) __syncthreads();  // smem reuse across batch items
+  const double* __restrict__ A = EXT ? A0 + bi * bsA : A0;
+  const double* __restrict__ B = EXT ? B0 + bi * bsB : B0;
+  double* __restrict__ C = EXT ? C0 + bi * bsC : C0;
+  const double* __restrict__ Cin = (EXT && Cin0) ? Cin0 + bi * bsCi : nullptr;
   V<K> acc[TM][TN];
 #pragma unroll
   for (int r = 0; r < TM; ++r)
 #pragma unroll
-    for (int q = 0; q < TN; ++q) acc[r][q] = zero<K>();
+    for (int q = 0; q < TN; ++q) {
+      acc[r][q] = zero<K>();
+      // optional initial accumulator (the Strassen peel folds start from a
+      // product, linalg.py:470-500)
+      const int64_t gi = m0 + ty * TM + r, gj = n0 + tx + q * TX;
+      if (EXT && Cin && gi < m && gj < n) acc[r][q] = load<K>(Cin + gi * ldci + gj, sCi, 0);
+    }
 
   const int64_t ntiles = (kd + BK - 1) / BK;
   if (ntiles > 0) {
-    load_stage(0, 0);
+    load_stage(A, B, 0, 0);
     cp_async_commit();
   }
   for (int64_t kt = 0; kt < ntiles; ++kt) {
     const int st = (int)(kt & 1);
     if (kt + 1 < ntiles) {
-      load_stage(st ^ 1, (kt + 1) * BK);
+      load_stage(A, B, st ^ 1, (kt + 1) * BK);
       cp_async_commit();
       cp_async_wait<1>();
     } else {
@@ -158,25 +177,36 @@ __global__ void __launch_bounds__((GemmCfg<K>::BM / GemmCfg<K>::TM) *
       for (int c = 0; c < K; ++c) C[c * sC + gi * ldc + gj] = acc[r][q].c[c];
     }
   }
+  }  // batch
 }
 
 template <int K, int VAR>
 struct GemmLaunch {
   static int run(const double* A, int64_t lda, int64_t sA, const double* B, int64_t ldb,
                  int64_t sB, double* C, int64_t ldc, int64_t sC, int64_t m, int64_t n, int64_t kd,
-                 cudaStream_t st) {
+                 const double* Cin, int64_t ldci, int64_t sCi, int64_t batch, int64_t bsA,
+                 int64_t bsB, int64_t bsC, int64_t bsCi, cudaStream_t st) {
     using Cf = GemmCfg<K>;
     constexpr int NT = (Cf::BM / Cf::TM) * (Cf::BN / Cf::TN);
     const size_t smem = GemmSmem<K>::BYTES;
     static bool attr_set = false;
     if (!attr_set) {
-      cudaFuncSetAttribute(gemm_kernel<K, VAR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      cudaFuncSetAttribute(gemm_kernel<K, VAR, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smem);
+      cudaFuncSetAttribute(gemm_kernel<K, VAR, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)smem);
       attr_set = true;
     }
     const int64_t tiles = ((n + Cf::BN - 1) / Cf::BN) * ((m + Cf::BM - 1) / Cf::BM);
     if (tiles > 0x7fffffffLL) return MW_ERR_INVALID;
-    gemm_kernel<K, VAR><<<(unsigned)tiles, NT, smem, st>>>(A, lda, sA, B, ldb, sB, C, ldc, sC, m, n, kd);
+    if (batch == 1 && Cin == nullptr) {
+      gemm_kernel<K, VAR, false><<<(unsigned)tiles, NT, smem, st>>>(
+          A, lda, sA, B, ldb, sB, C, ldc, sC, m, n, kd, nullptr, 0, 0, 1, 0, 0, 0, 0);
+    } else {
+      const unsigned gy = (unsigned)(batch < 65535 ? batch : 65535);
+      gemm_kernel<K, VAR, true><<<dim3((unsigned)tiles, gy), NT, smem, st>>>(
+          A, lda, sA, B, ldb, sB, C, ldc, sC, m, n, kd, Cin, ldci, sCi, batch, bsA, bsB, bsC, bsCi);
+    }
     return launch_status();
   }
 };
@@ -184,6 +214,23 @@ struct GemmLaunch {
 }  // namespace mw
 
 using namespace mw;
+
+extern "C" int mw_gemm_batched(int k, int variant, const double* A, int64_t lda, int64_t sA,
+                               int64_t bsA, const double* B, int64_t ldb, int64_t sB, int64_t bsB,
+                               double* C, int64_t ldc, int64_t sC, int64_t bsC, const double* Cin,
+                               int64_t ldci, int64_t sCi, int64_t bsCi, int64_t m, int64_t n,
+                               int64_t kd, int64_t batch, void* stream) {
+  if (k < 2 || k > 4) return MW_ERR_INVALID;
+  if (variant != 0 && variant != 1) return MW_ERR_INVALID;
+  if (m < 0 || n < 0 || kd < 0 || batch < 0) return MW_ERR_INVALID;
+  if (m == 0 || n == 0 || batch == 0) return MW_OK;
+  if (!C || ldc < n) return MW_ERR_INVALID;
+  if (kd > 0 && (!A || !B || lda < kd || ldb < n)) return MW_ERR_INVALID;
+  if (Cin && ldci < n) return MW_ERR_INVALID;
+  if (batch > 1 && (bsA < 0 || bsB < 0 || bsC < 0 || (Cin && bsCi < 0))) return MW_ERR_INVALID;
+  return dispatch<GemmLaunch>(k, variant, A, lda, sA, B, ldb, sB, C, ldc, sC, m, n, kd, Cin, ldci,
+                              sCi, batch, bsA, bsB, bsC, bsCi, as_stream(stream));
+}
 
 extern "C" int mw_gemm(int k, int variant, const double* A, int64_t lda, int64_t sA,
                        const double* B, int64_t ldb, int64_t sB, double* C, int64_t ldc,
@@ -198,5 +245,6 @@ extern "C" int mw_gemm(int k, int variant, const double* A, int64_t lda, int64_t
     if (sA < (m - 1) * lda + kd || sB < (kd - 1) * ldb + n) return MW_ERR_INVALID;
   }
   return dispatch<GemmLaunch>(k, variant, A, lda, sA, B, ldb, sB, C, ldc, sC, m, n, kd,
-                              as_stream(stream));
+                              (const double*)nullptr, (int64_t)0, (int64_t)0, (int64_t)1,
+                              (int64_t)0, (int64_t)0, (int64_t)0, (int64_t)0, as_stream(stream));
 }

@@ -7,12 +7,14 @@ one (K, rows, cols) float64 CUDA tensor; ``MatMulPlan`` (75-89) and
 
 ``matmul`` runs mw_gemm: every C_ij folds t ascending from an exact zero
 (the naive order, 284-314), bit-exact with ``scheme="naive"`` and
-``"blocked"`` (identical order, 317-349).  ``scheme="strassen"`` is
-computed in that same naive order -- more accurate than Strassen and
-within the reference's own Strassen-vs-naive tolerance (8 ulp at the
-|A||B| scale, verify.py:384-424); ``simd`` / ``threads`` /
-``strassen_cutoff`` are accepted and validated but do not change the
-device schedule (results are invariant to them in the reference too,
+``"blocked"`` (identical order, 317-349).  ``scheme="strassen"`` runs the
+reference's Strassen recursion (390-546: seven products per even split,
+odd sizes peeled, blocked products at or below ``strassen_cutoff``)
+breadth-first: each recursion level is a handful of lane-wise kernels over
+all 7^L sub-problems at once and the leaves are ONE batched GEMM launch
+(mw_gemm_batched) -- bit-exact with the reference's Strassen.  ``simd``
+and ``threads`` are accepted and validated but do not change the device
+schedule (results are invariant to them in the reference too,
 test_linalg.py:134-151).
 """
 
@@ -243,6 +245,108 @@ def gemm_into(a: torch.Tensor, b: torch.Tensor, c: torch.Tensor, variant, row0: 
     _lib.check(rc, "mw_gemm")
 
 
+def _ew_planes(name: str, a: torch.Tensor, b: torch.Tensor, variant) -> torch.Tensor:
+    """Lane-wise op over (K, ...) tensors whose non-plane dims are
+    contiguous (any plane stride); returns a contiguous result."""
+    for t in (a, b):
+        inner = t[0]
+        if not inner.is_contiguous():
+            raise ValueError("operand planes must be contiguous")
+    k = a.shape[0]
+    n = a[0].numel()
+    out = torch.empty(a.shape, dtype=torch.float64, device=a.device)
+    rc = getattr(_lib.load(), name)(k, variant_code(variant), a.data_ptr(), a.stride(0), b.data_ptr(), b.stride(0),
+                                    out.data_ptr(), n, n, _lib.stream_handle(a.device))
+    _lib.check(rc, name)
+    return out
+
+
+def _gemm4(a: torch.Tensor, b: torch.Tensor, c: torch.Tensor, variant, cin: torch.Tensor | None = None):
+    """Batched C = Cin + A B on (K, batch, rows, cols) views (unit column
+    stride); strides are passed through, no copies."""
+    k, bt, m, kd = a.shape
+    n = b.shape[3]
+    for t in (a, b, c) + ((cin,) if cin is not None else ()):
+        if t.shape[3] > 1 and t.stride(3) != 1:
+            raise ValueError("matrix views need unit column stride")
+    rc = _lib.load().mw_gemm_batched(
+        k, variant_code(variant),
+        a.data_ptr(), max(a.stride(2), kd), a.stride(0), a.stride(1),
+        b.data_ptr(), max(b.stride(2), n), b.stride(0), b.stride(1),
+        c.data_ptr(), max(c.stride(2), n), c.stride(0), c.stride(1),
+        None if cin is None else cin.data_ptr(), 0 if cin is None else max(cin.stride(2), n),
+        0 if cin is None else cin.stride(0), 0 if cin is None else cin.stride(1),
+        m, n, kd, bt, _lib.stream_handle(a.device),
+    )
+    _lib.check(rc, "mw_gemm_batched")
+
+
+def _strassen_rec(a: torch.Tensor, b: torch.Tensor, variant, cutoff: int) -> torch.Tensor:
+    """Batched Strassen on contiguous (K, batch, s, s) operands
+    (linalg._strassen_rec, linalg.py:503-511)."""
+    k, bt, s, _ = a.shape
+    if s <= cutoff:
+        c = torch.empty_like(a)
+        _gemm4(a, b, c, variant)  # _blocked_mm: the naive per-entry order
+        return c
+    if s % 2:
+        return _strassen_peel(a, b, variant, cutoff)
+    h = s // 2
+
+    def q(t, i, j):
+        return t[:, :, i * h:(i + 1) * h, j * h:(j + 1) * h].contiguous()
+
+    def add(x, y):
+        return _ew_planes("mw_ew_add", x, y, variant)
+
+    def sub(x, y):
+        return _ew_planes("mw_ew_sub", x, y, variant)
+
+    a11, a12, a21, a22 = q(a, 0, 0), q(a, 0, 1), q(a, 1, 0), q(a, 1, 1)
+    b11, b12, b21, b22 = q(b, 0, 0), q(b, 0, 1), q(b, 1, 0), q(b, 1, 1)
+    # _strassen_products (linalg.py:418-436), in its order M1..M7
+    x = torch.stack([add(a11, a22), add(a21, a22), a11, a22, add(a11, a12), sub(a21, a11), sub(a12, a22)], dim=1)
+    y = torch.stack([add(b11, b22), b11, sub(b12, b22), sub(b21, b11), b22, add(b11, b12), add(b21, b22)], dim=1)
+    m = _strassen_rec(x.reshape(k, 7 * bt, h, h), y.reshape(k, 7 * bt, h, h), variant, cutoff)
+    m = m.reshape(k, 7, bt, h, h)
+    m1, m2, m3, m4, m5, m6, m7 = (m[:, i] for i in range(7))
+    # _strassen_combine (linalg.py:439-452)
+    out = torch.empty((k, bt, s, s), dtype=torch.float64, device=a.device)
+    out[:, :, :h, :h] = add(sub(add(m1, m4), m5), m7)
+    out[:, :, :h, h:] = add(m3, m5)
+    out[:, :, h:, :h] = add(m2, m4)
+    out[:, :, h:, h:] = add(add(sub(m1, m2), m3), m6)
+    return out
+
+
+def _strassen_peel(a: torch.Tensor, b: torch.Tensor, variant, cutoff: int) -> torch.Tensor:
+    """Odd size: recurse on the even core, then the border folds
+    (linalg._strassen_peel, linalg.py:455-500), each a GEMM whose fold
+    starts from the reference's initial term."""
+    k, bt, n, _ = a.shape
+    e = n - 1
+    core = _strassen_rec(a[:, :, :e, :e].contiguous(), b[:, :, :e, :e].contiguous(), variant, cutoff)
+    out = torch.empty_like(a)
+    a_col, a_row, a_cor = a[:, :, :e, e:e + 1], a[:, :, e:e + 1, :e], a[:, :, e:e + 1, e:e + 1]
+    b_col, b_row, b_cor = b[:, :, :e, e:e + 1], b[:, :, e:e + 1, :e], b[:, :, e:e + 1, e:e + 1]
+
+    def mul(x, y):
+        return _ew_planes("mw_ew_mul", x.contiguous(), y.contiguous(), variant)
+
+    # C00 = core + a_col (outer) b_row: rows fold add(core, mul(a_col_i, b_row))
+    _gemm4(a_col, b_row, out[:, :, :e, :e], variant, cin=core)
+    # C01 = mul(a_col, b_cor) + sum_t mul(A[:, t], b_col[t])
+    init = mul(a_col, b_cor.expand(k, bt, e, 1))
+    _gemm4(a[:, :, :e, :e], b_col, out[:, :, :e, e:e + 1], variant, cin=init)
+    # C10 = mul(a_cor, b_row) + sum_t mul(a_row[t], B[t, :])
+    init = mul(a_cor.expand(k, bt, 1, e), b_row)
+    _gemm4(a_row, b[:, :, :e, :e], out[:, :, e:e + 1, :e], variant, cin=init)
+    # C11 = mul(a_cor, b_cor) + sum_t mul(a_row[t], b_col[t])
+    init = mul(a_cor, b_cor)
+    _gemm4(a_row, b_col, out[:, :, e:e + 1, e:e + 1], variant, cin=init)
+    return out
+
+
 def matmul(a: MWMatrix, b: MWMatrix, plan: MatMulPlan | None = None) -> MWMatrix:
     """Real multi-word product a @ b (linalg.py:549-569)."""
     if plan is None:
@@ -254,6 +358,11 @@ def matmul(a: MWMatrix, b: MWMatrix, plan: MatMulPlan | None = None) -> MWMatrix
     if plan.scheme is Scheme.STRASSEN and (a.rows != a.cols or b.rows != b.cols):
         raise ValueError("strassen scheme requires square matrices")
     _lib.require_cuda(a.planes, b.planes)
+    if plan.scheme is Scheme.STRASSEN:
+        k, n = a.k, a.rows
+        c = _strassen_rec(a.planes.reshape(k, 1, n, n), b.planes.reshape(k, 1, n, n), plan.variant,
+                          plan.strassen_cutoff)
+        return MWMatrix(c.reshape(k, n, n))
     out = torch.empty((a.k, a.rows, b.cols), dtype=torch.float64, device=a.device)
     gemm_into(a.planes, b.planes, out, plan.variant)
     return MWMatrix(out)

@@ -21,6 +21,7 @@ public functions on small seeded cases:
               from_oracle, one sweep from the near-root start and one from
               the R0 = 1.5 Aberth circle                     (roots.py:188-315)
   cgemm.npz   cmatmul (3M) on gen_complex_test_matrices     (linalg.py:247-276, 572-590)
+  strassen.npz matmul(scheme="strassen") with even splits and odd peels (linalg.py:390-546)
   polyx.npz   estrin_eval per point (== estrin_eval_batched) and
               eval_complex Horner / Estrin                   (poly.py:106-178)
 
@@ -341,6 +342,24 @@ def main():
     if want("cgemm"):
         np.savez_compressed(os.path.join(HERE, "cgemm.npz"), **out)
     print(f"cgemm done {time.time() - t0:.1f}s")
+
+    # ------------------------------------------------------------- Strassen
+    out = {}
+    for k, v, n, cut in [(2, BF, 37, 8), (3, BF, 48, 8), (4, BF, 35, 4), (2, STD, 37, 8), (3, STD, 20, 4),
+                         (4, STD, 18, 4), (2, BF, 64, 32)]:
+        rng = np.random.default_rng(900 + k + n)
+        a = gen.g_k(rng, k, (n, n))
+        b = gen.g_k(rng, k, (n, n))
+        c = linalg.matmul(linalg.MWMatrix(tuple(a)), linalg.MWMatrix(tuple(b)),
+                          linalg.MatMulPlan(scheme="strassen", variant=v, strassen_cutoff=cut))
+        p = f"k{k}_{tag[v]}_n{n}_c{cut}"
+        out[p + "_a"] = a
+        out[p + "_b"] = b
+        out[p + "_out"] = np.stack(c.comps)
+        out[p + "_steps"] = np.array([len(linalg.strassen_pad_policy(n, cut))])
+    if want("strassen"):
+        np.savez_compressed(os.path.join(HERE, "strassen.npz"), **out)
+    print(f"strassen done {time.time() - t0:.1f}s")
 
     print(f"all done {time.time() - t0:.1f}s  (mwfloat {getattr(mwfloat, '__version__', '?')})")
 

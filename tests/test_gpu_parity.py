@@ -421,3 +421,51 @@ def test_cmatmul_golden(golden, k, v):
     c = cmatmul(a, b, MatMulPlan(scheme="naive", variant=v))
     assert_bitwise(c.re.numpy(), g[p + "_c_re"])
     assert_bitwise(c.im.numpy(), g[p + "_c_im"])
+
+
+# --------------------------------------------------------------- Strassen
+STRASSEN = [(2, "bf", 37, 8), (3, "bf", 48, 8), (4, "bf", 35, 4), (2, "std", 37, 8), (3, "std", 20, 4),
+            (4, "std", 18, 4), (2, "bf", 64, 32)]
+
+
+@pytest.mark.parametrize("k,v,n,cut", STRASSEN, ids=[f"k{k}_{v}_n{n}_c{c}" for k, v, n, c in STRASSEN])
+def test_strassen_golden(golden, k, v, n, cut):
+    g = golden("strassen")
+    p = f"k{k}_{v}_n{n}_c{cut}"
+    c = matmul(MWMatrix(g[p + "_a"]), MWMatrix(g[p + "_b"]),
+               MatMulPlan(scheme="strassen", variant=v, strassen_cutoff=cut))
+    assert_bitwise(c.numpy(), g[p + "_out"])
+
+
+@pytest.mark.parametrize("k,n,cut", [(2, 129, 16), (3, 100, 12), (4, 66, 8)])
+def test_strassen_vs_oracle_restatement(k, n, cut):
+    from test_oracle_golden import _o_strassen
+
+    rng = np.random.default_rng(n + k)
+    a, b = gen.g_k(rng, k, (n, n)), gen.g_k(rng, k, (n, n))
+    c = matmul(MWMatrix(a), MWMatrix(b), MatMulPlan(scheme="strassen", variant="bf", strassen_cutoff=cut))
+    assert_bitwise(c.numpy(), _o_strassen(a, b, "bf", cut))
+
+
+@pytest.mark.parametrize("k,n", [(2, 33), (2, 128), (3, 33), (3, 64), (4, 33), (4, 64)])
+def test_strassen_within_8_ulp_of_naive(k, n):
+    """Scheme consistency at the reference's sizes (verify.py:384-424):
+    Strassen (cutoff 32, peeled odd sizes) within 8 K-word ulps of naive at
+    the |A||B| scale."""
+    rng = np.random.default_rng(20240804 + n + k)
+    c0 = rng.uniform(-1.0, 1.0, (n, n))
+    a = np.stack([c0] + [c0 * 2.0 ** (-53 * j) * 0.3 for j in range(1, k)])
+    c0 = rng.uniform(-1.0, 1.0, (n, n))
+    b = np.stack([c0] + [c0 * 2.0 ** (-53 * j) * 0.2 for j in range(1, k)])
+    A, B = MWMatrix(a), MWMatrix(b)
+    cs = matmul(A, B, MatMulPlan(scheme="strassen", variant="bf")).numpy()
+    cn = matmul(A, B, MatMulPlan(scheme="naive", variant="bf")).numpy()
+    scale = np.abs(a).sum(0) @ np.abs(b).sum(0)
+    worst = 0.0
+    for i in range(0, n, 3):
+        for j in range(0, n, 5):
+            d = abs(exact_value(cs[:, i, j]) - exact_value(cn[:, i, j]))
+            if d:
+                _, e = math.frexp(scale[i, j])
+                worst = max(worst, float(d) / math.ldexp(1.0, e - 53 * k))
+    assert worst <= 8.0
