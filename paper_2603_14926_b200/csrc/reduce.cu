@@ -204,6 +204,7 @@ __global__ void __launch_bounds__(128) gemv_exact_kernel(const double* __restric
 // (lane l of warp w, u = 32w + l) folds t = u, u+128, u+256, ... ascending
 // from exact zero; the partials combine by the in-place pairwise tree
 // (strides 1..64, pairs valid while the partner index < min(n, 128)).
+// (Measured on B200 at 2048^2: 128 partials beat 32 and 256.)
 // Four elements are loaded ahead of their arithmetic so HBM latency
 // overlaps the FP64 chain.
 constexpr int GEMV_WARPS = 4;
