@@ -165,7 +165,8 @@ def ncu_traffic(kernel):
     ncu --set full capture summary (profiles/ncu_summary.json), or None."""
     path = os.path.join(REPO, "profiles", "ncu_summary.json")
     try:
-        ent = json.load(open(path)).get(kernel)
+        summ = json.load(open(path))
+        ent = summ.get(kernel) or summ.get(kernel.replace(">", ",0>"))
         if ent is None:
             return None, None
         return int(ent["dram_bytes_per_launch"]), f"profiles/ncu_summary.json ({ent['round']}, {ent['report']})"
@@ -354,7 +355,7 @@ def run_ours(args):
     for i, (k, n, a, b, c) in enumerate(dev):
         rows = a.shape[1]
         ops = MAC_OPS[k] * rows * n * n
-        parts.append(dict(name=f"gemm_{['', '', 'dd', 'td', 'qd'][k]}_n{n}", kernel=f"gemm_kernel<{k},1>",
+        parts.append(dict(name=f"gemm_{['', '', 'dd', 'td', 'qd'][k]}_n{n}", kernel=f"gemm_kernel<{k},1,0>",
                           ms=part_ms[i], fp64_ops=ops,
                           mp_ops=2 * rows * n * n))
     hp = phi - plo

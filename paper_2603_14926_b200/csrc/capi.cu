@@ -4,17 +4,20 @@
 
 namespace mw {
 
+// Per-device cache (one process may drive several GPUs); a benign race
+// only repeats the query.
 int sm_count() {
-  static int cached = 0;
-  if (cached == 0) {
-    int dev = 0, v = 0;
-    if (cudaGetDevice(&dev) == cudaSuccess &&
-        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && v > 0)
-      cached = v;
-    else
-      cached = 148;
+  static int cached[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+  if (cached[dev] == 0) {
+    int v = 0;
+    cached[dev] = (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess &&
+                   v > 0)
+                      ? v
+                      : 148;
   }
-  return cached;
+  return cached[dev];
 }
 
 // CHAINS independent dependent chains per thread keep the FP64 pipe busy

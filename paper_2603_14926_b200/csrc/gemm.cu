@@ -189,13 +189,16 @@ struct GemmLaunch {
     using Cf = GemmCfg<K>;
     constexpr int NT = (Cf::BM / Cf::TM) * (Cf::BN / Cf::TN);
     const size_t smem = GemmSmem<K>::BYTES;
-    static bool attr_set = false;
-    if (!attr_set) {
+    // the dynamic-smem opt-in is per device; setting it twice is harmless
+    static bool attr_set[64] = {false};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64 || !attr_set[dev]) {
       cudaFuncSetAttribute(gemm_kernel<K, VAR, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)smem);
       cudaFuncSetAttribute(gemm_kernel<K, VAR, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)smem);
-      attr_set = true;
+      if (dev >= 0 && dev < 64) attr_set[dev] = true;
     }
     const int64_t tiles = ((n + Cf::BN - 1) / Cf::BN) * ((m + Cf::BM - 1) / Cf::BM);
     if (tiles > 0x7fffffffLL) return MW_ERR_INVALID;

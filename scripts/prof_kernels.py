@@ -70,6 +70,14 @@ def main():
                 jobs.append((name, lambda q=q, st=st: mw.dk_sweeps(q, st, 1, BF, exact_order=False, check=False)))
             if want(name + "_exact"):
                 jobs.append((name + "_exact", lambda q=q, st=st: mw.dk_sweeps(q, st, 1, BF, exact_order=True, check=False)))
+    if want("estrin_qd"):
+        coeffs, x = gen.config4_horner(npts=1 << 20)
+        P, X = mw.MWPolynomial(coeffs), mw.LaneBatch(x)
+        jobs.append(("estrin_qd", lambda P=P, X=X: mw.estrin_eval_batched(P, X, BF)))
+    if want("ew_qd_mul"):
+        rng = np.random.default_rng(0)
+        a, b = mw.LaneBatch(gen.g_k(rng, 4, 1 << 24)), mw.LaneBatch(gen.g_k(rng, 4, 1 << 24))
+        jobs.append(("ew_qd_mul", lambda a=a, b=b: mw.batch_mul(a, b, BF)))
     for name, fn in jobs:
         for _ in range(args.warm):
             fn()
