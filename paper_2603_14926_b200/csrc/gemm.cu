@@ -15,170 +15,28 @@
 // intensity is ~29/96/209 FP64 ops per (2K x 8 B) of smem traffic, so the
 // kernel is bound by FP64 issue, not memory; the only overhead on the
 // pipe is the exact-zero start (one add per output).
-#include "common.cuh"
+#include "gemm_kernel.cuh"
 
 namespace mw {
-
-constexpr int GEMM_GROUP_M = 16;
 
 template <int K>
 struct GemmCfg;
 // DD: 64x64 tile, 4x4 per thread, 256 threads.
 template <>
 struct GemmCfg<2> {
-  static constexpr int BM = 64, BN = 64, BK = 16, TM = 4, TN = 4;
+  static constexpr int BM = 64, BN = 64, BK = 16, TM = 4, TN = 4, MINB = 2;
 };
-// TD: 32x64 tile, 2x4 per thread, 256 threads.
+// TD and QD: 64x32 tile, 4x2 per thread, 256 threads.  (Tile sweep on
+// B200 with tune/gemm_tune.cu + scripts/tune_gemm.py: every non-spilling
+// configuration lands within 1-3 % of these; all are bit-identical.)
 template <>
 struct GemmCfg<3> {
-  static constexpr int BM = 32, BN = 64, BK = 16, TM = 2, TN = 4;
+  static constexpr int BM = 64, BN = 32, BK = 16, TM = 4, TN = 2, MINB = 2;
 };
-// QD: 32x32 tile, 2x2 per thread, 256 threads.
 template <>
 struct GemmCfg<4> {
-  static constexpr int BM = 32, BN = 32, BK = 16, TM = 2, TN = 2;
+  static constexpr int BM = 64, BN = 32, BK = 16, TM = 4, TN = 2, MINB = 2;
 };
-
-template <int K>
-struct GemmSmem {
-  using C = GemmCfg<K>;
-  static constexpr int APAD = C::BK + 2;  // row stride of the A tile (doubles)
-  static constexpr int A_ELEMS = K * C::BM * APAD;
-  static constexpr int B_ELEMS = K * C::BK * C::BN;
-  static constexpr int STAGE = A_ELEMS + B_ELEMS;
-  static constexpr int STAGES = 2;
-  static constexpr size_t BYTES = sizeof(double) * STAGE * STAGES;
-};
-
-// EXT = false: one product from an exact zero (the hot path); EXT = true:
-// a batch of products (blockIdx.y strides the batch) with an optional
-// initial accumulator Cin, used by the Strassen scheme.
-template <int K, int VAR, bool EXT>
-__global__ void __launch_bounds__((GemmCfg<K>::BM / GemmCfg<K>::TM) *
-                                  (GemmCfg<K>::BN / GemmCfg<K>::TN))
-    gemm_kernel(const double* __restrict__ A0, int64_t lda, int64_t sA,
-                const double* __restrict__ B0, int64_t ldb, int64_t sB, double* __restrict__ C0,
-                int64_t ldc, int64_t sC, int64_t m, int64_t n, int64_t kd,
-                const double* __restrict__ Cin0, int64_t ldci, int64_t sCi, int64_t batch,
-                int64_t bsA, int64_t bsB, int64_t bsC, int64_t bsCi) {
-  using Cf = GemmCfg<K>;
-  using S = GemmSmem<K>;
-  constexpr int BM = Cf::BM, BN = Cf::BN, BK = Cf::BK, TM = Cf::TM, TN = Cf::TN;
-  constexpr int TX = BN / TN, TY = BM / TM, NT = TX * TY;
-  extern __shared__ __align__(16) double smem[];
-
-  const int tid = threadIdx.x;
-  const int tx = tid % TX, ty = tid / TX;
-  // Grouped raster: consecutive CTAs walk GROUP_M tile-rows of one
-  // tile-column band, so the ~300 co-resident CTAs share A and B panels in
-  // L2 and B is streamed from HBM ~grid_m/GROUP_M times instead of grid_m.
-  const int64_t grid_m = (m + BM - 1) / BM, grid_n = (n + BN - 1) / BN;
-  const int64_t pid = blockIdx.x;
-  const int64_t per_group = (int64_t)GEMM_GROUP_M * grid_n;
-  const int64_t first_m = (pid / per_group) * GEMM_GROUP_M;
-  const int64_t gsize = (grid_m - first_m) < GEMM_GROUP_M ? (grid_m - first_m) : GEMM_GROUP_M;
-  const int64_t in_group = pid % per_group;
-  const int64_t m0 = (first_m + in_group % gsize) * BM, n0 = (in_group / gsize) * BN;
-
-  auto As = [&](int st, int c, int row, int t) -> double& {
-    return smem[st * S::STAGE + (c * BM + row) * S::APAD + t];
-  };
-  auto Bs = [&](int st, int c, int t, int col) -> double& {
-    return smem[st * S::STAGE + S::A_ELEMS + (c * BK + t) * BN + col];
-  };
-
-  auto load_stage = [&](const double* __restrict__ A, const double* __restrict__ B, int st,
-                        int64_t k0) {
-    // A tile: K x BM x BK, consecutive threads walk a row's BK doubles.
-#pragma unroll
-    for (int e = tid; e < K * BM * BK; e += NT) {
-      const int c = e / (BM * BK), rem = e % (BM * BK), row = rem / BK, t = rem % BK;
-      const int64_t gi = m0 + row, gt = k0 + t;
-      const bool ok = gi < m && gt < kd;
-      const double* src = ok ? A + c * sA + gi * lda + gt : A;
-      cp_async8(&As(st, c, row, t), src, ok ? 8 : 0);
-    }
-    // B tile: K x BK x BN, consecutive threads walk a row's BN doubles.
-#pragma unroll
-    for (int e = tid; e < K * BK * BN; e += NT) {
-      const int c = e / (BK * BN), rem = e % (BK * BN), t = rem / BN, col = rem % BN;
-      const int64_t gt = k0 + t, gj = n0 + col;
-      const bool ok = gt < kd && gj < n;
-      const double* src = ok ? B + c * sB + gt * ldb + gj : B;
-      cp_async8(&Bs(st, c, t, col), src, ok ? 8 : 0);
-    }
-  };
-
-  const int64_t nbatch = EXT ? batch : 1;
-  for (int64_t bi = EXT ? blockIdx.y : 0; bi < nbatch; bi += EXT ? gridDim.y : 1) {
-  if (EXT && bi != blockIdx.y) __syncthreads();  // smem reuse across batch items
-  const double* __restrict__ A = EXT ? A0 + bi * bsA : A0;
-  const double* __restrict__ B = EXT ? B0 + bi * bsB : B0;
-  double* __restrict__ C = EXT ? C0 + bi * bsC : C0;
-  const double* __restrict__ Cin = (EXT && Cin0) ? Cin0 + bi * bsCi : nullptr;
-  V<K> acc[TM][TN];
-#pragma unroll
-  for (int r = 0; r < TM; ++r)
-#pragma unroll
-    for (int q = 0; q < TN; ++q) {
-      acc[r][q] = zero<K>();
-      // optional initial accumulator (the Strassen peel folds start from a
-      // product, linalg.py:470-500)
-      const int64_t gi = m0 + ty * TM + r, gj = n0 + tx + q * TX;
-      if (EXT && Cin && gi < m && gj < n) acc[r][q] = load<K>(Cin + gi * ldci + gj, sCi, 0);
-    }
-
-  const int64_t ntiles = (kd + BK - 1) / BK;
-  if (ntiles > 0) {
-    load_stage(A, B, 0, 0);
-    cp_async_commit();
-  }
-  for (int64_t kt = 0; kt < ntiles; ++kt) {
-    const int st = (int)(kt & 1);
-    if (kt + 1 < ntiles) {
-      load_stage(A, B, st ^ 1, (kt + 1) * BK);
-      cp_async_commit();
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
-    __syncthreads();
-    const int64_t rem = kd - kt * BK;
-    const int tvalid = rem < BK ? (int)rem : BK;
-#pragma unroll 1
-    for (int t = 0; t < tvalid; ++t) {
-      V<K> a[TM], b[TN];
-#pragma unroll
-      for (int r = 0; r < TM; ++r)
-#pragma unroll
-        for (int c = 0; c < K; ++c) a[r].c[c] = As(st, c, ty * TM + r, t);
-#pragma unroll
-      for (int q = 0; q < TN; ++q)
-#pragma unroll
-        for (int c = 0; c < K; ++c) b[q].c[c] = Bs(st, c, t, tx + q * TX);
-#pragma unroll
-      for (int r = 0; r < TM; ++r)
-#pragma unroll
-        for (int q = 0; q < TN; ++q)
-          acc[r][q] = Ops<K, VAR>::add(acc[r][q], Ops<K, VAR>::mul(a[r], b[q]));
-    }
-    __syncthreads();
-  }
-
-#pragma unroll
-  for (int r = 0; r < TM; ++r) {
-    const int64_t gi = m0 + ty * TM + r;
-    if (gi >= m) continue;
-#pragma unroll
-    for (int q = 0; q < TN; ++q) {
-      const int64_t gj = n0 + tx + q * TX;
-      if (gj >= n) continue;
-#pragma unroll
-      for (int c = 0; c < K; ++c) C[c * sC + gi * ldc + gj] = acc[r][q].c[c];
-    }
-  }
-  }  // batch
-}
 
 template <int K, int VAR>
 struct GemmLaunch {
@@ -188,26 +46,26 @@ struct GemmLaunch {
                  int64_t bsB, int64_t bsC, int64_t bsCi, cudaStream_t st) {
     using Cf = GemmCfg<K>;
     constexpr int NT = (Cf::BM / Cf::TM) * (Cf::BN / Cf::TN);
-    const size_t smem = GemmSmem<K>::BYTES;
+    const size_t smem = GemmSmem<K, Cf>::BYTES;
     // the dynamic-smem opt-in is per device; setting it twice is harmless
     static bool attr_set[64] = {false};
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev < 0 || dev >= 64 || !attr_set[dev]) {
-      cudaFuncSetAttribute(gemm_kernel<K, VAR, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      cudaFuncSetAttribute(gemm_kernel<K, VAR, false, Cf>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)smem);
-      cudaFuncSetAttribute(gemm_kernel<K, VAR, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      cudaFuncSetAttribute(gemm_kernel<K, VAR, true, Cf>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)smem);
       if (dev >= 0 && dev < 64) attr_set[dev] = true;
     }
     const int64_t tiles = ((n + Cf::BN - 1) / Cf::BN) * ((m + Cf::BM - 1) / Cf::BM);
     if (tiles > 0x7fffffffLL) return MW_ERR_INVALID;
     if (batch == 1 && Cin == nullptr) {
-      gemm_kernel<K, VAR, false><<<(unsigned)tiles, NT, smem, st>>>(
+      gemm_kernel<K, VAR, false, Cf><<<(unsigned)tiles, NT, smem, st>>>(
           A, lda, sA, B, ldb, sB, C, ldc, sC, m, n, kd, nullptr, 0, 0, 1, 0, 0, 0, 0);
     } else {
       const unsigned gy = (unsigned)(batch < 65535 ? batch : 65535);
-      gemm_kernel<K, VAR, true><<<dim3((unsigned)tiles, gy), NT, smem, st>>>(
+      gemm_kernel<K, VAR, true, Cf><<<dim3((unsigned)tiles, gy), NT, smem, st>>>(
           A, lda, sA, B, ldb, sB, C, ldc, sC, m, n, kd, Cin, ldci, sCi, batch, bsA, bsB, bsC, bsCi);
     }
     return launch_status();

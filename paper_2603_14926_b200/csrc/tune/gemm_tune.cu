@@ -1,0 +1,75 @@
+// gemm_tune.cu — tuning harness (NOT part of the product library): the
+// product GEMM kernel template instantiated with alternative tile
+// configurations, so scripts/tune_gemm.py can time them on a B200 and
+// check their output is bit-identical to the product kernel.
+#include "../gemm_kernel.cuh"
+
+namespace mw {
+#define CFG(NAME, bm, bn, bk, tm, tn, minb) \
+  struct NAME {                              \
+    static constexpr int BM = bm, BN = bn, BK = bk, TM = tm, TN = tn, MINB = minb; \
+  };
+CFG(C64x64_44_2, 64, 64, 16, 4, 4, 2)
+CFG(C64x32_42_3, 64, 32, 16, 4, 2, 3)
+CFG(C32x64_24_3, 32, 64, 16, 2, 4, 3)
+CFG(C64x64_44_2_bk8, 64, 64, 8, 4, 4, 2)
+CFG(C32x64_24_2, 32, 64, 16, 2, 4, 2)
+CFG(C32x32_22_3, 32, 32, 16, 2, 2, 3)
+CFG(C64x32_42_2, 64, 32, 16, 4, 2, 2)
+CFG(C32x32_22_2, 32, 32, 16, 2, 2, 2)
+CFG(C16x32_12_4, 16, 32, 16, 1, 2, 4)
+CFG(C32x16_21_4, 32, 16, 16, 2, 1, 4)
+CFG(C32x32_22_2_bk32, 32, 32, 32, 2, 2, 2)
+CFG(C32x64_24_1, 32, 64, 16, 2, 4, 1)
+
+template <int K, class Cf>
+static int launch(const double* A, const double* B, double* C, int64_t n, cudaStream_t st) {
+  constexpr int NT = (Cf::BM / Cf::TM) * (Cf::BN / Cf::TN);
+  const size_t smem = GemmSmem<K, Cf>::BYTES;
+  cudaFuncSetAttribute(gemm_kernel<K, BRANCH_FREE, false, Cf>,
+                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int64_t tiles = ((n + Cf::BN - 1) / Cf::BN) * ((n + Cf::BM - 1) / Cf::BM);
+  gemm_kernel<K, BRANCH_FREE, false, Cf><<<(unsigned)tiles, NT, smem, st>>>(
+      A, n, n * n, B, n, n * n, C, n, n * n, n, n, n, nullptr, 0, 0, 1, 0, 0, 0, 0);
+  return launch_status();
+}
+
+template <int K>
+static int run(int cfg, const double* A, const double* B, double* C, int64_t n, cudaStream_t st) {
+  switch (cfg) {
+    case 0: return launch<K, C64x64_44_2>(A, B, C, n, st);
+    case 1: return launch<K, C64x32_42_3>(A, B, C, n, st);
+    case 2: return launch<K, C32x64_24_3>(A, B, C, n, st);
+    case 3: return launch<K, C64x64_44_2_bk8>(A, B, C, n, st);
+    case 4: return launch<K, C32x64_24_2>(A, B, C, n, st);
+    case 5: return launch<K, C32x32_22_3>(A, B, C, n, st);
+    case 6: return launch<K, C64x32_42_2>(A, B, C, n, st);
+    case 7: return launch<K, C32x32_22_2>(A, B, C, n, st);
+    case 8: return launch<K, C16x32_12_4>(A, B, C, n, st);
+    case 9: return launch<K, C32x16_21_4>(A, B, C, n, st);
+    case 10: return launch<K, C32x32_22_2_bk32>(A, B, C, n, st);
+    case 11: return launch<K, C32x64_24_1>(A, B, C, n, st);
+    default: return MW_ERR_INVALID;
+  }
+}
+
+int sm_count() { return 148; }
+}  // namespace mw
+
+using namespace mw;
+
+extern "C" int mwt_num_configs(void) { return 12; }
+extern "C" const char* mwt_config_name(int cfg) {
+  static const char* names[] = {"64x64_44_2", "64x32_42_3", "32x64_24_3", "64x64_44_2_bk8",
+                                "32x64_24_2", "32x32_22_3", "64x32_42_2", "32x32_22_2",
+                                "16x32_12_4", "32x16_21_4", "32x32_22_2_bk32", "32x64_24_1"};
+  return (cfg >= 0 && cfg < 12) ? names[cfg] : "?";
+}
+extern "C" int mwt_gemm(int cfg, int k, const double* A, const double* B, double* C, int64_t n,
+                        void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (k == 2) return run<2>(cfg, A, B, C, n, st);
+  if (k == 3) return run<3>(cfg, A, B, C, n, st);
+  if (k == 4) return run<4>(cfg, A, B, C, n, st);
+  return MW_ERR_INVALID;
+}
