@@ -109,7 +109,7 @@ def test_dd_standard_add_is_accurate_add(sass):
 
 def test_gemm_inner_loop_has_no_contraction(sass):
     """DD GEMM: the MAC body issues exactly one DFMA per product."""
-    hits = [f for f in sass if f.startswith("_ZN2mw11gemm_kernelILi2ELi1ELb0E")]
+    hits = [f for f in sass if f.startswith("_ZN2mw11gemm_kernelILi2ELi1ELb0E") and "GemmCfg" in f]
     assert len(hits) == 1
     a, m, f, _, _ = mix(sass[hits[0]])
     # 4x4 register tile per t step: 16 MACs -> 16 DFMA, 48 DMUL, 16*25 DADD
