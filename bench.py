@@ -275,59 +275,84 @@ def run_ours(args):
     # ---- e2e: public API, host buffers in / results out, every step
     e2e = None
     if not args.no_e2e:
+        # pinned host buffers, pre-split into row / point chunks so each chunk
+        # streams in (and its result out) while the previous one computes
+        # GEMMs are not split (a row chunk would add a partial last wave per
+        # launch); the smallest-input product goes first so the others' inputs
+        # stream in behind it, and Horner's points are chunked 8 ways so its
+        # output drains while the later chunks compute.
+        NCH_G, NCH_H = 1, 8
         a_pin, b_pin, c_pin = [], [], []
-        for g in gdata:
+        for g in sorted(gdata, key=lambda g: g["k"] * g["n"] ** 2):
             lo, hi = g["lo"], g["hi"]
-            a_pin.append(torch.from_numpy(np.ascontiguousarray(g["a_host"][:, lo:hi])).pin_memory())
+            cuts = np.linspace(lo, hi, NCH_G + 1).astype(int)
+            a_pin.append([torch.from_numpy(np.ascontiguousarray(g["a_host"][:, r0:r1])).pin_memory()
+                          for r0, r1 in zip(cuts[:-1], cuts[1:]) if r1 > r0])
             b_pin.append(torch.from_numpy(g["b_host"]).pin_memory())
-            c_pin.append(torch.empty((g["k"], hi - lo, g["n"]), dtype=torch.float64).pin_memory())
-        x_pin = torch.from_numpy(np.ascontiguousarray(xh[:, plo:phi])).pin_memory()
-        y_pin = torch.empty_like(x_pin).pin_memory()
+            c_pin.append([torch.empty((g["k"], r1 - r0, g["n"]), dtype=torch.float64).pin_memory()
+                          for r0, r1 in zip(cuts[:-1], cuts[1:]) if r1 > r0])
+        pcuts = np.linspace(plo, phi, NCH_H + 1).astype(int)
+        x_pin = [torch.from_numpy(np.ascontiguousarray(xh[:, p0:p1])).pin_memory()
+                 for p0, p1 in zip(pcuts[:-1], pcuts[1:]) if p1 > p0]
+        y_pin = [torch.empty_like(t).pin_memory() for t in x_pin]
         c_pin_coeffs = torch.from_numpy(coeffs).pin_memory()
-        h2d = sum(t.numel() * 8 for t in a_pin + b_pin) + x_pin.numel() * 8 + c_pin_coeffs.numel() * 8
-        d2h = sum(t.numel() * 8 for t in c_pin) + y_pin.numel() * 8
+        h2d = (sum(t.numel() * 8 for ts in a_pin for t in ts) + sum(t.numel() * 8 for t in b_pin)
+               + sum(t.numel() * 8 for t in x_pin) + c_pin_coeffs.numel() * 8)
+        d2h = sum(t.numel() * 8 for ts in c_pin for t in ts) + sum(t.numel() * 8 for t in y_pin)
         plan = mw.MatMulPlan(scheme="naive", variant=BF)
-
         h2d_stream = torch.cuda.Stream()
         d2h_stream = torch.cuda.Stream()
 
         def e2e_step():
-            """Public API end to end; H2D of all inputs is issued up front on a
-            copy stream (part i+1's inputs stream in while part i computes),
-            each result's D2H runs on a second copy stream behind its compute."""
+            """Public API end to end (MWMatrix / matmul / MWPolynomial /
+            horner_eval_batched) over pinned host buffers: every input chunk
+            is copied H2D on a copy stream, computed on the current stream as
+            soon as it lands, and its result copied D2H on a second copy stream
+            behind it, so transfers overlap compute."""
             cur = torch.cuda.current_stream()
             h2d_stream.wait_stream(cur)
             staged = []
             with torch.cuda.stream(h2d_stream):
-                for ap, bp in zip(a_pin, b_pin):
-                    A = ap.to("cuda", non_blocking=True)
+                for bp, chunks in zip(b_pin, a_pin):
                     B = bp.to("cuda", non_blocking=True)
+                    parts = []
+                    for ap in chunks:
+                        A = ap.to("cuda", non_blocking=True)
+                        ev = torch.cuda.Event()
+                        ev.record()
+                        parts.append((A, ev))
+                    staged.append((B, parts))
+                cf = c_pin_coeffs.to("cuda", non_blocking=True)
+                xs = []
+                for xp in x_pin:
+                    X = xp.to("cuda", non_blocking=True)
                     ev = torch.cuda.Event()
                     ev.record()
-                    staged.append((A, B, ev))
-                cf = c_pin_coeffs.to("cuda", non_blocking=True)
-                xd = x_pin.to("cuda", non_blocking=True)
-                evx = torch.cuda.Event()
-                evx.record()
-            for (A, B, ev), cp in zip(staged, c_pin):
-                cur.wait_event(ev)
-                A.record_stream(cur)
-                B.record_stream(cur)
-                if A.shape[1]:
-                    C = mw.matmul(mw.MWMatrix(A), mw.MWMatrix(B), plan).planes
-                    d2h_stream.wait_stream(cur)
-                    with torch.cuda.stream(d2h_stream):
-                        cp.copy_(C, non_blocking=True)
-                    C.record_stream(d2h_stream)
-            cur.wait_event(evx)
-            cf.record_stream(cur)
-            xd.record_stream(cur)
-            if xd.shape[1]:
-                yv = mw.horner_eval_batched(mw.MWPolynomial(cf), mw.LaneBatch(xd), BF).planes
+                    xs.append((X, ev))
+
+            def drain(dev_t, host_t):
                 d2h_stream.wait_stream(cur)
                 with torch.cuda.stream(d2h_stream):
-                    y_pin.copy_(yv, non_blocking=True)
-                yv.record_stream(d2h_stream)
+                    host_t.copy_(dev_t, non_blocking=True)
+                dev_t.record_stream(d2h_stream)
+
+            for (B, parts), cps in zip(staged, c_pin):
+                Bm = None
+                for (A, ev), cp in zip(parts, cps):
+                    cur.wait_event(ev)
+                    A.record_stream(cur)
+                    if Bm is None:
+                        B.record_stream(cur)
+                        Bm = mw.MWMatrix(B)
+                    drain(mw.matmul(mw.MWMatrix(A), Bm, plan).planes, cp)
+            P = None
+            for (X, ev), yp in zip(xs, y_pin):
+                cur.wait_event(ev)
+                X.record_stream(cur)
+                if P is None:
+                    cf.record_stream(cur)
+                    P = mw.MWPolynomial(cf)
+                drain(mw.horner_eval_batched(P, mw.LaneBatch(X), BF).planes, yp)
             cur.wait_stream(d2h_stream)
 
         for _ in range(max(1, min(args.warmup, 2))):
