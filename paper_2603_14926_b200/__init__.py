@@ -21,8 +21,10 @@ from .poly import (
     eval_complex_batched,
     horner_eval,
     horner_eval_batched,
+    random_polynomial,
 )
 from .roots import (
+    DKSweepGraph,
     CollisionError,
     MonicPoly,
     NoConvergence,
@@ -33,6 +35,8 @@ from .roots import (
     dk_solve,
     dk_sweeps,
     radius_estimate,
+    chebyshev_coeffs,
+    residual_check,
 )
 
 __version__ = "0.1.0"
@@ -43,7 +47,8 @@ __all__ = [
     "MatMulPlan", "MWMatrix", "CMWMatrix", "Scheme", "matmul", "cmatmul", "gen_complex_test_matrices",
     "BITS", "Variant", "ulp_k",
     "MWPolynomial", "horner_eval", "horner_eval_batched", "estrin_eval", "estrin_eval_batched",
-    "eval_complex", "eval_complex_batched",
+    "eval_complex", "eval_complex_batched", "random_polynomial",
     "MonicPoly", "RootState", "CollisionError", "NoConvergence", "aberth_init", "radius_estimate",
-    "default_tolerance", "dk_iterate", "dk_sweeps", "dk_solve",
+    "default_tolerance", "dk_iterate", "dk_sweeps", "dk_solve", "DKSweepGraph", "chebyshev_coeffs",
+    "residual_check",
 ]

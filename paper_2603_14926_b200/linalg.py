@@ -31,7 +31,7 @@ from .batch import LaneBatch, as_planes
 from .multiword import BITS, Variant, variant_code
 
 __all__ = ["Scheme", "MatMulPlan", "MWMatrix", "CMWMatrix", "matmul", "cmatmul", "gemv",
-           "gen_complex_test_matrices"]
+           "gen_complex_test_matrices", "gen_test_matrices", "sqrt_constant"]
 
 
 class Scheme(enum.Enum):
@@ -157,6 +157,46 @@ class CMWMatrix:
 
     def __repr__(self):
         return f"CMWMatrix(k={self.k}, rows={self.rows}, cols={self.cols})"
+
+
+def sqrt_constant(value: int, k: int) -> tuple:
+    """K-word rounding of sqrt(value) (linalg.sqrt_constant, 217-221): the
+    reference rounds its 300-bit oracle root; here mpmath at 400 bits, both
+    by greedy nearest-double extraction."""
+    import mpmath
+    from fractions import Fraction
+
+    from .multiword import from_fraction
+
+    mpmath.mp.prec = 400
+    sign, man, exp, _ = mpmath.sqrt(mpmath.mpf(value))._mpf_
+    fr = Fraction(int(man)) * (Fraction(2) ** int(exp))
+    return from_fraction(-fr if sign else fr, k)
+
+
+def gen_test_matrices(n: int, k: int, device=None):
+    """The paper's accuracy-benchmark pair (linalg.py:224-244):
+    a_ij = sqrt(5) (i+j-1), b_ij = sqrt(3) (n-i+1), 1-based; each entry the
+    K-word Standard product of the rounded constant with the exact integer
+    factor, computed on the device (batch_mul STANDARD)."""
+    if n < 1:
+        raise ValueError("n must be >= 1")
+    from .batch import LaneBatch, batch_mul
+
+    i_idx = np.arange(1, n + 1).reshape(n, 1)
+    j_idx = np.arange(1, n + 1).reshape(1, n)
+    fac_a = (i_idx + j_idx - 1).astype(np.float64)
+    fac_b = np.broadcast_to((n - i_idx + 1).astype(np.float64), (n, n)).copy()
+    out = []
+    for const, fac in ((sqrt_constant(5, k), fac_a), (sqrt_constant(3, k), fac_b)):
+        cst = np.zeros((k, n * n))
+        f = np.zeros((k, n * n))
+        for c in range(k):
+            cst[c] = const[c]
+        f[0] = fac.ravel()
+        prod = batch_mul(LaneBatch(cst, device=device), LaneBatch(f, device=device), Variant.STANDARD)
+        out.append(MWMatrix(prod.planes.reshape(k, n, n)))
+    return out[0], out[1]
 
 
 def gen_complex_test_matrices(n: int, seed: int, k: int, device=None):

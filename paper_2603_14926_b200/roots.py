@@ -44,6 +44,8 @@ __all__ = [
     "DKSweepGraph",
     "dk_solve",
     "default_tolerance",
+    "chebyshev_coeffs",
+    "residual_check",
 ]
 
 INT32_MAX = 2**31 - 1
@@ -390,3 +392,44 @@ def dk_solve(q: MonicPoly, variant: Variant = Variant.STANDARD, tol: float | Non
             state.converged = True
             return state, state.iteration
     raise NoConvergence(f"no convergence in {max_iter} sweeps", state)
+
+
+# ------------------------------------------------------ test problems (host)
+def chebyshev_coeffs(n: int, k: int, weight=None, device=None) -> MonicPoly:
+    """Even-coefficient integration test polynomial of degree n
+    (roots.py:343-368): a_n = 1, odd-from-top coefficients zero,
+    a_{n-2m} = -sum_{j=1..m} weight(j) a_{n-2(m-j)}, default weight
+    1/(2j+1); exact rationals rounded per coefficient to K words."""
+    if n < 2:
+        raise ValueError("n must be >= 2")
+    if weight is None:
+        def weight(j):
+            return Fraction(1, 2 * j + 1)
+    b = [Fraction(1)]
+    for m in range(1, n // 2 + 1):
+        b.append(-sum(weight(j) * b[m - j] for j in range(1, m + 1)))
+    arr = np.zeros((k, n))
+    for i in range(n):
+        d = n - i
+        if d % 2 == 0:
+            arr[:, i] = from_fraction(b[d // 2], k)
+    return MonicPoly(arr, device=device)
+
+
+def residual_check(q: MonicPoly, roots) -> float:
+    """max_i |q(z_i)| evaluated exactly (roots.py:371-385 uses a 300-bit
+    oracle; here exact rationals, then rounded to a float)."""
+    arr = q.planes.cpu().numpy()
+    coeffs = [sum(Fraction(float(c)) for c in arr[:, i]) for i in range(q.n)] + [Fraction(1)]
+    worst = 0.0
+    for zre, zim in roots:
+        zr = sum(Fraction(float(c)) for c in zre)
+        zi = sum(Fraction(float(c)) for c in zim)
+        ar, ai = coeffs[-1], Fraction(0)
+        for c in reversed(coeffs[:-1]):
+            ar, ai = ar * zr - ai * zi + c, ar * zi + ai * zr
+        mag2 = ar * ar + ai * ai
+        if mag2:
+            worst = max(worst, math.sqrt(float(mag2)) if float(mag2) > 0 else
+                        2.0 ** ((mag2.numerator.bit_length() - mag2.denominator.bit_length()) / 2.0))
+    return worst

@@ -22,6 +22,7 @@ public functions on small seeded cases:
               the R0 = 1.5 Aberth circle                     (roots.py:188-315)
   cgemm.npz   cmatmul (3M) on gen_complex_test_matrices     (linalg.py:247-276, 572-590)
   strassen.npz matmul(scheme="strassen") with even splits and odd peels (linalg.py:390-546)
+  testmats.npz gen_test_matrices(16, k) and chebyshev_coeffs(12, k) (linalg.py:224-244, roots.py:343-368)
   polyx.npz   estrin_eval per point (== estrin_eval_batched) and
               eval_complex Horner / Estrin                   (poly.py:106-178)
 
@@ -360,6 +361,17 @@ def main():
     if want("strassen"):
         np.savez_compressed(os.path.join(HERE, "strassen.npz"), **out)
     print(f"strassen done {time.time() - t0:.1f}s")
+
+    # ------------------------------------------------------------- accuracy inputs
+    out = {}
+    for k in (2, 3, 4):
+        a, b = linalg.gen_test_matrices(16, k)
+        out[f"k{k}_a"] = np.stack(a.comps)
+        out[f"k{k}_b"] = np.stack(b.comps)
+        q = roots.chebyshev_coeffs(12, k)
+        out[f"k{k}_cheb12"] = np.stack(q.comps)
+    if want("testmats"):
+        np.savez_compressed(os.path.join(HERE, "testmats.npz"), **out)
 
     print(f"all done {time.time() - t0:.1f}s  (mwfloat {getattr(mwfloat, '__version__', '?')})")
 
