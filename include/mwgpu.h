@@ -71,7 +71,12 @@ int mw_ew_div(int k, int variant, const double* a, int64_t sa, const double* b,
 int mw_axpy(int k, int variant, const double* alpha_host, const double* x,
             int64_t sx, double* y, int64_t sy, int64_t n, void* stream);
 
-/* Workspace (in doubles) mw_dot needs for length n (0 when n <= 4096). */
+/* Workspace (in doubles) mw_dot needs for length n (0 when n <= 4096).
+ * For 4096 < n <= 2^20 the tree dot is one launch whose last block folds
+ * the block partials; its ticket lives in ws[0], which must be zero before
+ * the first call (every call leaves it zero and never writes it
+ * otherwise, whatever n).  Do not share one workspace between concurrently
+ * running calls. */
 int64_t mw_dot_workspace(int k, int64_t n);
 
 /* out_dev[0..k) = sum_t x_t (*) y_t.  The definition is the naive-matmul

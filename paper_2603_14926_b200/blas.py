@@ -46,6 +46,21 @@ def _check_pair(x: LaneBatch, y: LaneBatch):
         raise ValueError("mixed lane widths")
 
 
+_WS: dict = {}
+
+
+def _workspace(device, n: int) -> torch.Tensor:
+    """Zero-initialised dot workspace, cached per (device, stream) and grown
+    on demand (the single-launch dot re-arms its ticket itself).  Calls on
+    one stream are serialised, so reuse is safe."""
+    key = (str(device), torch.cuda.current_stream(device).cuda_stream)
+    ws = _WS.get(key)
+    if ws is None or ws.numel() < max(n, 1):
+        ws = torch.zeros(max(n, 1), dtype=torch.float64, device=device)
+        _WS[key] = ws
+    return ws
+
+
 def dot_tensor(x: LaneBatch, y: LaneBatch, variant: Variant = Variant.BRANCH_FREE, order: str = "tree",
                out: torch.Tensor | None = None) -> torch.Tensor:
     """dot(x, y) as a (K,) device tensor (no host synchronisation)."""
@@ -58,7 +73,7 @@ def dot_tensor(x: LaneBatch, y: LaneBatch, variant: Variant = Variant.BRANCH_FRE
     if out is None:
         out = torch.empty(k, dtype=torch.float64, device=x.device)
     wsn = lib.mw_dot_workspace(k, n) if o == _lib.ORDER_TREE else 0
-    ws = torch.empty(max(wsn, 1), dtype=torch.float64, device=x.device)
+    ws = _workspace(x.device, wsn)
     rc = lib.mw_dot(k, v, x.planes.data_ptr(), n, y.planes.data_ptr(), n, n, ws.data_ptr(), out.data_ptr(), o,
                     _lib.stream_handle(x.device))
     _lib.check(rc, "mw_dot")

@@ -96,6 +96,55 @@ __global__ void __launch_bounds__(DOT_BLOCK) dot_partials_kernel(
   }
 }
 
+// Single-launch tree dot for 1 < nb <= 256 blocks: every block writes its
+// subtree root, the last block to finish (atomic ticket) folds the nb roots
+// with the same pairwise tree and re-arms the ticket for the next call.
+template <int K, int VAR>
+__global__ void __launch_bounds__(DOT_BLOCK) dot_fused_kernel(
+    const double* __restrict__ x, int64_t sx, const double* __restrict__ y, int64_t sy,
+    int64_t n, double* __restrict__ partials, unsigned int* __restrict__ ticket,
+    double* __restrict__ out) {
+  __shared__ bool is_last;
+  const int64_t base = blockIdx.x * DOT_PER_BLOCK + threadIdx.x;
+  const int64_t nb = gridDim.x;
+  V<K> acc = zero<K>();
+  if (blockIdx.x * DOT_PER_BLOCK + DOT_PER_BLOCK <= n) {
+    V<K> xs[DOT_LEAF], ys[DOT_LEAF];
+#pragma unroll
+    for (int j = 0; j < DOT_LEAF; ++j) {
+      xs[j] = load<K>(x, sx, base + j * DOT_BLOCK);
+      ys[j] = load<K>(y, sy, base + j * DOT_BLOCK);
+    }
+#pragma unroll
+    for (int j = 0; j < DOT_LEAF; ++j)
+      acc = Ops<K, VAR>::add(acc, Ops<K, VAR>::mul(xs[j], ys[j]));
+  } else {
+    for (int64_t t = base; t < n; t += DOT_BLOCK)
+      acc = Ops<K, VAR>::add(acc, Ops<K, VAR>::mul(load<K>(x, sx, t), load<K>(y, sy, t)));
+  }
+  V<K> r = block_tree<K, VAR>(acc, blockIdx.x * (int64_t)DOT_BLOCK, dot_partial_count(n));
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int c = 0; c < K; ++c) partials[c * nb + blockIdx.x] = r.c[c];
+    __threadfence();
+    is_last = atomicAdd(ticket, 1u) == (unsigned)(nb - 1);
+  }
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  V<K> v = zero<K>();
+  if (threadIdx.x < nb) {
+#pragma unroll
+    for (int c = 0; c < K; ++c) v.c[c] = __ldcg(partials + c * nb + threadIdx.x);
+  }
+  __syncthreads();  // block_tree reuses its shared buffer
+  V<K> root = block_tree<K, VAR>(v, 0, nb);
+  if (threadIdx.x == 0) {
+    store<K>(out, 1, 0, root);
+    *ticket = 0u;
+  }
+}
+
 // Tree stage above the leaves: groups of 256 values -> one subtree root.
 template <int K, int VAR>
 __global__ void __launch_bounds__(DOT_BLOCK) tree_fold_kernel(const double* __restrict__ in,
@@ -158,10 +207,19 @@ struct DotLaunch {
       dot_partials_kernel<K, VAR><<<1, DOT_BLOCK, 0, st>>>(x, sx, y, sy, n, out, 1);
       return launch_status();
     }
-    dot_partials_kernel<K, VAR><<<(unsigned)nb, DOT_BLOCK, 0, st>>>(x, sx, y, sy, n, ws, nb);
+    // ws[0] holds the single-launch ticket (zero before the first call,
+    // left zero by every call, never overwritten); partials start at ws + 1
+    unsigned int* ticket = reinterpret_cast<unsigned int*>(ws);
+    double* part = ws + 1;
+    if (nb <= DOT_BLOCK) {
+      dot_fused_kernel<K, VAR><<<(unsigned)nb, DOT_BLOCK, 0, st>>>(x, sx, y, sy, n, part, ticket,
+                                                                  out);
+      return launch_status();
+    }
+    dot_partials_kernel<K, VAR><<<(unsigned)nb, DOT_BLOCK, 0, st>>>(x, sx, y, sy, n, part, nb);
     int rc = launch_status();
     if (rc) return rc;
-    return fold_levels<K, VAR>(ws, nb, nb, ws + nb * K, out, st);
+    return fold_levels<K, VAR>(part, nb, nb, part + nb * K, out, st);
   }
 };
 
@@ -294,7 +352,9 @@ extern "C" int64_t mw_dot_workspace(int k, int64_t n) {
   if (k < 2 || k > 4 || n < 0) return 0;
   int64_t nb = ceil_div(n, DOT_PER_BLOCK);
   if (nb <= 1) return 0;
-  return nb * k + mw_tree_fold_workspace(k, nb);
+  // ws[0]: single-launch ticket; then nb*k partials (+ fold levels)
+  if (nb <= DOT_BLOCK) return 1 + nb * k;
+  return 1 + nb * k + mw_tree_fold_workspace(k, nb);
 }
 
 extern "C" int64_t mw_tree_fold_workspace(int k, int64_t count) {

@@ -81,9 +81,9 @@ def test_workspace_sizes():
     lib = _lib.load()
     assert lib.mw_dot_workspace(2, 4096) == 0
     assert lib.mw_dot_num_partials(4097) == 2
-    assert lib.mw_dot_workspace(2, 4097) == 2 * 2
-    assert lib.mw_dot_workspace(4, 65536) == 16 * 4
-    # 2^28 elements: 65536 partials, then 256 level-2 values
-    assert lib.mw_dot_workspace(2, 1 << 28) == 65536 * 2 + 256 * 2
+    assert lib.mw_dot_workspace(2, 4097) == 1 + 2 * 2  # ticket + partials
+    assert lib.mw_dot_workspace(4, 65536) == 1 + 16 * 4
+    # 2^28 elements: ticket, 65536 partials, then 256 level-2 values
+    assert lib.mw_dot_workspace(2, 1 << 28) == 1 + 65536 * 2 + 256 * 2
     assert lib.mw_tree_fold_workspace(3, 256) == 0
     assert lib.mw_tree_fold_workspace(3, 257) == 2 * 3

@@ -469,3 +469,19 @@ def test_strassen_within_8_ulp_of_naive(k, n):
                 _, e = math.frexp(scale[i, j])
                 worst = max(worst, float(d) / math.ldexp(1.0, e - 53 * k))
     assert worst <= 8.0
+
+
+def test_dot_single_launch_rearms_and_matches_two_stage():
+    """Repeated single-launch dots (ticket re-armed in-kernel) agree with the
+    two-stage path (mw_dot_partials + mw_tree_fold) bit for bit."""
+    from paper_2603_14926_b200 import dist as mwdist
+
+    rng = np.random.default_rng(12)
+    for n in (4097, 65536, 1 << 20):
+        x, y = gen.g_k(rng, 2, n), gen.g_k(rng, 2, n)
+        X, Y = LaneBatch(x), LaneBatch(y)
+        first = blas.dot_tensor(X, Y, Variant.BRANCH_FREE).cpu().numpy()
+        for _ in range(3):
+            assert_bitwise(blas.dot_tensor(X, Y, Variant.BRANCH_FREE).cpu().numpy(), first)
+        be = mwdist.gpu_dot_backend(Variant.BRANCH_FREE)
+        assert_bitwise(be.fold(be.partials(X.planes, Y.planes)).cpu().numpy(), first)
