@@ -53,6 +53,9 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline sample")
     ap.add_argument("--quick", action="store_true", help="small sizes (debug)")
     ap.add_argument("--no-secondary", action="store_true", help="skip configs 1, 2 and 5")
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend for N > 1 (gloo only to exercise the multi-rank "
+                         "logic where fewer GPUs than ranks exist; never for timing)")
     return ap.parse_args()
 
 
@@ -187,9 +190,13 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
+    dev_index = local % max(torch.cuda.device_count(), 1)
+    torch.cuda.set_device(dev_index)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev_index))
+        else:
+            dist.init_process_group("gloo")
     lib = _lib.load()
     stream = lambda: torch.cuda.current_stream().cuda_stream  # noqa: E731
 
@@ -250,7 +257,7 @@ def run_ours(args):
     barrier()
     torch.cuda.synchronize()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
+    with ClockSampler(dev_index) as clk:
         t0.record()
         for s in range(args.steps):
             step(ev[s])
@@ -547,7 +554,7 @@ def secondary(args, torch, dist, mw, world, rank, peak):
         fp = MAC_OPS[k] * m * m
         out[f"config2_gemv_{'td' if k == 3 else 'qd'}_n2048"] = {
             "ms": round(ms, 4), "G_MPops": round(2 * m * m / (ms / 1e3) / 1e9, 2),
-            "fp64_frac": round(fp / (ms / 1e3) / peak["dfma"], 4),
+            "fp64_frac": round(fp / (ms / 1e3) / peak["dfma"] / world, 4),
             "hbm_GBps": round(k * m * m * 8 / (ms / 1e3) / 1e9, 1), "order": "tree (128 partials per row)",
             "l2": "flushed before each call"}
         del A

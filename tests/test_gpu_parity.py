@@ -485,3 +485,34 @@ def test_dot_single_launch_rearms_and_matches_two_stage():
             assert_bitwise(blas.dot_tensor(X, Y, Variant.BRANCH_FREE).cpu().numpy(), first)
         be = mwdist.gpu_dot_backend(Variant.BRANCH_FREE)
         assert_bitwise(be.fold(be.partials(X.planes, Y.planes)).cpu().numpy(), first)
+
+
+# ------------------------------------------------------------ edge cases
+def test_empty_and_degenerate_shapes():
+    """Empty batches, 1x1 products, kd = 0, degree 0 and zero points all go
+    through the API without launching garbage (reference semantics)."""
+    e = LaneBatch(np.zeros((3, 0)))
+    assert batch_add(e, e, Variant.BRANCH_FREE).width == 0
+    assert blas.dot(e, e, Variant.BRANCH_FREE) == (0.0, 0.0, 0.0)
+    z = matmul(MWMatrix(np.zeros((2, 3, 0))), MWMatrix(np.zeros((2, 0, 4))), MatMulPlan(scheme="naive", variant="bf"))
+    assert z.numpy().shape == (2, 3, 4) and not z.numpy().any()
+    p0 = MWPolynomial(np.array([[2.5], [1e-20]]))
+    ys = horner_eval_batched(p0, LaneBatch(np.ones((2, 5))), Variant.BRANCH_FREE).numpy()
+    assert (ys[0] == 2.5).all() and (ys[1] == 1e-20).all()
+    assert horner_eval_batched(p0, LaneBatch(np.ones((2, 0))), Variant.BRANCH_FREE).width == 0
+    one = matmul(MWMatrix(np.array([[[3.0]], [[0.0]]])), MWMatrix(np.array([[[2.0]], [[0.0]]])),
+                 MatMulPlan(scheme="strassen", variant="bf"))
+    assert one.numpy()[0, 0, 0] == 6.0
+
+
+def test_nonfinite_values_propagate():
+    """Non-finite values propagate and never trap (multiword.py:18-20)."""
+    a = np.zeros((2, 4))
+    a[0] = [np.inf, -np.inf, np.nan, 1.0]
+    b = np.zeros((2, 4))
+    b[0] = [1.0, 1.0, 1.0, 0.0]
+    la, lb = LaneBatch(a), LaneBatch(b)
+    s = batch_add(la, lb, Variant.BRANCH_FREE).numpy()
+    assert not np.isfinite(s[0, :3]).any()
+    q = batch_div(la, lb, Variant.BRANCH_FREE).numpy()
+    assert not np.isfinite(q[0, 3])
