@@ -173,6 +173,10 @@ int mw_dk_sweep(int k, int variant, const double* coeffs, int64_t sc,
                 int64_t so, double* step_mag, int* flag_dev, int exact_order,
                 void* stream);
 
+/* Tuning knob of the exact-order sweep: roots per CTA (1..32, default 16).
+ * Results do not depend on it (each root is one chain in reference order). */
+int mw_dk_exact_set_roots_per_cta(int roots);
+
 /* FP64 pipe microbenchmark: 8 independent DFMA (op = 0) or DADD (op = 1)
  * chains per thread, 8 unrolled steps per iteration: executes
  * blocks * threads * iters * 64 FP64 ops, no memory traffic; the caller

@@ -51,6 +51,7 @@ _SIGS = {
     "mw_horner": ([I, I, P, I64, I64, P, I64, P, I64, I64, P], I),
     "mw_poly_eval": ([I, I, P, I64, I64, P, P, I64, P, P, I64, I64, I, P], I),
     "mw_dk_sweep": ([I, I, P, I64, I64, P, P, I64, I64, I64, P, P, I64, P, P, I, P], I),
+    "mw_dk_exact_set_roots_per_cta": ([I], I),
     "mw_fp64_peak_kernel": ([I, I, I, I, P, P], I),
     "mw_device_sm_count": ([], I),
 }

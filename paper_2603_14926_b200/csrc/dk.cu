@@ -12,9 +12,11 @@
 // with the local 3M complex product (roots.py:258-267).
 //
 // exact_order = 1: the numerator and the denominator of root i run on two
-// lanes of different warps (independent chains), each replaying the
-// reference order op for op; the tail follows on the numerator lane.  Bit
-// exact.  The reciprocal of mag is computed once and applied to both
+// lanes of different warps (independent chains, no block barrier between
+// them: the denominator warp stages z_j with warp-level syncs), each
+// replaying the reference order op for op; the tail follows on the
+// numerator lane.  Bit exact.  Each step is one dependent chain (8-cycle
+// FP64 latency, measured), so a sweep costs ~n steps of ~700 cycles (TD).  The reciprocal of mag is computed once and applied to both
 // parts, which is the identical op sequence the reference runs twice.
 //
 // exact_order = 0 (tree): four warps per root (definition below): 64
@@ -78,7 +80,10 @@ __device__ __forceinline__ void dk_tail(const Cx<K, VAR>& acc, const Cx<K, VAR>&
   step_mag[i] = hypot(step_re.c[0], step_im.c[0]);
 }
 
-constexpr int DK_EXACT_ROOTS = 32;  // roots per CTA (two warps: num + den)
+constexpr int DK_EXACT_ROOTS = 32;  // lanes per role warp (two warps: num + den)
+// Roots handled per CTA (<= 32; lanes beyond it idle).  Fewer roots per
+// CTA spread the 2n sequential chains over more SM sub-partitions.
+static int g_dk_exact_roots = 16;
 constexpr int DK_CH = 128;          // roots staged in smem per chunk
 
 template <int K, int VAR>
@@ -87,21 +92,25 @@ __global__ void __launch_bounds__(2 * DK_EXACT_ROOTS)
                     const double* __restrict__ zre, const double* __restrict__ zim, int64_t sz,
                     int64_t i0, int64_t i1, double* __restrict__ zre_out,
                     double* __restrict__ zim_out, int64_t so, double* __restrict__ step_mag,
-                    int* __restrict__ flag) {
+                    int* __restrict__ flag, int roots_per_cta) {
   using O = Ops<K, VAR>;
   __shared__ double zs[2][K][DK_CH];
   __shared__ double dx[2][K][DK_EXACT_ROOTS];
   const int lane = threadIdx.x & 31;
   const bool is_den = threadIdx.x >= 32;
-  const int64_t i = i0 + (int64_t)blockIdx.x * DK_EXACT_ROOTS + lane;
-  const bool live = i < i1;
+  const int64_t i = i0 + (int64_t)blockIdx.x * roots_per_cta + lane;
+  const bool live = lane < roots_per_cta && i < i1;
 
   Cx<K, VAR> z;
   z.re = live ? load<K>(zre, sz, i) : zero<K>();
   z.im = live ? load<K>(zim, sz, i) : zero<K>();
   Cx<K, VAR> acc = c_one<K, VAR>();
 
+  // unroll 2 lets the scheduler overlap consecutive steps (TD: 1.15x);
+  // QD's larger body does better rolled (register pressure)
+  constexpr int UNR = K < 4 ? 2 : 1;
   if (!is_den) {
+#pragma unroll UNR
     for (int64_t c = n - 1; c >= 0; --c) {
       acc = c_mul(acc, z);
       Cx<K, VAR> ci;
@@ -111,17 +120,20 @@ __global__ void __launch_bounds__(2 * DK_EXACT_ROOTS)
       acc.im = O::add(acc.im, ci.im);
     }
   }
-  // denominator: all threads stage z_j chunks (both warps join the syncs)
-  for (int64_t j0 = 0; j0 < n; j0 += DK_CH) {
-    const int cnt = (int)((n - j0) < DK_CH ? (n - j0) : DK_CH);
-    __syncthreads();
-    for (int e = threadIdx.x; e < K * cnt; e += 2 * DK_EXACT_ROOTS) {
-      const int c = e / cnt, jj = e % cnt;
-      zs[0][c][jj] = zre[c * sz + j0 + jj];
-      zs[1][c][jj] = zim[c * sz + j0 + jj];
-    }
-    __syncthreads();
-    if (is_den) {
+  // denominator: the den warp alone stages z_j chunks (warp-level syncs, so
+  // the numerator warp's Horner chain runs concurrently instead of waiting
+  // at block barriers)
+  if (is_den) {
+    for (int64_t j0 = 0; j0 < n; j0 += DK_CH) {
+      const int cnt = (int)((n - j0) < DK_CH ? (n - j0) : DK_CH);
+      __syncwarp();
+      for (int e = lane; e < K * cnt; e += 32) {
+        const int c = e / cnt, jj = e % cnt;
+        zs[0][c][jj] = zre[c * sz + j0 + jj];
+        zs[1][c][jj] = zim[c * sz + j0 + jj];
+      }
+      __syncwarp();
+#pragma unroll UNR
       for (int jj = 0; jj < cnt; ++jj) {
         const int64_t j = j0 + jj;
         Cx<K, VAR> zj, f;
@@ -345,9 +357,10 @@ struct DkLaunch {
                  cudaStream_t st) {
     const int64_t cnt = i1 - i0;
     if (exact) {
-      const int64_t blocks = (cnt + DK_EXACT_ROOTS - 1) / DK_EXACT_ROOTS;
+      const int r = g_dk_exact_roots;
+      const int64_t blocks = (cnt + r - 1) / r;
       dk_exact_kernel<K, VAR><<<(unsigned)blocks, 2 * DK_EXACT_ROOTS, 0, st>>>(
-          coeffs, sc, n, zre, zim, sz, i0, i1, zre_out, zim_out, so, step_mag, flag);
+          coeffs, sc, n, zre, zim, sz, i0, i1, zre_out, zim_out, so, step_mag, flag, r);
     } else {
       dk_tree_kernel<K, VAR><<<(unsigned)cnt, 96, 0, st>>>(
           coeffs, sc, n, zre, zim, sz, i0, i1, zre_out, zim_out, so, step_mag, flag);
@@ -359,6 +372,13 @@ struct DkLaunch {
 }  // namespace mw
 
 using namespace mw;
+
+// Tuning knob for the exact-order sweep: roots per CTA (1..32).
+extern "C" int mw_dk_exact_set_roots_per_cta(int r) {
+  if (r < 1 || r > 32) return MW_ERR_INVALID;
+  g_dk_exact_roots = r;
+  return MW_OK;
+}
 
 extern "C" int mw_dk_sweep(int k, int variant, const double* coeffs, int64_t sc, int64_t n,
                            const double* zre, const double* zim, int64_t sz, int64_t i0,
