@@ -25,6 +25,7 @@ struct GemmCfg;
 template <>
 struct GemmCfg<2> {
   static constexpr int BM = 64, BN = 64, BK = 16, TM = 4, TN = 4, MINB = 2;
+  static constexpr bool VEC = false;
 };
 // TD and QD: 64x32 tile, 4x2 per thread, 256 threads.  (Tile sweep on
 // B200 with tune/gemm_tune.cu + scripts/tune_gemm.py: every non-spilling
@@ -32,10 +33,12 @@ struct GemmCfg<2> {
 template <>
 struct GemmCfg<3> {
   static constexpr int BM = 64, BN = 32, BK = 16, TM = 4, TN = 2, MINB = 2;
+  static constexpr bool VEC = false;
 };
 template <>
 struct GemmCfg<4> {
   static constexpr int BM = 64, BN = 32, BK = 16, TM = 4, TN = 2, MINB = 2;
+  static constexpr bool VEC = false;
 };
 
 template <int K, int VAR>

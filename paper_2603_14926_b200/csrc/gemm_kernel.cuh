@@ -10,10 +10,14 @@ namespace mw {
 
 constexpr int GEMM_GROUP_M = 16;
 
+// Cf::VEC = true: A staged transposed (t-major, rows contiguous) and each
+// thread owns contiguous rows / columns, so register fragments load as
+// 128-bit double2 pairs (half the LDS instructions).  Same arithmetic and
+// order: results are bit-identical.
 template <int K, class C>
 struct GemmSmem {
-  static constexpr int APAD = C::BK + 2;  // row stride of the A tile (doubles)
-  static constexpr int A_ELEMS = K * C::BM * APAD;
+  static constexpr int APAD = C::VEC ? C::BM + 2 : C::BK + 2;  // A tile row stride (doubles)
+  static constexpr int A_ELEMS = C::VEC ? K * C::BK * APAD : K * C::BM * APAD;
   static constexpr int B_ELEMS = K * C::BK * C::BN;
   static constexpr int STAGE = A_ELEMS + B_ELEMS;
   static constexpr int STAGES = 2;
@@ -49,8 +53,11 @@ __global__ void __launch_bounds__((Cf::BM / Cf::TM) * (Cf::BN / Cf::TN), Cf::MIN
   const int64_t m0 = (first_m + in_group % gsize) * BM, n0 = (in_group / gsize) * BN;
 
   auto As = [&](int st, int c, int row, int t) -> double& {
+    if (Cf::VEC) return smem[st * S::STAGE + (c * BK + t) * S::APAD + row];
     return smem[st * S::STAGE + (c * BM + row) * S::APAD + t];
   };
+  // column of the thread's q-th output
+  auto col_of = [&](int q) { return Cf::VEC ? tx * TN + q : tx + q * TX; };
   auto Bs = [&](int st, int c, int t, int col) -> double& {
     return smem[st * S::STAGE + S::A_ELEMS + (c * BK + t) * BN + col];
   };
@@ -60,7 +67,8 @@ __global__ void __launch_bounds__((Cf::BM / Cf::TM) * (Cf::BN / Cf::TN), Cf::MIN
     // A tile: K x BM x BK, consecutive threads walk a row's BK doubles.
 #pragma unroll
     for (int e = tid; e < K * BM * BK; e += NT) {
-      const int c = e / (BM * BK), rem = e % (BM * BK), row = rem / BK, t = rem % BK;
+      const int c = e / (BM * BK), rem = e % (BM * BK);
+      const int row = Cf::VEC ? rem % BM : rem / BK, t = Cf::VEC ? rem / BM : rem % BK;
       const int64_t gi = m0 + row, gt = k0 + t;
       const bool ok = gi < m && gt < kd;
       const double* src = ok ? A + c * sA + gi * lda + gt : A;
@@ -92,7 +100,7 @@ __global__ void __launch_bounds__((Cf::BM / Cf::TM) * (Cf::BN / Cf::TN), Cf::MIN
       acc[r][q] = zero<K>();
       // optional initial accumulator (the Strassen peel folds start from a
       // product, linalg.py:470-500)
-      const int64_t gi = m0 + ty * TM + r, gj = n0 + tx + q * TX;
+      const int64_t gi = m0 + ty * TM + r, gj = n0 + col_of(q);
       if (EXT && Cin && gi < m && gj < n) acc[r][q] = load<K>(Cin + gi * ldci + gj, sCi, 0);
     }
 
@@ -116,14 +124,32 @@ __global__ void __launch_bounds__((Cf::BM / Cf::TM) * (Cf::BN / Cf::TN), Cf::MIN
 #pragma unroll 1
     for (int t = 0; t < tvalid; ++t) {
       V<K> a[TM], b[TN];
+      if (Cf::VEC) {
 #pragma unroll
-      for (int r = 0; r < TM; ++r)
+        for (int c = 0; c < K; ++c) {
 #pragma unroll
-        for (int c = 0; c < K; ++c) a[r].c[c] = As(st, c, ty * TM + r, t);
+          for (int r = 0; r < TM; r += 2) {
+            const double2 v = *reinterpret_cast<const double2*>(&As(st, c, ty * TM + r, t));
+            a[r].c[c] = v.x;
+            a[r + 1].c[c] = v.y;
+          }
 #pragma unroll
-      for (int q = 0; q < TN; ++q)
+          for (int q = 0; q < TN; q += 2) {
+            const double2 v = *reinterpret_cast<const double2*>(&Bs(st, c, t, tx * TN + q));
+            b[q].c[c] = v.x;
+            b[q + 1].c[c] = v.y;
+          }
+        }
+      } else {
 #pragma unroll
-        for (int c = 0; c < K; ++c) b[q].c[c] = Bs(st, c, t, tx + q * TX);
+        for (int r = 0; r < TM; ++r)
+#pragma unroll
+          for (int c = 0; c < K; ++c) a[r].c[c] = As(st, c, ty * TM + r, t);
+#pragma unroll
+        for (int q = 0; q < TN; ++q)
+#pragma unroll
+          for (int c = 0; c < K; ++c) b[q].c[c] = Bs(st, c, t, tx + q * TX);
+      }
 #pragma unroll
       for (int r = 0; r < TM; ++r)
 #pragma unroll
@@ -139,7 +165,7 @@ __global__ void __launch_bounds__((Cf::BM / Cf::TM) * (Cf::BN / Cf::TN), Cf::MIN
     if (gi >= m) continue;
 #pragma unroll
     for (int q = 0; q < TN; ++q) {
-      const int64_t gj = n0 + tx + q * TX;
+      const int64_t gj = n0 + col_of(q);
       if (gj >= n) continue;
 #pragma unroll
       for (int c = 0; c < K; ++c) C[c * sC + gi * ldc + gj] = acc[r][q].c[c];

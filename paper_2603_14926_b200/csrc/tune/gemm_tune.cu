@@ -5,10 +5,12 @@
 #include "../gemm_kernel.cuh"
 
 namespace mw {
-#define CFG(NAME, bm, bn, bk, tm, tn, minb) \
-  struct NAME {                              \
+#define CFGV(NAME, bm, bn, bk, tm, tn, minb, vec)                             \
+  struct NAME {                                                               \
     static constexpr int BM = bm, BN = bn, BK = bk, TM = tm, TN = tn, MINB = minb; \
+    static constexpr bool VEC = vec;                                          \
   };
+#define CFG(NAME, bm, bn, bk, tm, tn, minb) CFGV(NAME, bm, bn, bk, tm, tn, minb, false)
 CFG(C64x64_44_2, 64, 64, 16, 4, 4, 2)
 CFG(C64x32_42_3, 64, 32, 16, 4, 2, 3)
 CFG(C32x64_24_3, 32, 64, 16, 2, 4, 3)
@@ -21,6 +23,10 @@ CFG(C16x32_12_4, 16, 32, 16, 1, 2, 4)
 CFG(C32x16_21_4, 32, 16, 16, 2, 1, 4)
 CFG(C32x32_22_2_bk32, 32, 32, 32, 2, 2, 2)
 CFG(C32x64_24_1, 32, 64, 16, 2, 4, 1)
+CFGV(V64x64_44_2, 64, 64, 16, 4, 4, 2, true)
+CFGV(V64x32_42_2, 64, 32, 16, 4, 2, 2, true)
+CFGV(V32x32_22_2, 32, 32, 16, 2, 2, 2, true)
+CFGV(V64x64_44_2_bk8, 64, 64, 8, 4, 4, 2, true)
 
 template <int K, class Cf>
 static int launch(const double* A, const double* B, double* C, int64_t n, cudaStream_t st) {
@@ -49,6 +55,10 @@ static int run(int cfg, const double* A, const double* B, double* C, int64_t n, 
     case 9: return launch<K, C32x16_21_4>(A, B, C, n, st);
     case 10: return launch<K, C32x32_22_2_bk32>(A, B, C, n, st);
     case 11: return launch<K, C32x64_24_1>(A, B, C, n, st);
+    case 12: return launch<K, V64x64_44_2>(A, B, C, n, st);
+    case 13: return launch<K, V64x32_42_2>(A, B, C, n, st);
+    case 14: return launch<K, V32x32_22_2>(A, B, C, n, st);
+    case 15: return launch<K, V64x64_44_2_bk8>(A, B, C, n, st);
     default: return MW_ERR_INVALID;
   }
 }
@@ -58,12 +68,13 @@ int sm_count() { return 148; }
 
 using namespace mw;
 
-extern "C" int mwt_num_configs(void) { return 12; }
+extern "C" int mwt_num_configs(void) { return 16; }
 extern "C" const char* mwt_config_name(int cfg) {
   static const char* names[] = {"64x64_44_2", "64x32_42_3", "32x64_24_3", "64x64_44_2_bk8",
                                 "32x64_24_2", "32x32_22_3", "64x32_42_2", "32x32_22_2",
-                                "16x32_12_4", "32x16_21_4", "32x32_22_2_bk32", "32x64_24_1"};
-  return (cfg >= 0 && cfg < 12) ? names[cfg] : "?";
+                                "16x32_12_4", "32x16_21_4", "32x32_22_2_bk32", "32x64_24_1",
+                                "V64x64_44_2", "V64x32_42_2", "V32x32_22_2", "V64x64_44_2_bk8"};
+  return (cfg >= 0 && cfg < 16) ? names[cfg] : "?";
 }
 extern "C" int mwt_gemm(int cfg, int k, const double* A, const double* B, double* C, int64_t n,
                         void* stream) {
