@@ -269,39 +269,43 @@ constexpr int GEMV_WARPS = 4;
 constexpr int GEMV_P = 32 * GEMV_WARPS;
 constexpr int GEMV_ROWS_PER_CTA = 2;
 
-template <int K, int VAR>
-__global__ void __launch_bounds__(32 * GEMV_WARPS * GEMV_ROWS_PER_CTA)
+template <int K, int VAR, int WARPS = GEMV_WARPS, int RPC = GEMV_ROWS_PER_CTA, int D = 4>
+__global__ void __launch_bounds__(32 * WARPS * RPC)
     gemv_tree_kernel(const double* __restrict__ A, int64_t lda, int64_t sA,
                      const double* __restrict__ x, int64_t sx, double* __restrict__ y, int64_t sy,
                      int64_t m, int64_t n) {
-  __shared__ double red[GEMV_ROWS_PER_CTA][K][GEMV_WARPS];
+  constexpr int P = 32 * WARPS;
+  __shared__ double red[RPC][K][WARPS];
   const int lane = threadIdx.x & 31;
-  const int warp = (threadIdx.x >> 5) % GEMV_WARPS;
-  const int slot = (threadIdx.x >> 5) / GEMV_WARPS;
-  const int64_t i = blockIdx.x * (int64_t)GEMV_ROWS_PER_CTA + slot;
+  const int warp = (threadIdx.x >> 5) % WARPS;
+  const int slot = (threadIdx.x >> 5) / WARPS;
+  const int64_t i = blockIdx.x * (int64_t)RPC + slot;
   const bool live = i < m;
   const double* row = A + (live ? i : 0) * lda;
   const int u = warp * 32 + lane;
   V<K> acc = zero<K>();
   int64_t t = u;
-  constexpr int D = 4;
-  for (; t + (D - 1) * GEMV_P < n; t += D * GEMV_P) {
+  for (; t + (D - 1) * P < n; t += D * P) {
     V<K> a[D], xv[D];
 #pragma unroll
     for (int d = 0; d < D; ++d) {
-      a[d] = load<K>(row, sA, t + d * GEMV_P);
-      xv[d] = load<K>(x, sx, t + d * GEMV_P);
+      a[d] = load<K>(row, sA, t + d * P);
+      xv[d] = load<K>(x, sx, t + d * P);
     }
 #pragma unroll
     for (int d = 0; d < D; ++d) acc = Ops<K, VAR>::add(acc, Ops<K, VAR>::mul(a[d], xv[d]));
   }
-  for (; t < n; t += GEMV_P)
+  for (; t < n; t += P)
     acc = Ops<K, VAR>::add(acc, Ops<K, VAR>::mul(load<K>(row, sA, t), load<K>(x, sx, t)));
-  const int64_t valid = n < GEMV_P ? n : GEMV_P;
+  const int64_t valid = n < P ? n : P;
 #pragma unroll
   for (int s = 1; s < 32; s <<= 1) {
     V<K> o = shfl_down<K>(acc, s);
     if ((lane & (2 * s - 1)) == 0 && u + s < valid) acc = Ops<K, VAR>::add(acc, o);
+  }
+  if (WARPS == 1) {
+    if (lane == 0 && live) store<K>(y, sy, i, acc);
+    return;
   }
   if (lane == 0) {
 #pragma unroll
@@ -309,15 +313,15 @@ __global__ void __launch_bounds__(32 * GEMV_WARPS * GEMV_ROWS_PER_CTA)
   }
   __syncthreads();
   if (warp == 0 && lane == 0 && live) {
-    V<K> r[GEMV_WARPS];
+    V<K> r[WARPS];
 #pragma unroll
-    for (int w = 0; w < GEMV_WARPS; ++w)
+    for (int w = 0; w < WARPS; ++w)
 #pragma unroll
       for (int c = 0; c < K; ++c) r[w].c[c] = red[slot][c][w];
 #pragma unroll
-    for (int s = 1; s < GEMV_WARPS; s <<= 1)
+    for (int s = 1; s < WARPS; s <<= 1)
 #pragma unroll
-      for (int w = 0; w + s < GEMV_WARPS; w += 2 * s)
+      for (int w = 0; w + s < WARPS; w += 2 * s)
         if (32 * (w + s) < valid) r[w] = Ops<K, VAR>::add(r[w], r[w + s]);
     store<K>(y, sy, i, r[0]);
   }

@@ -3,6 +3,7 @@
 // configurations, so scripts/tune_gemm.py can time them on a B200 and
 // check their output is bit-identical to the product kernel.
 #include "../gemm_kernel.cuh"
+#include "../reduce.cu"  // GEMV kernel template (its C-ABI symbols stay private to this .so)
 
 namespace mw {
 #define CFGV(NAME, bm, bn, bk, tm, tn, minb, vec)                             \
@@ -82,5 +83,42 @@ extern "C" int mwt_gemm(int cfg, int k, const double* A, const double* B, double
   if (k == 2) return run<2>(cfg, A, B, C, n, st);
   if (k == 3) return run<3>(cfg, A, B, C, n, st);
   if (k == 4) return run<4>(cfg, A, B, C, n, st);
+  return MW_ERR_INVALID;
+}
+
+// ---- GEMV variants: (warps per row, rows per CTA, loads ahead)
+template <int K, int W, int R, int D>
+static int gemv_launch(const double* A, const double* x, double* y, int64_t m, int64_t n,
+                       cudaStream_t st) {
+  gemv_tree_kernel<K, BRANCH_FREE, W, R, D><<<(unsigned)((m + R - 1) / R), 32 * W * R, 0, st>>>(
+      A, n, m * n, x, n, y, m, m, n);
+  return launch_status();
+}
+template <int K>
+static int gemv_run(int cfg, const double* A, const double* x, double* y, int64_t m, int64_t n,
+                    cudaStream_t st) {
+  switch (cfg) {
+    case 0: return gemv_launch<K, 4, 2, 4>(A, x, y, m, n, st);
+    case 1: return gemv_launch<K, 1, 8, 8>(A, x, y, m, n, st);
+    case 2: return gemv_launch<K, 1, 8, 4>(A, x, y, m, n, st);
+    case 3: return gemv_launch<K, 2, 4, 4>(A, x, y, m, n, st);
+    case 4: return gemv_launch<K, 2, 4, 8>(A, x, y, m, n, st);
+    case 5: return gemv_launch<K, 4, 2, 2>(A, x, y, m, n, st);
+    case 6: return gemv_launch<K, 4, 1, 4>(A, x, y, m, n, st);
+    case 7: return gemv_launch<K, 8, 1, 2>(A, x, y, m, n, st);
+    default: return MW_ERR_INVALID;
+  }
+}
+extern "C" int mwt_gemv_num_configs(void) { return 8; }
+extern "C" const char* mwt_gemv_config_name(int cfg) {
+  static const char* names[] = {"W4_R2_D4", "W1_R8_D8", "W1_R8_D4", "W2_R4_D4",
+                                "W2_R4_D8", "W4_R2_D2", "W4_R1_D4", "W8_R1_D2"};
+  return (cfg >= 0 && cfg < 8) ? names[cfg] : "?";
+}
+extern "C" int mwt_gemv(int cfg, int k, const double* A, const double* x, double* y, int64_t m,
+                        int64_t n, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (k == 3) return gemv_run<3>(cfg, A, x, y, m, n, st);
+  if (k == 4) return gemv_run<4>(cfg, A, x, y, m, n, st);
   return MW_ERR_INVALID;
 }

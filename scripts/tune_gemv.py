@@ -1,0 +1,28 @@
+"""Time GEMV tree-kernel shapes (csrc/tune/libmwtune.so) at config 2, L2 flushed."""
+import ctypes, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+import paper_2603_14926_b200 as mw
+from paper_2603_14926_b200 import gen
+lib = ctypes.CDLL(os.path.join(os.path.dirname(mw._lib.LIB_PATH), "csrc", "tune", "libmwtune.so"))
+lib.mwt_gemv.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                         ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p]
+lib.mwt_gemv_config_name.restype = ctypes.c_char_p
+flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+MAC = {3: 96, 4: 209}
+for k in (3, 4):
+    a, x = gen.config2_gemv(k)
+    A, X = torch.from_numpy(a).cuda(), torch.from_numpy(x).cuda()
+    m, n = a.shape[1], a.shape[2]
+    y = torch.empty((k, m), dtype=torch.float64, device="cuda")
+    for cfg in range(lib.mwt_gemv_num_configs()):
+        st = torch.cuda.current_stream().cuda_stream
+        lib.mwt_gemv(cfg, k, A.data_ptr(), X.data_ptr(), y.data_ptr(), m, n, st)
+        ts = []
+        for _ in range(10):
+            flush.fill_(1)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(); lib.mwt_gemv(cfg, k, A.data_ptr(), X.data_ptr(), y.data_ptr(), m, n, st); e1.record()
+            torch.cuda.synchronize(); ts.append(e0.elapsed_time(e1))
+        ms = sorted(ts)[len(ts) // 2]
+        print(f"k={k} {lib.mwt_gemv_config_name(cfg).decode():10s} {ms*1e3:8.1f} us  {MAC[k]*m*n/(ms/1e3)/1e12:6.2f} T/s", flush=True)
