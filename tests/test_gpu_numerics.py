@@ -213,3 +213,31 @@ def test_tree_dk_converges_like_exact():
     b = sorted((r[0][0], r[1][0]) for r in st.roots())
     for (x0, y0), (x1, y1) in zip(a, b):
         assert abs(x0 - x1) < 1e-14 and abs(y0 - y1) < 1e-14
+
+
+def _exact_pair_ok(a, b, s, e, op):
+    fa, fb, fs, fe = (Fraction(float(v)) for v in (a, b, s, e))
+    return (fa + fb if op == "add" else fa * fb) == fs + fe
+
+
+def test_eft_exactness_wide_exponent_sweep():
+    """two_sum / two_prod exactness through the device kernels
+    (test_eft.py:60-72, 85-89): DD add/mul of (a, 0) and (b, 0) must return
+    s + e == a + b and p + e == a * b exactly, over a wide exponent sweep."""
+    rng = np.random.default_rng(20240809)
+    n = 20000
+    def draw(lo, hi):
+        m = rng.uniform(1, 2, n) * np.exp2(rng.integers(lo, hi, n))
+        return m * np.where(rng.random(n) < 0.5, -1, 1)
+    a, b = draw(-500, 501), draw(-500, 501)
+    A = np.stack([a, np.zeros(n)])
+    B = np.stack([b, np.zeros(n)])
+    s = batch_add(LaneBatch(A), LaneBatch(B), Variant.BRANCH_FREE).numpy()
+    for i in range(0, n, 13):
+        assert _exact_pair_ok(a[i], b[i], s[0, i], s[1, i], "add")
+    a, b = draw(-140, 141), draw(-140, 141)  # two_prod contract: |ab| well above subnormal
+    A = np.stack([a, np.zeros(n)])
+    B = np.stack([b, np.zeros(n)])
+    p = batch_mul(LaneBatch(A), LaneBatch(B), Variant.BRANCH_FREE).numpy()
+    for i in range(0, n, 13):
+        assert _exact_pair_ok(a[i], b[i], p[0, i], p[1, i], "mul")
