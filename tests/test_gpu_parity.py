@@ -516,3 +516,40 @@ def test_nonfinite_values_propagate():
     assert not np.isfinite(s[0, :3]).any()
     q = batch_div(la, lb, Variant.BRANCH_FREE).numpy()
     assert not np.isfinite(q[0, 3])
+
+
+def test_dist_paths_single_rank_nccl():
+    """The multi-GPU code paths (dist.py) on a one-rank NCCL group: device
+    all-gathers and the MIN all-reduce run, and results equal the 1-GPU
+    kernels bit for bit (the gloo tests cover world size 2 on CPU)."""
+    import os
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_2603_14926_b200 import dist as mwdist
+
+    if dist.is_initialized():
+        pytest.skip("process group already initialised")
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK="0", WORLD_SIZE="1")
+    dist.init_process_group("nccl", device_id=torch.device("cuda", 0))
+    try:
+        rng = np.random.default_rng(8)
+        x, y = gen.g_k(rng, 3, 70000), gen.g_k(rng, 3, 70000)
+        X, Y = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
+        got = mwdist.dot_allgather(X, Y, mwdist.gpu_dot_backend(Variant.BRANCH_FREE))
+        assert_bitwise(got.cpu().numpy(), oracle.dot(x, y, "bf", order=1))
+        coeffs = gen.config5_poly(3)
+        zre, zim = gen.config5_init(3)
+        re, im, first = mwdist.dk_sweeps_sharded(torch.from_numpy(coeffs).cuda(), torch.from_numpy(zre).cuda(),
+                                                 torch.from_numpy(zim).cuda(), 2, Variant.BRANCH_FREE)
+        assert first is None
+        ref = dk_sweeps(MonicPoly(coeffs), RootState(re=zre, im=zim), 2, Variant.BRANCH_FREE)
+        assert_bitwise(re.cpu().numpy(), ref.re.cpu().numpy())
+        assert_bitwise(im.cpu().numpy(), ref.im.cpu().numpy())
+    finally:
+        dist.destroy_process_group()
