@@ -64,7 +64,8 @@ def main():
         for r in rows[2:]:
             kname = short(r[hdr.index("Kernel Name")])
             base = re.sub(r"[^A-Za-z0-9]+", "_", kname).strip("_")
-            with open(os.path.join(PROF, f"{rnd}_ncu_{base}.csv"), "w", newline="") as fh:
+            stem = os.path.splitext(os.path.basename(rep))[0]
+            with open(os.path.join(PROF, f"{rnd}_ncu_{stem}_{base}.csv"), "w", newline="") as fh:
                 w = csv.writer(fh)
                 w.writerow(hdr)
                 w.writerow(units)
@@ -81,7 +82,10 @@ def main():
                     ent[k + ".unit"] = "byte" if "byte" in units[i] else ("s" if "second" in units[i] else units[i])
             if "dram__bytes_read.sum" in ent and "dram__bytes_write.sum" in ent:
                 ent["dram_bytes_per_launch"] = ent["dram__bytes_read.sum"] + ent["dram__bytes_write.sum"]
-            summary[kname] = ent
+            prev = summary.get(kname)
+            valid = "dram_bytes_per_launch" in ent and ent["dram_bytes_per_launch"] == ent["dram_bytes_per_launch"]
+            if valid or prev is None:  # keep an earlier complete capture over a partial one
+                summary[kname] = ent
             print(kname, json.dumps({k: v for k, v in ent.items() if not k.endswith(".unit")}, indent=None)[:400])
     json.dump(summary, open(path, "w"), indent=1, sort_keys=True)
 
