@@ -12,7 +12,7 @@ from . import _lib
 from .batch import LaneBatch, batch_add, batch_div, batch_mul, batch_sub, pack, unpack
 from .blas import axpy, axpy_, dot, dot_tensor, gemv
 from .linalg import CMWMatrix, MatMulPlan, MWMatrix, Scheme, cmatmul, gen_complex_test_matrices, matmul
-from .multiword import BITS, Variant, ulp_k
+from .multiword import BITS, DD, QD, TD, MultiWord, Variant, ulp_k
 from .poly import (
     MWPolynomial,
     estrin_eval,
@@ -45,7 +45,7 @@ __all__ = [
     "LaneBatch", "pack", "unpack", "batch_add", "batch_sub", "batch_mul", "batch_div",
     "dot", "dot_tensor", "axpy", "axpy_", "gemv",
     "MatMulPlan", "MWMatrix", "CMWMatrix", "Scheme", "matmul", "cmatmul", "gen_complex_test_matrices",
-    "BITS", "Variant", "ulp_k",
+    "BITS", "Variant", "ulp_k", "MultiWord", "DD", "TD", "QD",
     "MWPolynomial", "horner_eval", "horner_eval_batched", "estrin_eval", "estrin_eval_batched",
     "eval_complex", "eval_complex_batched", "random_polynomial",
     "MonicPoly", "RootState", "CollisionError", "NoConvergence", "aberth_init", "radius_estimate",

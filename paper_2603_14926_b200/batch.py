@@ -139,9 +139,11 @@ def pack(values, width: int | None = None, device=None) -> LaneBatch:
 
 
 def unpack(batch: LaneBatch) -> list:
-    """The first ``count`` lanes as K-word tuples (batch.py:115-119)."""
+    """The first ``count`` lanes as MultiWord values (batch.py:115-119)."""
+    from .multiword import MultiWord
+
     arr = batch.numpy()
-    return [tuple(float(c) for c in arr[:, i]) for i in range(batch.count)]
+    return [MultiWord.from_components(tuple(float(c) for c in arr[:, i])) for i in range(batch.count)]
 
 
 def _check_pair(a: LaneBatch, b: LaneBatch):

@@ -1,10 +1,13 @@
-"""Word counts, the Variant selector and small host-side helpers.
+"""Word counts, the Variant selector, scalar K-word operations and the
+DD / TD / QD value classes.
 
-Mirrors the parts of mwfloat.multiword (pkg/src/mwfloat/multiword.py) the
-array-level API needs: ``Variant`` (82-96), ``BITS`` (76), ``ulp_k``
-(722-730), ``from_basefloat`` (749-752) and the greedy ``from_oracle``
-rounding (760-775, here for exact Fractions).  The arithmetic itself lives
-only in the CUDA kernels.
+Mirrors mwfloat.multiword (pkg/src/mwfloat/multiword.py): ``Variant``
+(82-96), ``BITS`` (76), ``ulp_k`` (722-730), ``from_basefloat`` (749-752),
+the greedy ``from_oracle`` rounding (760-775, here for exact Fractions),
+decimal conversion (778-845), the scalar ``mw_*`` / complex ``c*``
+operations (617-702) and the immutable ``MultiWord``/``DD``/``TD``/``QD``
+classes (850-1004).  All arithmetic runs in the CUDA kernels; scalar
+operations are one-lane launches.
 """
 
 from __future__ import annotations
@@ -13,7 +16,11 @@ import enum
 import math
 from fractions import Fraction
 
-__all__ = ["Variant", "BITS", "DEFAULT_DIGITS", "ulp_k", "from_basefloat", "from_fraction", "variant_code"]
+__all__ = [
+    "Variant", "BITS", "DEFAULT_DIGITS", "ulp_k", "from_basefloat", "from_fraction", "variant_code",
+    "mw_add", "mw_sub", "mw_mul", "mw_div", "mw_neg", "cadd", "csub", "cmul", "cdiv",
+    "is_normalized", "from_decimal_string", "to_decimal_string", "MultiWord", "DD", "TD", "QD",
+]
 
 BITS = {2: 106, 3: 159, 4: 212}
 DEFAULT_DIGITS = {2: 34, 3: 49, 4: 64}
@@ -68,3 +75,275 @@ def from_fraction(value, k: int) -> tuple:
         out.append(c)
         fr -= Fraction(c)
     return tuple(out)
+
+
+# --------------------------------------------------------------------------
+# scalar K-word operations and the immutable value classes
+# (multiword.py:617-702, 850-1004).  Each scalar operation is a one-lane
+# launch of the same device kernels the batches use (no CPU arithmetic):
+# correct and bit-identical, but latency-bound -- batch work through
+# LaneBatch / MWMatrix instead.
+# --------------------------------------------------------------------------
+
+
+def _scalar_op(name: str, a, b, variant) -> tuple:
+    import numpy as np
+
+    from .batch import LaneBatch, batch_add, batch_div, batch_mul, batch_sub
+
+    a = tuple(float(c) for c in a)
+    b = tuple(float(c) for c in b)
+    if len(a) != len(b):
+        raise ValueError("mixed word counts")
+    if len(a) not in BITS:
+        raise ValueError(f"unsupported word count {len(a)}")
+    fn = {"add": batch_add, "sub": batch_sub, "mul": batch_mul, "div": batch_div}[name]
+    la = LaneBatch(np.array(a).reshape(-1, 1))
+    lb = LaneBatch(np.array(b).reshape(-1, 1))
+    return fn(la, lb, variant).lane(0)
+
+
+def mw_add(a, b, variant: Variant = Variant.STANDARD) -> tuple:
+    return _scalar_op("add", a, b, variant)
+
+
+def mw_sub(a, b, variant: Variant = Variant.STANDARD) -> tuple:
+    """add(a, -b) (multiword.py:629-630), one fused lane kernel."""
+    return _scalar_op("sub", a, b, variant)
+
+
+def mw_mul(a, b, variant: Variant = Variant.STANDARD) -> tuple:
+    return _scalar_op("mul", a, b, variant)
+
+
+def mw_div(a, b, variant: Variant = Variant.STANDARD) -> tuple:
+    """Newton reciprocal division (multiword.py:661-668)."""
+    return _scalar_op("div", a, b, variant)
+
+
+def mw_neg(a) -> tuple:
+    return tuple(-float(c) for c in a)
+
+
+def cadd(a, b, variant: Variant = Variant.STANDARD):
+    return mw_add(a[0], b[0], variant), mw_add(a[1], b[1], variant)
+
+
+def csub(a, b, variant: Variant = Variant.STANDARD):
+    return mw_sub(a[0], b[0], variant), mw_sub(a[1], b[1], variant)
+
+
+def cmul(a, b, variant: Variant = Variant.STANDARD):
+    """Three-multiplication complex product (multiword.py:683-692)."""
+    ar, ai = a
+    br, bi = b
+    p1 = mw_mul(ar, br, variant)
+    p2 = mw_mul(ai, bi, variant)
+    p3 = mw_mul(mw_add(ar, ai, variant), mw_add(br, bi, variant), variant)
+    return mw_sub(p1, p2, variant), mw_sub(mw_sub(p3, p1, variant), p2, variant)
+
+
+def cdiv(a, b, variant: Variant = Variant.STANDARD):
+    """(a conj(b)) / |b|^2 (multiword.py:695-702)."""
+    ar, ai = a
+    br, bi = b
+    den = mw_add(mw_mul(br, br, variant), mw_mul(bi, bi, variant), variant)
+    num_re = mw_add(mw_mul(ar, br, variant), mw_mul(ai, bi, variant), variant)
+    num_im = mw_sub(mw_mul(ai, br, variant), mw_mul(ar, bi, variant), variant)
+    return mw_div(num_re, den, variant), mw_div(num_im, den, variant)
+
+
+def is_normalized(comps) -> bool:
+    """Component-overlap invariant |c[i+1]| <= ulp(c[i]) / 2 (733-741)."""
+    for hi, lo in zip(comps, comps[1:]):
+        if hi == 0.0:
+            if lo != 0.0:
+                return False
+        elif abs(lo) > 0.5 * math.ulp(abs(hi)):
+            return False
+    return True
+
+
+def from_decimal_string(text: str, k: int) -> tuple:
+    """Parse a decimal literal to K words, correctly rounded (778-805)."""
+    if k not in BITS:
+        raise ValueError(f"unsupported word count {k}")
+    s = text.strip()
+    if not s:
+        raise ValueError("empty decimal string")
+    try:
+        mant, esep, exp_part = s.lower().partition("e")
+        if esep and not exp_part:
+            raise ValueError("dangling exponent")
+        exp = int(exp_part) if exp_part else 0
+        if "." in mant:
+            int_part, frac_part = mant.split(".", 1)
+            exp -= len(frac_part)
+            mant = int_part + frac_part
+        digits = int(mant)
+    except ValueError as err:
+        raise ValueError(f"malformed decimal string {text!r}") from err
+    fr = Fraction(digits * 10**exp) if exp >= 0 else Fraction(digits, 10**-exp)
+    return from_fraction(fr, k)
+
+
+def to_decimal_string(comps, digits: int | None = None) -> str:
+    """Scientific-notation string with `digits` significant digits (808-845)."""
+    k = len(comps)
+    if digits is None:
+        digits = DEFAULT_DIGITS[k]
+    fr = sum((Fraction(float(c)) for c in comps), Fraction(0))
+    if fr == 0:
+        return "0." + "0" * (digits - 1) + "e+0"
+    neg = fr < 0
+    fr = -fr if neg else fr
+    d10 = math.floor(math.log10(float(fr.numerator)) - math.log10(float(fr.denominator)))
+    scaled = fr * Fraction(10) ** (digits - 1 - d10)
+    n = int(scaled)
+    if scaled - n >= Fraction(1, 2):
+        n += 1
+    if n >= 10**digits:
+        n //= 10
+        d10 += 1
+    elif n < 10 ** (digits - 1):
+        n *= 10
+        d10 -= 1
+        scaled = fr * Fraction(10) ** (digits - 1 - d10)
+        n = int(scaled)
+        if scaled - n >= Fraction(1, 2):
+            n += 1
+    text = str(n)
+    body = f"{text[0]}.{text[1:]}e{d10:+d}"
+    return "-" + body if neg else body
+
+
+class MultiWord:
+    """Immutable K-word value over a component tuple (850-989).  Operators
+    use the Standard variant (as in the reference); arithmetic runs on the
+    device through one-lane kernels."""
+
+    __slots__ = ("comps",)
+
+    K: int | None = None
+
+    def __init__(self, *parts):
+        if len(parts) == 1 and isinstance(parts[0], (tuple, list)):
+            parts = tuple(parts[0])
+        k = self.K if self.K is not None else len(parts)
+        if k not in BITS:
+            raise ValueError(f"unsupported word count {k}")
+        if len(parts) > k:
+            raise ValueError(f"{len(parts)} components for a {k}-word value")
+        comps = tuple(float(p) for p in parts) + (0.0,) * (k - len(parts))
+        object.__setattr__(self, "comps", comps)
+
+    def __setattr__(self, name, value):
+        raise AttributeError("MultiWord values are immutable")
+
+    @property
+    def k(self) -> int:
+        return len(self.comps)
+
+    @classmethod
+    def from_components(cls, comps) -> "MultiWord":
+        return _CLASS_BY_K[len(comps)](*comps)
+
+    @classmethod
+    def from_float(cls, x: float, k: int | None = None) -> "MultiWord":
+        kk = cls.K if cls.K is not None else (k if k is not None else 2)
+        return _CLASS_BY_K[kk](*from_basefloat(x, kk))
+
+    @classmethod
+    def from_decimal(cls, text: str, k: int | None = None) -> "MultiWord":
+        kk = cls.K if cls.K is not None else (k if k is not None else 2)
+        return _CLASS_BY_K[kk](*from_decimal_string(text, kk))
+
+    def to_float(self) -> float:
+        acc = 0.0
+        for c in reversed(self.comps):
+            acc += c
+        return acc
+
+    def to_fraction(self) -> Fraction:
+        return sum((Fraction(c) for c in self.comps), Fraction(0))
+
+    def to_decimal(self, digits: int | None = None) -> str:
+        return to_decimal_string(self.comps, digits)
+
+    def _coerce(self, other):
+        if isinstance(other, MultiWord):
+            if other.k != self.k:
+                raise ValueError("mixed word counts")
+            return other.comps
+        if isinstance(other, (int, float)):
+            return from_basefloat(float(other), self.k)
+        return NotImplemented
+
+    def _wrap(self, comps):
+        return _CLASS_BY_K[len(comps)](*comps)
+
+    def __add__(self, other):
+        rhs = self._coerce(other)
+        return NotImplemented if rhs is NotImplemented else self._wrap(mw_add(self.comps, rhs))
+
+    __radd__ = __add__
+
+    def __sub__(self, other):
+        rhs = self._coerce(other)
+        return NotImplemented if rhs is NotImplemented else self._wrap(mw_sub(self.comps, rhs))
+
+    def __rsub__(self, other):
+        rhs = self._coerce(other)
+        return NotImplemented if rhs is NotImplemented else self._wrap(mw_sub(rhs, self.comps))
+
+    def __mul__(self, other):
+        rhs = self._coerce(other)
+        return NotImplemented if rhs is NotImplemented else self._wrap(mw_mul(self.comps, rhs))
+
+    __rmul__ = __mul__
+
+    def __truediv__(self, other):
+        rhs = self._coerce(other)
+        return NotImplemented if rhs is NotImplemented else self._wrap(mw_div(self.comps, rhs))
+
+    def __rtruediv__(self, other):
+        rhs = self._coerce(other)
+        return NotImplemented if rhs is NotImplemented else self._wrap(mw_div(rhs, self.comps))
+
+    def __neg__(self):
+        return self._wrap(mw_neg(self.comps))
+
+    def __abs__(self):
+        return -self if self.comps[0] < 0.0 else self
+
+    def __eq__(self, other):
+        if isinstance(other, MultiWord):
+            return other.k == self.k and self.to_fraction() == other.to_fraction()
+        if isinstance(other, (int, float)):
+            return self.to_fraction() == Fraction(float(other))
+        return NotImplemented
+
+    def __hash__(self):
+        return hash(self.to_fraction())
+
+    def __repr__(self):
+        name = type(self).__name__ if self.K is not None else f"MultiWord{self.k}"
+        return f"{name}({', '.join(repr(c) for c in self.comps)})"
+
+    def __str__(self):
+        return self.to_decimal()
+
+
+class DD(MultiWord):
+    K = 2
+
+
+class TD(MultiWord):
+    K = 3
+
+
+class QD(MultiWord):
+    K = 4
+
+
+_CLASS_BY_K = {2: DD, 3: TD, 4: QD}

@@ -553,3 +553,28 @@ def test_dist_paths_single_rank_nccl():
         assert_bitwise(im.cpu().numpy(), ref.im.cpu().numpy())
     finally:
         dist.destroy_process_group()
+
+
+def test_multiword_scalar_ops_match_golden(golden):
+    """DD/TD/QD value classes (Standard operators) and the scalar mw_*
+    functions reproduce the reference's lanes (one-lane device kernels)."""
+    from paper_2603_14926_b200 import multiword as mwm
+
+    g = golden("ew")
+    for k, v in CASES:
+        p = f"k{k}_{v}"
+        a, b = g[p + "_a"], g[p + "_b"]
+        for lane in (7, 100):
+            x, y = tuple(a[:, lane]), tuple(b[:, lane])
+            assert mwm.mw_add(x, y, V(v)) == tuple(g[p + "_add"][:, lane])
+            assert mwm.mw_mul(x, y, V(v)) == tuple(g[p + "_mul"][:, lane])
+            assert mwm.mw_sub(x, y, V(v)) == tuple(g[p + "_sub"][:, lane])
+            if v == "std":
+                X, Y = mwm.MultiWord.from_components(x), mwm.MultiWord.from_components(y)
+                assert (X + Y).comps == tuple(g[p + "_add"][:, lane])
+                assert (X * Y).comps == tuple(g[p + "_mul"][:, lane])
+                assert (X - Y).comps == tuple(g[p + "_sub"][:, lane])
+    q = mwm.DD(1.0) / 3.0
+    assert abs(q.to_fraction() - Fraction(1, 3)) < Fraction(1, 2**100)
+    z = mwm.cmul(((1.0, 0.0), (2.0, 0.0)), ((3.0, 0.0), (-1.0, 0.0)), Variant.BRANCH_FREE)
+    assert z == ((5.0, 0.0), (5.0, 0.0))

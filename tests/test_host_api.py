@@ -50,7 +50,7 @@ def test_lanebatch_validation():
 
 def test_pack_unpack_round_trip():
     vals = [(1.5, 2.0**-60), (-2.25, 0.0), (0.1, 0.0)]
-    assert unpack(pack(vals)) == vals
+    assert [v.comps for v in unpack(pack(vals))] == vals
     lb = pack([(1.0, 0.0)], width=8)
     assert lb.width == 8 and lb.count == 1
     assert all(lb.lane(i) == (0.0, 0.0) for i in range(1, 8))
@@ -191,3 +191,22 @@ def test_gen_complex_test_matrices_match_reference(golden, k, n):
     assert_bitwise(a.im.numpy(), g[p + "_a_im"])
     assert_bitwise(b.re.numpy(), g[p + "_b_re"])
     assert_bitwise(b.im.numpy(), g[p + "_b_im"])
+
+
+def test_multiword_value_class_host_parts():
+    from paper_2603_14926_b200 import DD, QD, MultiWord, TD
+    from paper_2603_14926_b200.multiword import from_decimal_string, is_normalized, to_decimal_string
+
+    assert DD(1.5).comps == (1.5, 0.0)
+    assert MultiWord.from_components((1.0, 2.0**-60, 0.0)).__class__ is TD
+    with pytest.raises(AttributeError):
+        DD(1.0).comps = (2.0, 0.0)
+    with pytest.raises(ValueError):
+        DD(1.0, 2.0, 3.0)
+    assert DD(1.0) == 1.0 and QD(2.0) == QD(2.0)
+    assert abs(DD(-3.0)) == DD(3.0)  # negation needs no arithmetic kernel
+    assert is_normalized((1.0, 2.0**-60)) and not is_normalized((1.0, 0.5))
+    v = from_decimal_string("0.1", 4)
+    assert to_decimal_string(v, 30) == "1.00000000000000000000000000000e-1"
+    with pytest.raises(ValueError):
+        from_decimal_string("1e", 2)
