@@ -45,6 +45,12 @@ extern "C" {
 const char* mw_version(void);
 const char* mw_status_string(int status);
 
+/* The error-free transformations over arrays (eft.py:51-83): op 0
+ * quick_two_sum (requires |a| >= |b|), 1 two_sum, 2 two_prod (one FMA);
+ * s[i] + e[i] == a[i] op b[i] exactly (within the EFT contracts). */
+int mw_eft(int op, const double* a, const double* b, double* s, double* e,
+           int64_t n, void* stream);
+
 /* out = a (+) b lane-wise.  Replaces batch.batch_add -> _BATCH_ADD[(k,v)]
  * (batch.py:204-207, 178-185).  Bit-exact with the reference. */
 int mw_ew_add(int k, int variant, const double* a, int64_t sa, const double* b,

@@ -9,6 +9,7 @@ the native library or a CUDA device is missing.
 """
 
 from . import _lib
+from .eft import assert_rounding_mode, quick_two_sum, two_prod, two_sum
 from .batch import LaneBatch, batch_add, batch_div, batch_mul, batch_sub, pack, unpack
 from .blas import axpy, axpy_, dot, dot_tensor, gemv
 from .linalg import CMWMatrix, MatMulPlan, MWMatrix, Scheme, cmatmul, gen_complex_test_matrices, matmul
@@ -42,6 +43,7 @@ from .roots import (
 __version__ = "0.1.0"
 
 __all__ = [
+    "quick_two_sum", "two_sum", "two_prod", "assert_rounding_mode",
     "LaneBatch", "pack", "unpack", "batch_add", "batch_sub", "batch_mul", "batch_div",
     "dot", "dot_tensor", "axpy", "axpy_", "gemv",
     "MatMulPlan", "MWMatrix", "CMWMatrix", "Scheme", "matmul", "cmatmul", "gen_complex_test_matrices",

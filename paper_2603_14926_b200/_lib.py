@@ -33,6 +33,7 @@ I64 = ctypes.c_int64
 _SIGS = {
     "mw_version": ([], ctypes.c_char_p),
     "mw_status_string": ([I], ctypes.c_char_p),
+    "mw_eft": ([I, P, P, P, P, I64, P], I),
     "mw_ew_add": ([I, I, P, I64, P, I64, P, I64, I64, P], I),
     "mw_ew_sub": ([I, I, P, I64, P, I64, P, I64, I64, P], I),
     "mw_ew_mul": ([I, I, P, I64, P, I64, P, I64, I64, P], I),

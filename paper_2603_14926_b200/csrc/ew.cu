@@ -148,3 +148,39 @@ extern "C" int mw_axpy(int k, int variant, const double* alpha_host, const doubl
   return dispatch<EwAxpy>(k, variant, x, sx, (const double*)y, sy, y, sy, n, alpha_host,
                           as_stream(stream));
 }
+
+// ------------------------------------------------------------- raw EFTs
+// The error-free transformations themselves over arrays (eft.py:51-83):
+// op 0 quick_two_sum, 1 two_sum, 2 two_prod; (s, e) per element.
+namespace mw {
+template <int OP>
+__global__ void __launch_bounds__(256) eft_kernel(const double* __restrict__ a,
+                                                  const double* __restrict__ b,
+                                                  double* __restrict__ s, double* __restrict__ e,
+                                                  int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double ss, ee;
+    if (OP == 0) quick_two_sum(a[i], b[i], ss, ee);
+    if (OP == 1) two_sum(a[i], b[i], ss, ee);
+    if (OP == 2) two_prod(a[i], b[i], ss, ee);
+    s[i] = ss;
+    e[i] = ee;
+  }
+}
+}  // namespace mw
+
+extern "C" int mw_eft(int op, const double* a, const double* b, double* s, double* e, int64_t n,
+                      void* stream) {
+  if (op < 0 || op > 2 || n < 0) return MW_ERR_INVALID;
+  if (n == 0) return MW_OK;
+  if (!a || !b || !s || !e) return MW_ERR_INVALID;
+  int64_t blocks = (n + 255) / 256;
+  const int64_t cap = (int64_t)sm_count() * 16;
+  if (blocks > cap) blocks = cap;
+  cudaStream_t st = as_stream(stream);
+  if (op == 0) eft_kernel<0><<<(unsigned)blocks, 256, 0, st>>>(a, b, s, e, n);
+  if (op == 1) eft_kernel<1><<<(unsigned)blocks, 256, 0, st>>>(a, b, s, e, n);
+  if (op == 2) eft_kernel<2><<<(unsigned)blocks, 256, 0, st>>>(a, b, s, e, n);
+  return launch_status();
+}

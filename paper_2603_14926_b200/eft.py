@@ -1,0 +1,63 @@
+"""Error-free transformations on binary64 (mwfloat.eft, eft.py:33-94).
+
+``quick_two_sum``, ``two_sum`` and ``two_prod`` take floats, numpy arrays
+or torch tensors and return the pair (rounded result, exact error); the
+work runs in the device kernel mw_eft (explicitly rounded intrinsics, one
+FMA in two_prod).  ``assert_rounding_mode`` checks round-to-nearest-even
+on the device (the _rn intrinsics fix it per instruction).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib
+
+__all__ = ["quick_two_sum", "two_sum", "two_prod", "assert_rounding_mode"]
+
+
+def _run(op: int, a, b):
+    scalar = isinstance(a, (int, float)) and isinstance(b, (int, float))
+    to_np = isinstance(a, np.ndarray) or isinstance(b, np.ndarray) or scalar
+    ta = torch.as_tensor(np.asarray(a, dtype=np.float64) if not isinstance(a, torch.Tensor) else a,
+                         dtype=torch.float64)
+    tb = torch.as_tensor(np.asarray(b, dtype=np.float64) if not isinstance(b, torch.Tensor) else b,
+                         dtype=torch.float64)
+    ta, tb = torch.broadcast_tensors(ta, tb)
+    dev = ta.device if ta.is_cuda else (tb.device if tb.is_cuda else torch.device("cuda"))
+    ta = ta.to(dev).contiguous()
+    tb = tb.to(dev).contiguous()
+    _lib.require_cuda(ta, tb)
+    s = torch.empty_like(ta)
+    e = torch.empty_like(ta)
+    rc = _lib.load().mw_eft(op, ta.data_ptr(), tb.data_ptr(), s.data_ptr(), e.data_ptr(), ta.numel(),
+                            _lib.stream_handle(dev))
+    _lib.check(rc, "mw_eft")
+    if scalar:
+        return float(s.item()), float(e.item())
+    if to_np:
+        return s.cpu().numpy(), e.cpu().numpy()
+    return s, e
+
+
+def quick_two_sum(a, b):
+    """(s, e), s = fl(a+b), a + b = s + e exactly; needs |a| >= |b|."""
+    return _run(0, a, b)
+
+
+def two_sum(a, b):
+    """(s, e), s = fl(a+b), a + b = s + e exactly, any magnitudes."""
+    return _run(1, a, b)
+
+
+def two_prod(a, b):
+    """(p, e), p = fl(a*b), a * b = p + e exactly (no overflow/underflow)."""
+    return _run(2, a, b)
+
+
+def assert_rounding_mode():
+    """Round-to-nearest-ties-even on the device (eft.py:86-94)."""
+    s, _ = two_sum(np.array([1.0, 1.0]), np.array([2.0**-53, 3.0 * 2.0**-54]))
+    if s[0] != 1.0 or s[1] != 1.0 + 2.0**-52:
+        raise RuntimeError("device FP arithmetic is not round-to-nearest-ties-even")

@@ -578,3 +578,27 @@ def test_multiword_scalar_ops_match_golden(golden):
     assert abs(q.to_fraction() - Fraction(1, 3)) < Fraction(1, 2**100)
     z = mwm.cmul(((1.0, 0.0), (2.0, 0.0)), ((3.0, 0.0), (-1.0, 0.0)), Variant.BRANCH_FREE)
     assert z == ((5.0, 0.0), (5.0, 0.0))
+
+
+def test_eft_kats_on_device():
+    """pkg/tests/test_eft.py known answers through the device EFTs."""
+    from paper_2603_14926_b200 import eft
+
+    eft.assert_rounding_mode()
+    assert eft.quick_two_sum(3.5, 0.0) == (3.5, 0.0)
+    assert eft.quick_two_sum(0.0, 1.25) == (1.25, 0.0)
+    assert eft.quick_two_sum(1.0, 2.0**-60) == (1.0, 2.0**-60)
+    assert eft.quick_two_sum(2.0**53, 1.0) == (2.0**53, 1.0)
+    assert eft.two_sum(0.0, 2.5) == (2.5, 0.0)
+    assert eft.two_prod(3.7, 1.0) == (3.7, 0.0)
+    p, e = eft.two_prod(2.0**30 + 1, 2.0**30 + 1)
+    assert p == 2.0**60 + 2.0**31 and e == 1.0
+    rng = np.random.default_rng(1)
+    a = rng.uniform(-1e10, 1e10, 256)
+    b = rng.uniform(-1e-10, 1e10, 256)
+    s, err = eft.two_sum(a, b)
+    for i in range(256):
+        assert Fraction(s[i]) + Fraction(err[i]) == Fraction(a[i]) + Fraction(b[i])
+    p, err = eft.two_prod(a, b)
+    for i in range(256):
+        assert Fraction(p[i]) + Fraction(err[i]) == Fraction(a[i]) * Fraction(b[i])

@@ -114,3 +114,16 @@ def test_gemm_inner_loop_has_no_contraction(sass):
     a, m, f, _, _ = mix(sass[hits[0]])
     # 4x4 register tile per t step: 16 MACs -> 16 DFMA, 48 DMUL, 16*25 DADD
     assert (a, m, f) == (400, 48, 16)
+
+
+@pytest.mark.parametrize("op,mix_expect", [(0, (3, 0, 0)), (1, (6, 0, 0)), (2, (0, 1, 1))])
+def test_raw_eft_kernels(sass, op, mix_expect):
+    """quick_two_sum = 3 DADD, two_sum = 6 DADD, two_prod = DMUL + DFMA per
+    element (eft.py:51-83), no compares."""
+    hits = [f for f in sass if f.startswith(f"_ZN2mw10eft_kernelILi{op}EEEv")]
+    assert len(hits) == 1, hits
+    a, m, f, _, dsetp = mix(sass[hits[0]])
+    assert dsetp == 0
+    da, dm, df = mix_expect
+    u = max(a // da if da else 0, m // dm if dm else 0)
+    assert u >= 1 and (a, m, f) == (u * da, u * dm, u * df)
