@@ -595,13 +595,18 @@ def secondary(args, torch, dist, mw, world, rank, peak):
                 g = DKSweepGraph(mw.MonicPoly(coeffs), mw.RootState(re=zre0, im=zim0), sweeps, BF, exact_order=exact)
                 ms = timed(g.replay, 3)
                 g.result()  # raises on a collision
+            elif args.backend == "nccl":
+                g = mwdist.DKShardedGraph(coeffs, zre0, zim0, sweeps, BF, exact_order=exact)
+                ms = timed(g.replay, 3)  # 200 x (sweep kernel + NCCL all-gather) in one graph
             else:
                 ms = timed(lambda: mwdist.dk_sweeps_sharded(coeffs, zre0, zim0, sweeps, BF, exact_order=exact), 2)
             out[f"config5_dk_{'td' if k == 3 else 'qd'}_n512_{'exact' if exact else 'tree'}"] = {
                 "ms_200_sweeps": round(ms, 3), "us_per_sweep": round(ms * 1e3 / sweeps, 2),
                 "G_MPops": round(mp_sweep * sweeps / (ms / 1e3) / 1e9, 3),
                 "fp64_frac": round(fp_sweep * sweeps / (ms / 1e3) / peak["dfma"] / world, 4),
-                "collective": "all_gather of (re, im) K-planes per sweep" if world > 1 else None}
+                "collective": ("all_gather of (re, im) K-planes per sweep"
+                               + (", sweeps + NCCL captured in one CUDA graph" if args.backend == "nccl" else ""))
+                if world > 1 else None}
     return out
 
 

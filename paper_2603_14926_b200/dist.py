@@ -36,7 +36,7 @@ import torch
 import torch.distributed as dist
 
 __all__ = ["shard_range", "aligned_shard_range", "DotBackend", "gpu_dot_backend", "dot_allgather",
-           "dk_sweeps_sharded", "allgather_planes"]
+           "dk_sweeps_sharded", "allgather_planes", "DKShardedGraph"]
 
 DOT_PARTIAL_SPAN = 4096  # elements per dot partial (mw_dot_partials)
 
@@ -163,3 +163,68 @@ def dk_sweeps_sharded(coeffs: torch.Tensor, zre: torch.Tensor, zim: torch.Tensor
     fl = f.cpu().tolist()
     first = next(((s, c) for s, c in enumerate(fl[:sweeps]) if c != INT32_MAX), None)
     return cur_re, cur_im, first
+
+
+class DKShardedGraph:
+    """``sweeps`` root-sharded DK sweeps with their per-sweep all-gathers,
+    captured once in a CUDA graph (kernel + NCCL all_gather_into_tensor +
+    re-interleave per sweep), so a fixed-sweep run is one graph launch per
+    rank ("capture 200 sweeps + NCCL in a CUDA graph").
+    Requires n divisible by the world size (equal shards)."""
+
+    def __init__(self, coeffs: torch.Tensor, zre: torch.Tensor, zim: torch.Tensor, sweeps: int, variant,
+                 exact_order: bool = True, group=None):
+        from .roots import INT32_MAX, sweep_into
+
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        k, n = zre.shape
+        if n % self.world:
+            raise ValueError("root count must be divisible by the world size")
+        self.k, self.n, self.sweeps = k, n, sweeps
+        per = n // self.world
+        lo, hi = self.rank * per, (self.rank + 1) * per
+        dev = zre.device
+        self.src = torch.cat([zre, zim], 0).contiguous()  # (2K, n) initial state
+        self.cur = torch.empty_like(self.src)
+        self.out = torch.empty_like(self.src)
+        self.send = torch.empty((2 * k, per), dtype=torch.float64, device=dev)
+        self.recv = torch.empty((self.world, 2 * k, per), dtype=torch.float64, device=dev)
+        self.mag = torch.empty(n, dtype=torch.float64, device=dev)
+        self.flags = torch.empty(sweeps, dtype=torch.int32, device=dev)
+
+        def body():
+            self.cur.copy_(self.src)
+            self.flags.fill_(INT32_MAX)
+            for s in range(sweeps):
+                sweep_into(coeffs, self.cur[:k], self.cur[k:], self.out[:k], self.out[k:], self.mag,
+                           self.flags[s:s + 1], variant, exact_order, lo, hi)
+                self.send.copy_(self.out[:, lo:hi])
+                dist.all_gather_into_tensor(self.recv, self.send, group=group)
+                # recv[r] holds rank r's slice: lay the slices back side by side
+                self.cur.view(2 * k, self.world, per).copy_(self.recv.permute(1, 0, 2))
+
+        side = torch.cuda.Stream(device=dev)
+        side.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(side):
+            body()  # warm-up (lazy kernel init, NCCL communicator setup)
+        torch.cuda.current_stream(dev).wait_stream(side)
+        torch.cuda.synchronize(dev)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            body()
+        self.group = group
+
+    def replay(self):
+        self.graph.replay()
+
+    def result(self):
+        """(re, im, first_collision) like dk_sweeps_sharded."""
+        from .roots import INT32_MAX
+
+        f = self.flags.clone()
+        if self.world > 1:
+            dist.all_reduce(f, op=dist.ReduceOp.MIN, group=self.group)
+        fl = f.cpu().tolist()
+        first = next(((s, c) for s, c in enumerate(fl) if c != INT32_MAX), None)
+        return self.cur[: self.k].clone(), self.cur[self.k:].clone(), first

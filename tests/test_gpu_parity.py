@@ -551,6 +551,15 @@ def test_dist_paths_single_rank_nccl():
         ref = dk_sweeps(MonicPoly(coeffs), RootState(re=zre, im=zim), 2, Variant.BRANCH_FREE)
         assert_bitwise(re.cpu().numpy(), ref.re.cpu().numpy())
         assert_bitwise(im.cpu().numpy(), ref.im.cpu().numpy())
+        # the captured form: sweeps + NCCL all-gathers in one CUDA graph
+        g = mwdist.DKShardedGraph(torch.from_numpy(coeffs).cuda(), torch.from_numpy(zre).cuda(),
+                                  torch.from_numpy(zim).cuda(), 2, Variant.BRANCH_FREE)
+        g.replay()
+        g.replay()
+        gre, gim, first = g.result()
+        assert first is None
+        assert_bitwise(gre.cpu().numpy(), ref.re.cpu().numpy())
+        assert_bitwise(gim.cpu().numpy(), ref.im.cpu().numpy())
     finally:
         dist.destroy_process_group()
 
