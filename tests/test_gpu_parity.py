@@ -611,3 +611,45 @@ def test_eft_kats_on_device():
     p, err = eft.two_prod(a, b)
     for i in range(256):
         assert Fraction(p[i]) + Fraction(err[i]) == Fraction(a[i]) * Fraction(b[i])
+
+
+# ------------------------------------------------- property-based (hypothesis)
+from hypothesis import given, settings  # noqa: E402
+from hypothesis import strategies as st  # noqa: E402
+
+_finite = st.floats(min_value=-1e250, max_value=1e250, allow_nan=False, allow_infinity=False).filter(
+    lambda x: x == 0.0 or abs(x) > 1e-250)
+
+
+@st.composite
+def _kword_batches(draw):
+    k = draw(st.sampled_from([2, 3, 4]))
+    w = draw(st.integers(min_value=1, max_value=9))
+    lead = draw(st.lists(_finite, min_size=2 * w, max_size=2 * w))
+    frac = draw(st.lists(st.floats(min_value=-0.49, max_value=0.49), min_size=2 * w * (k - 1),
+                         max_size=2 * w * (k - 1)))
+    a = np.zeros((k, w))
+    b = np.zeros((k, w))
+    a[0], b[0] = lead[:w], lead[w:]
+    it = iter(frac)
+    for c in range(1, k):
+        for i in range(w):
+            a[c, i] = a[c - 1, i] * 2.0**-53 * next(it)
+            b[c, i] = b[c - 1, i] * 2.0**-53 * next(it)
+    v = draw(st.sampled_from(["bf", "std"]))
+    return k, v, a, b
+
+
+@given(_kword_batches())
+@settings(max_examples=150, deadline=None)
+def test_property_lane_ops_match_oracle(case):
+    """Random K-word lanes over the whole binary64 range (the reference's
+    hypothesis strategies, test_eft.py:14-23): add / sub / mul equal the
+    oracle bit for bit (overflow-free range)."""
+    k, v, a, b = case
+    la, lb = LaneBatch(a), LaneBatch(b)
+    with np.errstate(all="ignore"):
+        for op, fn in (("add", batch_add), ("sub", batch_sub), ("mul", batch_mul)):
+            want = oracle.ew(op, a, b, v)
+            got = fn(la, lb, V(v)).numpy()
+            assert_bitwise(got, want, nan_ok=True)
