@@ -653,3 +653,77 @@ def test_property_lane_ops_match_oracle(case):
             want = oracle.ew(op, a, b, v)
             got = fn(la, lb, V(v)).numpy()
             assert_bitwise(got, want, nan_ok=True)
+
+
+# ----------------------------------------------------- out-of-bounds canaries
+_CANARY = np.frombuffer(np.uint64(0x7FF4DEADBEEFCAFE).tobytes(), dtype=np.float64)[0]  # a NaN payload
+
+
+def _guarded(shape, guard=4096):
+    """Device buffer of `shape` (K, ...) flattened per plane inside a
+    canary-filled allocation; returns (full_tensor, inner_view, plane_stride)."""
+    k = shape[0]
+    inner = int(np.prod(shape[1:]))
+    full = torch.full((k, inner + 2 * guard), float("nan"), dtype=torch.float64, device="cuda")
+    full.view(torch.int64).fill_(int(np.uint64(0x7FF4DEADBEEFCAFE).astype(np.int64)))
+    return full, guard, inner + 2 * guard
+
+
+def _guards_intact(full, guard, inner):
+    bits = full.view(torch.int64).cpu().numpy()
+    pat = np.int64(np.uint64(0x7FF4DEADBEEFCAFE).astype(np.int64))
+    return bool((bits[:, :guard] == pat).all() and (bits[:, guard + inner:] == pat).all())
+
+
+@pytest.mark.parametrize("k", [2, 3, 4])
+def test_no_out_of_bounds_writes(k):
+    """Outputs written through the C-ABI into canary-guarded buffers at
+    ragged sizes: every kernel stays inside its output (compute-sanitizer
+    is closed on this pool)."""
+    from paper_2603_14926_b200 import _lib
+
+    lib = _lib.load()
+    st = torch.cuda.current_stream().cuda_stream
+    rng = np.random.default_rng(k)
+    m, kd, n = 67, 45, 93
+    A = torch.from_numpy(gen.g_k(rng, k, (m, kd))).cuda()
+    B = torch.from_numpy(gen.g_k(rng, k, (kd, n))).cuda()
+    full, g, ps = _guarded((k, m, n))
+    assert lib.mw_gemm(k, 1, A.data_ptr(), kd, m * kd, B.data_ptr(), n, kd * n,
+                       full.data_ptr() + g * 8, n, ps, m, n, kd, st) == 0
+    torch.cuda.synchronize()
+    assert _guards_intact(full, g, m * n)
+    # lane ops, Horner, Estrin, GEMV, DK on 1001 lanes / roots
+    w = 1001
+    x = torch.from_numpy(gen.g_k(rng, k, w)).cuda()
+    full, g, ps = _guarded((k, w))
+    for fn in ("mw_ew_add", "mw_ew_mul", "mw_ew_div"):
+        assert getattr(lib, fn)(k, 1, x.data_ptr(), w, x.data_ptr(), w, full.data_ptr() + g * 8, ps, w, st) == 0
+    cf = torch.from_numpy(gen.g_k(rng, k, 77)).cuda()
+    assert lib.mw_horner(k, 1, cf.data_ptr(), 77, 76, x.data_ptr(), w, full.data_ptr() + g * 8, ps, w, st) == 0
+    assert lib.mw_poly_eval(k, 1, cf.data_ptr(), 77, 76, x.data_ptr(), None, w, full.data_ptr() + g * 8, None,
+                            ps, w, 1, st) == 0
+    Ag = torch.from_numpy(gen.g_k(rng, k, (w, 33))).cuda()
+    xg = torch.from_numpy(gen.g_k(rng, k, 33)).cuda()
+    for order in (0, 1):
+        assert lib.mw_gemv(k, 1, Ag.data_ptr(), 33, w * 33, xg.data_ptr(), 33, full.data_ptr() + g * 8, ps,
+                           w, 33, order, st) == 0
+    torch.cuda.synchronize()
+    assert _guards_intact(full, g, w)
+    nr = 40
+    coeffs = torch.from_numpy(gen.g_k(rng, k, nr) * 0.5).cuda()
+    ang = 2 * np.pi * np.arange(nr) / nr + 0.1
+    zr = np.zeros((k, nr))
+    zi = np.zeros((k, nr))
+    zr[0], zi[0] = 1.3 * np.cos(ang), 1.3 * np.sin(ang)
+    zr_t, zi_t = torch.from_numpy(zr).cuda(), torch.from_numpy(zi).cuda()
+    fre, g2, ps2 = _guarded((k, nr))
+    fim, _, _ = _guarded((k, nr))
+    mag, gm, _ = _guarded((1, nr))
+    flag = torch.full((1,), 2**31 - 1, dtype=torch.int32, device="cuda")
+    for exact in (1, 0):
+        assert lib.mw_dk_sweep(k, 1, coeffs.data_ptr(), nr, nr, zr_t.data_ptr(), zi_t.data_ptr(), nr, 3, 37,
+                               fre.data_ptr() + g2 * 8, fim.data_ptr() + g2 * 8, ps2, mag.data_ptr() + gm * 8,
+                               flag.data_ptr(), exact, st) == 0
+    torch.cuda.synchronize()
+    assert _guards_intact(fre, g2, nr) and _guards_intact(fim, g2, nr) and _guards_intact(mag, gm, nr)
