@@ -298,32 +298,40 @@ __global__ void __launch_bounds__(32 * WARPS * RPC)
   for (; t < n; t += P)
     acc = Ops<K, VAR>::add(acc, Ops<K, VAR>::mul(load<K>(row, sA, t), load<K>(x, sx, t)));
   const int64_t valid = n < P ? n : P;
+  // The pairwise tree, executed level by level over all RPC x P partials of
+  // the CTA in shared memory: each level's pairs are spread over the whole
+  // CTA, so a level costs ceil(pairs/32) warp-adds instead of one masked
+  // warp-add per warp and level (same pairs, same order, same bits).
+  __shared__ double part[RPC][K][P];
 #pragma unroll
-  for (int s = 1; s < 32; s <<= 1) {
-    V<K> o = shfl_down<K>(acc, s);
-    if ((lane & (2 * s - 1)) == 0 && u + s < valid) acc = Ops<K, VAR>::add(acc, o);
-  }
-  if (WARPS == 1) {
-    if (lane == 0 && live) store<K>(y, sy, i, acc);
-    return;
-  }
-  if (lane == 0) {
-#pragma unroll
-    for (int c = 0; c < K; ++c) red[slot][c][warp] = acc.c[c];
-  }
+  for (int c = 0; c < K; ++c) part[slot][c][u] = acc.c[c];
   __syncthreads();
+  const int tid = threadIdx.x;
+#pragma unroll 1
+  for (int s = 1; s < P; s <<= 1) {
+    const int per_row = P / (2 * s);
+    if (tid < RPC * per_row) {
+      const int r = tid / per_row, idx = 2 * s * (tid % per_row);
+      if (idx + s < valid) {
+        V<K> a, b;
+#pragma unroll
+        for (int c = 0; c < K; ++c) {
+          a.c[c] = part[r][c][idx];
+          b.c[c] = part[r][c][idx + s];
+        }
+        const V<K> sum = Ops<K, VAR>::add(a, b);
+#pragma unroll
+        for (int c = 0; c < K; ++c) part[r][c][idx] = sum.c[c];
+      }
+    }
+    __syncthreads();
+  }
+  (void)red;
   if (warp == 0 && lane == 0 && live) {
-    V<K> r[WARPS];
+    V<K> r0;
 #pragma unroll
-    for (int w = 0; w < WARPS; ++w)
-#pragma unroll
-      for (int c = 0; c < K; ++c) r[w].c[c] = red[slot][c][w];
-#pragma unroll
-    for (int s = 1; s < WARPS; s <<= 1)
-#pragma unroll
-      for (int w = 0; w + s < WARPS; w += 2 * s)
-        if (32 * (w + s) < valid) r[w] = Ops<K, VAR>::add(r[w], r[w + s]);
-    store<K>(y, sy, i, r[0]);
+    for (int c = 0; c < K; ++c) r0.c[c] = part[slot][c][0];
+    store<K>(y, sy, i, r0);
   }
 }
 
@@ -335,9 +343,10 @@ struct GemvLaunch {
       gemv_exact_kernel<K, VAR><<<(unsigned)ceil_div(m, 128), 128, 0, st>>>(A, lda, sA, x, sx, y,
                                                                             sy, m, n);
     } else {
-      gemv_tree_kernel<K, VAR><<<(unsigned)ceil_div(m, GEMV_ROWS_PER_CTA),
-                                 32 * GEMV_WARPS * GEMV_ROWS_PER_CTA, 0, st>>>(A, lda, sA, x, sx, y,
-                                                                               sy, m, n);
+      // rows per CTA: 2 for DD/TD, 1 for QD (measured; same tree, same bits)
+      constexpr int R = K == 4 ? 1 : GEMV_ROWS_PER_CTA;
+      gemv_tree_kernel<K, VAR, GEMV_WARPS, R><<<(unsigned)ceil_div(m, R), 32 * GEMV_WARPS * R, 0, st>>>(
+          A, lda, sA, x, sx, y, sy, m, n);
     }
     return launch_status();
   }
