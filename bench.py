@@ -53,6 +53,9 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline sample")
     ap.add_argument("--quick", action="store_true", help="small sizes (debug)")
     ap.add_argument("--no-secondary", action="store_true", help="skip configs 1, 2 and 5")
+    ap.add_argument("--peer-dk", action="store_true",
+                    help="N > 1: also time the DK sweep with the exchange fused in (DKPeerGraph, cudaIpc peer "
+                         "memory); off by default until it has been run on a multi-GPU node")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="process-group backend for N > 1 (gloo only to exercise the multi-rank "
                          "logic where fewer GPUs than ranks exist; never for timing)")
@@ -600,13 +603,27 @@ def secondary(args, torch, dist, mw, world, rank, peak):
                 ms = timed(g.replay, 3)  # 200 x (sweep kernel + NCCL all-gather) in one graph
             else:
                 ms = timed(lambda: mwdist.dk_sweeps_sharded(coeffs, zre0, zim0, sweeps, BF, exact_order=exact), 2)
+            # the exchange fused into the sweep kernel (peer stores over
+            # NVLink + completion slots; at N = 1 this times the protocol's
+            # overhead: self stores, ticket, slot publication and wait)
+            peer = None
+            if world == 1 or (args.backend == "nccl" and args.peer_dk):
+                try:
+                    pg = mwdist.DKPeerGraph(coeffs, zre0, zim0, sweeps, BF, exact_order=exact)
+                    ms_p = timed(pg.replay, 3)
+                    pg.result()
+                    pg.close()
+                    peer = {"ms_200_sweeps": round(ms_p, 3), "us_per_sweep": round(ms_p * 1e3 / sweeps, 2)}
+                except Exception as e:  # reported, never fatal to the bench line
+                    peer = {"error": f"{type(e).__name__}: {e}"[:200]}
             out[f"config5_dk_{'td' if k == 3 else 'qd'}_n512_{'exact' if exact else 'tree'}"] = {
                 "ms_200_sweeps": round(ms, 3), "us_per_sweep": round(ms * 1e3 / sweeps, 2),
                 "G_MPops": round(mp_sweep * sweeps / (ms / 1e3) / 1e9, 3),
                 "fp64_frac": round(fp_sweep * sweeps / (ms / 1e3) / peak["dfma"] / world, 4),
                 "collective": ("all_gather of (re, im) K-planes per sweep"
                                + (", sweeps + NCCL captured in one CUDA graph" if args.backend == "nccl" else ""))
-                if world > 1 else None}
+                if world > 1 else None,
+                "fused_peer_exchange": peer}
     return out
 
 

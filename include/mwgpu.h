@@ -179,6 +179,42 @@ int mw_dk_sweep(int k, int variant, const double* coeffs, int64_t sc,
                 int64_t so, double* step_mag, int* flag_dev, int exact_order,
                 void* stream);
 
+/* Root-sharded DK sweep with the per-sweep state exchange fused into the
+ * kernel (replaces the all-gather that follows mw_dk_sweep
+ * in dist.dk_sweeps_sharded, the reference's thread-pool join over the
+ * shared state, roots.py:240-315).  Every rank holds the full state
+ * twice, as (2k, n) planes (re planes then im planes, plane stride n):
+ * state_in is read; the lane finishing root i (i in [i0, i1)) writes it
+ * to state_out_local and to peer_out[p] for every other rank p (device
+ * array of world pointers, cudaIpc-mapped) -- the transfer overlaps the
+ * remaining roots' arithmetic.  The last CTA then stores the value
+ * epoch*sweeps + sweep + 1 into slot [rank] of every peer_slot[p] (device
+ * array of world pointers to world-u64 slot arrays; st.release.sys) and
+ * waits, at most spin_limit polls of ~0.25 us, until every entry of
+ * my_slot reaches it; on expiry it sets *timeout = 1 and returns (no
+ * hang).  done (u32, zero-initialised) is a self-resetting CTA ticket;
+ * epoch (u64) counts completed runs and is advanced by the sweep
+ * == sweeps - 1 launch.  Arithmetic and order are those of mw_dk_sweep
+ * (exact_order as there), so results are bitwise independent of world. */
+int mw_dk_sweep_peer(int k, int variant, const double* coeffs, int64_t sc,
+                     int64_t n, const double* state_in, int64_t i0, int64_t i1,
+                     double* const* peer_out,
+                     unsigned long long* const* peer_slot,
+                     double* state_out_local, unsigned long long* my_slot,
+                     unsigned int* done, unsigned long long* epoch, int* timeout,
+                     int world, int rank, int sweep, int sweeps,
+                     long long spin_limit, double* step_mag, int* flag_dev,
+                     int exact_order, void* stream);
+
+/* Peer buffers for mw_dk_sweep_peer: a zeroed cudaMalloc allocation (one
+ * IPC handle covers exactly one buffer), its 64-byte cudaIpcMemHandle_t,
+ * and open/close of a peer's handle (cudaIpcMemLazyEnablePeerAccess). */
+int mw_peer_alloc(int64_t bytes, void** out);
+int mw_peer_free(void* p);
+int mw_ipc_get_handle(void* p, void* handle64);
+int mw_ipc_open_handle(const void* handle64, void** out);
+int mw_ipc_close_handle(void* p);
+
 /* Tuning knob of the exact-order sweep: roots per CTA (1..32, default 16).
  * Results do not depend on it (each root is one chain in reference order). */
 int mw_dk_exact_set_roots_per_cta(int roots);

@@ -53,6 +53,13 @@ _SIGS = {
     "mw_poly_eval": ([I, I, P, I64, I64, P, P, I64, P, P, I64, I64, I, P], I),
     "mw_dk_sweep": ([I, I, P, I64, I64, P, P, I64, I64, I64, P, P, I64, P, P, I, P], I),
     "mw_dk_exact_set_roots_per_cta": ([I], I),
+    "mw_dk_sweep_peer": ([I, I, P, I64, I64, P, I64, I64, P, P, P, P, P, P, P, I, I, I, I, ctypes.c_longlong, P, P,
+                          I, P], I),
+    "mw_peer_alloc": ([I64, ctypes.POINTER(P)], I),
+    "mw_peer_free": ([P], I),
+    "mw_ipc_get_handle": ([P, P], I),
+    "mw_ipc_open_handle": ([P, ctypes.POINTER(P)], I),
+    "mw_ipc_close_handle": ([P], I),
     "mw_fp64_peak_kernel": ([I, I, I, I, P, P], I),
     "mw_device_sm_count": ([], I),
 }

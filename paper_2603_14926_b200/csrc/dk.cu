@@ -24,6 +24,7 @@
 // numerator scaled by powers of z^B, pairwise trees.  Same arithmetic per
 // term, reassociated: within the n*2^-p relative bound.
 #include <climits>
+#include <cstring>
 
 #include "common.cuh"
 
@@ -63,11 +64,83 @@ __device__ __forceinline__ Cx<K, VAR> c_one() {
   return r;
 }
 
+// Peer-memory exchange for the root-sharded sweep: every
+// rank keeps the FULL (2K, n) state twice (read buffer / write buffer,
+// swapped each sweep); the lane that finishes root i stores its new K-word
+// (re, im) straight into the write buffer of EVERY rank over NVLink
+// (cudaIpc-mapped peer pointers), so the exchange overlaps the other
+// roots' arithmetic instead of following the kernel as an all-gather.
+// Completion: after a warp/CTA sync over its storing threads, one thread
+// per CTA takes a ticket with a gpu-scope acq_rel atomic (cumulative: it
+// releases the CTA's peer stores); the last CTA has thereby acquired every
+// CTA's stores and publishes "sweep s done" to every rank as a monotonic
+// per-source slot value (epoch * sweeps + s + 1) with st.release.sys,
+// which is cumulative over all it has observed
+// and then waits (ld.acquire.sys, bounded) until every source's slot on
+// THIS rank reached the same value.  The kernel therefore ends only when
+// the full next state has landed locally, so the next sweep's kernel reads
+// it after an ordinary stream boundary.  One slot per source takes plain
+// release stores (no remote atomics) and only ever grows, so nothing is
+// reset between runs.  A wait that exceeds spin_limit sets *timeout and
+// returns instead of hanging the GPU.  tests/test_peer_protocol.py checks
+// the protocol (with the host's run-parity rule, dist.DKPeerGraph) under
+// random interleavings.
+struct DkPeers {
+  double* const* out;              // [world] peer write buffers, (2K, n) planes, stride n
+  unsigned long long* const* slot; // [world] peer slot arrays ([world] u64 each)
+  unsigned long long* my_slot;     // this rank's slot array
+  unsigned int* done;              // CTA completion ticket (self-resetting)
+  unsigned long long* epoch;       // completed replays (advanced by the last sweep)
+  int* timeout;                    // set to 1 when a wait gave up
+  long long spin_limit;
+  int world, rank, sweep, sweeps;
+};
+
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ unsigned atom_add_acq_rel_gpu(unsigned* p, unsigned v) {
+  unsigned old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+
+// Called by exactly one thread per CTA, after a sync over the CTA's
+// storing threads.
+__device__ __noinline__ void dk_peer_ticket(const DkPeers& P) {
+  if (atom_add_acq_rel_gpu(P.done, 1u) != gridDim.x - 1) return;
+  *(volatile unsigned*)P.done = 0;  // the next launch in the stream starts from zero
+  const unsigned long long e = *(volatile unsigned long long*)P.epoch;
+  const unsigned long long v = e * (unsigned long long)P.sweeps + (unsigned long long)P.sweep + 1ull;
+  for (int p = 0; p < P.world; ++p) st_release_sys(P.slot[p] + P.rank, v);
+  int gave_up = *(volatile int*)P.timeout;
+  for (int src = 0; src < P.world && !gave_up; ++src) {
+    long long spins = 0;
+    while (ld_acquire_sys(P.my_slot + src) < v) {
+      if (++spins > P.spin_limit) {
+        atomicExch(P.timeout, 1);
+        gave_up = 1;
+        break;
+      }
+      __nanosleep(256);
+    }
+  }
+  if (P.sweep == P.sweeps - 1) *(volatile unsigned long long*)P.epoch = e + 1;
+}
+
 // Shared tail: step = acc * conj(den) / |den|^2, z - step (roots.py:297-308).
-template <int K, int VAR>
+// PEER: the new value also goes to every other rank's write buffer.
+template <int K, int VAR, bool PEER = false>
 __device__ __forceinline__ void dk_tail(const Cx<K, VAR>& acc, const Cx<K, VAR>& den,
                                         const Cx<K, VAR>& z, double* zre_out, double* zim_out,
-                                        int64_t so, double* step_mag, int64_t i) {
+                                        int64_t so, double* step_mag, int64_t i,
+                                        const DkPeers* P = nullptr) {
   using O = Ops<K, VAR>;
   V<K> mag = O::add(O::mul(den.re, den.re), O::mul(den.im, den.im));
   V<K> num_re = O::add(O::mul(acc.re, den.re), O::mul(acc.im, den.im));
@@ -75,9 +148,18 @@ __device__ __forceinline__ void dk_tail(const Cx<K, VAR>& acc, const Cx<K, VAR>&
   V<K> rcp = recip_newton<K, VAR>(mag);
   V<K> step_re = O::mul(num_re, rcp);
   V<K> step_im = O::mul(num_im, rcp);
-  store<K>(zre_out, so, i, O::add(z.re, neg(step_re)));
-  store<K>(zim_out, so, i, O::add(z.im, neg(step_im)));
+  const V<K> nre = O::add(z.re, neg(step_re));
+  const V<K> nim = O::add(z.im, neg(step_im));
+  store<K>(zre_out, so, i, nre);
+  store<K>(zim_out, so, i, nim);
   step_mag[i] = hypot(step_re.c[0], step_im.c[0]);
+  if constexpr (PEER) {
+    for (int p = 0; p < P->world; ++p) {
+      if (p == P->rank) continue;
+      store<K>(P->out[p], so, i, nre);
+      store<K>(P->out[p] + (int64_t)K * so, so, i, nim);
+    }
+  }
 }
 
 constexpr int DK_EXACT_ROOTS = 32;  // lanes per role warp (two warps: num + den)
@@ -86,13 +168,13 @@ constexpr int DK_EXACT_ROOTS = 32;  // lanes per role warp (two warps: num + den
 static int g_dk_exact_roots = 16;
 constexpr int DK_CH = 128;          // roots staged in smem per chunk
 
-template <int K, int VAR>
+template <int K, int VAR, bool PEER = false>
 __global__ void __launch_bounds__(2 * DK_EXACT_ROOTS)
     dk_exact_kernel(const double* __restrict__ coeffs, int64_t sc, int64_t n,
                     const double* __restrict__ zre, const double* __restrict__ zim, int64_t sz,
                     int64_t i0, int64_t i1, double* __restrict__ zre_out,
                     double* __restrict__ zim_out, int64_t so, double* __restrict__ step_mag,
-                    int* __restrict__ flag, int roots_per_cta) {
+                    int* __restrict__ flag, int roots_per_cta, DkPeers peers = DkPeers{}) {
   using O = Ops<K, VAR>;
   __shared__ double zs[2][K][DK_CH];
   __shared__ double dx[2][K][DK_EXACT_ROOTS];
@@ -169,7 +251,13 @@ __global__ void __launch_bounds__(2 * DK_EXACT_ROOTS)
       den.re.c[c] = dx[0][c][lane];
       den.im.c[c] = dx[1][c][lane];
     }
-    dk_tail<K, VAR>(acc, den, z, zre_out, zim_out, so, step_mag, i);
+    dk_tail<K, VAR, PEER>(acc, den, z, zre_out, zim_out, so, step_mag, i, &peers);
+  }
+  if constexpr (PEER) {
+    if (!is_den) {
+      __syncwarp();
+      if (lane == 0) dk_peer_ticket(peers);
+    }
   }
 }
 
@@ -208,13 +296,13 @@ __device__ __forceinline__ Cx<K, VAR> shfl_cx(const Cx<K, VAR>& v, int s, bool u
 //   warp 1  numerator:   lane l owns blocks l and l+32 (two Horner chains)
 //   warp 2  powers:      w = z^B, w^32, the scan x_l = w^l and x_l * w^32,
 //                        handed to warp 1 through shared memory.
-template <int K, int VAR>
+template <int K, int VAR, bool PEER = false>
 __global__ void __launch_bounds__(96)
     dk_tree_kernel(const double* __restrict__ coeffs, int64_t sc, int64_t n,
                    const double* __restrict__ zre, const double* __restrict__ zim, int64_t sz,
                    int64_t i0, int64_t i1, double* __restrict__ zre_out,
                    double* __restrict__ zim_out, int64_t so, double* __restrict__ step_mag,
-                   int* __restrict__ flag) {
+                   int* __restrict__ flag, DkPeers peers = DkPeers{}) {
   using O = Ops<K, VAR>;
   __shared__ double den_s[2][K];
   __shared__ double pw[2][2][K][32];  // [lo/hi][re/im][c][lane]
@@ -345,7 +433,8 @@ __global__ void __launch_bounds__(96)
       den.re.c[c] = den_s[0][c];
       den.im.c[c] = den_s[1][c];
     }
-    dk_tail<K, VAR>(t[0], den, z, zre_out, zim_out, so, step_mag, i);
+    dk_tail<K, VAR, PEER>(t[0], den, z, zre_out, zim_out, so, step_mag, i, &peers);
+    if constexpr (PEER) dk_peer_ticket(peers);
   }
 }
 
@@ -364,6 +453,29 @@ struct DkLaunch {
     } else {
       dk_tree_kernel<K, VAR><<<(unsigned)cnt, 96, 0, st>>>(
           coeffs, sc, n, zre, zim, sz, i0, i1, zre_out, zim_out, so, step_mag, flag);
+    }
+    return launch_status();
+  }
+};
+
+template <int K, int VAR>
+struct DkPeerLaunch {
+  static int run(const double* coeffs, int64_t sc, int64_t n, const double* state_in,
+                 int64_t i0, int64_t i1, double* state_out, double* step_mag, int* flag,
+                 int exact, DkPeers peers, cudaStream_t st) {
+    const int64_t cnt = i1 - i0;
+    const double* zre = state_in;
+    const double* zim = state_in + (int64_t)K * n;
+    double* ore = state_out;
+    double* oim = state_out + (int64_t)K * n;
+    if (exact) {
+      const int r = g_dk_exact_roots;
+      const int64_t blocks = (cnt + r - 1) / r;
+      dk_exact_kernel<K, VAR, true><<<(unsigned)blocks, 2 * DK_EXACT_ROOTS, 0, st>>>(
+          coeffs, sc, n, zre, zim, n, i0, i1, ore, oim, n, step_mag, flag, r, peers);
+    } else {
+      dk_tree_kernel<K, VAR, true><<<(unsigned)cnt, 96, 0, st>>>(
+          coeffs, sc, n, zre, zim, n, i0, i1, ore, oim, n, step_mag, flag, peers);
     }
     return launch_status();
   }
@@ -393,4 +505,80 @@ extern "C" int mw_dk_sweep(int k, int variant, const double* coeffs, int64_t sc,
   if (sc < n || sz < n || so < n) return MW_ERR_INVALID;
   return dispatch<DkLaunch>(k, variant, coeffs, sc, n, zre, zim, sz, i0, i1, zre_out, zim_out,
                             so, step_mag, flag_dev, exact_order ? 1 : 0, as_stream(stream));
+}
+
+// Root-sharded sweep with the state exchange fused in (peer stores over
+// NVLink + per-source completion slots, see DkPeers).  state_in / the
+// peer_out[rank] buffer hold (2K, n) planes (re planes, then im planes,
+// plane stride n).  peer_out and peer_slot are DEVICE arrays of world
+// pointers.  Roots [i0, i1) are this rank's shard.
+extern "C" int mw_dk_sweep_peer(int k, int variant, const double* coeffs, int64_t sc, int64_t n,
+                                const double* state_in, int64_t i0, int64_t i1,
+                                double* const* peer_out, unsigned long long* const* peer_slot,
+                                double* state_out_local, unsigned long long* my_slot,
+                                unsigned int* done, unsigned long long* epoch, int* timeout,
+                                int world, int rank, int sweep, int sweeps, long long spin_limit,
+                                double* step_mag, int* flag_dev, int exact_order, void* stream) {
+  if (k < 2 || k > 4) return MW_ERR_INVALID;
+  if (variant != 0 && variant != 1) return MW_ERR_INVALID;
+  if (n < 1 || i0 < 0 || i1 <= i0 || i1 > n) return MW_ERR_INVALID;
+  if (world < 1 || rank < 0 || rank >= world || sweeps < 1 || sweep < 0 || sweep >= sweeps)
+    return MW_ERR_INVALID;
+  if (spin_limit < 1) return MW_ERR_INVALID;
+  if (!coeffs || !state_in || !peer_out || !peer_slot || !state_out_local || !my_slot || !done ||
+      !epoch || !timeout || !step_mag || !flag_dev)
+    return MW_ERR_INVALID;
+  if (sc < n) return MW_ERR_INVALID;
+  DkPeers P{peer_out, peer_slot, my_slot, done, epoch, timeout, spin_limit, world, rank, sweep, sweeps};
+  return dispatch<DkPeerLaunch>(k, variant, coeffs, sc, n, state_in, i0, i1, state_out_local,
+                                step_mag, flag_dev, exact_order ? 1 : 0, P, as_stream(stream));
+}
+
+// Peer buffers: plain cudaMalloc allocations (zeroed) so one IPC handle
+// covers exactly one buffer.
+extern "C" int mw_peer_alloc(int64_t bytes, void** out) {
+  if (bytes < 1 || !out) return MW_ERR_INVALID;
+  void* p = nullptr;
+  cudaError_t e = cudaMalloc(&p, (size_t)bytes);
+  if (e != cudaSuccess) return (int)e;
+  e = cudaMemset(p, 0, (size_t)bytes);
+  if (e != cudaSuccess) {
+    cudaFree(p);
+    return (int)e;
+  }
+  e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) return (int)e;
+  *out = p;
+  return MW_OK;
+}
+
+extern "C" int mw_peer_free(void* p) {
+  if (!p) return MW_ERR_INVALID;
+  return (int)cudaFree(p);
+}
+
+// 64-byte opaque handle (cudaIpcMemHandle_t) for a mw_peer_alloc buffer.
+extern "C" int mw_ipc_get_handle(void* p, void* handle64) {
+  if (!p || !handle64) return MW_ERR_INVALID;
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, p);
+  if (e != cudaSuccess) return (int)e;
+  memcpy(handle64, &h, sizeof(h));
+  return MW_OK;
+}
+
+extern "C" int mw_ipc_open_handle(const void* handle64, void** out) {
+  if (!handle64 || !out) return MW_ERR_INVALID;
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle64, sizeof(h));
+  void* p = nullptr;
+  cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) return (int)e;
+  *out = p;
+  return MW_OK;
+}
+
+extern "C" int mw_ipc_close_handle(void* p) {
+  if (!p) return MW_ERR_INVALID;
+  return (int)cudaIpcCloseMemHandle(p);
 }

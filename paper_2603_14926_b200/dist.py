@@ -11,6 +11,11 @@ Only the paths that shard naturally are partitioned:
               (Jacobi), then ONE all-gather of the new (re, im) K-planes per
               sweep rebuilds the full state on every rank.  The exact-order
               kernel makes the result bitwise independent of the GPU count.
+             ``DKPeerGraph`` fuses that exchange into the sweep kernel
+              itself: each finished root is stored straight into every
+              rank's next-state buffer over NVLink (cudaIpc peer memory)
+              while the other roots are still being computed, and a
+              per-source completion slot replaces the collective.
 * dot      -- all-gather-then-sum: each rank produces the tree partials of
               its slice (slices cut at multiples of 4096 elements, one
               partial per 4096), all ranks all-gather them and fold the full
@@ -36,7 +41,8 @@ import torch
 import torch.distributed as dist
 
 __all__ = ["shard_range", "aligned_shard_range", "DotBackend", "gpu_dot_backend", "dot_allgather",
-           "dk_sweeps_sharded", "allgather_planes", "DKShardedGraph"]
+           "dk_sweeps_sharded", "allgather_planes", "DKShardedGraph", "PeerLayout", "peer_tables",
+           "exchange_handles", "DKPeerGraph"]
 
 DOT_PARTIAL_SPAN = 4096  # elements per dot partial (mw_dot_partials)
 
@@ -228,3 +234,207 @@ class DKShardedGraph:
         fl = f.cpu().tolist()
         first = next(((s, c) for s, c in enumerate(fl) if c != INT32_MAX), None)
         return self.cur[: self.k].clone(), self.cur[self.k:].clone(), first
+
+
+# ---------------------------------------------------------------------------
+# Fused compute + exchange over peer memory (mw_dk_sweep_peer)
+
+
+@dataclass(frozen=True)
+class PeerLayout:
+    """One cudaMalloc buffer per rank, identical layout on every rank:
+    state parity 0 | state parity 1 | world u64 completion slots.  A state
+    is (2K, n) float64 planes: K re planes, then K im planes."""
+
+    k: int
+    n: int
+    world: int
+
+    @property
+    def state_bytes(self) -> int:
+        return 2 * self.k * self.n * 8
+
+    def state_off(self, parity: int) -> int:
+        return parity * self.state_bytes
+
+    @property
+    def slot_off(self) -> int:
+        return 2 * self.state_bytes
+
+    @property
+    def total_bytes(self) -> int:
+        return self.slot_off + 8 * self.world
+
+
+def peer_tables(bases: list[int], layout: PeerLayout):
+    """Device-pointer tables for mw_dk_sweep_peer from the per-rank buffer
+    bases (own base for self, the IPC-mapped address for peers).  Sweep s
+    reads parity s % 2 and writes parity 1 - s % 2, so
+    ``outs[parity][p]`` = rank p's write buffer for a sweep reading
+    ``parity``; ``slots[p]`` = rank p's slot array."""
+    outs = [[b + layout.state_off(1 - par) for b in bases] for par in (0, 1)]
+    slots = [b + layout.slot_off for b in bases]
+    return outs, slots
+
+
+def exchange_handles(local: bytes, group=None) -> list[bytes]:
+    """All ranks' 64-byte IPC handles, in rank order."""
+    world = dist.get_world_size(group)
+    out: list = [None] * world
+    dist.all_gather_object(out, local, group=group)
+    return out
+
+
+class _DevView:
+    """Zero-copy torch view of raw device memory (CUDA array interface)."""
+
+    def __init__(self, addr: int, shape: tuple):
+        self.__cuda_array_interface__ = {"shape": shape, "typestr": "<f8", "data": (addr, False), "version": 3,
+                                         "strides": None}
+
+
+class DKPeerGraph:
+    """``sweeps`` root-sharded DK sweeps whose state exchange happens inside
+    the sweep kernel (mw_dk_sweep_peer): no collective on the data path.
+    Same interface as ``DKShardedGraph`` (replay / result) and bitwise the
+    same result for either order.  All sweeps are captured in one CUDA
+    graph; replays need no reset (completion slots are monotonic across
+    replays through a device-side epoch).  Requires n divisible by the
+    world size.  ``spin_limit`` bounds every completion wait (~0.25 us per
+    poll); a wait that expires makes ``result()`` raise instead of hanging."""
+
+    def __init__(self, coeffs: torch.Tensor, zre: torch.Tensor, zim: torch.Tensor, sweeps: int, variant,
+                 exact_order: bool = True, group=None, spin_limit: int = 8_000_000):
+        import ctypes
+
+        from . import _lib
+        from .multiword import variant_code
+        from .roots import INT32_MAX
+
+        lib = _lib.load()
+        _lib.require_cuda(coeffs, zre, zim)
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.group = group
+        k, n = zre.shape
+        if n % self.world:
+            raise ValueError("root count must be divisible by the world size")
+        if sweeps < 1:
+            raise ValueError("sweeps must be >= 1")
+        self.k, self.n, self.sweeps = k, n, sweeps
+        per = n // self.world
+        lo, hi = self.rank * per, (self.rank + 1) * per
+        dev = zre.device
+        self.layout = lay = PeerLayout(k, n, self.world)
+        self._lib = lib
+        buf = ctypes.c_void_p()
+        with torch.cuda.device(dev):
+            _lib.check(lib.mw_peer_alloc(lay.total_bytes, ctypes.byref(buf)), "mw_peer_alloc")
+        self._base = buf.value
+        self._opened: list[int] = []
+        bases = [self._base] * self.world
+        if self.world > 1:
+            h = (ctypes.c_char * 64)()
+            _lib.check(lib.mw_ipc_get_handle(self._base, h), "mw_ipc_get_handle")
+            handles = exchange_handles(bytes(h), group)
+            for p, hp in enumerate(handles):
+                if p == self.rank:
+                    continue
+                q = ctypes.c_void_p()
+                with torch.cuda.device(dev):
+                    _lib.check(lib.mw_ipc_open_handle(hp, ctypes.byref(q)), "mw_ipc_open_handle")
+                self._opened.append(q.value)
+                bases[p] = q.value
+        outs, slots = peer_tables(bases, lay)
+        self._outs = [torch.tensor(o, dtype=torch.int64, device=dev) for o in outs]
+        self._slots = torch.tensor(slots, dtype=torch.int64, device=dev)
+        self._state = [torch.as_tensor(_DevView(self._base + lay.state_off(par), (2 * k, n)), device=dev)
+                       for par in (0, 1)]
+        my_slot = self._base + lay.slot_off
+        self._done = torch.zeros(1, dtype=torch.int32, device=dev)
+        self._epoch = torch.zeros(1, dtype=torch.int64, device=dev)
+        self._timeout = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.src = torch.cat([zre, zim], 0).contiguous()
+        self.mag = torch.empty(n, dtype=torch.float64, device=dev)
+        self.flags = torch.empty(sweeps, dtype=torch.int32, device=dev)
+        self._coeffs = coeffs.contiguous()
+        v = variant_code(variant)
+        exact = 1 if exact_order else 0
+        if self.world > 1:
+            torch.cuda.synchronize(dev)
+            dist.barrier(group)  # every buffer allocated, zeroed and mapped before the first peer store
+
+        def body(start: int):
+            # sweeps are numbered globally across runs (g = run * sweeps + s)
+            # and sweep g reads parity g % 2: the buffer holding a finished
+            # run's result is then only rewritten by this rank's own next
+            # start copy, never by a peer that is already one run ahead
+            stream = _lib.stream_handle(dev)
+            self._state[start].copy_(self.src)
+            self.flags.fill_(INT32_MAX)
+            for s in range(sweeps):
+                par = (start + s) & 1
+                rc = lib.mw_dk_sweep_peer(
+                    k, v, self._coeffs.data_ptr(), self._coeffs.shape[1], n, self._state[par].data_ptr(), lo, hi,
+                    self._outs[par].data_ptr(), self._slots.data_ptr(), self._state[1 - par].data_ptr(), my_slot,
+                    self._done.data_ptr(), self._epoch.data_ptr(), self._timeout.data_ptr(), self.world,
+                    self.rank, s, sweeps, spin_limit, self.mag.data_ptr(), self.flags[s:s + 1].data_ptr(), exact,
+                    stream)
+                _lib.check(rc, "mw_dk_sweep_peer")
+
+        side = torch.cuda.Stream(device=dev)
+        side.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(side):
+            body(0)  # warm-up run (every rank runs it: epochs stay in step)
+        torch.cuda.current_stream(dev).wait_stream(side)
+        torch.cuda.synchronize(dev)
+        self._runs = 1
+        self._check_timeout()
+        # start parity of run r is (r * sweeps) % 2: one graph for an even
+        # sweep count, two alternating graphs for an odd one
+        self.graphs = {}
+        for start in sorted({(r * sweeps) & 1 for r in (1, 2)}):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                body(start)
+            self.graphs[start] = g
+
+    def _check_timeout(self):
+        if int(self._timeout.item()):
+            raise RuntimeError("DKPeerGraph: a peer completion wait expired (a rank stalled or diverged)")
+
+    def replay(self):
+        self.graphs[(self._runs * self.sweeps) & 1].replay()
+        self._runs += 1
+
+    def result(self):
+        """(re, im, first_collision) of the latest run, like
+        DKShardedGraph.result() (call it before the next replay)."""
+        from .roots import INT32_MAX
+
+        self._check_timeout()
+        f = self.flags.clone()
+        if self.world > 1:
+            dist.all_reduce(f, op=dist.ReduceOp.MIN, group=self.group)
+        fl = f.cpu().tolist()
+        first = next(((s, c) for s, c in enumerate(fl) if c != INT32_MAX), None)
+        fin = self._state[(self._runs * self.sweeps) & 1]
+        return fin[: self.k].clone(), fin[self.k:].clone(), first
+
+    def close(self):
+        """Release the peer mappings and the buffer (collective: every rank
+        calls it, after its last replay)."""
+        if self._base is None:
+            return
+        torch.cuda.synchronize(self._state[0].device)
+        if self.world > 1:
+            dist.barrier(self.group)  # no peer still storing into our buffer
+        self.graphs = None
+        self._state = None
+        for q in self._opened:
+            self._lib.mw_ipc_close_handle(q)
+        self._opened = []
+        if self.world > 1:
+            dist.barrier(self.group)  # every peer unmapped our buffer
+        self._lib.mw_peer_free(self._base)
+        self._base = None

@@ -77,6 +77,34 @@ def test_other_entry_checks():
     assert lib.mw_fp64_peak_kernel(0, 1, 512, 1, p, None) == _lib.MW_ERR_INVALID
 
 
+def test_peer_sweep_checks():
+    import ctypes
+
+    lib = _lib.load()
+    p = 0x1000
+    f = lib.mw_dk_sweep_peer
+    ok = dict(k=3, variant=1, coeffs=p, sc=8, n=8, state_in=p, i0=0, i1=8, peer_out=p, peer_slot=p, out=p,
+              my_slot=p, done=p, epoch=p, timeout=p, world=2, rank=1, sweep=0, sweeps=4, spin=1000,
+              mag=p, flag=p, exact=1, stream=None)
+
+    def call(**kw):
+        a = dict(ok, **kw)
+        return f(*a.values())
+
+    assert call(rank=2) == _lib.MW_ERR_INVALID          # rank outside world
+    assert call(sweep=4) == _lib.MW_ERR_INVALID         # sweep outside [0, sweeps)
+    assert call(i1=0) == _lib.MW_ERR_INVALID            # empty shard
+    assert call(i1=9) == _lib.MW_ERR_INVALID            # past n
+    assert call(spin=0) == _lib.MW_ERR_INVALID
+    assert call(peer_slot=None) == _lib.MW_ERR_INVALID
+    assert call(sc=7) == _lib.MW_ERR_INVALID
+    out = ctypes.c_void_p()
+    assert lib.mw_peer_alloc(0, ctypes.byref(out)) == _lib.MW_ERR_INVALID
+    assert lib.mw_peer_free(None) == _lib.MW_ERR_INVALID
+    assert lib.mw_ipc_get_handle(None, p) == _lib.MW_ERR_INVALID
+    assert lib.mw_ipc_open_handle(None, ctypes.byref(out)) == _lib.MW_ERR_INVALID
+
+
 def test_workspace_sizes():
     lib = _lib.load()
     assert lib.mw_dot_workspace(2, 4096) == 0

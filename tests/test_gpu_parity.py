@@ -727,3 +727,134 @@ def test_no_out_of_bounds_writes(k):
                                flag.data_ptr(), exact, st) == 0
     torch.cuda.synchronize()
     assert _guards_intact(fre, g2, nr) and _guards_intact(fim, g2, nr) and _guards_intact(mag, gm, nr)
+
+
+@pytest.mark.parametrize("k", [2, 3, 4])
+@pytest.mark.parametrize("exact", [True, False])
+def test_dk_peer_graph_matches_sweeps(k, exact):
+    """The fused-exchange sweep (mw_dk_sweep_peer through DKPeerGraph, one
+    rank: stores, ticket, slot publication and wait all run) equals the
+    plain sweeps bit for bit, for odd and even sweep counts and across
+    replays (monotonic slots, alternating start parity)."""
+    from paper_2603_14926_b200 import dist as mwdist
+
+    rng = np.random.default_rng(40 + k)
+    n = 96
+    coeffs = gen.g_k(rng, k, n) * 0.5
+    ang = 2 * np.pi * np.arange(n) / n + 0.1
+    zre = np.zeros((k, n)); zim = np.zeros((k, n))
+    zre[0] = 1.3 * np.cos(ang); zim[0] = 1.3 * np.sin(ang)
+    C, R, I = (torch.from_numpy(a).cuda() for a in (coeffs, zre, zim))
+    for sweeps in (3, 4):
+        ref = dk_sweeps(MonicPoly(coeffs), RootState(re=zre, im=zim), sweeps, Variant.BRANCH_FREE,
+                        exact_order=exact)
+        g = mwdist.DKPeerGraph(C, R, I, sweeps, Variant.BRANCH_FREE, exact_order=exact)
+        try:
+            for _ in range(3):
+                g.replay()
+                gre, gim, first = g.result()
+                assert first is None
+                assert_bitwise(gre.cpu().numpy(), ref.re.cpu().numpy())
+                assert_bitwise(gim.cpu().numpy(), ref.im.cpu().numpy())
+        finally:
+            g.close()
+
+
+def test_dk_peer_wait_times_out_instead_of_hanging():
+    """A peer that never publishes (world 2, rank 1 absent: both table
+    entries point at this rank's own buffer) makes the last CTA's wait
+    expire after spin_limit polls; the kernel returns and sets *timeout."""
+    import ctypes
+
+    from paper_2603_14926_b200 import _lib
+    from paper_2603_14926_b200 import dist as mwdist
+
+    lib = _lib.load()
+    k, n = 2, 64
+    lay = mwdist.PeerLayout(k, n, 2)
+    buf = ctypes.c_void_p()
+    _lib.check(lib.mw_peer_alloc(lay.total_bytes, ctypes.byref(buf)), "alloc")
+    try:
+        base = buf.value
+        outs, slots = mwdist.peer_tables([base, base], lay)
+        dev = torch.device("cuda", 0)
+        o = torch.tensor(outs[0], dtype=torch.int64, device=dev)
+        sl = torch.tensor(slots, dtype=torch.int64, device=dev)
+        rng = np.random.default_rng(3)
+        coeffs = torch.from_numpy(gen.g_k(rng, k, n) * 0.5).cuda()
+        done = torch.zeros(1, dtype=torch.int32, device=dev)
+        epoch = torch.zeros(1, dtype=torch.int64, device=dev)
+        tout = torch.zeros(1, dtype=torch.int32, device=dev)
+        mag = torch.empty(n, dtype=torch.float64, device=dev)
+        flag = torch.full((1,), 2**31 - 1, dtype=torch.int32, device=dev)
+        rc = lib.mw_dk_sweep_peer(k, 1, coeffs.data_ptr(), n, n, base, 0, n // 2, o.data_ptr(), sl.data_ptr(),
+                                  base + lay.state_off(1), base + lay.slot_off, done.data_ptr(), epoch.data_ptr(),
+                                  tout.data_ptr(), 2, 0, 0, 2, 2000, mag.data_ptr(), flag.data_ptr(), 0,
+                                  _lib.stream_handle(dev))
+        _lib.check(rc, "mw_dk_sweep_peer")
+        torch.cuda.synchronize()
+        assert int(tout.item()) == 1
+        assert int(done.item()) == 0  # ticket reset by the last CTA
+        # own slot from rank 0 was published (value epoch*sweeps + 0 + 1)
+        sv = torch.as_tensor(mwdist._DevView(base + lay.slot_off, (2,)), device=dev).view(torch.int64)
+        assert sv.cpu().tolist() == [1, 0]
+    finally:
+        lib.mw_peer_free(buf)
+
+
+def _ipc_worker(rank, port, outdir):
+    import ctypes
+    import os
+
+    import torch.distributed as dist
+
+    from paper_2603_14926_b200 import _lib
+    from paper_2603_14926_b200 import dist as mwdist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=2)
+    torch.cuda.set_device(0)
+    lib = _lib.load()
+    buf = ctypes.c_void_p()
+    _lib.check(lib.mw_peer_alloc(4096, ctypes.byref(buf)), "alloc")
+    own = torch.as_tensor(mwdist._DevView(buf.value, (512,)), device="cuda:0")
+    own[:256].fill_(rank + 1.0)
+    torch.cuda.synchronize()
+    h = (ctypes.c_char * 64)()
+    _lib.check(lib.mw_ipc_get_handle(buf, h), "handle")
+    hs = mwdist.exchange_handles(bytes(h))
+    peer = ctypes.c_void_p()
+    _lib.check(lib.mw_ipc_open_handle(hs[1 - rank], ctypes.byref(peer)), "open")
+    pv = torch.as_tensor(mwdist._DevView(peer.value, (512,)), device="cuda:0")
+    seen = float(pv[:256].sum().item())
+    pv[256 + rank].fill_(10.0 + rank)  # a store into the peer's buffer
+    torch.cuda.synchronize()
+    dist.barrier()
+    got = own[256:258].cpu().tolist()
+    with open(os.path.join(outdir, f"r{rank}.txt"), "w") as fh:
+        fh.write(f"{seen} {got[0]} {got[1]}")
+    dist.barrier()
+    lib.mw_ipc_close_handle(peer)
+    dist.barrier()
+    lib.mw_peer_free(buf)
+    dist.destroy_process_group()
+
+
+def test_ipc_peer_mapping_two_processes():
+    """mw_peer_alloc / mw_ipc_* between two processes on one GPU: each
+    reads the other's buffer and stores into it through the mapping (no
+    kernel waits on another process)."""
+    import tempfile
+
+    import torch.multiprocessing as mp
+
+    from test_dist_gloo import _free_port
+
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_ipc_worker, args=(_free_port(), d), nprocs=2, join=True)
+        r0 = open(f"{d}/r0.txt").read().split()
+        r1 = open(f"{d}/r1.txt").read().split()
+    assert float(r0[0]) == 256 * 2.0 and float(r1[0]) == 256 * 1.0
+    # rank p stored 10 + p at index 256 + p of the other rank's buffer
+    assert float(r0[2]) == 11.0 and float(r1[1]) == 10.0
