@@ -4,6 +4,7 @@
 // check their output is bit-identical to the product kernel.
 #include "../gemm_kernel.cuh"
 #include "../reduce.cu"  // GEMV kernel template (its C-ABI symbols stay private to this .so)
+#include "gemv_staged.cuh"
 
 namespace mw {
 #define CFGV(NAME, bm, bn, bk, tm, tn, minb, vec)                             \
@@ -94,6 +95,15 @@ static int gemv_launch(const double* A, const double* x, double* y, int64_t m, i
       A, n, m * n, x, n, y, m, m, n);
   return launch_status();
 }
+template <int K, int R, int D, int S, bool XS>
+static int gemv_staged_launch(const double* A, const double* x, double* y, int64_t m, int64_t n,
+                              cudaStream_t st) {
+  constexpr size_t smem = gemv_staged_smem<K, R, D, S, XS>();
+  auto kern = gemv_staged_kernel<K, BRANCH_FREE, R, D, S, XS>;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  kern<<<(unsigned)((m + R - 1) / R), 128 * R, smem, st>>>(A, n, m * n, x, n, y, m, m, n);
+  return launch_status();
+}
 template <int K>
 static int gemv_run(int cfg, const double* A, const double* x, double* y, int64_t m, int64_t n,
                     cudaStream_t st) {
@@ -106,14 +116,26 @@ static int gemv_run(int cfg, const double* A, const double* x, double* y, int64_
     case 5: return gemv_launch<K, 4, 2, 2>(A, x, y, m, n, st);
     case 6: return gemv_launch<K, 4, 1, 4>(A, x, y, m, n, st);
     case 7: return gemv_launch<K, 8, 1, 2>(A, x, y, m, n, st);
+    case 8: return gemv_staged_launch<K, 2, 4, 2, false>(A, x, y, m, n, st);
+    case 9: return gemv_staged_launch<K, 2, 4, 3, false>(A, x, y, m, n, st);
+    case 10: return gemv_staged_launch<K, 1, 4, 2, false>(A, x, y, m, n, st);
+    case 11: return gemv_staged_launch<K, 1, 4, 3, false>(A, x, y, m, n, st);
+    case 12: return gemv_staged_launch<K, 2, 2, 2, false>(A, x, y, m, n, st);
+    case 13: return gemv_staged_launch<K, 2, 2, 4, false>(A, x, y, m, n, st);
+    case 14: return gemv_staged_launch<K, 1, 4, 2, true>(A, x, y, m, n, st);
+    case 15: return gemv_staged_launch<K, 2, 4, 2, true>(A, x, y, m, n, st);
+    case 16: return gemv_staged_launch<K, 1, 8, 2, false>(A, x, y, m, n, st);
+    case 17: return gemv_staged_launch<K, 1, 2, 4, false>(A, x, y, m, n, st);
     default: return MW_ERR_INVALID;
   }
 }
-extern "C" int mwt_gemv_num_configs(void) { return 8; }
+extern "C" int mwt_gemv_num_configs(void) { return 18; }
 extern "C" const char* mwt_gemv_config_name(int cfg) {
-  static const char* names[] = {"W4_R2_D4", "W1_R8_D8", "W1_R8_D4", "W2_R4_D4",
-                                "W2_R4_D8", "W4_R2_D2", "W4_R1_D4", "W8_R1_D2"};
-  return (cfg >= 0 && cfg < 8) ? names[cfg] : "?";
+  static const char* names[] = {"W4_R2_D4", "W1_R8_D8", "W1_R8_D4", "W2_R4_D4", "W2_R4_D8",
+                                "W4_R2_D2", "W4_R1_D4", "W8_R1_D2", "st_R2_D4_S2", "st_R2_D4_S3",
+                                "st_R1_D4_S2", "st_R1_D4_S3", "st_R2_D2_S2", "st_R2_D2_S4",
+                                "stx_R1_D4_S2", "stx_R2_D4_S2", "st_R1_D8_S2", "st_R1_D2_S4"};
+  return (cfg >= 0 && cfg < 18) ? names[cfg] : "?";
 }
 extern "C" int mwt_gemv(int cfg, int k, const double* A, const double* x, double* y, int64_t m,
                         int64_t n, void* stream) {

@@ -15,9 +15,16 @@ for k in (3, 4):
     A, X = torch.from_numpy(a).cuda(), torch.from_numpy(x).cuda()
     m, n = a.shape[1], a.shape[2]
     y = torch.empty((k, m), dtype=torch.float64, device="cuda")
+    ref = None
     for cfg in range(lib.mwt_gemv_num_configs()):
         st = torch.cuda.current_stream().cuda_stream
         lib.mwt_gemv(cfg, k, A.data_ptr(), X.data_ptr(), y.data_ptr(), m, n, st)
+        torch.cuda.synchronize()
+        same = ""
+        if cfg == 0:
+            ref = y.clone()
+        elif cfg >= 8:  # staged variants keep the P = 128 order: must be bit-identical
+            same = " bits==W4" if torch.equal(y.view(torch.int64), ref.view(torch.int64)) else " BITS DIFFER"
         ts = []
         for _ in range(10):
             flush.fill_(1)
@@ -25,4 +32,4 @@ for k in (3, 4):
             e0.record(); lib.mwt_gemv(cfg, k, A.data_ptr(), X.data_ptr(), y.data_ptr(), m, n, st); e1.record()
             torch.cuda.synchronize(); ts.append(e0.elapsed_time(e1))
         ms = sorted(ts)[len(ts) // 2]
-        print(f"k={k} {lib.mwt_gemv_config_name(cfg).decode():10s} {ms*1e3:8.1f} us  {MAC[k]*m*n/(ms/1e3)/1e12:6.2f} T/s", flush=True)
+        print(f"k={k} {lib.mwt_gemv_config_name(cfg).decode():10s} {ms*1e3:8.1f} us  {MAC[k]*m*n/(ms/1e3)/1e12:6.2f} T/s{same}", flush=True)
