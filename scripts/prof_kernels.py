@@ -70,6 +70,13 @@ def main():
                 jobs.append((name, lambda q=q, st=st: mw.dk_sweeps(q, st, 1, BF, exact_order=False, check=False)))
             if want(name + "_exact"):
                 jobs.append((name + "_exact", lambda q=q, st=st: mw.dk_sweeps(q, st, 1, BF, exact_order=True, check=False)))
+    if want("dk_td_peer"):
+        from paper_2603_14926_b200 import dist as mwdist
+
+        coeffs = torch.from_numpy(gen.config5_poly(3)).cuda()
+        zre, zim = (torch.from_numpy(t).cuda() for t in gen.config5_init(3))
+        pg = mwdist.DKPeerGraph(coeffs, zre, zim, 2, BF, exact_order=False)
+        jobs.append(("dk_td_peer", pg.replay))
     if want("estrin_qd"):
         coeffs, x = gen.config4_horner(npts=1 << 20)
         P, X = mw.MWPolynomial(coeffs), mw.LaneBatch(x)

@@ -731,7 +731,8 @@ def test_no_out_of_bounds_writes(k):
 
 @pytest.mark.parametrize("k", [2, 3, 4])
 @pytest.mark.parametrize("exact", [True, False])
-def test_dk_peer_graph_matches_sweeps(k, exact):
+@pytest.mark.parametrize("v", ["bf", "std"])
+def test_dk_peer_graph_matches_sweeps(k, exact, v):
     """The fused-exchange sweep (mw_dk_sweep_peer through DKPeerGraph, one
     rank: stores, ticket, slot publication and wait all run) equals the
     plain sweeps bit for bit, for odd and even sweep counts and across
@@ -746,9 +747,9 @@ def test_dk_peer_graph_matches_sweeps(k, exact):
     zre[0] = 1.3 * np.cos(ang); zim[0] = 1.3 * np.sin(ang)
     C, R, I = (torch.from_numpy(a).cuda() for a in (coeffs, zre, zim))
     for sweeps in (3, 4):
-        ref = dk_sweeps(MonicPoly(coeffs), RootState(re=zre, im=zim), sweeps, Variant.BRANCH_FREE,
+        ref = dk_sweeps(MonicPoly(coeffs), RootState(re=zre, im=zim), sweeps, V(v),
                         exact_order=exact)
-        g = mwdist.DKPeerGraph(C, R, I, sweeps, Variant.BRANCH_FREE, exact_order=exact)
+        g = mwdist.DKPeerGraph(C, R, I, sweeps, V(v), exact_order=exact)
         try:
             for _ in range(3):
                 g.replay()
