@@ -19,7 +19,7 @@
 // FP64 latency, measured), so a sweep costs ~n steps of ~700 cycles (TD).  The reciprocal of mag is computed once and applied to both
 // parts, which is the identical op sequence the reference runs twice.
 //
-// exact_order = 0 (tree): four warps per root (definition below): 64
+// exact_order = 0 (tree): three warps per root (definition below): 64
 // strided partial products for the denominator, 64 Horner blocks for the
 // numerator scaled by powers of z^B, pairwise trees.  Same arithmetic per
 // term, reassociated: within the n*2^-p relative bound.
