@@ -53,9 +53,10 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline sample")
     ap.add_argument("--quick", action="store_true", help="small sizes (debug)")
     ap.add_argument("--no-secondary", action="store_true", help="skip configs 1, 2 and 5")
-    ap.add_argument("--peer-dk", action="store_true",
-                    help="N > 1: also time the DK sweep with the exchange fused in (DKPeerGraph, cudaIpc peer "
-                         "memory); off by default until it has been run on a multi-GPU node")
+    ap.add_argument("--peer-exchange", "--peer-dk", dest="peer_dk", action="store_true",
+                    help="N > 1: also time the dot and the DK sweep with the exchange fused into the kernel "
+                         "(DotPeer / DKPeerGraph, cudaIpc peer memory); off by default until it has been run "
+                         "on a multi-GPU node")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="process-group backend for N > 1 (gloo only to exercise the multi-rank "
                          "logic where fewer GPUs than ranks exist; never for timing)")
@@ -530,6 +531,20 @@ def secondary(args, torch, dist, mw, world, rank, peak):
     else:
         be = mwdist.gpu_dot_backend(BF)
         ms_dot = timed(lambda: mwdist.dot_allgather(X.planes, Y.planes, be), 50)
+    # the all-gather-then-sum fused into one kernel per rank (DotPeer)
+    peer_dot = None
+    if world == 1 or (args.backend == "nccl" and args.peer_dk):
+        try:
+            dp = mwdist.DotPeer(2, n1, BF, device=X.planes.device)
+            pres = torch.empty(2, dtype=torch.float64, device="cuda")
+            ms_p = timed(lambda: dp(X.planes, Y.planes, out=pres), 200)
+            ms_pg = timed_graph(lambda: dp(X.planes, Y.planes, out=pres)) if world == 1 else None
+            dp.check()
+            dp.close()
+            peer_dot = {"us_per_call": round(ms_p * 1e3, 2),
+                        "us_per_call_graph": None if ms_pg is None else round(ms_pg * 1e3, 2)}
+        except Exception as e:  # reported, never fatal to the bench line
+            peer_dot = {"error": f"{type(e).__name__}: {e}"[:200]}
     Xs, Ys = mw.LaneBatch(x[:, lo:hi]), mw.LaneBatch(y[:, lo:hi])
     ms_axpy = timed(lambda: blas.axpy_(tuple(alpha), Xs, Ys, BF), 200)
     if world == 1:
@@ -540,7 +555,8 @@ def secondary(args, torch, dist, mw, world, rank, peak):
         "G_MPops_graph": None if ms_dot_graph is None else round(2 * n1 / (ms_dot_graph / 1e3) / 1e9, 3),
         "hbm_frac": round(2 * 2 * n1 * 8 / (ms_dot / 1e3) / hbm, 4),
         "order": "tree (256 strided partials per 4096-element block + pairwise tree)" + (", all-gather-then-sum over ranks" if world > 1 else ""),
-        "note": "2 MiB input is L2-resident and launch-bound; hbm_frac is bytes/time vs HBM copy peak"}
+        "note": "2 MiB input is L2-resident and launch-bound; hbm_frac is bytes/time vs HBM copy peak",
+        "fused_peer_exchange": peer_dot}
     out["config1_axpy_dd_n65536"] = {
         "us_per_call": round(ms_axpy * 1e3, 2), "G_MPops": round(2 * n1 / (ms_axpy / 1e3) / 1e9, 3),
         "us_per_call_graph": None if ms_axpy_graph is None else round(ms_axpy_graph * 1e3, 2),

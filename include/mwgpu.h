@@ -206,7 +206,29 @@ int mw_dk_sweep_peer(int k, int variant, const double* coeffs, int64_t sc,
                      long long spin_limit, double* step_mag, int* flag_dev,
                      int exact_order, void* stream);
 
-/* Peer buffers for mw_dk_sweep_peer: a zeroed cudaMalloc allocation (one
+/* Sharded tree dot with the all-gather-then-sum fused into one kernel per
+ * rank ("dot products by a custom multi-component
+ * all-gather-then-sum, since NCCL's sum is not error-free"; replaces
+ * mw_dot_partials + all-gather + mw_tree_fold of dist.dot_allgather).
+ * x, y: this rank's slice (n_local elements) starting at global element
+ * 4096*b0 (slices cut at multiples of 4096; only the last may be ragged).
+ * nbt = ceil(n_total/4096) <= 65536 block roots over all ranks.  Each block
+ * stores its root into slot b0 + b of every rank's root buffer
+ * (peer_roots: device array of world pointers; buffer = 2 parities x k
+ * planes x nbt doubles, parity = *epoch & 1); the last block publishes
+ * *epoch + 1 into peer_slot (as mw_dk_sweep_peer), waits (bounded by
+ * spin_limit, then *timeout = 1), folds the nbt roots with the pairwise
+ * tree and writes k doubles to out_dev; *epoch is then incremented.
+ * Bit-identical to mw_dot(order TREE) over the full vectors. */
+int mw_dot_peer(int k, int variant, const double* x, int64_t sx,
+                const double* y, int64_t sy, int64_t n_local, int64_t b0,
+                int64_t nbt, double* const* peer_roots,
+                unsigned long long* const* peer_slot,
+                unsigned long long* my_slot, unsigned int* done,
+                unsigned long long* epoch, int* timeout, int world, int rank,
+                long long spin_limit, double* out_dev, void* stream);
+
+/* Peer buffers for mw_dk_sweep_peer / mw_dot_peer: a zeroed cudaMalloc allocation (one
  * IPC handle covers exactly one buffer), its 64-byte cudaIpcMemHandle_t,
  * and open/close of a peer's handle (cudaIpcMemLazyEnablePeerAccess). */
 int mw_peer_alloc(int64_t bytes, void** out);

@@ -55,6 +55,7 @@ _SIGS = {
     "mw_dk_exact_set_roots_per_cta": ([I], I),
     "mw_dk_sweep_peer": ([I, I, P, I64, I64, P, I64, I64, P, P, P, P, P, P, P, I, I, I, I, ctypes.c_longlong, P, P,
                           I, P], I),
+    "mw_dot_peer": ([I, I, P, I64, P, I64, I64, I64, I64, P, P, P, P, P, P, I, I, ctypes.c_longlong, P, P], I),
     "mw_peer_alloc": ([I64, ctypes.POINTER(P)], I),
     "mw_peer_free": ([P], I),
     "mw_ipc_get_handle": ([P, P], I),

@@ -27,6 +27,7 @@
 #include <cstring>
 
 #include "common.cuh"
+#include "peer.cuh"
 
 namespace mw {
 
@@ -96,21 +97,6 @@ struct DkPeers {
   int world, rank, sweep, sweeps;
 };
 
-__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-
-__device__ __forceinline__ unsigned atom_add_acq_rel_gpu(unsigned* p, unsigned v) {
-  unsigned old;
-  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
-  return old;
-}
-
 // Called by exactly one thread per CTA, after a sync over the CTA's
 // storing threads.
 __device__ __noinline__ void dk_peer_ticket(const DkPeers& P) {
@@ -118,19 +104,7 @@ __device__ __noinline__ void dk_peer_ticket(const DkPeers& P) {
   *(volatile unsigned*)P.done = 0;  // the next launch in the stream starts from zero
   const unsigned long long e = *(volatile unsigned long long*)P.epoch;
   const unsigned long long v = e * (unsigned long long)P.sweeps + (unsigned long long)P.sweep + 1ull;
-  for (int p = 0; p < P.world; ++p) st_release_sys(P.slot[p] + P.rank, v);
-  int gave_up = *(volatile int*)P.timeout;
-  for (int src = 0; src < P.world && !gave_up; ++src) {
-    long long spins = 0;
-    while (ld_acquire_sys(P.my_slot + src) < v) {
-      if (++spins > P.spin_limit) {
-        atomicExch(P.timeout, 1);
-        gave_up = 1;
-        break;
-      }
-      __nanosleep(256);
-    }
-  }
+  peer_publish_wait(P.slot, P.my_slot, P.world, P.rank, v, P.spin_limit, P.timeout);
   if (P.sweep == P.sweeps - 1) *(volatile unsigned long long*)P.epoch = e + 1;
 }
 

@@ -18,6 +18,7 @@
 //   gemv: 128 partials per row; partial u folds t = u, u+128, ... ascending
 //         from exact zero; the partials combine by the same pairwise tree.
 #include "common.cuh"
+#include "peer.cuh"
 
 namespace mw {
 
@@ -223,6 +224,111 @@ struct DotLaunch {
   }
 };
 
+// Sharded tree dot with the all-gather-then-sum fused in (peer memory):
+// rank r's slice covers global blocks [b0, b0 + nb_local); block b stores
+// its subtree root into slot b0 + b of EVERY rank's root buffer (cudaIpc
+// mapping), takes a ticket; the last block publishes and waits (peer.cuh),
+// then folds all nbt block roots from the local buffer with the pairwise
+// tree (<= 256: one block tree; <= 65536: two levels of 256, the tree_fold
+// order) -- bit-identical to the 1-GPU tree dot on every rank.  Root
+// buffers are double-buffered by call parity (epoch & 1) so a rank already
+// in call c+1 never overwrites roots a slower rank is still folding.
+template <int K, int VAR>
+__global__ void __launch_bounds__(DOT_BLOCK) dot_peer_kernel(
+    const double* __restrict__ x, int64_t sx, const double* __restrict__ y, int64_t sy,
+    int64_t n_local, int64_t b0, int64_t nbt, double* const* peer_roots,
+    unsigned long long* const* peer_slot, unsigned long long* my_slot, unsigned int* done,
+    unsigned long long* epoch, int* timeout, int world, int rank, long long spin_limit,
+    double* __restrict__ out) {
+  __shared__ bool is_last;
+  __shared__ double lvl[K][DOT_BLOCK];
+  const int tid = threadIdx.x;
+  const unsigned long long e = *(volatile unsigned long long*)epoch;  // before the ticket
+  const int64_t par_off = (int64_t)(e & 1ull) * K * nbt;
+  const int64_t nbl = n_local > 0 ? (n_local + DOT_PER_BLOCK - 1) / DOT_PER_BLOCK : 0;
+  if (blockIdx.x < nbl) {
+    const int64_t base = blockIdx.x * DOT_PER_BLOCK + tid;
+    V<K> acc = zero<K>();
+    if (blockIdx.x * DOT_PER_BLOCK + DOT_PER_BLOCK <= n_local) {
+      V<K> xs[DOT_LEAF], ys[DOT_LEAF];
+#pragma unroll
+      for (int j = 0; j < DOT_LEAF; ++j) {
+        xs[j] = load<K>(x, sx, base + j * DOT_BLOCK);
+        ys[j] = load<K>(y, sy, base + j * DOT_BLOCK);
+      }
+#pragma unroll
+      for (int j = 0; j < DOT_LEAF; ++j)
+        acc = Ops<K, VAR>::add(acc, Ops<K, VAR>::mul(xs[j], ys[j]));
+    } else {
+      for (int64_t t = base; t < n_local; t += DOT_BLOCK)
+        acc = Ops<K, VAR>::add(acc, Ops<K, VAR>::mul(load<K>(x, sx, t), load<K>(y, sy, t)));
+    }
+    V<K> r = block_tree<K, VAR>(acc, blockIdx.x * (int64_t)DOT_BLOCK, dot_partial_count(n_local));
+    if (tid == 0) {
+      for (int p = 0; p < world; ++p) {
+        double* dst = peer_roots[p] + par_off + b0 + blockIdx.x;
+#pragma unroll
+        for (int c = 0; c < K; ++c) dst[c * nbt] = r.c[c];
+      }
+    }
+  }
+  if (tid == 0) is_last = atom_add_acq_rel_gpu(done, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!is_last) return;
+  if (tid == 0) {
+    *(volatile unsigned*)done = 0u;
+    peer_publish_wait(peer_slot, my_slot, world, rank, e + 1ull, spin_limit, timeout);
+  }
+  __syncthreads();
+  const double* roots = peer_roots[rank] + par_off;
+  const int64_t groups = (nbt + DOT_BLOCK - 1) / DOT_BLOCK;
+  V<K> fin;
+  for (int64_t g = 0; g < groups; ++g) {
+    V<K> v = zero<K>();
+    const int64_t i = g * DOT_BLOCK + tid;
+    if (i < nbt) {
+#pragma unroll
+      for (int c = 0; c < K; ++c) v.c[c] = __ldcg(roots + c * nbt + i);
+    }
+    __syncthreads();  // block_tree reuses its shared buffer
+    V<K> r = block_tree<K, VAR>(v, g * (int64_t)DOT_BLOCK, nbt);
+    if (tid == 0) {
+#pragma unroll
+      for (int c = 0; c < K; ++c) lvl[c][g] = r.c[c];
+    }
+    fin = r;
+  }
+  if (groups > 1) {
+    __syncthreads();
+    V<K> v = zero<K>();
+    if (tid < groups) {
+#pragma unroll
+      for (int c = 0; c < K; ++c) v.c[c] = lvl[c][tid];
+    }
+    __syncthreads();
+    fin = block_tree<K, VAR>(v, 0, groups);
+  }
+  if (tid == 0) {
+    store<K>(out, 1, 0, fin);
+    *(volatile unsigned long long*)epoch = e + 1ull;
+  }
+}
+
+template <int K, int VAR>
+struct DotPeerLaunch {
+  static int run(const double* x, int64_t sx, const double* y, int64_t sy, int64_t n_local,
+                 int64_t b0, int64_t nbt, double* const* peer_roots,
+                 unsigned long long* const* peer_slot, unsigned long long* my_slot,
+                 unsigned int* done, unsigned long long* epoch, int* timeout, int world, int rank,
+                 long long spin_limit, double* out, cudaStream_t st) {
+    const int64_t nbl = n_local > 0 ? ceil_div(n_local, DOT_PER_BLOCK) : 0;
+    dot_peer_kernel<K, VAR><<<(unsigned)(nbl > 0 ? nbl : 1), DOT_BLOCK, 0, st>>>(
+        x, sx, y, sy, n_local, b0, nbt, peer_roots, peer_slot, my_slot, done, epoch, timeout,
+        world, rank, spin_limit, out);
+    return launch_status();
+  }
+};
+
 template <int K, int VAR>
 struct DotPartialsLaunch {
   static int run(const double* x, int64_t sx, const double* y, int64_t sy, int64_t n,
@@ -423,4 +529,30 @@ extern "C" int mw_gemv(int k, int variant, const double* A, int64_t lda, int64_t
   if (n > 0 && sA < (m - 1) * lda + n) return MW_ERR_INVALID;
   return dispatch<GemvLaunch>(k, variant, A, lda, sA, x, sx, y, sy, m, n, order,
                               as_stream(stream));
+}
+
+// Sharded tree dot, exchange fused in (dot_peer_kernel).  x, y: this
+// rank's slice (n_local elements, starting at global element 4096 * b0;
+// only the last rank's slice may end ragged).  nbt: block roots over all
+// ranks (ceil(n_total / 4096), <= 65536).  peer_roots: device array of
+// world pointers to each rank's root buffer (2 parities x k planes x nbt);
+// peer_slot / my_slot / done / epoch / timeout as for mw_dk_sweep_peer.
+// out_dev (k doubles) receives the full dot on every rank.
+extern "C" int mw_dot_peer(int k, int variant, const double* x, int64_t sx, const double* y,
+                           int64_t sy, int64_t n_local, int64_t b0, int64_t nbt,
+                           double* const* peer_roots, unsigned long long* const* peer_slot,
+                           unsigned long long* my_slot, unsigned int* done,
+                           unsigned long long* epoch, int* timeout, int world, int rank,
+                           long long spin_limit, double* out_dev, void* stream) {
+  int rc = variant_ok(k, variant);
+  if (rc) return rc;
+  if (world < 1 || rank < 0 || rank >= world || spin_limit < 1) return MW_ERR_INVALID;
+  if (nbt < 1 || nbt > (int64_t)DOT_BLOCK * DOT_BLOCK || b0 < 0 || n_local < 0) return MW_ERR_INVALID;
+  if (b0 + ceil_div(n_local, DOT_PER_BLOCK) > nbt) return MW_ERR_INVALID;
+  if (n_local > 0 && (!x || !y || sx < n_local || sy < n_local)) return MW_ERR_INVALID;
+  if (!peer_roots || !peer_slot || !my_slot || !done || !epoch || !timeout || !out_dev)
+    return MW_ERR_INVALID;
+  return dispatch<DotPeerLaunch>(k, variant, x, sx, y, sy, n_local, b0, nbt, peer_roots, peer_slot,
+                                 my_slot, done, epoch, timeout, world, rank, spin_limit, out_dev,
+                                 as_stream(stream));
 }

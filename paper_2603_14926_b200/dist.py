@@ -21,7 +21,10 @@ Only the paths that shard naturally are partitioned:
               partial per 4096), all ranks all-gather them and fold the full
               partial list with the same pairwise tree -- bit-identical to
               the 1-GPU tree dot and on every rank.  NCCL's sum would not be
-              error-free, so no reduction collective is used.
+              error-free, so no reduction collective is used.  ``DotPeer``
+              does the same inside one kernel per rank: block roots are
+              stored straight into every rank's root buffer over NVLink and
+              the last block folds them after a bounded completion wait.
 
 Every partition is over disjoint outputs with a fixed combine order, so
 results are invariant to the number of GPUs (the reference's thread
@@ -42,7 +45,7 @@ import torch.distributed as dist
 
 __all__ = ["shard_range", "aligned_shard_range", "DotBackend", "gpu_dot_backend", "dot_allgather",
            "dk_sweeps_sharded", "allgather_planes", "DKShardedGraph", "PeerLayout", "peer_tables",
-           "exchange_handles", "DKPeerGraph"]
+           "exchange_handles", "PeerBuffer", "DKPeerGraph", "DotPeer"]
 
 DOT_PARTIAL_SPAN = 4096  # elements per dot partial (mw_dot_partials)
 
@@ -293,6 +296,62 @@ class _DevView:
                                          "strides": None}
 
 
+class PeerBuffer:
+    """One zeroed cudaMalloc buffer per rank, cross-mapped into every rank
+    with cudaIpc handles (exchanged over ``group``).  ``bases[p]`` is rank
+    p's buffer as seen from this process (own pointer for p == rank).
+    Construction and ``close()`` are collective."""
+
+    def __init__(self, nbytes: int, device: torch.device, group=None):
+        import ctypes
+
+        from . import _lib
+
+        self._lib = lib = _lib.load()
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.device = device
+        buf = ctypes.c_void_p()
+        with torch.cuda.device(device):
+            _lib.check(lib.mw_peer_alloc(nbytes, ctypes.byref(buf)), "mw_peer_alloc")
+        self.base = buf.value
+        self._opened: list[int] = []
+        self.bases = [self.base] * self.world
+        if self.world > 1:
+            h = (ctypes.c_char * 64)()
+            _lib.check(lib.mw_ipc_get_handle(self.base, h), "mw_ipc_get_handle")
+            handles = exchange_handles(bytes(h), group)
+            for p, hp in enumerate(handles):
+                if p == self.rank:
+                    continue
+                q = ctypes.c_void_p()
+                with torch.cuda.device(device):
+                    _lib.check(lib.mw_ipc_open_handle(hp, ctypes.byref(q)), "mw_ipc_open_handle")
+                self._opened.append(q.value)
+                self.bases[p] = q.value
+            torch.cuda.synchronize(device)
+            dist.barrier(group)  # every buffer allocated, zeroed and mapped before the first peer store
+
+    def view(self, offset: int, shape: tuple) -> torch.Tensor:
+        """float64 tensor view of this rank's buffer at byte ``offset``."""
+        return torch.as_tensor(_DevView(self.base + offset, shape), device=self.device)
+
+    def close(self):
+        if self.base is None:
+            return
+        torch.cuda.synchronize(self.device)
+        if self.world > 1:
+            dist.barrier(self.group)  # no peer still storing into our buffer
+        for q in self._opened:
+            self._lib.mw_ipc_close_handle(q)
+        self._opened = []
+        if self.world > 1:
+            dist.barrier(self.group)  # every peer unmapped our buffer
+        self._lib.mw_peer_free(self.base)
+        self.base = None
+
+
 class DKPeerGraph:
     """``sweeps`` root-sharded DK sweeps whose state exchange happens inside
     the sweep kernel (mw_dk_sweep_peer): no collective on the data path.
@@ -305,8 +364,6 @@ class DKPeerGraph:
 
     def __init__(self, coeffs: torch.Tensor, zre: torch.Tensor, zim: torch.Tensor, sweeps: int, variant,
                  exact_order: bool = True, group=None, spin_limit: int = 8_000_000):
-        import ctypes
-
         from . import _lib
         from .multiword import variant_code
         from .roots import INT32_MAX
@@ -326,31 +383,13 @@ class DKPeerGraph:
         lo, hi = self.rank * per, (self.rank + 1) * per
         dev = zre.device
         self.layout = lay = PeerLayout(k, n, self.world)
-        self._lib = lib
-        buf = ctypes.c_void_p()
-        with torch.cuda.device(dev):
-            _lib.check(lib.mw_peer_alloc(lay.total_bytes, ctypes.byref(buf)), "mw_peer_alloc")
-        self._base = buf.value
-        self._opened: list[int] = []
-        bases = [self._base] * self.world
-        if self.world > 1:
-            h = (ctypes.c_char * 64)()
-            _lib.check(lib.mw_ipc_get_handle(self._base, h), "mw_ipc_get_handle")
-            handles = exchange_handles(bytes(h), group)
-            for p, hp in enumerate(handles):
-                if p == self.rank:
-                    continue
-                q = ctypes.c_void_p()
-                with torch.cuda.device(dev):
-                    _lib.check(lib.mw_ipc_open_handle(hp, ctypes.byref(q)), "mw_ipc_open_handle")
-                self._opened.append(q.value)
-                bases[p] = q.value
+        self._buf = PeerBuffer(lay.total_bytes, dev, group)
+        bases = self._buf.bases
         outs, slots = peer_tables(bases, lay)
         self._outs = [torch.tensor(o, dtype=torch.int64, device=dev) for o in outs]
         self._slots = torch.tensor(slots, dtype=torch.int64, device=dev)
-        self._state = [torch.as_tensor(_DevView(self._base + lay.state_off(par), (2 * k, n)), device=dev)
-                       for par in (0, 1)]
-        my_slot = self._base + lay.slot_off
+        self._state = [self._buf.view(lay.state_off(par), (2 * k, n)) for par in (0, 1)]
+        my_slot = self._buf.base + lay.slot_off
         self._done = torch.zeros(1, dtype=torch.int32, device=dev)
         self._epoch = torch.zeros(1, dtype=torch.int64, device=dev)
         self._timeout = torch.zeros(1, dtype=torch.int32, device=dev)
@@ -360,9 +399,6 @@ class DKPeerGraph:
         self._coeffs = coeffs.contiguous()
         v = variant_code(variant)
         exact = 1 if exact_order else 0
-        if self.world > 1:
-            torch.cuda.synchronize(dev)
-            dist.barrier(group)  # every buffer allocated, zeroed and mapped before the first peer store
 
         def body(start: int):
             # sweeps are numbered globally across runs (g = run * sweeps + s)
@@ -424,17 +460,71 @@ class DKPeerGraph:
     def close(self):
         """Release the peer mappings and the buffer (collective: every rank
         calls it, after its last replay)."""
-        if self._base is None:
-            return
-        torch.cuda.synchronize(self._state[0].device)
-        if self.world > 1:
-            dist.barrier(self.group)  # no peer still storing into our buffer
         self.graphs = None
         self._state = None
-        for q in self._opened:
-            self._lib.mw_ipc_close_handle(q)
-        self._opened = []
-        if self.world > 1:
-            dist.barrier(self.group)  # every peer unmapped our buffer
-        self._lib.mw_peer_free(self._base)
-        self._base = None
+        self._buf.close()
+
+
+class DotPeer:
+    """Sharded tree dot with the all-gather-then-sum inside ONE kernel per
+    rank (mw_dot_peer): each block's subtree root is stored into every
+    rank's root buffer over NVLink, the last block waits for all ranks'
+    roots (bounded) and folds them with the pairwise tree.  Same shards and
+    bits as ``dot_allgather`` (the 1-GPU tree dot) on every rank, no NCCL
+    on the data path.  One instance per (k, n); calls are stream-ordered
+    and graph-capturable (device-side epoch selects the root-buffer
+    parity)."""
+
+    def __init__(self, k: int, n: int, variant, device=None, group=None, spin_limit: int = 8_000_000):
+        from . import _lib
+        from .multiword import variant_code
+
+        if n < 1:
+            raise ValueError("n must be >= 1")
+        dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.k, self.n, self.v = k, n, variant_code(variant)
+        self.nbt = (n + DOT_PARTIAL_SPAN - 1) // DOT_PARTIAL_SPAN
+        if self.nbt > 256 * 256:
+            raise ValueError("n too large for the fused dot (at most 2^28 elements)")
+        self._buf = PeerBuffer(2 * k * self.nbt * 8 + 8 * (dist.get_world_size(group) if dist.is_initialized()
+                                                              else 1), dev, group)
+        self.world, self.rank = self._buf.world, self._buf.rank
+        self.lo, self.hi = aligned_shard_range(n, self.rank, self.world, DOT_PARTIAL_SPAN)
+        slot_off = 2 * k * self.nbt * 8
+        self._roots = torch.tensor(self._buf.bases, dtype=torch.int64, device=dev)
+        self._slots = torch.tensor([b + slot_off for b in self._buf.bases], dtype=torch.int64, device=dev)
+        self._my_slot = self._buf.base + slot_off
+        self._done = torch.zeros(1, dtype=torch.int32, device=dev)
+        self._epoch = torch.zeros(1, dtype=torch.int64, device=dev)
+        self._timeout = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.spin_limit = spin_limit
+        self.device = dev
+        self._lib = _lib
+
+    def __call__(self, x: torch.Tensor, y: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        """x, y: the full (K, n) planes (each rank reads only its slice).
+        Returns the (K,) dot on every rank."""
+        _lib = self._lib
+        if x.shape != (self.k, self.n) or y.shape != (self.k, self.n):
+            raise ValueError("operand shape does not match this DotPeer")
+        if x.device != self.device or y.device != self.device:
+            raise ValueError("operands on a different device")
+        if x.stride(1) != 1 or y.stride(1) != 1:
+            raise ValueError("planes must be contiguous along the element axis")
+        out = torch.empty(self.k, dtype=torch.float64, device=self.device) if out is None else out
+        nl = self.hi - self.lo
+        rc = _lib.load().mw_dot_peer(
+            self.k, self.v, x.data_ptr() + 8 * self.lo, x.stride(0), y.data_ptr() + 8 * self.lo, y.stride(0), nl,
+            self.lo // DOT_PARTIAL_SPAN, self.nbt, self._roots.data_ptr(), self._slots.data_ptr(), self._my_slot,
+            self._done.data_ptr(), self._epoch.data_ptr(), self._timeout.data_ptr(), self.world, self.rank,
+            self.spin_limit, out.data_ptr(), _lib.stream_handle(self.device))
+        _lib.check(rc, "mw_dot_peer")
+        return out
+
+    def check(self):
+        """Raise if any completion wait expired."""
+        if int(self._timeout.item()):
+            raise RuntimeError("DotPeer: a peer completion wait expired (a rank stalled or diverged)")
+
+    def close(self):
+        self._buf.close()

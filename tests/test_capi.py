@@ -98,6 +98,14 @@ def test_peer_sweep_checks():
     assert call(spin=0) == _lib.MW_ERR_INVALID
     assert call(peer_slot=None) == _lib.MW_ERR_INVALID
     assert call(sc=7) == _lib.MW_ERR_INVALID
+    d = lib.mw_dot_peer
+    #          k  v  x  sx y  sy nl  b0 nbt roots slot my done ep to world rank spin out stream
+    assert d(2, 1, p, 8, p, 8, 8, 0, 0, p, p, p, p, p, p, 2, 0, 100, p, None) == _lib.MW_ERR_INVALID  # nbt
+    assert d(2, 1, p, 8, p, 8, 8, 1, 1, p, p, p, p, p, p, 2, 0, 100, p, None) == _lib.MW_ERR_INVALID  # past nbt
+    assert d(2, 1, p, 8, p, 8, 8, 0, 1, p, p, p, p, p, p, 2, 2, 100, p, None) == _lib.MW_ERR_INVALID  # rank
+    assert d(2, 1, p, 8, p, 8, 8, 0, 1, p, p, p, p, p, p, 2, 0, 0, p, None) == _lib.MW_ERR_INVALID  # spin
+    assert d(2, 1, p, 8, p, 8, 8, 0, 65537, p, p, p, p, p, p, 2, 0, 9, p, None) == _lib.MW_ERR_INVALID
+    assert d(2, 1, p, 4, p, 8, 8, 0, 1, p, p, p, p, p, p, 2, 0, 9, p, None) == _lib.MW_ERR_INVALID  # sx
     out = ctypes.c_void_p()
     assert lib.mw_peer_alloc(0, ctypes.byref(out)) == _lib.MW_ERR_INVALID
     assert lib.mw_peer_free(None) == _lib.MW_ERR_INVALID

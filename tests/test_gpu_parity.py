@@ -859,3 +859,65 @@ def test_ipc_peer_mapping_two_processes():
     assert float(r0[0]) == 256 * 2.0 and float(r1[0]) == 256 * 1.0
     # rank p stored 10 + p at index 256 + p of the other rank's buffer
     assert float(r0[2]) == 11.0 and float(r1[1]) == 10.0
+
+
+@pytest.mark.parametrize("k", [2, 3, 4])
+def test_dot_peer_matches_tree_dot(k):
+    """DotPeer (mw_dot_peer: roots stored to every rank's buffer, ticket,
+    slot publication, wait, in-kernel fold) on one rank equals the 1-GPU
+    tree dot and its oracle restatement bit for bit: ragged n, n below one
+    block, n needing the two-level fold (> 256 block roots), and repeated
+    calls (alternating root-buffer parity)."""
+    from paper_2603_14926_b200 import blas
+    from paper_2603_14926_b200 import dist as mwdist
+
+    for n in (1, 100, 4096, 70001, (1 << 20) + 4097):
+        rng = np.random.default_rng(n + k)
+        x, y = gen.g_k(rng, k, n), gen.g_k(rng, k, n)
+        X, Y = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
+        want = blas.dot_tensor(LaneBatch(X), LaneBatch(Y), Variant.BRANCH_FREE).cpu().numpy()
+        if n <= 70001:
+            assert_bitwise(want, oracle.dot(x, y, "bf", order=1))
+        dp = mwdist.DotPeer(k, n, Variant.BRANCH_FREE)
+        try:
+            for _ in range(3):
+                got = dp(X, Y)
+                assert_bitwise(got.cpu().numpy(), want)
+            dp.check()
+        finally:
+            dp.close()
+
+
+def test_dot_peer_wait_times_out_instead_of_hanging():
+    """World 2 with the absent peer's table entries pointing at this rank:
+    the last block's wait expires and the kernel returns with *timeout set."""
+    import ctypes
+
+    from paper_2603_14926_b200 import _lib
+
+    lib = _lib.load()
+    k, n = 2, 8192
+    nbt = 2
+    nbytes = 2 * k * nbt * 8 + 2 * 8
+    buf = ctypes.c_void_p()
+    _lib.check(lib.mw_peer_alloc(nbytes, ctypes.byref(buf)), "alloc")
+    try:
+        base = buf.value
+        dev = torch.device("cuda", 0)
+        roots = torch.tensor([base, base], dtype=torch.int64, device=dev)
+        slot_off = 2 * k * nbt * 8
+        slots = torch.tensor([base + slot_off] * 2, dtype=torch.int64, device=dev)
+        rng = np.random.default_rng(2)
+        X = torch.from_numpy(gen.g_k(rng, k, n)).cuda()
+        done = torch.zeros(1, dtype=torch.int32, device=dev)
+        epoch = torch.zeros(1, dtype=torch.int64, device=dev)
+        tout = torch.zeros(1, dtype=torch.int32, device=dev)
+        out = torch.empty(k, dtype=torch.float64, device=dev)
+        rc = lib.mw_dot_peer(k, 1, X.data_ptr(), n, X.data_ptr(), n, 4096, 0, nbt, roots.data_ptr(),
+                             slots.data_ptr(), base + slot_off, done.data_ptr(), epoch.data_ptr(),
+                             tout.data_ptr(), 2, 0, 2000, out.data_ptr(), _lib.stream_handle(dev))
+        _lib.check(rc, "mw_dot_peer")
+        torch.cuda.synchronize()
+        assert int(tout.item()) == 1 and int(done.item()) == 0 and int(epoch.item()) == 1
+    finally:
+        lib.mw_peer_free(buf)
