@@ -12,7 +12,10 @@ mw_dk_sweep_peer in csrc/dk.cu) that need no GPU:
   peer has not finished reading, and that each run's result is intact
   when the host reads it.  Variants that publish completion before the
   stores, or that restart every run from parity 0, are caught by the same
-  model (so it has teeth).
+  model (so it has teeth);
+* the same for the fused dot (mw_dot_peer): roots stored, slot published,
+  wait, then the fold reads every root; a single (not double) root buffer
+  is caught.
 """
 
 import os
@@ -169,3 +172,63 @@ def test_model_catches_fixed_start_parity_with_odd_sweeps():
     """Restarting every run at parity 0 with an odd sweep count lets a peer
     already in the next run overwrite the previous result."""
     assert _breaks(world=3, sweeps=3, runs=3, per=2, fixed_start=True) > 0
+
+
+def _dot_model(world, calls, seed, single_buffer=False):
+    """The mw_dot_peer protocol: per call c each rank stores its root into
+    slot [rank] of every rank's buffer (parity c % 2), publishes c + 1,
+    waits for all sources, then folds (reads) its own buffer."""
+    rng = random.Random(seed)
+    buf = [[[None] * world for _ in range(2)] for _ in range(world)]
+    slots = [[0] * world for _ in range(world)]
+
+    def check(cond, msg):
+        if not cond:
+            raise _Hazard(msg)
+
+    def program(r):
+        for c in range(calls):
+            par = 0 if single_buffer else c & 1
+            peers = list(range(world))
+            rng.shuffle(peers)
+            for p in peers:
+                buf[p][par][r] = c
+                yield
+            for p in range(world):
+                slots[p][r] = c + 1
+                yield
+            for src in range(world):
+                while slots[r][src] < c + 1:
+                    yield
+            order = list(range(world))
+            rng.shuffle(order)
+            for i in order:  # the last block's fold reads every root
+                check(buf[r][par][i] == c, f"rank {r} call {c} folded root {i} = {buf[r][par][i]}")
+                yield
+
+    progs = [program(r) for r in range(world)]
+    live = set(range(world))
+    steps = 0
+    while live:
+        r = rng.choice(sorted(live))
+        try:
+            next(progs[r])
+        except StopIteration:
+            live.discard(r)
+        steps += 1
+        assert steps < 1_000_000, "deadlock"
+
+
+def test_dot_protocol_model():
+    for seed in range(80):
+        _dot_model(2 + seed % 4, calls=4, seed=seed)
+
+
+def test_dot_model_catches_single_buffer():
+    broke = 0
+    for seed in range(100):
+        try:
+            _dot_model(3, calls=4, seed=seed, single_buffer=True)
+        except _Hazard:
+            broke += 1
+    assert broke > 0
