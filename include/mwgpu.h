@@ -241,6 +241,13 @@ int mw_ipc_close_handle(void* p);
  * Results do not depend on it (each root is one chain in reference order). */
 int mw_dk_exact_set_roots_per_cta(int roots);
 
+/* Tuning knob of the exact-order sweep: 1 (default) splits each QD root's
+ * numerator and denominator chains over a pair of warps along the 3M
+ * product's independent branches (halves the per-warp issue load; DD/TD
+ * keep one warp per chain, measured faster); 0 runs every chain on one
+ * warp.  Same ops, same order, identical results. */
+int mw_dk_exact_set_split(int on);
+
 /* FP64 pipe microbenchmark: 8 independent DFMA (op = 0) or DADD (op = 1)
  * chains per thread, 8 unrolled steps per iteration: executes
  * blocks * threads * iters * 64 FP64 ops, no memory traffic; the caller

@@ -140,6 +140,12 @@ constexpr int DK_EXACT_ROOTS = 32;  // lanes per role warp (two warps: num + den
 // Roots handled per CTA (<= 32; lanes beyond it idle).  Fewer roots per
 // CTA spread the 2n sequential chains over more SM sub-partitions.
 static int g_dk_exact_roots = 16;
+// 1: split-pair exact kernel (dk_exact2_kernel) for QD, 0: single-warp
+// chains everywhere.  Measured (config 5, us/sweep, single -> split): QD
+// 746 -> 556; TD 355 -> 355 (already near its chain latency: one TD add
+// is 226 cycles dependent, csrc/tune/mw_latency.cu); DD 165 -> 211 (the
+// per-step barriers cost more than the short DD chain) -- so QD only.
+static int g_dk_exact_split = 1;
 constexpr int DK_CH = 128;          // roots staged in smem per chunk
 
 template <int K, int VAR, bool PEER = false>
@@ -229,6 +235,179 @@ __global__ void __launch_bounds__(2 * DK_EXACT_ROOTS)
   }
   if constexpr (PEER) {
     if (!is_den) {
+      __syncwarp();
+      if (lane == 0) dk_peer_ticket(peers);
+    }
+  }
+}
+
+// ------------------------------------------------ exact order, split pairs
+// The single-warp exact kernel above issues every op of a step from one
+// warp: ~460 FP64 warp-instructions per TD step at 2 cycles each bound it
+// (~1300 cycles/step measured) above the chain latency.  Here each chain
+// is split over a PAIR of warps along the 3M product's independent
+// branches, lanes = roots, same ops in the same order (bit-exact):
+//   warp B: p1 = acc.re*b.re, p2 = acc.im*b.im  -> smem, bar.arrive
+//           acc.re = (p1 - p2) [+ coef]          -> smem[step parity]
+//   warp A: s = acc.re + acc.im, p3 = s*(b.re+b.im); bar.sync; read p1, p2
+//           acc.im = (p3 - p1) - p2 [+ 0]         -> smem[step parity]
+//   both:   bar.sync (full pair barrier) -> next step
+// A holds acc.im, B holds acc.re; each reads the other's previous value
+// from the parity slot.  Numerator pair = warps 0/1 (b = z, plus the
+// reference's (coef, 0) add), denominator pair = warps 2/3 (b = f_j =
+// z_i - z_j, j == i pinned to (1, 0); B also forms f_{j+1} and
+// fs_{j+1} = f.re + f.im one step ahead and hands fs to A).  Named
+// barriers 1..4 (0 is __syncthreads).  Tail on warp 0 as before.
+__device__ __forceinline__ void named_sync(int id) {
+  asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory");
+}
+__device__ __forceinline__ void named_arrive(int id) {
+  asm volatile("bar.arrive %0, 64;" ::"r"(id) : "memory");
+}
+
+template <int K>
+__device__ __forceinline__ void sm_put(double (*buf)[32], int lane, const V<K>& v) {
+#pragma unroll
+  for (int c = 0; c < K; ++c) buf[c][lane] = v.c[c];
+}
+template <int K>
+__device__ __forceinline__ V<K> sm_get(const double (*buf)[32], int lane) {
+  V<K> v;
+#pragma unroll
+  for (int c = 0; c < K; ++c) v.c[c] = buf[c][lane];
+  return v;
+}
+
+template <int K, int VAR, bool PEER = false>
+__global__ void __launch_bounds__(128)
+    dk_exact2_kernel(const double* __restrict__ coeffs, int64_t sc, int64_t n,
+                     const double* __restrict__ zre, const double* __restrict__ zim, int64_t sz,
+                     int64_t i0, int64_t i1, double* __restrict__ zre_out,
+                     double* __restrict__ zim_out, int64_t so, double* __restrict__ step_mag,
+                     int* __restrict__ flag, int roots_per_cta, DkPeers peers = DkPeers{}) {
+  using O = Ops<K, VAR>;
+  // [pair][parity][K][lane]: acc.re (from B), acc.im (from A); p1, p2; fs
+  __shared__ double s_re[2][2][K][32], s_im[2][2][K][32];
+  __shared__ double s_p1[2][K][32], s_p2[2][K][32], s_fs[2][K][32];
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int pair = warp >> 1;      // 0 numerator, 1 denominator
+  const bool is_b = warp & 1;      // B: real part, A: imaginary part
+  const int64_t i = i0 + (int64_t)blockIdx.x * roots_per_cta + lane;
+  const bool live = lane < roots_per_cta && i < i1;
+  const int bar_x = 1 + 2 * pair, bar_full = 2 + 2 * pair;
+
+  Cx<K, VAR> z;
+  z.re = live ? load<K>(zre, sz, i) : zero<K>();
+  z.im = live ? load<K>(zim, sz, i) : zero<K>();
+
+  // acc = (1, 0): B owns re = 1, A owns im = 0; seed the "previous" slots
+  V<K> own = is_b ? constant<K>(1.0) : zero<K>();
+  if (is_b) sm_put<K>(s_re[pair][1], lane, own);
+  else sm_put<K>(s_im[pair][1], lane, own);
+
+  if (pair == 0) {
+    // ---------------- numerator: for c = n-1..0: acc = acc*z; acc += (a_c, 0)
+    const V<K> zsum = O::add(z.re, z.im);  // add(b.re, b.im) of the 3M product
+    V<K> coef = load<K>(coeffs, sc, n - 1);  // B: next coefficient, loaded a step ahead
+    named_sync(bar_full);
+#pragma unroll 1
+    for (int64_t st = 0; st < n; ++st) {
+      const int q = (int)(st & 1);
+      const int64_t c = n - 1 - st;
+      if (is_b) {
+        const V<K> ci = coef;
+        if (c > 0) coef = load<K>(coeffs, sc, c - 1);
+        const V<K> im_prev = sm_get<K>(s_im[0][q ^ 1], lane);
+        const V<K> p1 = O::mul(own, z.re);
+        const V<K> p2 = O::mul(im_prev, z.im);
+        sm_put<K>(s_p1[0], lane, p1);
+        sm_put<K>(s_p2[0], lane, p2);
+        named_arrive(bar_x);
+        own = O::add(O::add(p1, neg(p2)), ci);
+        sm_put<K>(s_re[0][q], lane, own);
+      } else {
+        const V<K> re_prev = sm_get<K>(s_re[0][q ^ 1], lane);
+        const V<K> p3 = O::mul(O::add(re_prev, own), zsum);
+        named_sync(bar_x);
+        const V<K> p1 = sm_get<K>(s_p1[0], lane);
+        const V<K> p2 = sm_get<K>(s_p2[0], lane);
+        own = O::add(O::add(O::add(p3, neg(p1)), neg(p2)), zero<K>());
+        sm_put<K>(s_im[0][q], lane, own);
+      }
+      named_sync(bar_full);
+    }
+  } else {
+    // ---------------- denominator: for j = 0..n-1: acc = acc * f_j
+    Cx<K, VAR> f, zn;  // zn: z_{j+1}, loaded a step ahead
+    auto factor = [&](int64_t j, const Cx<K, VAR>& zj) {
+      Cx<K, VAR> g;
+      g.re = O::add(z.re, neg(zj.re));
+      g.im = O::add(z.im, neg(zj.im));
+      if (j == i) g = c_one<K, VAR>();
+      if (live && fabs(g.re.c[0]) + fabs(g.im.c[0]) == 0.0) {
+        const long long key = (long long)j * n + i;
+        atomicMin(flag, key > INT_MAX ? INT_MAX : (int)key);
+      }
+      return g;
+    };
+    if (is_b) {
+      zn.re = load<K>(zre, sz, 0);
+      zn.im = load<K>(zim, sz, 0);
+      f = factor(0, zn);
+      sm_put<K>(s_fs[0], lane, O::add(f.re, f.im));
+      if (n > 1) {
+        zn.re = load<K>(zre, sz, 1);
+        zn.im = load<K>(zim, sz, 1);
+      }
+    }
+    named_sync(bar_full);
+#pragma unroll 1
+    for (int64_t j = 0; j < n; ++j) {
+      const int q = (int)(j & 1);
+      if (is_b) {
+        const Cx<K, VAR> zj1 = zn;
+        if (j + 2 < n) {
+          zn.re = load<K>(zre, sz, j + 2);
+          zn.im = load<K>(zim, sz, j + 2);
+        }
+        const V<K> im_prev = sm_get<K>(s_im[1][q ^ 1], lane);
+        const V<K> p1 = O::mul(own, f.re);
+        const V<K> p2 = O::mul(im_prev, f.im);
+        sm_put<K>(s_p1[1], lane, p1);
+        sm_put<K>(s_p2[1], lane, p2);
+        named_arrive(bar_x);
+        own = O::add(p1, neg(p2));
+        sm_put<K>(s_re[1][q], lane, own);
+        if (j + 1 < n) {
+          f = factor(j + 1, zj1);
+          sm_put<K>(s_fs[q ^ 1], lane, O::add(f.re, f.im));
+        }
+      } else {
+        const V<K> re_prev = sm_get<K>(s_re[1][q ^ 1], lane);
+        const V<K> fs = sm_get<K>(s_fs[q], lane);
+        const V<K> p3 = O::mul(O::add(re_prev, own), fs);
+        named_sync(bar_x);
+        const V<K> p1 = sm_get<K>(s_p1[1], lane);
+        const V<K> p2 = sm_get<K>(s_p2[1], lane);
+        own = O::add(O::add(p3, neg(p1)), neg(p2));
+        sm_put<K>(s_im[1][q], lane, own);
+      }
+      named_sync(bar_full);
+    }
+  }
+  __syncthreads();
+  if (warp == 0) {
+    const int q = (int)((n - 1) & 1);
+    if (live) {
+      Cx<K, VAR> acc, den;
+      acc.re = sm_get<K>(s_re[0][q], lane);
+      acc.im = own;
+      den.re = sm_get<K>(s_re[1][q], lane);
+      den.im = sm_get<K>(s_im[1][q], lane);
+      dk_tail<K, VAR, PEER>(acc, den, z, zre_out, zim_out, so, step_mag, i, &peers);
+    }
+    if constexpr (PEER) {
       __syncwarp();
       if (lane == 0) dk_peer_ticket(peers);
     }
@@ -422,8 +601,12 @@ struct DkLaunch {
     if (exact) {
       const int r = g_dk_exact_roots;
       const int64_t blocks = (cnt + r - 1) / r;
-      dk_exact_kernel<K, VAR><<<(unsigned)blocks, 2 * DK_EXACT_ROOTS, 0, st>>>(
-          coeffs, sc, n, zre, zim, sz, i0, i1, zre_out, zim_out, so, step_mag, flag, r);
+      if (g_dk_exact_split && K == 4)
+        dk_exact2_kernel<K, VAR><<<(unsigned)blocks, 128, 0, st>>>(
+            coeffs, sc, n, zre, zim, sz, i0, i1, zre_out, zim_out, so, step_mag, flag, r);
+      else
+        dk_exact_kernel<K, VAR><<<(unsigned)blocks, 2 * DK_EXACT_ROOTS, 0, st>>>(
+            coeffs, sc, n, zre, zim, sz, i0, i1, zre_out, zim_out, so, step_mag, flag, r);
     } else {
       dk_tree_kernel<K, VAR><<<(unsigned)cnt, 96, 0, st>>>(
           coeffs, sc, n, zre, zim, sz, i0, i1, zre_out, zim_out, so, step_mag, flag);
@@ -445,8 +628,12 @@ struct DkPeerLaunch {
     if (exact) {
       const int r = g_dk_exact_roots;
       const int64_t blocks = (cnt + r - 1) / r;
-      dk_exact_kernel<K, VAR, true><<<(unsigned)blocks, 2 * DK_EXACT_ROOTS, 0, st>>>(
-          coeffs, sc, n, zre, zim, n, i0, i1, ore, oim, n, step_mag, flag, r, peers);
+      if (g_dk_exact_split && K == 4)
+        dk_exact2_kernel<K, VAR, true><<<(unsigned)blocks, 128, 0, st>>>(
+            coeffs, sc, n, zre, zim, n, i0, i1, ore, oim, n, step_mag, flag, r, peers);
+      else
+        dk_exact_kernel<K, VAR, true><<<(unsigned)blocks, 2 * DK_EXACT_ROOTS, 0, st>>>(
+            coeffs, sc, n, zre, zim, n, i0, i1, ore, oim, n, step_mag, flag, r, peers);
     } else {
       dk_tree_kernel<K, VAR, true><<<(unsigned)cnt, 96, 0, st>>>(
           coeffs, sc, n, zre, zim, n, i0, i1, ore, oim, n, step_mag, flag, peers);
@@ -463,6 +650,14 @@ using namespace mw;
 extern "C" int mw_dk_exact_set_roots_per_cta(int r) {
   if (r < 1 || r > 32) return MW_ERR_INVALID;
   g_dk_exact_roots = r;
+  return MW_OK;
+}
+
+// Tuning knob: exact-order kernel form (1 = split warp pairs for QD,
+// default; 0 = one warp per chain).  Results are identical.
+extern "C" int mw_dk_exact_set_split(int on) {
+  if (on != 0 && on != 1) return MW_ERR_INVALID;
+  g_dk_exact_split = on;
   return MW_OK;
 }
 

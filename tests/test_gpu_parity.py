@@ -921,3 +921,28 @@ def test_dot_peer_wait_times_out_instead_of_hanging():
         assert int(tout.item()) == 1 and int(done.item()) == 0 and int(epoch.item()) == 1
     finally:
         lib.mw_peer_free(buf)
+
+
+@pytest.mark.parametrize("k", [3, 4])
+@pytest.mark.parametrize("v", ["bf", "std"])
+def test_dk_exact_split_and_single_warp_forms_agree(k, v):
+    """The split-pair exact kernel (QD default) and the single-warp one give
+    the same bits, and both equal the oracle's reference-order sweep."""
+    from paper_2603_14926_b200 import _lib
+
+    lib = _lib.load()
+    rng = np.random.default_rng(70 + k)
+    n = 80
+    coeffs = gen.g_k(rng, k, n) * 0.5
+    ang = 2 * np.pi * np.arange(n) / n + 0.1
+    zre = np.zeros((k, n)); zim = np.zeros((k, n))
+    zre[0] = 1.3 * np.cos(ang); zim[0] = 1.3 * np.sin(ang)
+    want_re, want_im, _, _ = oracle.dk_sweep(coeffs, zre, zim, v, exact=True)
+    try:
+        for split in (0, 1):
+            lib.mw_dk_exact_set_split(split)
+            out = dk_sweeps(MonicPoly(coeffs), RootState(re=zre, im=zim), 1, V(v), exact_order=True)
+            assert_bitwise(out.re.cpu().numpy(), want_re)
+            assert_bitwise(out.im.cpu().numpy(), want_im)
+    finally:
+        lib.mw_dk_exact_set_split(1)
