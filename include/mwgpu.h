@@ -194,7 +194,8 @@ int mw_dk_sweep(int k, int variant, const double* coeffs, int64_t sc,
  * my_slot reaches it; on expiry it sets *timeout = 1 and returns (no
  * hang).  done (u32, zero-initialised) is a self-resetting CTA ticket;
  * epoch (u64) counts completed runs and is advanced by the sweep
- * == sweeps - 1 launch.  Arithmetic and order are those of mw_dk_sweep
+ * == sweeps - 1 launch.  ws: optional workspace as for mw_dk_sweep_ws
+ * (NULL allowed).  Arithmetic and order are those of mw_dk_sweep
  * (exact_order as there), so results are bitwise independent of world. */
 int mw_dk_sweep_peer(int k, int variant, const double* coeffs, int64_t sc,
                      int64_t n, const double* state_in, int64_t i0, int64_t i1,
@@ -204,7 +205,7 @@ int mw_dk_sweep_peer(int k, int variant, const double* coeffs, int64_t sc,
                      unsigned int* done, unsigned long long* epoch, int* timeout,
                      int world, int rank, int sweep, int sweeps,
                      long long spin_limit, double* step_mag, int* flag_dev,
-                     int exact_order, void* stream);
+                     int exact_order, double* ws, void* stream);
 
 /* Sharded tree dot with the all-gather-then-sum fused into one kernel per
  * rank ("dot products by a custom multi-component
@@ -236,6 +237,20 @@ int mw_peer_free(void* p);
 int mw_ipc_get_handle(void* p, void* handle64);
 int mw_ipc_open_handle(const void* handle64, void** out);
 int mw_ipc_close_handle(void* p);
+
+/* mw_dk_sweep with a caller workspace of mw_dk_sweep_workspace(k, i0, i1)
+ * doubles (device memory, stream-ordered, not shared between concurrent
+ * calls).  Tree order: w = z^B and w^32 of every root are then computed
+ * by a lane-per-root kernel and the sweep kernel is a programmatic
+ * dependent launch whose powers warp waits for them (griddepcontrol), so
+ * no warp computes a value its 32 lanes duplicate.  Identical results;
+ * ignored for the exact order. */
+int64_t mw_dk_sweep_workspace(int k, int64_t i0, int64_t i1);
+int mw_dk_sweep_ws(int k, int variant, const double* coeffs, int64_t sc,
+                   int64_t n, const double* zre, const double* zim, int64_t sz,
+                   int64_t i0, int64_t i1, double* zre_out, double* zim_out,
+                   int64_t so, double* step_mag, int* flag_dev, int exact_order,
+                   double* ws, void* stream);
 
 /* Tuning knob of the exact-order sweep: roots per CTA (1..32, default 16).
  * Results do not depend on it (each root is one chain in reference order). */

@@ -449,13 +449,58 @@ __device__ __forceinline__ Cx<K, VAR> shfl_cx(const Cx<K, VAR>& v, int s, bool u
 //   warp 1  numerator:   lane l owns blocks l and l+32 (two Horner chains)
 //   warp 2  powers:      w = z^B, w^32, the scan x_l = w^l and x_l * w^32,
 //                        handed to warp 1 through shared memory.
-template <int K, int VAR, bool PEER = false>
+// w = z^B by right-to-left square-and-multiply from (1, 0); w32 = five
+// squarings of w (the tree order's definition, see above).
+template <int K, int VAR>
+__device__ __forceinline__ void dk_powers(const Cx<K, VAR>& z, int64_t B, Cx<K, VAR>& w,
+                                          Cx<K, VAR>& w32) {
+  w = c_one<K, VAR>();
+  Cx<K, VAR> sq = z;
+  for (int64_t e = B; e > 0; e >>= 1) {
+    if (e & 1) w = c_mul_ol(w, sq);
+    if (e > 1) sq = c_mul_ol(sq, sq);
+  }
+  w32 = w;
+#pragma unroll 1
+  for (int r = 0; r < 5; ++r) w32 = c_mul_ol(w32, w32);
+}
+
+// One thread per root: w = z^B and w^32 for the tree sweep that follows
+// (programmatic dependent launch: the sweep starts as soon as every CTA
+// here has issued launch_dependents, and only its powers warp waits).
+template <int K, int VAR>
+__global__ void __launch_bounds__(128)
+    dk_pow_kernel(const double* __restrict__ zre, const double* __restrict__ zim, int64_t sz,
+                  int64_t n, int64_t i0, int64_t i1, double* __restrict__ wbuf, int64_t ws) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const int64_t i = i0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= i1) return;
+  const int64_t B = (n + 1 + DK_P - 1) / DK_P;
+  Cx<K, VAR> z, w, w32;
+  z.re = load<K>(zre, sz, i);
+  z.im = load<K>(zim, sz, i);
+  dk_powers<K, VAR>(z, B, w, w32);
+  const int64_t r = i - i0;
+  store<K>(wbuf, ws, r, w.re);
+  store<K>(wbuf + (int64_t)K * ws, ws, r, w.im);
+  store<K>(wbuf + (int64_t)2 * K * ws, ws, r, w32.re);
+  store<K>(wbuf + (int64_t)3 * K * ws, ws, r, w32.im);
+}
+
+// EXTPOW: w = z^B and w^32 come from dk_pow_kernel (lane = root, so no
+// warp spends 10 complex products per root on a value all 32 lanes
+// duplicate); the powers warp waits for it with griddepcontrol.wait while
+// the denominator and Horner warps already run (programmatic dependent
+// launch).  wbuf: 4K planes (w.re, w.im, w32.re, w32.im), plane stride
+// ws, indexed by i - i0.
+template <int K, int VAR, bool PEER = false, bool EXTPOW = false>
 __global__ void __launch_bounds__(96)
     dk_tree_kernel(const double* __restrict__ coeffs, int64_t sc, int64_t n,
                    const double* __restrict__ zre, const double* __restrict__ zim, int64_t sz,
                    int64_t i0, int64_t i1, double* __restrict__ zre_out,
                    double* __restrict__ zim_out, int64_t so, double* __restrict__ step_mag,
-                   int* __restrict__ flag, DkPeers peers = DkPeers{}) {
+                   int* __restrict__ flag, DkPeers peers, const double* __restrict__ wbuf,
+                   int64_t ws) {
   using O = Ops<K, VAR>;
   __shared__ double den_s[2][K];
   __shared__ double pw[2][2][K][32];  // [lo/hi][re/im][c][lane]
@@ -530,14 +575,17 @@ __global__ void __launch_bounds__(96)
     }
   } else {
     // ---- powers: w = z^B, w^32, x_l = w^l (scan), x_l * w^32
-    Cx<K, VAR> w = c_one<K, VAR>(), sq = z;
-    for (int64_t e = B; e > 0; e >>= 1) {
-      if (e & 1) w = c_mul_ol(w, sq);
-      if (e > 1) sq = c_mul_ol(sq, sq);
+    Cx<K, VAR> w, w32;
+    if constexpr (EXTPOW) {
+      asm volatile("griddepcontrol.wait;" ::: "memory");
+      const int64_t r = i - i0;
+      w.re = load<K>(wbuf, ws, r);
+      w.im = load<K>(wbuf + (int64_t)K * ws, ws, r);
+      w32.re = load<K>(wbuf + (int64_t)2 * K * ws, ws, r);
+      w32.im = load<K>(wbuf + (int64_t)3 * K * ws, ws, r);
+    } else {
+      dk_powers<K, VAR>(z, B, w, w32);
     }
-    Cx<K, VAR> w32 = w;
-#pragma unroll 1
-    for (int r = 0; r < 5; ++r) w32 = c_mul_ol(w32, w32);
     Cx<K, VAR> x = lane == 0 ? c_one<K, VAR>() : w;
 #pragma unroll 1
     for (int s = 1; s < 32; s <<= 1) {
@@ -591,11 +639,47 @@ __global__ void __launch_bounds__(96)
   }
 }
 
+// Tree sweep launch: with a workspace (4K doubles per root) the powers come
+// from dk_pow_kernel and the sweep is a programmatic dependent launch;
+// without one the powers warp computes them itself.  Same bits.
+template <int K, int VAR, bool PEER>
+static int dk_tree_launch(const double* coeffs, int64_t sc, int64_t n, const double* zre,
+                          const double* zim, int64_t sz, int64_t i0, int64_t i1, double* zre_out,
+                          double* zim_out, int64_t so, double* step_mag, int* flag, DkPeers peers,
+                          double* ws, cudaStream_t st) {
+  const int64_t cnt = i1 - i0;
+  if (!ws) {
+    dk_tree_kernel<K, VAR, PEER, false><<<(unsigned)cnt, 96, 0, st>>>(
+        coeffs, sc, n, zre, zim, sz, i0, i1, zre_out, zim_out, so, step_mag, flag, peers,
+        (const double*)nullptr, (int64_t)0);
+    return launch_status();
+  }
+  dk_pow_kernel<K, VAR><<<(unsigned)((cnt + 127) / 128), 128, 0, st>>>(zre, zim, sz, n, i0, i1, ws,
+                                                                       cnt);
+  int rc = launch_status();
+  if (rc) return rc;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)cnt);
+  cfg.blockDim = dim3(96);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, dk_tree_kernel<K, VAR, PEER, true>, coeffs, sc, n, zre,
+                                     zim, sz, i0, i1, zre_out, zim_out, so, step_mag, flag, peers,
+                                     (const double*)ws, cnt);
+  if (e != cudaSuccess) return (int)e;
+  return launch_status();
+}
+
 template <int K, int VAR>
 struct DkLaunch {
   static int run(const double* coeffs, int64_t sc, int64_t n, const double* zre,
                  const double* zim, int64_t sz, int64_t i0, int64_t i1, double* zre_out,
-                 double* zim_out, int64_t so, double* step_mag, int* flag, int exact,
+                 double* zim_out, int64_t so, double* step_mag, int* flag, int exact, double* ws,
                  cudaStream_t st) {
     const int64_t cnt = i1 - i0;
     if (exact) {
@@ -608,8 +692,8 @@ struct DkLaunch {
         dk_exact_kernel<K, VAR><<<(unsigned)blocks, 2 * DK_EXACT_ROOTS, 0, st>>>(
             coeffs, sc, n, zre, zim, sz, i0, i1, zre_out, zim_out, so, step_mag, flag, r);
     } else {
-      dk_tree_kernel<K, VAR><<<(unsigned)cnt, 96, 0, st>>>(
-          coeffs, sc, n, zre, zim, sz, i0, i1, zre_out, zim_out, so, step_mag, flag);
+      return dk_tree_launch<K, VAR, false>(coeffs, sc, n, zre, zim, sz, i0, i1, zre_out, zim_out,
+                                           so, step_mag, flag, DkPeers{}, ws, st);
     }
     return launch_status();
   }
@@ -619,7 +703,7 @@ template <int K, int VAR>
 struct DkPeerLaunch {
   static int run(const double* coeffs, int64_t sc, int64_t n, const double* state_in,
                  int64_t i0, int64_t i1, double* state_out, double* step_mag, int* flag,
-                 int exact, DkPeers peers, cudaStream_t st) {
+                 int exact, DkPeers peers, double* ws, cudaStream_t st) {
     const int64_t cnt = i1 - i0;
     const double* zre = state_in;
     const double* zim = state_in + (int64_t)K * n;
@@ -635,8 +719,8 @@ struct DkPeerLaunch {
         dk_exact_kernel<K, VAR, true><<<(unsigned)blocks, 2 * DK_EXACT_ROOTS, 0, st>>>(
             coeffs, sc, n, zre, zim, n, i0, i1, ore, oim, n, step_mag, flag, r, peers);
     } else {
-      dk_tree_kernel<K, VAR, true><<<(unsigned)cnt, 96, 0, st>>>(
-          coeffs, sc, n, zre, zim, n, i0, i1, ore, oim, n, step_mag, flag, peers);
+      return dk_tree_launch<K, VAR, true>(coeffs, sc, n, zre, zim, n, i0, i1, ore, oim, n,
+                                          step_mag, flag, peers, ws, st);
     }
     return launch_status();
   }
@@ -673,7 +757,33 @@ extern "C" int mw_dk_sweep(int k, int variant, const double* coeffs, int64_t sc,
     return MW_ERR_INVALID;
   if (sc < n || sz < n || so < n) return MW_ERR_INVALID;
   return dispatch<DkLaunch>(k, variant, coeffs, sc, n, zre, zim, sz, i0, i1, zre_out, zim_out,
-                            so, step_mag, flag_dev, exact_order ? 1 : 0, as_stream(stream));
+                            so, step_mag, flag_dev, exact_order ? 1 : 0, (double*)nullptr,
+                            as_stream(stream));
+}
+
+extern "C" int64_t mw_dk_sweep_workspace(int k, int64_t i0, int64_t i1) {
+  if (k < 2 || k > 4 || i1 < i0 || i0 < 0) return 0;
+  return 4 * (int64_t)k * (i1 - i0);
+}
+
+// mw_dk_sweep with a caller workspace of mw_dk_sweep_workspace(k, i0, i1)
+// doubles: the tree order then takes z^B and w^32 from a lane-per-root
+// kernel (programmatic dependent launch).  Same results.
+extern "C" int mw_dk_sweep_ws(int k, int variant, const double* coeffs, int64_t sc, int64_t n,
+                              const double* zre, const double* zim, int64_t sz, int64_t i0,
+                              int64_t i1, double* zre_out, double* zim_out, int64_t so,
+                              double* step_mag, int* flag_dev, int exact_order, double* ws,
+                              void* stream) {
+  if (k < 2 || k > 4) return MW_ERR_INVALID;
+  if (variant != 0 && variant != 1) return MW_ERR_INVALID;
+  if (n < 1 || i0 < 0 || i1 < i0 || i1 > n) return MW_ERR_INVALID;
+  if (i1 == i0) return MW_OK;
+  if (!coeffs || !zre || !zim || !zre_out || !zim_out || !step_mag || !flag_dev)
+    return MW_ERR_INVALID;
+  if (sc < n || sz < n || so < n) return MW_ERR_INVALID;
+  return dispatch<DkLaunch>(k, variant, coeffs, sc, n, zre, zim, sz, i0, i1, zre_out, zim_out,
+                            so, step_mag, flag_dev, exact_order ? 1 : 0, ws,
+                            as_stream(stream));
 }
 
 // Root-sharded sweep with the state exchange fused in (peer stores over
@@ -687,7 +797,8 @@ extern "C" int mw_dk_sweep_peer(int k, int variant, const double* coeffs, int64_
                                 double* state_out_local, unsigned long long* my_slot,
                                 unsigned int* done, unsigned long long* epoch, int* timeout,
                                 int world, int rank, int sweep, int sweeps, long long spin_limit,
-                                double* step_mag, int* flag_dev, int exact_order, void* stream) {
+                                double* step_mag, int* flag_dev, int exact_order, double* ws,
+                                void* stream) {
   if (k < 2 || k > 4) return MW_ERR_INVALID;
   if (variant != 0 && variant != 1) return MW_ERR_INVALID;
   if (n < 1 || i0 < 0 || i1 <= i0 || i1 > n) return MW_ERR_INVALID;
@@ -700,7 +811,8 @@ extern "C" int mw_dk_sweep_peer(int k, int variant, const double* coeffs, int64_
   if (sc < n) return MW_ERR_INVALID;
   DkPeers P{peer_out, peer_slot, my_slot, done, epoch, timeout, spin_limit, world, rank, sweep, sweeps};
   return dispatch<DkPeerLaunch>(k, variant, coeffs, sc, n, state_in, i0, i1, state_out_local,
-                                step_mag, flag_dev, exact_order ? 1 : 0, P, as_stream(stream));
+                                step_mag, flag_dev, exact_order ? 1 : 0, P, ws,
+                                as_stream(stream));
 }
 
 // Peer buffers: plain cudaMalloc allocations (zeroed) so one IPC handle

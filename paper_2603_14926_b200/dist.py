@@ -397,6 +397,7 @@ class DKPeerGraph:
         self.mag = torch.empty(n, dtype=torch.float64, device=dev)
         self.flags = torch.empty(sweeps, dtype=torch.int32, device=dev)
         self._coeffs = coeffs.contiguous()
+        self._ws = torch.empty(max(lib.mw_dk_sweep_workspace(k, lo, hi), 1), dtype=torch.float64, device=dev)
         v = variant_code(variant)
         exact = 1 if exact_order else 0
 
@@ -415,7 +416,7 @@ class DKPeerGraph:
                     self._outs[par].data_ptr(), self._slots.data_ptr(), self._state[1 - par].data_ptr(), my_slot,
                     self._done.data_ptr(), self._epoch.data_ptr(), self._timeout.data_ptr(), self.world,
                     self.rank, s, sweeps, spin_limit, self.mag.data_ptr(), self.flags[s:s + 1].data_ptr(), exact,
-                    stream)
+                    self._ws.data_ptr(), stream)
                 _lib.check(rc, "mw_dk_sweep_peer")
 
         side = torch.cuda.Stream(device=dev)

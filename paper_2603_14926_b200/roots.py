@@ -251,10 +251,15 @@ def sweep_into(coeffs: torch.Tensor, zre: torch.Tensor, zim: torch.Tensor, out_r
     INT32_MAX beforehand; it is lowered to min(j*n + i) on a collision."""
     k, n = zre.shape
     i1 = n if i1 is None else i1
-    rc = _lib.load().mw_dk_sweep(
+    lib = _lib.load()
+    ws = None
+    if not exact_order and i1 > i0:
+        # stream-ordered scratch for the lane-per-root powers kernel
+        ws = torch.empty(lib.mw_dk_sweep_workspace(k, i0, i1), dtype=torch.float64, device=zre.device)
+    rc = lib.mw_dk_sweep_ws(
         k, variant_code(variant), coeffs.data_ptr(), coeffs.shape[1], n, zre.data_ptr(), zim.data_ptr(), n,
         i0, i1, out_re.data_ptr(), out_im.data_ptr(), n, step_mag.data_ptr(), flag.data_ptr(),
-        1 if exact_order else 0, _lib.stream_handle(zre.device),
+        1 if exact_order else 0, None if ws is None else ws.data_ptr(), _lib.stream_handle(zre.device),
     )
     _lib.check(rc, "mw_dk_sweep")
 

@@ -85,7 +85,7 @@ def test_peer_sweep_checks():
     f = lib.mw_dk_sweep_peer
     ok = dict(k=3, variant=1, coeffs=p, sc=8, n=8, state_in=p, i0=0, i1=8, peer_out=p, peer_slot=p, out=p,
               my_slot=p, done=p, epoch=p, timeout=p, world=2, rank=1, sweep=0, sweeps=4, spin=1000,
-              mag=p, flag=p, exact=1, stream=None)
+              mag=p, flag=p, exact=1, ws=None, stream=None)
 
     def call(**kw):
         a = dict(ok, **kw)

@@ -791,7 +791,7 @@ def test_dk_peer_wait_times_out_instead_of_hanging():
         rc = lib.mw_dk_sweep_peer(k, 1, coeffs.data_ptr(), n, n, base, 0, n // 2, o.data_ptr(), sl.data_ptr(),
                                   base + lay.state_off(1), base + lay.slot_off, done.data_ptr(), epoch.data_ptr(),
                                   tout.data_ptr(), 2, 0, 0, 2, 2000, mag.data_ptr(), flag.data_ptr(), 0,
-                                  _lib.stream_handle(dev))
+                                  None, _lib.stream_handle(dev))
         _lib.check(rc, "mw_dk_sweep_peer")
         torch.cuda.synchronize()
         assert int(tout.item()) == 1
@@ -946,3 +946,43 @@ def test_dk_exact_split_and_single_warp_forms_agree(k, v):
             assert_bitwise(out.im.cpu().numpy(), want_im)
     finally:
         lib.mw_dk_exact_set_split(1)
+
+
+@pytest.mark.parametrize("k", [2, 3, 4])
+@pytest.mark.parametrize("v", ["bf", "std"])
+def test_dk_tree_powers_kernel_path_matches_in_warp_path(k, v):
+    """Tree sweep with the lane-per-root powers kernel + programmatic
+    dependent launch (mw_dk_sweep_ws) equals the in-warp powers path
+    (mw_dk_sweep) and the oracle bit for bit, on a sub-range of roots."""
+    from paper_2603_14926_b200 import _lib
+    from paper_2603_14926_b200.multiword import variant_code
+
+    lib = _lib.load()
+    rng = np.random.default_rng(90 + k)
+    n = 150
+    coeffs = gen.g_k(rng, k, n) * 0.5
+    ang = 2 * np.pi * np.arange(n) / n + 0.1
+    zre = np.zeros((k, n)); zim = np.zeros((k, n))
+    zre[0] = 1.3 * np.cos(ang); zim[0] = 1.3 * np.sin(ang)
+    C, R, I = (torch.from_numpy(a).cuda() for a in (coeffs, zre, zim))
+    i0, i1 = 7, 141
+    outs = []
+    for use_ws in (False, True):
+        ore, oim = torch.zeros_like(R), torch.zeros_like(I)
+        mag = torch.zeros(n, dtype=torch.float64, device="cuda")
+        flag = torch.full((1,), 2**31 - 1, dtype=torch.int32, device="cuda")
+        args = [k, variant_code(V(v)), C.data_ptr(), n, n, R.data_ptr(), I.data_ptr(), n, i0, i1, ore.data_ptr(),
+                oim.data_ptr(), n, mag.data_ptr(), flag.data_ptr(), 0]
+        if use_ws:
+            ws = torch.empty(lib.mw_dk_sweep_workspace(k, i0, i1), dtype=torch.float64, device="cuda")
+            rc = lib.mw_dk_sweep_ws(*args, ws.data_ptr(), _lib.stream_handle(R.device))
+        else:
+            rc = lib.mw_dk_sweep(*args, _lib.stream_handle(R.device))
+        _lib.check(rc, "sweep")
+        outs.append((ore.cpu().numpy(), oim.cpu().numpy(), mag.cpu().numpy()))
+    assert_bitwise(outs[0][0], outs[1][0])
+    assert_bitwise(outs[0][1], outs[1][1])
+    assert_bitwise(outs[0][2], outs[1][2])
+    want_re, want_im, _, _ = oracle.dk_sweep(coeffs, zre, zim, v, exact=False, rows=(i0, i1))
+    assert_bitwise(outs[1][0][:, i0:i1], want_re[:, i0:i1])
+    assert_bitwise(outs[1][1][:, i0:i1], want_im[:, i0:i1])
