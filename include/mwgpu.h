@@ -256,11 +256,11 @@ int mw_dk_sweep_ws(int k, int variant, const double* coeffs, int64_t sc,
  * Results do not depend on it (each root is one chain in reference order). */
 int mw_dk_exact_set_roots_per_cta(int roots);
 
-/* Tuning knob of the exact-order sweep: 1 (default) splits each QD root's
- * numerator and denominator chains over a pair of warps along the 3M
- * product's independent branches (halves the per-warp issue load; DD/TD
- * keep one warp per chain, measured faster); 0 runs every chain on one
- * warp.  Same ops, same order, identical results. */
+/* Tuning knob of the exact-order sweep: 1 (default) splits each TD/QD
+ * root's numerator and denominator chains over a pair of warps (real and
+ * imaginary halves of the 3M product, one hand-off per step); DD keeps one
+ * warp per chain (measured faster); 0 runs every chain on one warp.  Same
+ * ops, same order, identical results. */
 int mw_dk_exact_set_split(int on);
 
 /* FP64 pipe microbenchmark: 8 independent DFMA (op = 0) or DADD (op = 1)

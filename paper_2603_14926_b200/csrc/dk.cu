@@ -140,12 +140,12 @@ constexpr int DK_EXACT_ROOTS = 32;  // lanes per role warp (two warps: num + den
 // Roots handled per CTA (<= 32; lanes beyond it idle).  Fewer roots per
 // CTA spread the 2n sequential chains over more SM sub-partitions.
 static int g_dk_exact_roots = 16;
-// 1: split-pair exact kernel (dk_exact2_kernel) for QD, 0: single-warp
-// chains everywhere.  Measured (config 5, us/sweep, single -> split): QD
-// 746 -> 556; TD 355 -> 355 (already near its chain latency: one TD add
-// is 226 cycles dependent, csrc/tune/mw_latency.cu); DD 165 -> 211 (the
-// per-step barriers cost more than the short DD chain) -- so QD only.
+// 1: split-pair exact kernel (dk_exact2_kernel) for TD and QD, 0:
+// single-warp chains everywhere.  Measured (config 5, us/sweep, eager,
+// single -> split): TD 353 -> 295 (one hand-off per step), QD 745 -> 575
+// (XP: p1, p2 handed over too); DD 165 -> 173, so DD stays single-warp.
 static int g_dk_exact_split = 1;
+constexpr int DK_SPLIT_MIN_K = 3;
 constexpr int DK_CH = 128;          // roots staged in smem per chunk
 
 template <int K, int VAR, bool PEER = false>
@@ -243,21 +243,23 @@ __global__ void __launch_bounds__(2 * DK_EXACT_ROOTS)
 
 // ------------------------------------------------ exact order, split pairs
 // The single-warp exact kernel above issues every op of a step from one
-// warp: ~460 FP64 warp-instructions per TD step at 2 cycles each bound it
-// (~1300 cycles/step measured) above the chain latency.  Here each chain
-// is split over a PAIR of warps along the 3M product's independent
-// branches, lanes = roots, same ops in the same order (bit-exact):
-//   warp B: p1 = acc.re*b.re, p2 = acc.im*b.im  -> smem, bar.arrive
-//           acc.re = (p1 - p2) [+ coef]          -> smem[step parity]
-//   warp A: s = acc.re + acc.im, p3 = s*(b.re+b.im); bar.sync; read p1, p2
-//           acc.im = (p3 - p1) - p2 [+ 0]         -> smem[step parity]
-//   both:   bar.sync (full pair barrier) -> next step
-// A holds acc.im, B holds acc.re; each reads the other's previous value
-// from the parity slot.  Numerator pair = warps 0/1 (b = z, plus the
-// reference's (coef, 0) add), denominator pair = warps 2/3 (b = f_j =
-// z_i - z_j, j == i pinned to (1, 0); B also forms f_{j+1} and
-// fs_{j+1} = f.re + f.im one step ahead and hands fs to A).  Named
-// barriers 1..4 (0 is __syncthreads).  Tail on warp 0 as before.
+// warp; one warp sustains only ~1 FP64 instruction per 2.6-3.5 cycles on
+// this code (csrc/tune/mw_latency.cu), so a QD step (~1000 instructions)
+// is issue-bound well above its dependent-chain latency.  Here each chain
+// runs on a PAIR of warps, lanes = roots, same ops in the same order
+// (bit-exact), with ONE hand-off per step:
+//   warp A (imaginary part): s = re + im, p3 = s * bsum, p1 = re * b.re,
+//           p2 = im * b.im, im' = (p3 - p1) - p2 [+ 0]
+//   warp B (real part):      p1, p2 (the same products, recomputed),
+//           re' = (p1 - p2) [+ coef]
+//   both write their new half to a step-parity slot, one 64-thread named
+//   barrier, each reads the other's half.
+// XP (QD): B hands p1, p2 to A through a second barrier instead (A's QD
+// issue load would otherwise exceed the chain latency).
+// Numerator pair = warps 0/1 (b = z, plus the reference's (coef, 0) add),
+// denominator pair = warps 2/3 (b = f_j = z_i - z_j, j == i pinned to
+// (1, 0); B forms f_{j+1} and bsum = f.re + f.im one step ahead and hands
+// them to A through the slot).  Tail on warp 0 as before.
 __device__ __forceinline__ void named_sync(int id) {
   asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory");
 }
@@ -278,7 +280,7 @@ __device__ __forceinline__ V<K> sm_get(const double (*buf)[32], int lane) {
   return v;
 }
 
-template <int K, int VAR, bool PEER = false>
+template <int K, int VAR, bool PEER = false, bool XP = (K == 4)>
 __global__ void __launch_bounds__(128)
     dk_exact2_kernel(const double* __restrict__ coeffs, int64_t sc, int64_t n,
                      const double* __restrict__ zre, const double* __restrict__ zim, int64_t sz,
@@ -286,31 +288,31 @@ __global__ void __launch_bounds__(128)
                      double* __restrict__ zim_out, int64_t so, double* __restrict__ step_mag,
                      int* __restrict__ flag, int roots_per_cta, DkPeers peers = DkPeers{}) {
   using O = Ops<K, VAR>;
-  // [pair][parity][K][lane]: acc.re (from B), acc.im (from A); p1, p2; fs
+  // [pair][parity][K][lane]
   __shared__ double s_re[2][2][K][32], s_im[2][2][K][32];
-  __shared__ double s_p1[2][K][32], s_p2[2][K][32], s_fs[2][K][32];
+  // denominator factor for the next step: f.re, f.im, f.re + f.im
+  __shared__ double s_fr[2][K][32], s_fi[2][K][32], s_fs[2][K][32];
+  // XP: B hands its p1, p2 to A (A skips two products, one more barrier)
+  __shared__ double s_p1[2][K][32], s_p2[2][K][32];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
-  const int pair = warp >> 1;      // 0 numerator, 1 denominator
-  const bool is_b = warp & 1;      // B: real part, A: imaginary part
+  const int pair = warp >> 1;  // 0 numerator, 1 denominator
+  const bool is_b = warp & 1;  // B: real part, A: imaginary part
   const int64_t i = i0 + (int64_t)blockIdx.x * roots_per_cta + lane;
   const bool live = lane < roots_per_cta && i < i1;
-  const int bar_x = 1 + 2 * pair, bar_full = 2 + 2 * pair;
+  const int bar = 1 + pair, bar_x = 3 + pair;
 
   Cx<K, VAR> z;
   z.re = live ? load<K>(zre, sz, i) : zero<K>();
   z.im = live ? load<K>(zim, sz, i) : zero<K>();
 
-  // acc = (1, 0): B owns re = 1, A owns im = 0; seed the "previous" slots
-  V<K> own = is_b ? constant<K>(1.0) : zero<K>();
-  if (is_b) sm_put<K>(s_re[pair][1], lane, own);
-  else sm_put<K>(s_im[pair][1], lane, own);
+  // acc = (1, 0): B owns re, A owns im; the other half is read per step
+  V<K> re = constant<K>(1.0), im = zero<K>();
 
   if (pair == 0) {
     // ---------------- numerator: for c = n-1..0: acc = acc*z; acc += (a_c, 0)
-    const V<K> zsum = O::add(z.re, z.im);  // add(b.re, b.im) of the 3M product
-    V<K> coef = load<K>(coeffs, sc, n - 1);  // B: next coefficient, loaded a step ahead
-    named_sync(bar_full);
+    const V<K> zsum = O::add(z.re, z.im);
+    V<K> coef = load<K>(coeffs, sc, n - 1);
 #pragma unroll 1
     for (int64_t st = 0; st < n; ++st) {
       const int q = (int)(st & 1);
@@ -318,28 +320,35 @@ __global__ void __launch_bounds__(128)
       if (is_b) {
         const V<K> ci = coef;
         if (c > 0) coef = load<K>(coeffs, sc, c - 1);
-        const V<K> im_prev = sm_get<K>(s_im[0][q ^ 1], lane);
-        const V<K> p1 = O::mul(own, z.re);
-        const V<K> p2 = O::mul(im_prev, z.im);
-        sm_put<K>(s_p1[0], lane, p1);
-        sm_put<K>(s_p2[0], lane, p2);
-        named_arrive(bar_x);
-        own = O::add(O::add(p1, neg(p2)), ci);
-        sm_put<K>(s_re[0][q], lane, own);
+        const V<K> p1 = O::mul(re, z.re);
+        const V<K> p2 = O::mul(im, z.im);
+        if constexpr (XP) {
+          sm_put<K>(s_p1[0], lane, p1);
+          sm_put<K>(s_p2[0], lane, p2);
+          named_arrive(bar_x);
+        }
+        re = O::add(O::add(p1, neg(p2)), ci);
+        sm_put<K>(s_re[0][q], lane, re);
       } else {
-        const V<K> re_prev = sm_get<K>(s_re[0][q ^ 1], lane);
-        const V<K> p3 = O::mul(O::add(re_prev, own), zsum);
-        named_sync(bar_x);
-        const V<K> p1 = sm_get<K>(s_p1[0], lane);
-        const V<K> p2 = sm_get<K>(s_p2[0], lane);
-        own = O::add(O::add(O::add(p3, neg(p1)), neg(p2)), zero<K>());
-        sm_put<K>(s_im[0][q], lane, own);
+        const V<K> p3 = O::mul(O::add(re, im), zsum);
+        V<K> p1, p2;
+        if constexpr (XP) {
+          named_sync(bar_x);
+          p1 = sm_get<K>(s_p1[0], lane);
+          p2 = sm_get<K>(s_p2[0], lane);
+        } else {
+          p1 = O::mul(re, z.re);
+          p2 = O::mul(im, z.im);
+        }
+        im = O::add(O::add(O::add(p3, neg(p1)), neg(p2)), zero<K>());
+        sm_put<K>(s_im[0][q], lane, im);
       }
-      named_sync(bar_full);
+      named_sync(bar);
+      if (is_b) im = sm_get<K>(s_im[0][q], lane);
+      else re = sm_get<K>(s_re[0][q], lane);
     }
   } else {
     // ---------------- denominator: for j = 0..n-1: acc = acc * f_j
-    Cx<K, VAR> f, zn;  // zn: z_{j+1}, loaded a step ahead
     auto factor = [&](int64_t j, const Cx<K, VAR>& zj) {
       Cx<K, VAR> g;
       g.re = O::add(z.re, neg(zj.re));
@@ -351,17 +360,22 @@ __global__ void __launch_bounds__(128)
       }
       return g;
     };
+    Cx<K, VAR> f, zn;  // B: current factor and z_{j+1} (loaded a step ahead)
+    V<K> fs;
     if (is_b) {
       zn.re = load<K>(zre, sz, 0);
       zn.im = load<K>(zim, sz, 0);
       f = factor(0, zn);
-      sm_put<K>(s_fs[0], lane, O::add(f.re, f.im));
+      fs = O::add(f.re, f.im);
+      sm_put<K>(s_fr[0], lane, f.re);
+      sm_put<K>(s_fi[0], lane, f.im);
+      sm_put<K>(s_fs[0], lane, fs);
       if (n > 1) {
         zn.re = load<K>(zre, sz, 1);
         zn.im = load<K>(zim, sz, 1);
       }
     }
-    named_sync(bar_full);
+    named_sync(bar);
 #pragma unroll 1
     for (int64_t j = 0; j < n; ++j) {
       const int q = (int)(j & 1);
@@ -371,29 +385,39 @@ __global__ void __launch_bounds__(128)
           zn.re = load<K>(zre, sz, j + 2);
           zn.im = load<K>(zim, sz, j + 2);
         }
-        const V<K> im_prev = sm_get<K>(s_im[1][q ^ 1], lane);
-        const V<K> p1 = O::mul(own, f.re);
-        const V<K> p2 = O::mul(im_prev, f.im);
-        sm_put<K>(s_p1[1], lane, p1);
-        sm_put<K>(s_p2[1], lane, p2);
-        named_arrive(bar_x);
-        own = O::add(p1, neg(p2));
-        sm_put<K>(s_re[1][q], lane, own);
+        const V<K> p1 = O::mul(re, f.re);
+        const V<K> p2 = O::mul(im, f.im);
+        if constexpr (XP) {
+          sm_put<K>(s_p1[1], lane, p1);
+          sm_put<K>(s_p2[1], lane, p2);
+          named_arrive(bar_x);
+        }
+        re = O::add(p1, neg(p2));
+        sm_put<K>(s_re[1][q], lane, re);
         if (j + 1 < n) {
           f = factor(j + 1, zj1);
+          sm_put<K>(s_fr[q ^ 1], lane, f.re);
+          sm_put<K>(s_fi[q ^ 1], lane, f.im);
           sm_put<K>(s_fs[q ^ 1], lane, O::add(f.re, f.im));
         }
       } else {
-        const V<K> re_prev = sm_get<K>(s_re[1][q ^ 1], lane);
-        const V<K> fs = sm_get<K>(s_fs[q], lane);
-        const V<K> p3 = O::mul(O::add(re_prev, own), fs);
-        named_sync(bar_x);
-        const V<K> p1 = sm_get<K>(s_p1[1], lane);
-        const V<K> p2 = sm_get<K>(s_p2[1], lane);
-        own = O::add(O::add(p3, neg(p1)), neg(p2));
-        sm_put<K>(s_im[1][q], lane, own);
+        const V<K> fsum = sm_get<K>(s_fs[q], lane);
+        const V<K> p3 = O::mul(O::add(re, im), fsum);
+        V<K> p1, p2;
+        if constexpr (XP) {
+          named_sync(bar_x);
+          p1 = sm_get<K>(s_p1[1], lane);
+          p2 = sm_get<K>(s_p2[1], lane);
+        } else {
+          p1 = O::mul(re, sm_get<K>(s_fr[q], lane));
+          p2 = O::mul(im, sm_get<K>(s_fi[q], lane));
+        }
+        im = O::add(O::add(p3, neg(p1)), neg(p2));
+        sm_put<K>(s_im[1][q], lane, im);
       }
-      named_sync(bar_full);
+      named_sync(bar);
+      if (is_b) im = sm_get<K>(s_im[1][q], lane);
+      else re = sm_get<K>(s_re[1][q], lane);
     }
   }
   __syncthreads();
@@ -401,8 +425,8 @@ __global__ void __launch_bounds__(128)
     const int q = (int)((n - 1) & 1);
     if (live) {
       Cx<K, VAR> acc, den;
-      acc.re = sm_get<K>(s_re[0][q], lane);
-      acc.im = own;
+      acc.re = re;
+      acc.im = im;
       den.re = sm_get<K>(s_re[1][q], lane);
       den.im = sm_get<K>(s_im[1][q], lane);
       dk_tail<K, VAR, PEER>(acc, den, z, zre_out, zim_out, so, step_mag, i, &peers);
@@ -685,7 +709,7 @@ struct DkLaunch {
     if (exact) {
       const int r = g_dk_exact_roots;
       const int64_t blocks = (cnt + r - 1) / r;
-      if (g_dk_exact_split && K == 4)
+      if (g_dk_exact_split && K >= DK_SPLIT_MIN_K)
         dk_exact2_kernel<K, VAR><<<(unsigned)blocks, 128, 0, st>>>(
             coeffs, sc, n, zre, zim, sz, i0, i1, zre_out, zim_out, so, step_mag, flag, r);
       else
@@ -712,7 +736,7 @@ struct DkPeerLaunch {
     if (exact) {
       const int r = g_dk_exact_roots;
       const int64_t blocks = (cnt + r - 1) / r;
-      if (g_dk_exact_split && K == 4)
+      if (g_dk_exact_split && K >= DK_SPLIT_MIN_K)
         dk_exact2_kernel<K, VAR, true><<<(unsigned)blocks, 128, 0, st>>>(
             coeffs, sc, n, zre, zim, n, i0, i1, ore, oim, n, step_mag, flag, r, peers);
       else
@@ -737,7 +761,7 @@ extern "C" int mw_dk_exact_set_roots_per_cta(int r) {
   return MW_OK;
 }
 
-// Tuning knob: exact-order kernel form (1 = split warp pairs for QD,
+// Tuning knob: exact-order kernel form (1 = split warp pairs for TD/QD,
 // default; 0 = one warp per chain).  Results are identical.
 extern "C" int mw_dk_exact_set_split(int on) {
   if (on != 0 && on != 1) return MW_ERR_INVALID;
