@@ -695,6 +695,15 @@ static int dk_tree_launch(const double* coeffs, int64_t sc, int64_t n, const dou
   cudaError_t e = cudaLaunchKernelEx(&cfg, dk_tree_kernel<K, VAR, PEER, true>, coeffs, sc, n, zre,
                                      zim, sz, i0, i1, zre_out, zim_out, so, step_mag, flag, peers,
                                      (const double*)ws, cnt);
+  if (e == cudaErrorNotSupported) {
+    // no programmatic launch here: plain stream order (griddepcontrol.wait
+    // is then a no-op and the powers are complete before the sweep starts)
+    (void)cudaGetLastError();
+    dk_tree_kernel<K, VAR, PEER, true><<<(unsigned)cnt, 96, 0, st>>>(
+        coeffs, sc, n, zre, zim, sz, i0, i1, zre_out, zim_out, so, step_mag, flag, peers,
+        (const double*)ws, cnt);
+    return launch_status();
+  }
   if (e != cudaSuccess) return (int)e;
   return launch_status();
 }
