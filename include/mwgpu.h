@@ -263,6 +263,12 @@ int mw_dk_exact_set_roots_per_cta(int roots);
  * ops, same order, identical results. */
 int mw_dk_exact_set_split(int on);
 
+/* Tuning knob of the tree-order sweep with a workspace (mw_dk_sweep_ws):
+ * roots per CTA, 4 (default) or 2 = one chain per lane and the pairwise
+ * trees packed level by level over the CTA's roots; 0 = the 3-warp
+ * single-root kernel.  Same tree order, identical results. */
+int mw_dk_tree_set_roots_per_cta(int roots);
+
 /* FP64 pipe microbenchmark: 8 independent DFMA (op = 0) or DADD (op = 1)
  * chains per thread, 8 unrolled steps per iteration: executes
  * blocks * threads * iters * 64 FP64 ops, no memory traffic; the caller

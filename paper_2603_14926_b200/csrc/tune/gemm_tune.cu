@@ -5,6 +5,8 @@
 #include "../gemm_kernel.cuh"
 #include "../reduce.cu"  // GEMV kernel template (its C-ABI symbols stay private to this .so)
 #include "gemv_staged.cuh"
+#include "../gemv_bulk.cuh"
+#include "gemv_probe.cuh"
 
 namespace mw {
 #define CFGV(NAME, bm, bn, bk, tm, tn, minb, vec)                             \
@@ -104,6 +106,31 @@ static int gemv_staged_launch(const double* A, const double* x, double* y, int64
   kern<<<(unsigned)((m + R - 1) / R), 128 * R, smem, st>>>(A, n, m * n, x, n, y, m, m, n);
   return launch_status();
 }
+template <int K, int G, int CH, int S>
+static int gemv_bulk_launch(const double* A, const double* x, double* y, int64_t m, int64_t n,
+                            cudaStream_t st) {
+  const size_t smem = gemv_bulk_smem<K, G, CH, S>(n);
+  if (smem > 227 * 1024) return MW_ERR_INVALID;
+  auto kern = gemv_bulk_kernel<K, BRANCH_FREE, G, CH, S>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int grid = sm_count();
+  if ((int64_t)grid * G > m) grid = (int)((m + G - 1) / G);
+  kern<<<grid, 128 * G, smem, st>>>(A, n, m * n, x, n, y, m, m, n);
+  return launch_status();
+}
+template <int K, int MODE>
+static int gemv_probe_launch(const double* A, const double* x, double* y, int64_t m, int64_t n,
+                             cudaStream_t st) {
+  gemv_probe_kernel<K, BRANCH_FREE, MODE><<<(unsigned)((m + 1) / 2), 256, 0, st>>>(A, n, m * n, x, n, y, m, m, n);
+  return launch_status();
+}
+template <int K, int RT, int D, bool PIPE, int MINB = 1>
+static int gemv_rt_launch(const double* A, const double* x, double* y, int64_t m, int64_t n,
+                          cudaStream_t st) {
+  gemv_rt_kernel<K, BRANCH_FREE, RT, D, PIPE, MINB><<<(unsigned)((m + RT - 1) / RT), 128, 0, st>>>(
+      A, n, m * n, x, n, y, m, m, n);
+  return launch_status();
+}
 template <int K>
 static int gemv_run(int cfg, const double* A, const double* x, double* y, int64_t m, int64_t n,
                     cudaStream_t st) {
@@ -126,16 +153,40 @@ static int gemv_run(int cfg, const double* A, const double* x, double* y, int64_
     case 15: return gemv_staged_launch<K, 2, 4, 2, true>(A, x, y, m, n, st);
     case 16: return gemv_staged_launch<K, 1, 8, 2, false>(A, x, y, m, n, st);
     case 17: return gemv_staged_launch<K, 1, 2, 4, false>(A, x, y, m, n, st);
+    case 18: return gemv_bulk_launch<K, 8, 256, 2>(A, x, y, m, n, st);
+    case 19: return gemv_bulk_launch<K, 6, 256, 3>(A, x, y, m, n, st);
+    case 20: return gemv_bulk_launch<K, 4, 512, 2>(A, x, y, m, n, st);
+    case 21: return gemv_bulk_launch<K, 8, 128, 3>(A, x, y, m, n, st);
+    case 22: return gemv_bulk_launch<K, 6, 256, 2>(A, x, y, m, n, st);
+    case 23: return gemv_bulk_launch<K, 4, 256, 3>(A, x, y, m, n, st);
+    case 24: return gemv_bulk_launch<K, 5, 256, 2>(A, x, y, m, n, st);
+    case 25: return gemv_bulk_launch<K, 7, 128, 4>(A, x, y, m, n, st);
+    case 26: return gemv_probe_launch<K, 1>(A, x, y, m, n, st);
+    case 27: return gemv_probe_launch<K, 2>(A, x, y, m, n, st);
+    case 28: return gemv_rt_launch<K, 1, 4, false>(A, x, y, m, n, st);
+    case 29: return gemv_rt_launch<K, 1, 2, true>(A, x, y, m, n, st);
+    case 30: return gemv_rt_launch<K, 1, 4, true>(A, x, y, m, n, st);
+    case 31: return gemv_rt_launch<K, 2, 2, false>(A, x, y, m, n, st);
+    case 32: return gemv_rt_launch<K, 2, 4, false>(A, x, y, m, n, st);
+    case 33: return gemv_rt_launch<K, 2, 2, true>(A, x, y, m, n, st);
+    case 34: return gemv_rt_launch<K, 2, 1, true>(A, x, y, m, n, st);
+    case 35: return gemv_rt_launch<K, 1, 2, true, 8>(A, x, y, m, n, st);
+    case 36: return gemv_rt_launch<K, 2, 2, true, 4>(A, x, y, m, n, st);
+    case 37: return gemv_rt_launch<K, 1, 1, true, 12>(A, x, y, m, n, st);
     default: return MW_ERR_INVALID;
   }
 }
-extern "C" int mwt_gemv_num_configs(void) { return 18; }
+extern "C" int mwt_gemv_num_configs(void) { return 38; }
 extern "C" const char* mwt_gemv_config_name(int cfg) {
   static const char* names[] = {"W4_R2_D4", "W1_R8_D8", "W1_R8_D4", "W2_R4_D4", "W2_R4_D8",
                                 "W4_R2_D2", "W4_R1_D4", "W8_R1_D2", "st_R2_D4_S2", "st_R2_D4_S3",
                                 "st_R1_D4_S2", "st_R1_D4_S3", "st_R2_D2_S2", "st_R2_D2_S4",
-                                "stx_R1_D4_S2", "stx_R2_D4_S2", "st_R1_D8_S2", "st_R1_D2_S4"};
-  return (cfg >= 0 && cfg < 18) ? names[cfg] : "?";
+                                "stx_R1_D4_S2", "stx_R2_D4_S2", "st_R1_D8_S2", "st_R1_D2_S4",
+                                "bk_G8_C256_S2", "bk_G6_C256_S3", "bk_G4_C512_S2", "bk_G8_C128_S3",
+                                "bk_G6_C256_S2", "bk_G4_C256_S3", "bk_G5_C256_S2", "bk_G7_C128_S4", "probe_fp64", "probe_mem",
+                                "rt1_D4", "rt1_D2_P", "rt1_D4_P", "rt2_D2", "rt2_D4", "rt2_D2_P",
+                                "rt2_D1_P", "rt1_D2_P_b8", "rt2_D2_P_b4", "rt1_D1_P_b12"};
+  return (cfg >= 0 && cfg < 38) ? names[cfg] : "?";
 }
 extern "C" int mwt_gemv(int cfg, int k, const double* A, const double* x, double* y, int64_t m,
                         int64_t n, void* stream) {

@@ -6,6 +6,9 @@ import paper_2603_14926_b200 as mw
 from paper_2603_14926_b200 import gen
 from paper_2603_14926_b200.roots import DKSweepGraph
 orders = sys.argv[1:] or ["tree", "exact"]
+from paper_2603_14926_b200 import _lib
+if os.environ.get("DK_TREE_ROOTS"):
+    _lib.load().mw_dk_tree_set_roots_per_cta(int(os.environ["DK_TREE_ROOTS"]))
 for k in (3, 4):
     q = mw.MonicPoly(torch.from_numpy(gen.config5_poly(k)).cuda())
     zre, zim = (torch.from_numpy(t).cuda() for t in gen.config5_init(k))

@@ -9,6 +9,7 @@ lib.mwt_gemv.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_v
                          ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p]
 lib.mwt_gemv_config_name.restype = ctypes.c_char_p
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+NOFLUSH = "--noflush" in sys.argv
 MAC = {3: 96, 4: 209}
 for k in (3, 4):
     a, x = gen.config2_gemv(k)
@@ -16,18 +17,24 @@ for k in (3, 4):
     m, n = a.shape[1], a.shape[2]
     y = torch.empty((k, m), dtype=torch.float64, device="cuda")
     ref = None
-    for cfg in range(lib.mwt_gemv_num_configs()):
+    sel = [int(c) for c in os.environ.get("CFGS", "").split(",") if c]
+    for cfg in (sel or range(lib.mwt_gemv_num_configs())):
         st = torch.cuda.current_stream().cuda_stream
-        lib.mwt_gemv(cfg, k, A.data_ptr(), X.data_ptr(), y.data_ptr(), m, n, st)
+        y.fill_(float("nan"))
+        rc = lib.mwt_gemv(cfg, k, A.data_ptr(), X.data_ptr(), y.data_ptr(), m, n, st)
         torch.cuda.synchronize()
+        if rc != 0:
+            print(f"k={k} {lib.mwt_gemv_config_name(cfg).decode():10s} rc={rc} (skipped)", flush=True)
+            continue
         same = ""
         if cfg == 0:
             ref = y.clone()
-        elif cfg >= 8:  # staged variants keep the P = 128 order: must be bit-identical
+        elif cfg >= 8 or cfg == 6:  # staged variants keep the P = 128 order: must be bit-identical
             same = " bits==W4" if torch.equal(y.view(torch.int64), ref.view(torch.int64)) else " BITS DIFFER"
         ts = []
         for _ in range(10):
-            flush.fill_(1)
+            if not NOFLUSH:
+                flush.fill_(1)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(); lib.mwt_gemv(cfg, k, A.data_ptr(), X.data_ptr(), y.data_ptr(), m, n, st); e1.record()
             torch.cuda.synchronize(); ts.append(e0.elapsed_time(e1))

@@ -953,7 +953,9 @@ def test_dk_exact_split_and_single_warp_forms_agree(k, v):
 def test_dk_tree_powers_kernel_path_matches_in_warp_path(k, v):
     """Tree sweep with the lane-per-root powers kernel + programmatic
     dependent launch (mw_dk_sweep_ws) equals the in-warp powers path
-    (mw_dk_sweep) and the oracle bit for bit, on a sub-range of roots."""
+    (mw_dk_sweep) and the oracle bit for bit, on a sub-range of roots
+    (134 roots: ragged last CTA for 4 roots per CTA), for the 3-warp
+    single-root kernel and the 2- and 4-roots-per-CTA kernels."""
     from paper_2603_14926_b200 import _lib
     from paper_2603_14926_b200.multiword import variant_code
 
@@ -967,7 +969,8 @@ def test_dk_tree_powers_kernel_path_matches_in_warp_path(k, v):
     C, R, I = (torch.from_numpy(a).cuda() for a in (coeffs, zre, zim))
     i0, i1 = 7, 141
     outs = []
-    for use_ws in (False, True):
+    for use_ws, roots in ((False, 2), (True, 0), (True, 2), (True, 4)):
+        lib.mw_dk_tree_set_roots_per_cta(roots)
         ore, oim = torch.zeros_like(R), torch.zeros_like(I)
         mag = torch.zeros(n, dtype=torch.float64, device="cuda")
         flag = torch.full((1,), 2**31 - 1, dtype=torch.int32, device="cuda")
@@ -978,11 +981,13 @@ def test_dk_tree_powers_kernel_path_matches_in_warp_path(k, v):
             rc = lib.mw_dk_sweep_ws(*args, ws.data_ptr(), _lib.stream_handle(R.device))
         else:
             rc = lib.mw_dk_sweep(*args, _lib.stream_handle(R.device))
+        lib.mw_dk_tree_set_roots_per_cta(4)
         _lib.check(rc, "sweep")
         outs.append((ore.cpu().numpy(), oim.cpu().numpy(), mag.cpu().numpy()))
-    assert_bitwise(outs[0][0], outs[1][0])
-    assert_bitwise(outs[0][1], outs[1][1])
-    assert_bitwise(outs[0][2], outs[1][2])
+    for o in outs[1:]:  # in-warp powers == powers kernel, for every roots-per-CTA form
+        assert_bitwise(outs[0][0], o[0])
+        assert_bitwise(outs[0][1], o[1])
+        assert_bitwise(outs[0][2], o[2])
     want_re, want_im, _, _ = oracle.dk_sweep(coeffs, zre, zim, v, exact=False, rows=(i0, i1))
     assert_bitwise(outs[1][0][:, i0:i1], want_re[:, i0:i1])
     assert_bitwise(outs[1][1][:, i0:i1], want_im[:, i0:i1])
