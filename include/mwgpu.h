@@ -264,9 +264,10 @@ int mw_dk_exact_set_roots_per_cta(int roots);
 int mw_dk_exact_set_split(int on);
 
 /* Tuning knob of the tree-order sweep with a workspace (mw_dk_sweep_ws):
- * roots per CTA, 4 (default) or 2 = one chain per lane and the pairwise
- * trees packed level by level over the CTA's roots; 0 = the 3-warp
- * single-root kernel.  Same tree order, identical results. */
+ * roots per CTA, 1, 2 or 4 = one chain per lane and the pairwise trees
+ * packed level by level over the CTA's roots; -1 (default) = by shard
+ * size (4 from 512 roots, 2 from 256, else 1); 0 = the 3-warp single-root
+ * kernel.  Same tree order, identical results. */
 int mw_dk_tree_set_roots_per_cta(int roots);
 
 /* FP64 pipe microbenchmark: 8 independent DFMA (op = 0) or DADD (op = 1)

@@ -5,7 +5,7 @@ namespace mw {
 
 int g_dk_exact_roots = 16;
 int g_dk_exact_split = 1;
-int g_dk_tree_roots = 4;
+int g_dk_tree_roots = -1;
 
 #define MW_DK_EXTERN(FN) \
   MW_DK_FOR_K(extern template, FN, 2) MW_DK_FOR_K(extern template, FN, 3) MW_DK_FOR_K(extern template, FN, 4)
@@ -55,9 +55,10 @@ extern "C" int mw_dk_exact_set_roots_per_cta(int r) {
 }
 
 // Tuning knob for the tree-order sweep: roots per CTA (0 = the 3-warp
-// single-root kernel, 2 or 4 = dk_treem_kernel).  Results are identical.
+// single-root kernel, 1, 2 or 4 = dk_treem_kernel, -1 = auto by shard
+// size).  Results are identical.
 extern "C" int mw_dk_tree_set_roots_per_cta(int r) {
-  if (r != 0 && r != 2 && r != 4) return MW_ERR_INVALID;
+  if (r != -1 && r != 0 && r != 1 && r != 2 && r != 4) return MW_ERR_INVALID;
   g_dk_tree_roots = r;
   return MW_OK;
 }

@@ -481,7 +481,7 @@ __device__ __forceinline__ Cx<K, VAR> shfl_cx(const Cx<K, VAR>& v, int s, bool u
 // squarings of w (the tree order's definition, see above).
 template <int K, int VAR>
 __device__ __forceinline__ void dk_powers(const Cx<K, VAR>& z, int64_t B, Cx<K, VAR>& w,
-                                          Cx<K, VAR>& w32) {
+                                          Cx<K, VAR>& w32, bool with_w32 = true) {
   w = c_one<K, VAR>();
   Cx<K, VAR> sq = z;
   for (int64_t e = B; e > 0; e >>= 1) {
@@ -489,17 +489,19 @@ __device__ __forceinline__ void dk_powers(const Cx<K, VAR>& z, int64_t B, Cx<K, 
     if (e > 1) sq = c_mul_ol(sq, sq);
   }
   w32 = w;
+  if (!with_w32) return;
 #pragma unroll 1
   for (int r = 0; r < 5; ++r) w32 = c_mul_ol(w32, w32);
 }
 
-// One thread per root: w = z^B and w^32 for the tree sweep that follows
-// (programmatic dependent launch: the sweep starts as soon as every CTA
-// here has issued launch_dependents, and only its powers warp waits).
+// One thread per root: w = z^B and (with_w32) w^32 for the tree sweep that
+// follows (programmatic dependent launch: the sweep starts as soon as every
+// CTA here has issued launch_dependents, and only its powers warps wait).
 template <int K, int VAR>
 __global__ void __launch_bounds__(128)
     dk_pow_kernel(const double* __restrict__ zre, const double* __restrict__ zim, int64_t sz,
-                  int64_t n, int64_t i0, int64_t i1, double* __restrict__ wbuf, int64_t ws) {
+                  int64_t n, int64_t i0, int64_t i1, double* __restrict__ wbuf, int64_t ws,
+                  int with_w32) {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int64_t i = i0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= i1) return;
@@ -507,7 +509,7 @@ __global__ void __launch_bounds__(128)
   Cx<K, VAR> z, w, w32;
   z.re = load<K>(zre, sz, i);
   z.im = load<K>(zim, sz, i);
-  dk_powers<K, VAR>(z, B, w, w32);
+  dk_powers<K, VAR>(z, B, w, w32, with_w32 != 0);
   const int64_t r = i - i0;
   store<K>(wbuf, ws, r, w.re);
   store<K>(wbuf + (int64_t)K * ws, ws, r, w.im);
@@ -681,8 +683,10 @@ __global__ void __launch_bounds__(96)
 // masked.  The per-root tail runs on lane r of warp 2R.
 template <int K>
 __host__ __device__ constexpr size_t dk_treem_smem(int R) {
-  // den + num partials [R][64] complex, powers [R][2][2][K][32]
-  return (size_t)R * 64 * 2 * K * sizeof(double) * 2 + (size_t)R * 2 * 2 * K * 32 * sizeof(double);
+  // den + num partials [R][64] complex, powers [R][2][2][K][32], and for
+  // R = 1 the w^32 hand-off [2K][64] (slot 0)
+  return (size_t)R * 64 * 2 * K * sizeof(double) * 2 + (size_t)R * 2 * 2 * K * 32 * sizeof(double) +
+         (R == 1 ? (size_t)2 * K * 64 * sizeof(double) : 0);
 }
 
 template <int K, int VAR>
@@ -705,8 +709,16 @@ __device__ __forceinline__ Cx<K, VAR> cx_get(const double* base, int idx) {
   return v;
 }
 
+// Warps per CTA: 5R, plus (R = 1) a w^32 warp, so that the five squarings
+// w -> w^32 run beside the scan instead of before it: with one root per
+// CTA the powers path, not the FP64 pipe, bounds the sweep (measured,
+// scripts/time_dk_shard.py: TD 18.6 -> 17.2, QD 36.4 -> 32.5 us at 64
+// roots; with 2 roots per CTA the extra warps cost more than they save).
+template <int R>
+__host__ __device__ constexpr int dk_treem_warps() { return R == 1 ? 6 : 5 * R; }
+
 template <int K, int VAR, int R, bool PEER = false>
-__global__ void __launch_bounds__(160 * R, 4 / R)
+__global__ void __launch_bounds__(32 * dk_treem_warps<R>(), R == 2 ? 2 : 1)
     dk_treem_kernel(const double* __restrict__ coeffs, int64_t sc, int64_t n,
                     const double* __restrict__ zre, const double* __restrict__ zim, int64_t sz,
                     int64_t i0, int64_t i1, double* __restrict__ zre_out,
@@ -772,7 +784,7 @@ __global__ void __launch_bounds__(160 * R, 4 / R)
       }
     }
     cx_put<K, VAR>(num_s + (size_t)r * 2 * K * 64, u, p);
-  } else {
+  } else if (warp < 5 * R) {
     // ---- powers of root r: x_l = w^l (Hillis-Steele scan), x_l * w^32
     const int r = warp - 4 * R;
     const int64_t i = rbase + r;
@@ -782,14 +794,20 @@ __global__ void __launch_bounds__(160 * R, 4 / R)
       const int64_t q = i - i0;
       w.re = load<K>(wbuf, ws, q);
       w.im = load<K>(wbuf + (int64_t)K * ws, ws, q);
-      w32.re = load<K>(wbuf + (int64_t)2 * K * ws, ws, q);
-      w32.im = load<K>(wbuf + (int64_t)3 * K * ws, ws, q);
+      if constexpr (R > 1) {
+        w32.re = load<K>(wbuf + (int64_t)2 * K * ws, ws, q);
+        w32.im = load<K>(wbuf + (int64_t)3 * K * ws, ws, q);
+      }
     }
     Cx<K, VAR> x = lane == 0 ? c_one<K, VAR>() : w;
 #pragma unroll 1
     for (int s = 1; s < 32; s <<= 1) {
       Cx<K, VAR> o = shfl_cx(x, s, true);
       if (lane >= s) x = c_mul_ol(x, o);
+    }
+    if constexpr (R == 1) {
+      named_sync(1 + r);  // w^32 from warp 5R + r
+      w32 = cx_get<K, VAR>(pw + (size_t)R * 2 * 2 * K * 32 + (size_t)r * 2 * K * 64, 0);
     }
     const Cx<K, VAR> xh = c_mul_ol(x, w32);
     double* pr = pw + (size_t)r * 2 * 2 * K * 32;
@@ -800,6 +818,21 @@ __global__ void __launch_bounds__(160 * R, 4 / R)
       pr[(1 * 2 * K + c) * 32 + lane] = xh.re.c[c];
       pr[(1 * 2 * K + K + c) * 32 + lane] = xh.im.c[c];
     }
+  } else if constexpr (R == 1) {
+    // ---- w^32 of root r: five squarings of w (beside the scan)
+    const int r = warp - 5 * R;
+    const int64_t i = rbase + r;
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    Cx<K, VAR> w32 = c_one<K, VAR>();
+    if (i < i1) {
+      const int64_t q = i - i0;
+      w32.re = load<K>(wbuf, ws, q);
+      w32.im = load<K>(wbuf + (int64_t)K * ws, ws, q);
+#pragma unroll 1
+      for (int t = 0; t < 5; ++t) w32 = c_mul_ol(w32, w32);
+    }
+    if (lane == 0) cx_put<K, VAR>(pw + (size_t)R * 2 * 2 * K * 32 + (size_t)r * 2 * K * 64, 0, w32);
+    named_sync(1 + r);
   }
   __syncthreads();
 
@@ -893,7 +926,8 @@ __global__ void __launch_bounds__(160 * R, 4 / R)
 }
 
 // Roots per CTA of the tree sweep: 0 = the 3-warp single-root kernel
-// (dk_tree_kernel), 2 or 4 = dk_treem_kernel<R>.  Results are identical.
+// (dk_tree_kernel), 1, 2 or 4 = dk_treem_kernel<R>, -1 = by shard size
+// (4 from 512 roots, 2 from 256, else 1).  Results are identical.
 extern int g_dk_tree_roots;  // default 2 (dk.cu)
 
 // dk_treem_kernel<R> as a programmatic dependent launch after dk_pow_kernel
@@ -915,7 +949,7 @@ static int dk_treem_launch(const double* coeffs, int64_t sc, int64_t n, const do
   const unsigned grid = (unsigned)((cnt + R - 1) / R);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(160 * R);
+  cfg.blockDim = dim3(32 * dk_treem_warps<R>());
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -927,7 +961,7 @@ static int dk_treem_launch(const double* coeffs, int64_t sc, int64_t n, const do
                                      zim_out, so, step_mag, flag, peers, (const double*)ws, cnt);
   if (e == cudaErrorNotSupported) {
     (void)cudaGetLastError();
-    kern<<<grid, 160 * R, smem, st>>>(coeffs, sc, n, zre, zim, sz, i0, i1, zre_out, zim_out, so,
+    kern<<<grid, 32 * dk_treem_warps<R>(), smem, st>>>(coeffs, sc, n, zre, zim, sz, i0, i1, zre_out, zim_out, so,
                                       step_mag, flag, peers, (const double*)ws, cnt);
     return launch_status();
   }
@@ -950,12 +984,16 @@ int dk_tree_launch(const double* coeffs, int64_t sc, int64_t n, const double* zr
         (const double*)nullptr, (int64_t)0);
     return launch_status();
   }
+  int roots = g_dk_tree_roots;
+  if (roots < 0) roots = cnt >= 512 ? 4 : cnt >= 256 ? 2 : 1;  // auto: ~128+ CTAs when possible
+  // R = 1 squares w -> w^32 inside the sweep (beside the scan)
   dk_pow_kernel<K, VAR><<<(unsigned)((cnt + 127) / 128), 128, 0, st>>>(zre, zim, sz, n, i0, i1, ws,
-                                                                       cnt);
+                                                                       cnt, roots == 1 ? 0 : 1);
   int rc = launch_status();
   if (rc) return rc;
-  if (g_dk_tree_roots == 2) return dk_treem_launch<K, VAR, PEER, 2>(coeffs, sc, n, zre, zim, sz, i0, i1, zre_out, zim_out, so, step_mag, flag, peers, ws, st);
-  if (g_dk_tree_roots == 4) return dk_treem_launch<K, VAR, PEER, 4>(coeffs, sc, n, zre, zim, sz, i0, i1, zre_out, zim_out, so, step_mag, flag, peers, ws, st);
+  if (roots == 1) return dk_treem_launch<K, VAR, PEER, 1>(coeffs, sc, n, zre, zim, sz, i0, i1, zre_out, zim_out, so, step_mag, flag, peers, ws, st);
+  if (roots == 2) return dk_treem_launch<K, VAR, PEER, 2>(coeffs, sc, n, zre, zim, sz, i0, i1, zre_out, zim_out, so, step_mag, flag, peers, ws, st);
+  if (roots == 4) return dk_treem_launch<K, VAR, PEER, 4>(coeffs, sc, n, zre, zim, sz, i0, i1, zre_out, zim_out, so, step_mag, flag, peers, ws, st);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)cnt);
   cfg.blockDim = dim3(96);

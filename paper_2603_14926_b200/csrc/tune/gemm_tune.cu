@@ -5,7 +5,7 @@
 #include "../gemm_kernel.cuh"
 #include "../reduce.cu"  // GEMV kernel template (its C-ABI symbols stay private to this .so)
 #include "gemv_staged.cuh"
-#include "../gemv_bulk.cuh"
+#include "gemv_bulk.cuh"
 #include "gemv_probe.cuh"
 
 namespace mw {

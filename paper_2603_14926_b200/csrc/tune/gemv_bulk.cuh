@@ -1,4 +1,5 @@
-// gemv_bulk.cuh — tree-order GEMV with the A stream on the bulk-copy (TMA)
+// gemv_bulk.cuh (tuning harness only; measured slower than gemv_tree_kernel,
+// see scripts/tune_gemv.py) — tree-order GEMV with the A stream on the bulk-copy (TMA)
 // engine.  Same partials and pairwise tree as gemv_tree_kernel (reduce.cu:
 // 128 partials per row, partial u folds t = u, u+128, ... ascending from
 // exact zero), so the results are bit-identical; only the data movement and
@@ -19,7 +20,7 @@
 // used): n even, lda and sA even, A and x 16-byte aligned, x stride even,
 // and the shared-memory footprint below <= the opt-in maximum.
 #pragma once
-#include "common.cuh"
+#include "../common.cuh"
 
 namespace mw {
 
