@@ -587,6 +587,37 @@ def secondary(args, torch, dist, mw, world, rank, peak):
         "us_per_call_graph": None if ms_axpy_graph is None else round(ms_axpy_graph * 1e3, 2),
         "hbm_frac": round(3 * 2 * (hi - lo) * 8 * world / (ms_axpy / 1e3) / hbm, 4)}
 
+    # ---- config 1's kernels at a streaming size (DD, n = 2^26: 1 GiB per
+    # operand, far above L2), where dot and axpy are HBM-bound: GB/s vs the
+    # HBM peak.  Timing-only inputs drawn on the device (BF cost is
+    # data-independent).
+    if world == 1 and not args.quick:
+        nbig = 1 << 26
+        gdev = torch.Generator(device="cuda")
+        gdev.manual_seed(0)
+
+        def dd_planes():
+            t = torch.empty((2, nbig), dtype=torch.float64, device="cuda")
+            t[0].uniform_(-1, 1, generator=gdev)
+            t[1].uniform_(-1, 1, generator=gdev)
+            t[1].mul_(t[0]).mul_(2.0 ** -53)
+            return t
+
+        Xb, Yb = mw.LaneBatch(dd_planes()), mw.LaneBatch(dd_planes())
+        dres_b = torch.empty(2, dtype=torch.float64, device="cuda")
+        ms_dot_b = timed(lambda: blas.dot_tensor(Xb, Yb, BF, out=dres_b), 10, flush_l2=True)
+        ms_axpy_b = timed(lambda: blas.axpy_(tuple(alpha), Xb, Yb, BF), 10, flush_l2=True)
+        out["config1_kernels_dd_n2p26_stream"] = {
+            "dot_us": round(ms_dot_b * 1e3, 1),
+            "dot_GBps": round(32 * nbig / (ms_dot_b / 1e3) / 1e9, 1),
+            "dot_hbm_frac": round(32 * nbig / (ms_dot_b / 1e3) / hbm, 4),
+            "axpy_us": round(ms_axpy_b * 1e3, 1),
+            "axpy_GBps": round(48 * nbig / (ms_axpy_b / 1e3) / 1e9, 1),
+            "axpy_hbm_frac": round(48 * nbig / (ms_axpy_b / 1e3) / hbm, 4),
+            "bytes": {"dot": 32 * nbig, "axpy": 48 * nbig},
+            "l2": "flushed before each call", "note": "same kernels as config 1 at n = 2^26 (HBM-bound regime)"}
+        del Xb, Yb
+
     # ---- config 2: GEMV TD / QD 2048 x 2048, row blocks per rank, L2 flushed
     for k in (3, 4):
         a, xv = gen.config2_gemv(k)
