@@ -45,6 +45,30 @@ extern "C" {
 const char* mw_version(void);
 const char* mw_status_string(int status);
 
+/* Named kernels outside the (K, Variant) dispatch, over component planes
+ * (plane strides sa / sb / so, n lanes):
+ *   MW_NAMED_DW_ADD_SLOPPY  DD, replaces multiword.dw_add_sloppy
+ *                           (multiword.py:104-115)
+ *   MW_NAMED_TW_MUL_CLEANED TD, replaces multiword.tw_mul_cleaned
+ *                           (multiword.py:325-358)                       */
+#define MW_NAMED_DW_ADD_SLOPPY 0
+#define MW_NAMED_TW_MUL_CLEANED 1
+int mw_named_op(int op, const double* a, int64_t sa, const double* b, int64_t sb,
+                double* out, int64_t so, int64_t n, void* stream);
+
+/* Renormalisation of raw expansions (replaces multiword.tw_renormalize /
+ * qw_renormalize, multiword.py:191-241, and normalize 710-719): k = 2 reads
+ * 2 planes (quick_two_sum), k = 3 reads 4 planes (s0, s1, s2, t0), k = 4
+ * reads 5 planes (x0..x4); writes k planes.  Value-dependent branches per
+ * lane, as in the reference. */
+int mw_renormalize(int k, const double* in, int64_t si, double* out, int64_t so,
+                   int64_t n, void* stream);
+
+/* Correctly rounded a*b + c per element (replaces eft.fma, eft.py:33-48 /
+ * _fmaext.c:16-40). */
+int mw_fma(const double* a, const double* b, const double* c, double* out, int64_t n,
+           void* stream);
+
 /* The error-free transformations over arrays (eft.py:51-83): op 0
  * quick_two_sum (requires |a| >= |b|), 1 two_sum, 2 two_prod (one FMA);
  * s[i] + e[i] == a[i] op b[i] exactly (within the EFT contracts). */

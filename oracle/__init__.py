@@ -56,6 +56,9 @@ def lib():
         L.mwo_poly_eval.argtypes = [I, I, P, I64, I64, P, P, I64, P, P, I64, I64, I, P, I64]
         L.mwo_dk_sweep.argtypes = [I, I, P, I64, I64, P, P, I64, I64, I64, P, P, I64, P, P, I]
         L.mwo_set_threads.argtypes = [I]
+        L.mwo_named.argtypes = [I, P, I64, P, I64, P, I64, I64]
+        L.mwo_renormalize.argtypes = [I, P, I64, P, I64, I64]
+        L.mwo_fma.argtypes = [P, P, P, P, I64]
         L.mwo_max_threads.restype = I
         _lib = L
     return _lib
@@ -219,3 +222,29 @@ def dk_sweep(coeffs, zre, zim, variant=BRANCH_FREE, exact: bool = True, rows=Non
         )
     c = int(coll[0])
     return ore, oim, mag, (None if c < 0 else (c // n, c % n))
+
+
+def named(op: str, a, b) -> np.ndarray:
+    """dw_add_sloppy (op "dw_add_sloppy", DD) or tw_mul_cleaned ("tw_mul_cleaned", TD)."""
+    code = {"dw_add_sloppy": 0, "tw_mul_cleaned": 1}[op]
+    a, b = _planes(a), _planes(b)
+    out = np.empty_like(a)
+    n = a.shape[1]
+    _check(lib().mwo_named(code, _ptr(a), n, _ptr(b), n, _ptr(out), n, n))
+    return out
+
+
+def renormalize(k: int, raw) -> np.ndarray:
+    """k = 2: quick_two_sum of 2 planes; 3: tw_renormalize of 4; 4: qw_renormalize of 5."""
+    raw = _planes(raw)
+    n = raw.shape[1]
+    out = np.empty((k, n))
+    _check(lib().mwo_renormalize(k, _ptr(raw), n, _ptr(out), n, n))
+    return out
+
+
+def fma(a, b, c) -> np.ndarray:
+    a, b, c = (np.ascontiguousarray(v, dtype=np.float64).ravel() for v in (a, b, c))
+    out = np.empty_like(a)
+    _check(lib().mwo_fma(_ptr(a), _ptr(b), _ptr(c), _ptr(out), a.size))
+    return out

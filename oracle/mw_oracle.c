@@ -336,6 +336,44 @@ static mwv tw_mul_std(const mwv* a, const mwv* b) {
   (void)s2;
   return tw_renorm(p0, p1, s0, t0);
 }
+/* multiword.py:104-115 dw_add_sloppy (not in any dispatch table) */
+static mwv dw_add_sloppy(const mwv* a, const mwv* b) {
+  double s, e;
+  mwv r = {{0}};
+  two_sum(a->c[0], b->c[0], &s, &e);
+  e = e + (a->c[1] + b->c[1]);
+  quick_two_sum(s, e, &r.c[0], &r.c[1]);
+  return r;
+}
+/* multiword.py:325-358 tw_mul_cleaned: tw_mul with the error chain of
+ * q0, q3, q4, q5 folded into the tail (t0 = s1 + t0 + t1, left to right) */
+static mwv tw_mul_cleaned(const mwv* a, const mwv* b) {
+  double p0, q0, p1, q1, p2, q2, p3, q3, p4, q4, p5, q5, i1, i2, i3, s0, t0, s1, t1;
+  two_prod(a->c[0], b->c[0], &p0, &q0);
+  two_prod(a->c[0], b->c[1], &p1, &q1);
+  two_prod(a->c[1], b->c[0], &p2, &q2);
+  two_prod(a->c[0], b->c[2], &p3, &q3);
+  two_prod(a->c[1], b->c[1], &p4, &q4);
+  two_prod(a->c[2], b->c[0], &p5, &q5);
+  two_sum(p1, p2, &i1, &i2);
+  two_sum(q0, i1, &p1, &i3);
+  two_sum(i2, i3, &p2, &q0);
+  two_sum(p2, q1, &i1, &i2);
+  two_sum(q2, i1, &p2, &i3);
+  two_sum(i2, i3, &q1, &q2);
+  two_sum(p3, p4, &i1, &i2);
+  two_sum(p5, i1, &p3, &i3);
+  two_sum(i2, i3, &p4, &p5);
+  two_sum(p2, p3, &s0, &t0);
+  two_sum(q1, p4, &s1, &t1);
+  two_sum(s1, t0, &s1, &t0); /* its t0 only fed the dead s2 */
+  two_sum(q0, q3, &q0, &q3);
+  two_sum(q4, q5, &q4, &q5);
+  two_sum(q0, q4, &t0, &t1);
+  t1 = t1 + (q3 + q5);
+  t0 = (s1 + t0) + t1;
+  return tw_renorm(p0, p1, s0, t0);
+}
 /* multiword.py:410-415 _three_sum */
 static void three_sum(double* a, double* b, double* c) {
   double t1, t2, t3;
@@ -909,5 +947,42 @@ int mwo_dk_sweep(int k, int variant, const double* coeffs, int64_t sc, int64_t n
     dk_tail(&acc, &den, &z, k, add, mul, zre_out, zim_out, so, step_mag, i);
   }
   *collision = coll;
+  return 0;
+}
+
+/* Named kernels outside the dispatch (mw_named_op): op 0 dw_add_sloppy (DD),
+ * op 1 tw_mul_cleaned (TD). */
+int mwo_named(int op, const double* a, int64_t sa, const double* b, int64_t sb, double* out,
+              int64_t so, int64_t n) {
+  if (op != 0 && op != 1) return -1;
+  const int k = op == 0 ? 2 : 3;
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < n; ++i) {
+    mwv x = ld(a, sa, i, k), y = ld(b, sb, i, k);
+    mwv r = op == 0 ? dw_add_sloppy(&x, &y) : tw_mul_cleaned(&x, &y);
+    st(out, so, i, k, &r);
+  }
+  return 0;
+}
+
+/* Renormalisers (multiword.py:191-241): k = 2 quick_two_sum of 2 planes,
+ * k = 3 tw_renormalize of 4 planes, k = 4 qw_renormalize of 5 planes. */
+int mwo_renormalize(int k, const double* in, int64_t si, double* out, int64_t so, int64_t n) {
+  if (k < 2 || k > 4) return -1;
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < n; ++i) {
+    mwv r = {{0}};
+    if (k == 2) quick_two_sum(in[i], in[si + i], &r.c[0], &r.c[1]);
+    else if (k == 3) r = tw_renorm(in[i], in[si + i], in[2 * si + i], in[3 * si + i]);
+    else r = qw_renorm(in[i], in[si + i], in[2 * si + i], in[3 * si + i], in[4 * si + i]);
+    st(out, so, i, k, &r);
+  }
+  return 0;
+}
+
+/* eft.py:33-48 fma: correctly rounded a*b + c (libm fma, as _fmaext.c). */
+int mwo_fma(const double* a, const double* b, const double* c, double* out, int64_t n) {
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < n; ++i) out[i] = fma(a[i], b[i], c[i]);
   return 0;
 }

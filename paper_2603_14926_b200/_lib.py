@@ -37,6 +37,9 @@ _SIGS = {
     "mw_ew_add": ([I, I, P, I64, P, I64, P, I64, I64, P], I),
     "mw_ew_sub": ([I, I, P, I64, P, I64, P, I64, I64, P], I),
     "mw_ew_mul": ([I, I, P, I64, P, I64, P, I64, I64, P], I),
+    "mw_named_op": ([I, P, I64, P, I64, P, I64, I64, P], I),
+    "mw_renormalize": ([I, P, I64, P, I64, I64, P], I),
+    "mw_fma": ([P, P, P, P, I64, P], I),
     "mw_ew_div": ([I, I, P, I64, P, I64, P, I64, I64, P], I),
     "mw_axpy": ([I, I, P, P, I64, P, I64, I64, P], I),
     "mw_dot_workspace": ([I, I64], I64),

@@ -184,3 +184,95 @@ extern "C" int mw_eft(int op, const double* a, const double* b, double* s, doubl
   if (op == 2) eft_kernel<2><<<(unsigned)blocks, 256, 0, st>>>(a, b, s, e, n);
   return launch_status();
 }
+
+// ------------------------------------------- kernels outside the dispatch
+// The reference's named kernels that no (K, Variant) entry selects
+// (multiword.py:104-115 dw_add_sloppy, 325-358 tw_mul_cleaned), the
+// renormalisers (191-241 tw_/qw_renormalize, 710-719 normalize) and the
+// correctly rounded fma (eft.py:33-48), over component planes.
+namespace mw {
+template <int OP>
+__global__ void __launch_bounds__(256) named_kernel(const double* __restrict__ a, int64_t sa,
+                                                    const double* __restrict__ b, int64_t sb,
+                                                    double* __restrict__ out, int64_t so,
+                                                    int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if constexpr (OP == MW_NAMED_DW_ADD_SLOPPY) {
+      store<2>(out, so, i, dd_add_sloppy(load<2>(a, sa, i), load<2>(b, sb, i)));
+    } else {
+      store<3>(out, so, i, tw_mul_cleaned(load<3>(a, sa, i), load<3>(b, sb, i)));
+    }
+  }
+}
+
+// in: M = 2 / 4 / 5 planes (K = 2: quick_two_sum(c0, c1); K = 3:
+// tw_renormalize(s0, s1, s2, t0); K = 4: qw_renormalize(x0..x4)) -> K planes
+template <int K>
+__global__ void __launch_bounds__(256) renorm_kernel(const double* __restrict__ in, int64_t si,
+                                                     double* __restrict__ out, int64_t so,
+                                                     int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    V<K> r;
+    if constexpr (K == 2) {
+      quick_two_sum(in[i], in[si + i], r.c[0], r.c[1]);
+    } else if constexpr (K == 3) {
+      r = tw_renormalize(in[i], in[si + i], in[2 * si + i], in[3 * si + i]);
+    } else {
+      r = qw_renormalize(in[i], in[si + i], in[2 * si + i], in[3 * si + i], in[4 * si + i]);
+    }
+    store<K>(out, so, i, r);
+  }
+}
+
+__global__ void __launch_bounds__(256) fma_kernel(const double* __restrict__ a,
+                                                  const double* __restrict__ b,
+                                                  const double* __restrict__ c,
+                                                  double* __restrict__ out, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = MW_FMA(a[i], b[i], c[i]);
+}
+
+static unsigned lane_blocks(int64_t n) {
+  int64_t blocks = (n + 255) / 256;
+  const int64_t cap = (int64_t)sm_count() * 16;
+  return (unsigned)(blocks > cap ? cap : blocks);
+}
+}  // namespace mw
+
+extern "C" int mw_named_op(int op, const double* a, int64_t sa, const double* b, int64_t sb,
+                           double* out, int64_t so, int64_t n, void* stream) {
+  if (op != MW_NAMED_DW_ADD_SLOPPY && op != MW_NAMED_TW_MUL_CLEANED) return MW_ERR_INVALID;
+  if (n < 0) return MW_ERR_INVALID;
+  if (n == 0) return MW_OK;
+  if (!a || !b || !out || sa < n || sb < n || so < n) return MW_ERR_INVALID;
+  cudaStream_t st = as_stream(stream);
+  if (op == MW_NAMED_DW_ADD_SLOPPY)
+    named_kernel<MW_NAMED_DW_ADD_SLOPPY><<<lane_blocks(n), 256, 0, st>>>(a, sa, b, sb, out, so, n);
+  else
+    named_kernel<MW_NAMED_TW_MUL_CLEANED><<<lane_blocks(n), 256, 0, st>>>(a, sa, b, sb, out, so, n);
+  return launch_status();
+}
+
+extern "C" int mw_renormalize(int k, const double* in, int64_t si, double* out, int64_t so,
+                              int64_t n, void* stream) {
+  if (k < 2 || k > 4 || n < 0) return MW_ERR_INVALID;
+  if (n == 0) return MW_OK;
+  if (!in || !out || si < n || so < n) return MW_ERR_INVALID;
+  cudaStream_t st = as_stream(stream);
+  if (k == 2) renorm_kernel<2><<<lane_blocks(n), 256, 0, st>>>(in, si, out, so, n);
+  if (k == 3) renorm_kernel<3><<<lane_blocks(n), 256, 0, st>>>(in, si, out, so, n);
+  if (k == 4) renorm_kernel<4><<<lane_blocks(n), 256, 0, st>>>(in, si, out, so, n);
+  return launch_status();
+}
+
+extern "C" int mw_fma(const double* a, const double* b, const double* c, double* out, int64_t n,
+                      void* stream) {
+  if (n < 0) return MW_ERR_INVALID;
+  if (n == 0) return MW_OK;
+  if (!a || !b || !c || !out) return MW_ERR_INVALID;
+  fma_kernel<<<lane_blocks(n), 256, 0, as_stream(stream)>>>(a, b, c, out, n);
+  return launch_status();
+}

@@ -397,6 +397,49 @@ MW_HD V<3> tw_mul_std(const V<3>& a, const V<3>& b) {
   return tw_renormalize(p0, p1, s0, t0);
 }
 
+// ------------------------------------------------ kernels outside dispatch
+// multiword.py:104-115 dw_add_sloppy: the low-part sum's error is dropped.
+MW_HD V<2> dd_add_sloppy(const V<2>& a, const V<2>& b) {
+  double s, e;
+  two_sum(a.c[0], b.c[0], s, e);
+  e = MW_ADD(e, MW_ADD(a.c[1], b.c[1]));
+  V<2> r;
+  quick_two_sum(s, e, r.c[0], r.c[1]);
+  return r;
+}
+
+// multiword.py:325-358 tw_mul_cleaned = tw_renormalize(_tw_mul_cleaned_core):
+// the dangling error chain of tw_mul folded into the tail term.
+MW_HD V<3> tw_mul_cleaned(const V<3>& a, const V<3>& b) {
+  double p0, q0, p1, q1, p2, q2, p3, q3, p4, q4, p5, q5, i1, i2, i3, s0, t0, s1, t1;
+  two_prod(a.c[0], b.c[0], p0, q0);
+  two_prod(a.c[0], b.c[1], p1, q1);
+  two_prod(a.c[1], b.c[0], p2, q2);
+  two_prod(a.c[0], b.c[2], p3, q3);
+  two_prod(a.c[1], b.c[1], p4, q4);
+  two_prod(a.c[2], b.c[0], p5, q5);
+  two_sum(p1, p2, i1, i2);
+  two_sum(q0, i1, p1, i3);
+  two_sum(i2, i3, p2, q0);
+  two_sum(p2, q1, i1, i2);
+  two_sum(q2, i1, p2, i3);
+  two_sum(i2, i3, q1, q2);
+  two_sum(p3, p4, i1, i2);
+  two_sum(p5, i1, p3, i3);
+  two_sum(i2, i3, p4, p5);
+  two_sum(p2, p3, s0, t0);
+  two_sum(q1, p4, s1, t1);
+  two_sum(s1, t0, s1, t0);  // (the reference's s2 chain is dead: not computed)
+  two_sum(q0, q3, q0, q3);
+  two_sum(q4, q5, q4, q5);
+  double u0, u1;
+  two_sum(q0, q4, u0, u1);
+  u1 = MW_ADD(u1, MW_ADD(q3, q5));
+  const double tail = MW_ADD(MW_ADD(s1, u0), u1);  // s1 + t0 + t1, left to right
+  (void)t1;
+  return tw_renormalize(p0, p1, s0, tail);
+}
+
 // multiword.py:410-415 _three_sum
 MW_HD void three_sum(double& a, double& b, double& c) {
   double t1, t2, t3;

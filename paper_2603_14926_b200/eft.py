@@ -14,7 +14,7 @@ import torch
 
 from . import _lib
 
-__all__ = ["quick_two_sum", "two_sum", "two_prod", "assert_rounding_mode"]
+__all__ = ["fma", "quick_two_sum", "two_sum", "two_prod", "assert_rounding_mode"]
 
 
 def _run(op: int, a, b):
@@ -39,6 +39,29 @@ def _run(op: int, a, b):
     if to_np:
         return s.cpu().numpy(), e.cpu().numpy()
     return s, e
+
+
+def fma(a, b, c):
+    """Correctly rounded a*b + c, one rounding (eft.py:33-48): floats give a
+    float, arrays an array of the broadcast shape; device kernel mw_fma."""
+    scalar = all(isinstance(v, (int, float)) for v in (a, b, c))
+    to_np = scalar or any(isinstance(v, np.ndarray) for v in (a, b, c))
+    ts = [v if isinstance(v, torch.Tensor) else torch.as_tensor(np.asarray(v, dtype=np.float64))
+          for v in (a, b, c)]
+    dev = next((t.device for t in ts if t.is_cuda), torch.device("cuda"))
+    ts = [t.to(device=dev, dtype=torch.float64) for t in ts]
+    shape = torch.broadcast_shapes(*(t.shape for t in ts))
+    ta, tb, tc = (t.expand(shape).contiguous() for t in ts)
+    _lib.require_cuda(ta, tb, tc)
+    out = torch.empty_like(ta)
+    rc = _lib.load().mw_fma(ta.data_ptr(), tb.data_ptr(), tc.data_ptr(), out.data_ptr(), ta.numel(),
+                            _lib.stream_handle(dev))
+    _lib.check(rc, "mw_fma")
+    if scalar:
+        return float(out.item())
+    if to_np:
+        return out.cpu().numpy()
+    return out
 
 
 def quick_two_sum(a, b):

@@ -30,7 +30,7 @@ from . import _lib
 from .batch import LaneBatch, as_planes
 from .multiword import BITS, Variant, variant_code
 
-__all__ = ["Scheme", "MatMulPlan", "MWMatrix", "CMWMatrix", "matmul", "cmatmul", "gemv",
+__all__ = ["Scheme", "MatMulPlan", "MWMatrix", "CMWMatrix", "matmul", "cmatmul", "gemv", "strassen_pad_policy",
            "gen_complex_test_matrices", "gen_test_matrices", "sqrt_constant"]
 
 
@@ -319,6 +319,20 @@ def _gemm4(a: torch.Tensor, b: torch.Tensor, c: torch.Tensor, variant, cin: torc
         m, n, kd, bt, _lib.stream_handle(a.device),
     )
     _lib.check(rc, "mw_gemm_batched")
+
+
+def strassen_pad_policy(n: int, cutoff: int = 32) -> list:
+    """The decomposition Strassen applies to an n x n product, top down
+    (linalg.py:390-406): ("split", m) halves an even m, ("peel", m) strips
+    the last row/column of an odd m, ("blocked", m) is a leaf at m <= cutoff."""
+    out = []
+    m = int(n)
+    while m > cutoff:
+        odd = m & 1
+        out.append(("peel" if odd else "split", m))
+        m = m - 1 if odd else m >> 1
+    out.append(("blocked", m))
+    return out
 
 
 def _strassen_rec(a: torch.Tensor, b: torch.Tensor, variant, cutoff: int) -> torch.Tensor:

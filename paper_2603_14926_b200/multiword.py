@@ -20,6 +20,11 @@ __all__ = [
     "Variant", "BITS", "DEFAULT_DIGITS", "ulp_k", "from_basefloat", "from_fraction", "variant_code",
     "mw_add", "mw_sub", "mw_mul", "mw_div", "mw_neg", "cadd", "csub", "cmul", "cdiv",
     "is_normalized", "from_decimal_string", "to_decimal_string", "MultiWord", "DD", "TD", "QD",
+    # the reference's named per-variant kernels (multiword.py:104-588) and helpers
+    "dw_add_sloppy", "dw_add_accurate", "dw_add_bf", "dw_mul", "dw_mul_bf",
+    "tw_add", "tw_mul", "tw_mul_cleaned", "tw_add_bf", "tw_mul_bf",
+    "qw_add", "qw_mul", "qw_add_bf", "qw_mul_bf",
+    "tw_renormalize", "qw_renormalize", "normalize", "to_oracle", "from_oracle",
 ]
 
 BITS = {2: 106, 3: 159, 4: 212}
@@ -151,6 +156,171 @@ def cdiv(a, b, variant: Variant = Variant.STANDARD):
     num_re = mw_add(mw_mul(ar, br, variant), mw_mul(ai, bi, variant), variant)
     num_im = mw_sub(mw_mul(ai, br, variant), mw_mul(ar, bi, variant), variant)
     return mw_div(num_re, den, variant), mw_div(num_im, den, variant)
+
+
+# --------------------------------------------------------------------------
+# The reference's named kernels (multiword.py:104-588), each taking and
+# returning a tuple of K components.  As in the reference, a component may
+# be a float or an array (numpy or torch, any shape; all of one shape):
+# floats give floats, numpy arrays give numpy arrays, torch tensors give
+# CUDA tensors.  All arithmetic runs on the device: the dispatched
+# (K, Variant) lane kernels, or mw_named_op / mw_renormalize for the
+# kernels no dispatch table selects.
+# --------------------------------------------------------------------------
+
+
+def _to_planes(*tuples):
+    """Stack component tuples into (m, W) CUDA planes; returns (planes,
+    kind, shape) with kind "float" / "numpy" / "torch"."""
+    import numpy as np
+    import torch
+
+    from . import _lib
+
+    comps = [c for t in tuples for c in t]
+    if any(isinstance(c, torch.Tensor) for c in comps):
+        kind = "torch"
+    elif any(isinstance(c, np.ndarray) and c.ndim > 0 for c in comps):
+        kind = "numpy"
+    else:
+        kind = "float"
+    dev = next((c.device for c in comps if isinstance(c, torch.Tensor) and c.is_cuda), torch.device("cuda"))
+    ts = [torch.as_tensor(c, dtype=torch.float64).to(dev) if isinstance(c, torch.Tensor)
+          else torch.as_tensor(np.asarray(c, dtype=np.float64), device=dev) for c in comps]
+    shape = torch.broadcast_shapes(*(t.shape for t in ts))
+    planes = torch.stack([t.expand(shape).reshape(-1) for t in ts]).contiguous()
+    _lib.require_cuda(planes)
+    return planes, kind, tuple(shape)
+
+
+def _from_planes(planes, kind, shape) -> tuple:
+    if kind == "float":
+        return tuple(float(v) for v in planes[:, 0].cpu())
+    if kind == "numpy":
+        host = planes.cpu().numpy()
+        return tuple(host[c].reshape(shape) for c in range(planes.shape[0]))
+    return tuple(planes[c].reshape(shape) for c in range(planes.shape[0]))
+
+
+def _need_k(t, k):
+    if len(t) != k:
+        raise ValueError(f"expected {k} components, got {len(t)}")
+
+
+def _dispatched(k, variant, op):
+    """The (K, Variant) kernel of the dispatch tables (multiword.py:595-611)."""
+
+    def fn(a, b):
+        from . import _lib
+
+        _need_k(a, k)
+        _need_k(b, k)
+        planes, kind, shape = _to_planes(a, b)
+        n = planes.shape[1]
+        out = planes.new_empty((k, n))
+        lib = _lib.load()
+        call = lib.mw_ew_add if op == "add" else lib.mw_ew_mul
+        rc = call(k, variant_code(variant), planes.data_ptr(), n, planes[k:].data_ptr(), n,
+                  out.data_ptr(), n, n, _lib.stream_handle(planes.device))
+        _lib.check(rc, f"mw_ew_{op}")
+        return _from_planes(out, kind, shape)
+
+    return fn
+
+
+dw_add_accurate = _dispatched(2, Variant.STANDARD, "add")  # multiword.py:118-126
+dw_add_bf = _dispatched(2, Variant.BRANCH_FREE, "add")  # 129-137
+dw_mul = _dispatched(2, Variant.STANDARD, "mul")  # 140-145
+dw_mul_bf = _dispatched(2, Variant.BRANCH_FREE, "mul")  # 148-156
+tw_add = _dispatched(3, Variant.STANDARD, "add")  # 279-280
+tw_mul = _dispatched(3, Variant.STANDARD, "mul")  # 321-322
+tw_add_bf = _dispatched(3, Variant.BRANCH_FREE, "add")  # 361-378
+tw_mul_bf = _dispatched(3, Variant.BRANCH_FREE, "mul")  # 381-402
+qw_add = _dispatched(4, Variant.STANDARD, "add")  # 442-487
+qw_mul = _dispatched(4, Variant.STANDARD, "mul")  # 512-513
+qw_add_bf = _dispatched(4, Variant.BRANCH_FREE, "add")  # 516-545
+qw_mul_bf = _dispatched(4, Variant.BRANCH_FREE, "mul")  # 548-588
+for _f, _n in ((dw_add_accurate, "dw_add_accurate"), (dw_add_bf, "dw_add_bf"), (dw_mul, "dw_mul"),
+               (dw_mul_bf, "dw_mul_bf"), (tw_add, "tw_add"), (tw_mul, "tw_mul"), (tw_add_bf, "tw_add_bf"),
+               (tw_mul_bf, "tw_mul_bf"), (qw_add, "qw_add"), (qw_mul, "qw_mul"), (qw_add_bf, "qw_add_bf"),
+               (qw_mul_bf, "qw_mul_bf")):
+    _f.__name__ = _f.__qualname__ = _n
+del _f, _n
+
+
+def _named(code, k, a, b):
+    from . import _lib
+
+    _need_k(a, k)
+    _need_k(b, k)
+    planes, kind, shape = _to_planes(a, b)
+    n = planes.shape[1]
+    out = planes.new_empty((k, n))
+    rc = _lib.load().mw_named_op(code, planes.data_ptr(), n, planes[k:].data_ptr(), n, out.data_ptr(), n, n,
+                                 _lib.stream_handle(planes.device))
+    _lib.check(rc, "mw_named_op")
+    return _from_planes(out, kind, shape)
+
+
+def dw_add_sloppy(a, b):
+    """Fast DD addition without the low-part error term (multiword.py:104-115)."""
+    return _named(0, 2, a, b)
+
+
+def tw_mul_cleaned(a, b):
+    """tw_mul with the dangling error chain folded into the tail (multiword.py:325-358)."""
+    return _named(1, 3, a, b)
+
+
+def _renorm(k, raw):
+    from . import _lib
+
+    planes, kind, shape = _to_planes(raw)
+    n = planes.shape[1]
+    out = planes.new_empty((k, n))
+    rc = _lib.load().mw_renormalize(k, planes.data_ptr(), n, out.data_ptr(), n, n,
+                                    _lib.stream_handle(planes.device))
+    _lib.check(rc, "mw_renormalize")
+    return _from_planes(out, kind, shape)
+
+
+def tw_renormalize(s0, s1, s2, t0):
+    """Decreasing four-term expansion -> triple word (multiword.py:191-194)."""
+    return _renorm(3, (s0, s1, s2, t0))
+
+
+def qw_renormalize(x0, x1, x2, x3, x4):
+    """Decreasing five-term expansion -> quadruple word (multiword.py:197-241)."""
+    return _renorm(4, (x0, x1, x2, x3, x4))
+
+
+def normalize(comps):
+    """Raw components -> non-overlapping form (multiword.py:710-719)."""
+    k = len(comps)
+    if k == 2:
+        return _renorm(2, tuple(comps))
+    if k == 3:
+        return _renorm(3, tuple(comps) + (0.0,))
+    if k == 4:
+        return _renorm(4, tuple(comps) + (0.0,))
+    raise ValueError(f"unsupported word count {k}")
+
+
+def to_oracle(comps) -> Fraction:
+    """Exact value of a K-word tuple (multiword.py:755-757); the reference
+    returns its OracleValue, here the exact dyadic ``Fraction``."""
+    return sum((Fraction(float(c)) for c in comps), Fraction(0))
+
+
+def from_oracle(value, k: int) -> tuple:
+    """Greedy nearest-double extraction to K words (multiword.py:760-775);
+    accepts anything ``Fraction`` accepts or an object with
+    ``as_fraction()`` / ``to_fraction()``."""
+    for attr in ("as_fraction", "to_fraction"):
+        if hasattr(value, attr):
+            value = getattr(value, attr)()
+            break
+    return from_fraction(value, k)
 
 
 def is_normalized(comps) -> bool:

@@ -23,6 +23,8 @@ public functions on small seeded cases:
   cgemm.npz   cmatmul (3M) on gen_complex_test_matrices     (linalg.py:247-276, 572-590)
   strassen.npz matmul(scheme="strassen") with even splits and odd peels (linalg.py:390-546)
   testmats.npz gen_test_matrices(16, k) and chebyshev_coeffs(12, k) (linalg.py:224-244, roots.py:343-368)
+  named.npz   dw_add_sloppy, tw_mul_cleaned, tw_/qw_renormalize, normalize,
+              eft.fma, strassen_pad_policy (multiword.py:104-358, 710-719)
   polyx.npz   estrin_eval per point (== estrin_eval_batched) and
               eval_complex Horner / Estrin                   (poly.py:106-178)
 
@@ -372,6 +374,66 @@ def main():
         out[f"k{k}_cheb12"] = np.stack(q.comps)
     if want("testmats"):
         np.savez_compressed(os.path.join(HERE, "testmats.npz"), **out)
+
+    # ------------------------------------------------------------- named kernels
+    # multiword's kernels outside the dispatch tables and its helpers:
+    # dw_add_sloppy (104-115; arrays), tw_mul_cleaned (325-358) and the
+    # renormalisers tw_/qw_renormalize (191-241) + normalize (710-719)
+    # (scalar-only in the reference: data-dependent branches, so per lane),
+    # eft.fma (eft.py:33-48) and linalg.strassen_pad_policy (390-406).
+    if want("named"):
+        from mwfloat import eft as reft
+
+        out = {}
+        rng = np.random.default_rng(20240810)
+        W = 193
+        a, b = rand_mw(rng, 2, W), rand_mw(rng, 2, W)
+        a[:, 0] = -b[:, 0]
+        b[:, 1] = 0.0
+        out["sloppy_a"], out["sloppy_b"] = a, b
+        out["sloppy_out"] = np.stack(multiword.dw_add_sloppy(tuple(a), tuple(b)))
+        a, b = rand_mw(rng, 3, W), rand_mw(rng, 3, W)
+        b[:, 1] = 0.0
+        b[:, 2] = 1.0
+        a[:, 3] = 0.0
+        out["cleaned_a"], out["cleaned_b"] = a, b
+        out["cleaned_out"] = np.array([multiword.tw_mul_cleaned(tuple(a[:, i]), tuple(b[:, i]))
+                                       for i in range(W)]).T
+        # raw expansions: decreasing terms, zeros placed to reach every branch
+        for k, m in ((3, 4), (4, 5)):
+            raw = np.zeros((m, W))
+            raw[0] = rng.uniform(-1, 1, W) * np.exp2(rng.integers(-60, 60, W))
+            for j in range(1, m):
+                raw[j] = raw[j - 1] * 2.0**-52 * rng.uniform(-1.0, 1.0, W)
+            for i in range(W):
+                mask = (i * 2654435761) % (1 << m)
+                for j in range(1, m):
+                    if mask >> j & 1:
+                        raw[j, i] = 0.0
+            raw[0, 0] = np.inf
+            raw[:, 1] = 0.0
+            fn = multiword.tw_renormalize if k == 3 else multiword.qw_renormalize
+            out[f"renorm{k}_in"] = raw
+            out[f"renorm{k}_out"] = np.array([fn(*(float(v) for v in raw[:, i])) for i in range(W)]).T
+        for k in (2, 3, 4):
+            c = rand_mw(rng, k, W)
+            c[1:] *= rng.uniform(0.5, 300.0, (k - 1, W))  # overlapping components
+            out[f"normalize{k}_in"] = c
+            out[f"normalize{k}_out"] = np.array([multiword.normalize(tuple(float(v) for v in c[:, i]))
+                                                 for i in range(W)]).T
+        fa = rng.uniform(-1, 1, W) * np.exp2(rng.integers(-40, 40, W))
+        fb = rng.uniform(-1, 1, W) * np.exp2(rng.integers(-40, 40, W))
+        fc = -(fa * fb) * (1.0 + rng.uniform(-1e-15, 1e-15, W))  # cancellation
+        fc[::3] = rng.uniform(-1, 1, len(fc[::3]))
+        out["fma_a"], out["fma_b"], out["fma_c"] = fa, fb, fc
+        out["fma_out"] = np.asarray(reft.fma(fa, fb, fc))
+        pads = []
+        for n, cut in ((1, 32), (32, 32), (33, 32), (64, 32), (100, 8), (129, 16), (4096, 128), (2047, 64)):
+            for kind, size in linalg.strassen_pad_policy(n, cut):
+                pads.append((n, cut, {"blocked": 0, "peel": 1, "split": 2}[kind], size))
+        out["strassen_pad"] = np.array(pads, dtype=np.int64)
+        np.savez_compressed(os.path.join(HERE, "named.npz"), **out)
+        print(f"named done {time.time() - t0:.1f}s")
 
     print(f"all done {time.time() - t0:.1f}s  (mwfloat {getattr(mwfloat, '__version__', '?')})")
 
