@@ -7,6 +7,7 @@
 #include "gemv_staged.cuh"
 #include "gemv_bulk.cuh"
 #include "gemv_probe.cuh"
+#include "gemv_wring.cuh"
 
 namespace mw {
 #define CFGV(NAME, bm, bn, bk, tm, tn, minb, vec)                             \
@@ -131,6 +132,19 @@ static int gemv_rt_launch(const double* A, const double* x, double* y, int64_t m
       A, n, m * n, x, n, y, m, m, n);
   return launch_status();
 }
+template <int K, int Q, int J, int S>
+static int gemv_wring_launch(const double* A, const double* x, double* y, int64_t m, int64_t n,
+                             cudaStream_t st) {
+  if (n % (128 * J)) return MW_ERR_INVALID;
+  const size_t smem = gemv_wring_smem<K, Q, J, S>();
+  if (smem > 227 * 1024) return MW_ERR_INVALID;
+  auto kern = gemv_wring_kernel<K, BRANCH_FREE, Q, J, S>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int grid = sm_count();
+  if ((int64_t)grid * Q > m) grid = (int)((m + Q - 1) / Q);
+  kern<<<grid, 128 * Q, smem, st>>>(A, n, m * n, x, n, y, m, m, n);
+  return launch_status();
+}
 template <int K>
 static int gemv_run(int cfg, const double* A, const double* x, double* y, int64_t m, int64_t n,
                     cudaStream_t st) {
@@ -173,10 +187,17 @@ static int gemv_run(int cfg, const double* A, const double* x, double* y, int64_
     case 35: return gemv_rt_launch<K, 1, 2, true, 8>(A, x, y, m, n, st);
     case 36: return gemv_rt_launch<K, 2, 2, true, 4>(A, x, y, m, n, st);
     case 37: return gemv_rt_launch<K, 1, 1, true, 12>(A, x, y, m, n, st);
+    case 38: return gemv_wring_launch<K, 8, 2, 4>(A, x, y, m, n, st);
+    case 39: return gemv_wring_launch<K, 8, 2, 3>(A, x, y, m, n, st);
+    case 40: return gemv_wring_launch<K, 6, 2, 4>(A, x, y, m, n, st);
+    case 41: return gemv_wring_launch<K, 6, 4, 2>(A, x, y, m, n, st);
+    case 42: return gemv_wring_launch<K, 4, 4, 3>(A, x, y, m, n, st);
+    case 43: return gemv_wring_launch<K, 8, 1, 6>(A, x, y, m, n, st);
+    case 44: return gemv_wring_launch<K, 6, 2, 3>(A, x, y, m, n, st);
     default: return MW_ERR_INVALID;
   }
 }
-extern "C" int mwt_gemv_num_configs(void) { return 38; }
+extern "C" int mwt_gemv_num_configs(void) { return 45; }
 extern "C" const char* mwt_gemv_config_name(int cfg) {
   static const char* names[] = {"W4_R2_D4", "W1_R8_D8", "W1_R8_D4", "W2_R4_D4", "W2_R4_D8",
                                 "W4_R2_D2", "W4_R1_D4", "W8_R1_D2", "st_R2_D4_S2", "st_R2_D4_S3",
@@ -185,8 +206,10 @@ extern "C" const char* mwt_gemv_config_name(int cfg) {
                                 "bk_G8_C256_S2", "bk_G6_C256_S3", "bk_G4_C512_S2", "bk_G8_C128_S3",
                                 "bk_G6_C256_S2", "bk_G4_C256_S3", "bk_G5_C256_S2", "bk_G7_C128_S4", "probe_fp64", "probe_mem",
                                 "rt1_D4", "rt1_D2_P", "rt1_D4_P", "rt2_D2", "rt2_D4", "rt2_D2_P",
-                                "rt2_D1_P", "rt1_D2_P_b8", "rt2_D2_P_b4", "rt1_D1_P_b12"};
-  return (cfg >= 0 && cfg < 38) ? names[cfg] : "?";
+                                "rt2_D1_P", "rt1_D2_P_b8", "rt2_D2_P_b4", "rt1_D1_P_b12",
+                                "wr_Q8_J2_S4", "wr_Q8_J2_S3", "wr_Q6_J2_S4", "wr_Q6_J4_S2", "wr_Q4_J4_S3",
+                                "wr_Q8_J1_S6", "wr_Q6_J2_S3"};
+  return (cfg >= 0 && cfg < 45) ? names[cfg] : "?";
 }
 extern "C" int mwt_gemv(int cfg, int k, const double* A, const double* x, double* y, int64_t m,
                         int64_t n, void* stream) {
