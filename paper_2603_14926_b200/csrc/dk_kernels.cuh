@@ -940,11 +940,13 @@ static int dk_treem_launch(const double* coeffs, int64_t sc, int64_t n, const do
   const int64_t cnt = i1 - i0;
   const size_t smem = dk_treem_smem<K>(R);
   auto kern = dk_treem_kernel<K, VAR, R, PEER>;
-  static bool attr_set = false;  // per instantiation
-  if (!attr_set) {
+  static bool attr_set[64] = {false};  // per instantiation and device
+  int dev = -1;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64 || !attr_set[dev]) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return (int)e;
-    attr_set = true;
+    if (dev >= 0 && dev < 64) attr_set[dev] = true;
   }
   const unsigned grid = (unsigned)((cnt + R - 1) / R);
   cudaLaunchConfig_t cfg = {};
