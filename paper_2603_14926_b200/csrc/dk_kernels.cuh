@@ -717,6 +717,22 @@ __device__ __forceinline__ Cx<K, VAR> cx_get(const double* base, int idx) {
 template <int R>
 __host__ __device__ constexpr int dk_treem_warps() { return R == 1 ? 6 : 5 * R; }
 
+// Phase timestamps for the tuning harness only (csrc/tune/dk_phase.cu
+// defines MW_DK_PROFILE); compiled out of the product.
+#ifdef MW_DK_PROFILE
+__device__ unsigned long long g_dk_prof[4096][12];
+#define MW_DK_MARK(slot)                                                              \
+  do {                                                                                \
+    unsigned long long t_;                                                            \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                            \
+    if (blockIdx.x < 4096) g_dk_prof[blockIdx.x][slot] = t_;                          \
+  } while (0)
+#else
+#define MW_DK_MARK(slot) \
+  do {                   \
+  } while (0)
+#endif
+
 template <int K, int VAR, int R, bool PEER = false>
 __global__ void __launch_bounds__(32 * dk_treem_warps<R>(), R == 2 ? 2 : 1)
     dk_treem_kernel(const double* __restrict__ coeffs, int64_t sc, int64_t n,
@@ -738,6 +754,7 @@ __global__ void __launch_bounds__(32 * dk_treem_warps<R>(), R == 2 ? 2 : 1)
   const int v32 = (int)(valid < 32 ? valid : 32);
   const int b32 = (int)(nblocks < 32 ? nblocks : 32);
   const int64_t rbase = i0 + (int64_t)blockIdx.x * R;
+  if (threadIdx.x == 0) MW_DK_MARK(0);
 
   if (warp < 2 * R) {
     // ---- denominator partial u = lane + 32h of root r
@@ -762,6 +779,7 @@ __global__ void __launch_bounds__(32 * dk_treem_warps<R>(), R == 2 ? 2 : 1)
       }
     }
     cx_put<K, VAR>(den_s + (size_t)r * 2 * K * 64, u, v);
+    if (threadIdx.x == 0) MW_DK_MARK(1);
   } else if (warp < 4 * R) {
     // ---- numerator block u = lane + 32h of root r (Horner from its top)
     const int r = (warp - 2 * R) >> 1, h = warp & 1;
@@ -784,11 +802,13 @@ __global__ void __launch_bounds__(32 * dk_treem_warps<R>(), R == 2 ? 2 : 1)
       }
     }
     cx_put<K, VAR>(num_s + (size_t)r * 2 * K * 64, u, p);
+    if (threadIdx.x == 64 * R) MW_DK_MARK(2);
   } else if (warp < 5 * R) {
     // ---- powers of root r: x_l = w^l (Hillis-Steele scan), x_l * w^32
     const int r = warp - 4 * R;
     const int64_t i = rbase + r;
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (threadIdx.x == 128 * R) MW_DK_MARK(3);
     Cx<K, VAR> w = c_one<K, VAR>(), w32 = c_one<K, VAR>();
     if (i < i1) {
       const int64_t q = i - i0;
@@ -810,6 +830,7 @@ __global__ void __launch_bounds__(32 * dk_treem_warps<R>(), R == 2 ? 2 : 1)
       w32 = cx_get<K, VAR>(pw + (size_t)R * 2 * 2 * K * 32 + (size_t)r * 2 * K * 64, 0);
     }
     const Cx<K, VAR> xh = c_mul_ol(x, w32);
+    if (threadIdx.x == 128 * R) MW_DK_MARK(4);
     double* pr = pw + (size_t)r * 2 * 2 * K * 32;
 #pragma unroll
     for (int c = 0; c < K; ++c) {
@@ -836,6 +857,7 @@ __global__ void __launch_bounds__(32 * dk_treem_warps<R>(), R == 2 ? 2 : 1)
   }
   __syncthreads();
 
+  if (threadIdx.x == 0) MW_DK_MARK(5);
   // t_u = p_u * x_u (numerator warps); denominator level A (v_l * v_{l+32})
   if (warp < 2 * R) {
     const int tau = threadIdx.x;  // < 64R: first 32R threads act
@@ -861,6 +883,7 @@ __global__ void __launch_bounds__(32 * dk_treem_warps<R>(), R == 2 ? 2 : 1)
   }
   __syncthreads();
 
+  if (threadIdx.x == 0) MW_DK_MARK(6);
   // Level by level: the numerator runs level lev (A, 1, 2, 4, 8, 16), the
   // denominator one level ahead (1, 2, 4, 8, 16).
 #pragma unroll 1
@@ -906,6 +929,7 @@ __global__ void __launch_bounds__(32 * dk_treem_warps<R>(), R == 2 ? 2 : 1)
     __syncthreads();
   }
 
+  if (threadIdx.x == 0) MW_DK_MARK(7);
   if (warp == 2 * R) {
     if (lane < R) {
       const int64_t i = rbase + lane;
@@ -918,6 +942,7 @@ __global__ void __launch_bounds__(32 * dk_treem_warps<R>(), R == 2 ? 2 : 1)
         dk_tail<K, VAR, PEER>(acc, den, z, zre_out, zim_out, so, step_mag, i, &peers);
       }
     }
+    if (lane == 0) MW_DK_MARK(8);
     if constexpr (PEER) {
       __syncwarp();
       if (lane == 0) dk_peer_ticket(peers);
