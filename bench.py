@@ -658,6 +658,41 @@ def secondary(args, torch, dist, mw, world, rank, peak):
                 "note": "bit-exact with the reference's matmul(scheme='strassen') at this cutoff"}
             del A, B
 
+    # ---- the paper's comparisons on the GPU (1 GPU): branch-free vs
+    # Standard (renormalising, per-lane branches) kernels, and Horner vs
+    # Estrin (§4.1).  Same generators, smaller sizes; both variants
+    # are bit-exact with the reference's own kernels.
+    if world == 1 and not args.quick:
+        from paper_2603_14926_b200.linalg import gemm_into
+        from paper_2603_14926_b200.poly import horner_into
+
+        STD = mw.Variant.STANDARD
+        cmp = {}
+        for k in (2, 3, 4):
+            a, b = gen.config3_gemm(k, 1024)
+            A, B = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+            C = torch.empty_like(A)
+            ms_bf = timed(lambda: gemm_into(A, B, C, BF), 3)
+            ms_std = timed(lambda: gemm_into(A, B, C, STD), 3)
+            cmp[f"gemm_{['', '', 'dd', 'td', 'qd'][k]}_n1024"] = {
+                "bf_ms": round(ms_bf, 3), "std_ms": round(ms_std, 3), "bf_speedup": round(ms_std / ms_bf, 3)}
+            del A, B, C
+        coeffs4, x4 = gen.config4_horner(npts=1 << 20)
+        c4, xd4 = torch.from_numpy(coeffs4).cuda(), torch.from_numpy(x4).cuda()
+        y4 = torch.empty_like(xd4)
+        ms_bf = timed(lambda: horner_into(c4, xd4, y4, BF), 3)
+        ms_std = timed(lambda: horner_into(c4, xd4, y4, STD), 3)
+        cmp["horner_qd_deg1024_pts2p20"] = {
+            "bf_ms": round(ms_bf, 3), "std_ms": round(ms_std, 3), "bf_speedup": round(ms_std / ms_bf, 3)}
+        P4, X4 = mw.MWPolynomial(c4), mw.LaneBatch(xd4)
+        ms_est = timed(lambda: mw.estrin_eval_batched(P4, X4, BF), 3)
+        cmp["estrin_vs_horner_qd_deg1024_pts2p20"] = {
+            "horner_ms": round(ms_bf, 3), "estrin_ms": round(ms_est, 3),
+            "estrin_over_horner": round(ms_est / ms_bf, 3),
+            "note": "Estrin executes extra squarings; Horner keeps the FP64 pipe full with 2 chains per thread"}
+        out["paper_comparisons"] = cmp
+        del c4, xd4, y4, P4, X4
+
     # ---- config 5: DK, n = 512, 200 sweeps (near-root init)
     for k in (3, 4):
         coeffs = torch.from_numpy(gen.config5_poly(k)).cuda()
