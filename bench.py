@@ -421,7 +421,10 @@ def run_ours(args):
 
     sec = None
     if not args.no_secondary:
-        sec = secondary(args, torch, dist, mw, world, rank, peak)
+        try:
+            sec = secondary(args, torch, dist, mw, world, rank, peak)
+        except Exception as e:  # reported in the line; the headline stands on its own
+            sec = {"error": f"{type(e).__name__}: {e}"[:300]}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
