@@ -727,6 +727,32 @@ def test_no_out_of_bounds_writes(k):
                                flag.data_ptr(), exact, st) == 0
     torch.cuda.synchronize()
     assert _guards_intact(fre, g2, nr) and _guards_intact(fim, g2, nr) and _guards_intact(mag, gm, nr)
+    # tree sweeps with a workspace: every roots-per-CTA form, ragged last CTA
+    i0, i1 = 3, 37  # 34 roots: 4 per CTA leaves 2 in the last
+    try:
+        for roots in (0, 1, 2, 4):
+            assert lib.mw_dk_tree_set_roots_per_cta(roots) == 0
+            wsn = lib.mw_dk_sweep_workspace(k, i0, i1)
+            wsf, gw, _ = _guarded((1, wsn))
+            assert lib.mw_dk_sweep_ws(k, 1, coeffs.data_ptr(), nr, nr, zr_t.data_ptr(), zi_t.data_ptr(), nr, i0,
+                                      i1, fre.data_ptr() + g2 * 8, fim.data_ptr() + g2 * 8, ps2,
+                                      mag.data_ptr() + gm * 8, flag.data_ptr(), 0, wsf.data_ptr() + gw * 8,
+                                      st) == 0
+            torch.cuda.synchronize()
+            assert _guards_intact(fre, g2, nr) and _guards_intact(fim, g2, nr) and _guards_intact(mag, gm, nr)
+            assert _guards_intact(wsf, gw, wsn)
+    finally:
+        lib.mw_dk_tree_set_roots_per_cta(-1)
+    # kernels outside the dispatch tables, renormalisation, fma
+    full, g, ps = _guarded((k, w))
+    if k in (2, 3):
+        xs = torch.from_numpy(gen.g_k(rng, k, w)).cuda()
+        assert lib.mw_named_op(k - 2, xs.data_ptr(), w, xs.data_ptr(), w, full.data_ptr() + g * 8, ps, w, st) == 0
+    raw = torch.from_numpy(gen.g_k(rng, {2: 2, 3: 4, 4: 5}[k], w)).cuda()
+    assert lib.mw_renormalize(k, raw.data_ptr(), w, full.data_ptr() + g * 8, ps, w, st) == 0
+    assert lib.mw_fma(x.data_ptr(), x.data_ptr(), x.data_ptr(), full.data_ptr() + g * 8, w, st) == 0
+    torch.cuda.synchronize()
+    assert _guards_intact(full, g, w)
 
 
 @pytest.mark.parametrize("k", [2, 3, 4])
