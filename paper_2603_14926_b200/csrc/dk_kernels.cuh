@@ -733,6 +733,57 @@ __device__ unsigned long long g_dk_prof[4096][12];
   } while (0)
 #endif
 
+// One denominator tree level (stride s over 32 values per root) on the
+// 2R denominator warps with THREE lanes per complex product: lane roles
+// 0 / 1 / 2 hold p1 = a.re b.re, p2 = a.im b.im, p3 = (a.re + a.im)(b.re +
+// b.im) of multiword.cmul (683-692); roles 0 and 1 first form the two sums
+// in one SIMD add, then the three products are one SIMD mul, then role 0
+// forms re = p1 - p2 while role 1 forms p3 - p1 (one SIMD add) and then
+// (p3 - p1) - p2.  The same operations on the same operands as c_mul, so
+// the same bits, with about half the instructions a warp issues per level
+// (a level's few products are latency/issue bound on one warp each).
+template <int K, int VAR>
+__device__ __forceinline__ V<K> shfl_v(const V<K>& v, int src) {
+  V<K> r;
+#pragma unroll
+  for (int c = 0; c < K; ++c) r.c[c] = __shfl_sync(0xffffffffu, v.c[c], src);
+  return r;
+}
+template <int K>
+__device__ __forceinline__ V<K> sel(bool t, const V<K>& a, const V<K>& b) {
+  V<K> r;
+#pragma unroll
+  for (int c = 0; c < K; ++c) r.c[c] = t ? a.c[c] : b.c[c];
+  return r;
+}
+template <int K, int VAR, int R>
+__device__ __forceinline__ void dk_den_level_split(double* den_s, int s, int v32) {
+  using O = Ops<K, VAR>;
+  const int lane = threadIdx.x & 31, wd = threadIdx.x >> 5;  // wd < 2R
+  const int per = 16 / s;                                    // pairs per root
+  const int pair = wd * 10 + lane / 3, role = lane % 3;
+  const bool have = lane < 30 && pair < R * per;
+  const int r = have ? pair / per : 0;
+  const int idx = have ? 2 * s * (pair % per) : 0;
+  const bool act = have && idx + s < v32;
+  double* b = den_s + (size_t)r * 2 * K * 64;
+  const Cx<K, VAR> x = cx_get<K, VAR>(b, idx), y = cx_get<K, VAR>(b, idx + s);
+  // roles 0 / 1: x.re + x.im and y.re + y.im
+  const V<K> sum = O::add(sel<K>(role == 0, x.re, y.re), sel<K>(role == 0, x.im, y.im));
+  const V<K> sa = shfl_v<K, VAR>(sum, lane - 2), sb = shfl_v<K, VAR>(sum, lane - 1);
+  // roles 0 / 1 / 2: p1 / p2 / p3
+  const V<K> p = O::mul(role == 2 ? sa : sel<K>(role == 0, x.re, x.im),
+                        role == 2 ? sb : sel<K>(role == 0, y.re, y.im));
+  const V<K> nxt = shfl_v<K, VAR>(p, lane + 1), prv = shfl_v<K, VAR>(p, lane - 1);
+  // role 0: re = p1 - p2 (p2 from lane + 1); role 1: p3 - p1 (p3 from lane + 1, p1 from lane - 1)
+  V<K> q = O::add(sel<K>(role == 0, p, nxt), neg(sel<K>(role == 0, nxt, prv)));
+  if (role == 1) q = O::add(q, neg(p));  // (p3 - p1) - p2
+  if (act && role < 2) {
+#pragma unroll
+    for (int c = 0; c < K; ++c) b[(role * K + c) * 64 + idx] = q.c[c];
+  }
+}
+
 template <int K, int VAR, int R, bool PEER = false>
 __global__ void __launch_bounds__(32 * dk_treem_warps<R>(), R == 2 ? 2 : 1)
     dk_treem_kernel(const double* __restrict__ coeffs, int64_t sc, int64_t n,
@@ -891,12 +942,18 @@ __global__ void __launch_bounds__(32 * dk_treem_warps<R>(), R == 2 ? 2 : 1)
     if (warp < 2 * R) {
       if (lev < 5) {
         const int s = 1 << lev, per = 16 >> lev;  // pairs per root
-        const int tau = threadIdx.x;
-        if (tau < R * per) {
-          const int r = tau / per, idx = 2 * s * (tau % per);
-          if (idx + s < v32) {
-            double* b = den_s + (size_t)r * 2 * K * 64;
-            cx_put<K, VAR>(b, idx, c_mul_ol(cx_get<K, VAR>(b, idx), cx_get<K, VAR>(b, idx + s)));
+        if constexpr (K == 4) {
+          // measured (scripts/dk_phases.py): QD trees 7.9 -> 6.1 us at 2 roots
+          // per CTA, 5.9 -> 5.0 at 1; TD does not gain (4.7 -> 5.5 at 4)
+          dk_den_level_split<K, VAR, R>(den_s, s, v32);
+        } else {
+          const int tau = threadIdx.x;
+          if (tau < R * per) {
+            const int r = tau / per, idx = 2 * s * (tau % per);
+            if (idx + s < v32) {
+              double* b = den_s + (size_t)r * 2 * K * 64;
+              cx_put<K, VAR>(b, idx, c_mul_ol(cx_get<K, VAR>(b, idx), cx_get<K, VAR>(b, idx + s)));
+            }
           }
         }
       }
