@@ -1,0 +1,8 @@
+// dk_tree_k3_std.cu — instantiates the tree-order DK sweep launchers for
+// K = 3, variant std (split out of dk.cu so the kernels compile in parallel).
+#include "dk_kernels.cuh"
+
+namespace mw {
+template MW_DK_LAUNCH_SIG(dk_tree_launch, 3, 0, false);
+template MW_DK_LAUNCH_SIG(dk_tree_launch, 3, 0, true);
+}  // namespace mw
