@@ -635,6 +635,8 @@ def secondary(args, torch, dist, mw, world, rank, peak):
             "ms": round(ms, 4), "G_MPops": round(2 * m * m / (ms / 1e3) / 1e9, 2),
             "fp64_frac": round(fp / (ms / 1e3) / peak["dfma"] / world, 4),
             "hbm_GBps": round(k * m * m * 8 / (ms / 1e3) / 1e9, 1), "order": "tree (128 partials per row)",
+            "fp64_bound_us": round(fp / peak["dfma"] / world * 1e6, 1),
+            "hbm_bound_us": round(k * m * m * 8 / hbm / world * 1e6, 1),
             "l2": "flushed before each call",
             "timing": "one call per CUDA-graph replay (device time, no host API gap); ms_eager = the same call launched eagerly through the Python API",
             "ms_eager": round(ms_eager, 4)}
