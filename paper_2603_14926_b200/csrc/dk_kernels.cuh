@@ -742,6 +742,9 @@ __device__ unsigned long long g_dk_prof[4096][12];
 // (p3 - p1) - p2.  The same operations on the same operands as c_mul, so
 // the same bits, with about half the instructions a warp issues per level
 // (a level's few products are latency/issue bound on one warp each).
+__device__ __forceinline__ void bar_sync_n(int id, int threads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
 template <int K, int VAR>
 __device__ __forceinline__ V<K> shfl_v(const V<K>& v, int src) {
   V<K> r;
@@ -935,29 +938,77 @@ __global__ void __launch_bounds__(32 * dk_treem_warps<R>(), R == 2 ? 2 : 1)
   __syncthreads();
 
   if (threadIdx.x == 0) MW_DK_MARK(6);
-  // Level by level: the numerator runs level lev (A, 1, 2, 4, 8, 16), the
-  // denominator one level ahead (1, 2, 4, 8, 16).
+  // The two trees run decoupled, each under its own named barrier (so the
+  // denominator's levels -- the longer path -- never wait for numerator
+  // levels): numerator warps the levels A, 1, 2, 4, 8, 16 (complex adds);
+  // denominator warps the levels 1..16 (level A is done above).  With >= 2
+  // roots per CTA each denominator level's products are split over three
+  // warp groups (roles p1 = a.re b.re, p2 = a.im b.im, p3 = (a.re + a.im)
+  // (b.re + b.im) of multiword.cmul, 683-692), then roles 0 / 1 form re =
+  // p1 - p2 and im = (p3 - p1) - p2: the ops and operands of c_mul, so the
+  // same bits, at about half a product's latency per level.  The powers
+  // area (free after the barrier above) holds the role products.
+  if (warp < 2 * R) {
 #pragma unroll 1
-  for (int lev = 0; lev < 6; ++lev) {
-    if (warp < 2 * R) {
-      if (lev < 5) {
-        const int s = 1 << lev, per = 16 >> lev;  // pairs per root
-        if constexpr (K == 4) {
-          // measured (scripts/dk_phases.py): QD trees 7.9 -> 6.1 us at 2 roots
-          // per CTA, 5.9 -> 5.0 at 1; TD does not gain (4.7 -> 5.5 at 4)
-          dk_den_level_split<K, VAR, R>(den_s, s, v32);
-        } else {
-          const int tau = threadIdx.x;
-          if (tau < R * per) {
-            const int r = tau / per, idx = 2 * s * (tau % per);
-            if (idx + s < v32) {
-              double* b = den_s + (size_t)r * 2 * K * 64;
-              cx_put<K, VAR>(b, idx, c_mul_ol(cx_get<K, VAR>(b, idx), cx_get<K, VAR>(b, idx + s)));
-            }
+    for (int lev = 0; lev < 5; ++lev) {
+      const int s = 1 << lev, per = 16 >> lev;  // pairs per root
+      if constexpr (R >= 2) {
+        const int pairs = R * per;
+        const int wpr = (pairs + 31) >> 5;  // warps per role (3 * wpr <= 2R)
+        const int role = warp / wpr;
+        const int pair = (warp % wpr) * 32 + lane;
+        int r = 0, idx = 0;
+        bool act = false;
+        if (role < 3 && pair < pairs) {
+          r = pair / per;
+          idx = 2 * s * (pair % per);
+          act = idx + s < v32;
+        }
+        double* b = den_s + (size_t)r * 2 * K * 64;
+        double* xs = pw;  // [3][K][64]
+        if (act) {
+          const Cx<K, VAR> a = cx_get<K, VAR>(b, idx), c = cx_get<K, VAR>(b, idx + s);
+          V<K> p;
+          if (role == 0)
+            p = O::mul(a.re, c.re);
+          else if (role == 1)
+            p = O::mul(a.im, c.im);
+          else
+            p = O::mul(O::add(a.re, a.im), O::add(c.re, c.im));
+#pragma unroll
+          for (int cc = 0; cc < K; ++cc) xs[(role * K + cc) * 64 + pair] = p.c[cc];
+        }
+        bar_sync_n(14, 64 * R);
+        if (act && role < 2) {
+          V<K> p1, p2, p3;
+#pragma unroll
+          for (int cc = 0; cc < K; ++cc) {
+            p1.c[cc] = xs[(0 * K + cc) * 64 + pair];
+            p2.c[cc] = xs[(1 * K + cc) * 64 + pair];
+            p3.c[cc] = xs[(2 * K + cc) * 64 + pair];
+          }
+          const V<K> q = role == 0 ? O::add(p1, neg(p2)) : O::add(O::add(p3, neg(p1)), neg(p2));
+#pragma unroll
+          for (int cc = 0; cc < K; ++cc) b[(role * K + cc) * 64 + idx] = q.c[cc];
+        }
+      } else if constexpr (K == 4) {
+        // one root: the three-lane split (QD trees 5.9 -> 5.0 us, measured)
+        dk_den_level_split<K, VAR, R>(den_s, s, v32);
+      } else {
+        const int tau = threadIdx.x;
+        if (tau < R * per) {
+          const int r = tau / per, idx = 2 * s * (tau % per);
+          if (idx + s < v32) {
+            double* b = den_s + (size_t)r * 2 * K * 64;
+            cx_put<K, VAR>(b, idx, c_mul_ol(cx_get<K, VAR>(b, idx), cx_get<K, VAR>(b, idx + s)));
           }
         }
       }
-    } else if (warp < 4 * R) {
+      bar_sync_n(14, 64 * R);
+    }
+  } else if (warp < 4 * R) {
+#pragma unroll 1
+    for (int lev = 0; lev < 6; ++lev) {
       const int tau = threadIdx.x - 64 * R;
       int r, idx, s, lim;
       bool act;
@@ -982,9 +1033,10 @@ __global__ void __launch_bounds__(32 * dk_treem_warps<R>(), R == 2 ? 2 : 1)
         a.im = O::add(a.im, o.im);
         cx_put<K, VAR>(b, idx, a);
       }
+      bar_sync_n(13, 64 * R);
     }
-    __syncthreads();
   }
+  __syncthreads();
 
   if (threadIdx.x == 0) MW_DK_MARK(7);
   if (warp == 2 * R) {
