@@ -100,7 +100,18 @@ def load() -> ctypes.CDLL:
     return _lib
 
 
+_raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+
+
 def stream_handle(device: torch.device | None = None) -> int:
+    """cudaStream_t of torch's current stream on ``device`` (as an int).
+    Uses torch's raw-handle accessor when present (no Stream object: this
+    is on every call's host path), else torch.cuda.current_stream."""
+    if _raw_stream is not None:
+        idx = getattr(device, "index", None)
+        if idx is None:
+            idx = torch.cuda.current_device()
+        return _raw_stream(idx)
     return torch.cuda.current_stream(device).cuda_stream
 
 

@@ -49,11 +49,11 @@ def _check_pair(x: LaneBatch, y: LaneBatch):
 _WS: dict = {}
 
 
-def _workspace(device, n: int) -> torch.Tensor:
+def _workspace(device, n: int, stream: int | None = None) -> torch.Tensor:
     """Zero-initialised dot workspace, cached per (device, stream) and grown
     on demand (the single-launch dot re-arms its ticket itself).  Calls on
     one stream are serialised, so reuse is safe."""
-    key = (str(device), torch.cuda.current_stream(device).cuda_stream)
+    key = (str(device), _lib.stream_handle(device) if stream is None else stream)
     ws = _WS.get(key)
     if ws is None or ws.numel() < max(n, 1):
         ws = torch.zeros(max(n, 1), dtype=torch.float64, device=device)
@@ -73,9 +73,9 @@ def dot_tensor(x: LaneBatch, y: LaneBatch, variant: Variant = Variant.BRANCH_FRE
     if out is None:
         out = torch.empty(k, dtype=torch.float64, device=x.device)
     wsn = lib.mw_dot_workspace(k, n) if o == _lib.ORDER_TREE else 0
-    ws = _workspace(x.device, wsn)
-    rc = lib.mw_dot(k, v, x.planes.data_ptr(), n, y.planes.data_ptr(), n, n, ws.data_ptr(), out.data_ptr(), o,
-                    _lib.stream_handle(x.device))
+    st = _lib.stream_handle(x.device)
+    ws = _workspace(x.device, wsn, st)
+    rc = lib.mw_dot(k, v, x.planes.data_ptr(), n, y.planes.data_ptr(), n, n, ws.data_ptr(), out.data_ptr(), o, st)
     _lib.check(rc, "mw_dot")
     return out
 
