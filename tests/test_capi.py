@@ -75,6 +75,18 @@ def test_other_entry_checks():
     assert lib.mw_dot(2, 1, p, 8, p, 8, 8, None, p, 9, None) == _lib.MW_ERR_INVALID
     assert lib.mw_dk_sweep(3, 1, p, 8, 8, p, p, 8, 4, 2, p, p, 8, p, p, 1, None) == _lib.MW_ERR_INVALID  # i1 < i0
     assert lib.mw_fp64_peak_kernel(0, 1, 512, 1, p, None) == _lib.MW_ERR_INVALID
+    # kernels outside the dispatch tables, renormalisation, fma, the tree-sweep knob
+    assert lib.mw_named_op(2, p, 8, p, 8, p, 8, 8, None) == _lib.MW_ERR_INVALID  # unknown op
+    assert lib.mw_named_op(0, p, 4, p, 8, p, 8, 8, None) == _lib.MW_ERR_INVALID  # plane stride < n
+    assert lib.mw_named_op(1, p, 8, p, 8, p, 8, 0, None) == _lib.MW_OK  # empty: nothing launched
+    assert lib.mw_renormalize(5, p, 8, p, 8, 8, None) == _lib.MW_ERR_INVALID
+    assert lib.mw_renormalize(3, None, 8, p, 8, 8, None) == _lib.MW_ERR_INVALID
+    assert lib.mw_fma(p, p, None, p, 8, None) == _lib.MW_ERR_INVALID
+    assert lib.mw_fma(p, p, p, p, -1, None) == _lib.MW_ERR_INVALID
+    for bad in (3, 5, -2):
+        assert lib.mw_dk_tree_set_roots_per_cta(bad) == _lib.MW_ERR_INVALID
+    for good in (0, 1, 2, 4, -1):
+        assert lib.mw_dk_tree_set_roots_per_cta(good) == _lib.MW_OK
 
 
 def test_peer_sweep_checks():
