@@ -383,20 +383,61 @@ def dk_solve(q: MonicPoly, variant: Variant = Variant.STANDARD, tol: float | Non
              state: RootState | None = None, exact_order: bool = True):
     """Iterate until the largest update falls below tol * max|z| or the
     budget runs out (NoConvergence carrying the state).  Returns
-    (state, iterations) (roots.py:318-340)."""
+    (state, iterations) (roots.py:318-340).
+
+    Same sweeps, same per-sweep test and the same result as calling
+    dk_iterate until converged, but the sweeps run in growing chunks (2, 4,
+    ..., 32) back to back on the device, each sweep writing its own state,
+    update magnitudes and collision flag; the per-sweep convergence test is
+    evaluated on the device and the host reads one small vector per chunk
+    and returns the first converged sweep's state (a collision raises at
+    its own sweep, before that sweep's convergence test, as in the
+    reference loop).  The up to 31 sweeps computed past convergence cost
+    device time only."""
     if tol is None:
         tol = default_tolerance(q.k)
     if tol <= 0:
         raise ValueError("tol must be positive")
     if state is None:
         state = aberth_init(q, variant)
-    for _ in range(max_iter):
-        state = dk_iterate(q, state, variant, exact_order)
-        zmag = float(torch.max(torch.hypot(state.re[0], state.im[0])).item())
-        if state.last_max_update <= tol * max(zmag, 1e-300):
-            state.converged = True
-            return state, state.iteration
-    raise NoConvergence(f"no convergence in {max_iter} sweeps", state)
+    if state.k != q.k:
+        raise ValueError("mixed word counts")
+    if state.n != q.n:
+        raise ValueError("state size does not match the polynomial degree")
+    _lib.require_cuda(q.planes, state.re, state.im)
+    dev = state.re.device
+    k, n = state.k, state.n
+    cur_re, cur_im, it = state.re, state.im, state.iteration
+    done, chunk = 0, 2
+    last = state
+    while done < max_iter:
+        m = min(chunk, max_iter - done)
+        res_re = torch.empty((m, k, n), dtype=torch.float64, device=dev)
+        res_im = torch.empty_like(res_re)
+        mag = torch.empty((m, n), dtype=torch.float64, device=dev)
+        flags = torch.full((m,), INT32_MAX, dtype=torch.int32, device=dev)
+        src_re, src_im = cur_re, cur_im
+        for s in range(m):
+            sweep_into(q.planes, src_re, src_im, res_re[s], res_im[s], mag[s], flags[s:s + 1], variant,
+                       exact_order)
+            src_re, src_im = res_re[s], res_im[s]
+        upd = mag.max(dim=1).values
+        zmag = torch.hypot(res_re[:, 0], res_im[:, 0]).max(dim=1).values
+        conv = upd <= tol * torch.clamp(zmag, min=1e-300)
+        host = torch.stack([flags.to(torch.float64), conv.to(torch.float64), upd]).cpu().numpy()
+        for s in range(m):
+            if int(host[0, s]) != INT32_MAX:
+                _raise_collision(int(host[0, s]), n)
+            if host[1, s]:
+                st = RootState(re=res_re[s], im=res_im[s], iteration=it + s + 1, converged=True,
+                               last_max_update=float(host[2, s]))
+                return st, st.iteration
+        last = RootState(re=res_re[m - 1], im=res_im[m - 1], iteration=it + m, converged=False,
+                         last_max_update=float(host[2, m - 1]))
+        cur_re, cur_im, it = last.re, last.im, last.iteration
+        done += m
+        chunk = min(2 * chunk, 32)
+    raise NoConvergence(f"no convergence in {max_iter} sweeps", last)
 
 
 # ------------------------------------------------------ test problems (host)

@@ -241,3 +241,37 @@ def test_eft_exactness_wide_exponent_sweep():
     p = batch_mul(LaneBatch(A), LaneBatch(B), Variant.BRANCH_FREE).numpy()
     for i in range(0, n, 13):
         assert _exact_pair_ok(a[i], b[i], p[0, i], p[1, i], "mul")
+
+
+def _dk_solve_stepwise(q, variant, tol, max_iter, exact_order):
+    """The reference loop (roots.py:318-340): one dk_iterate per sweep and
+    the convergence test after each."""
+    state = roots.aberth_init(q, variant)
+    for _ in range(max_iter):
+        state = roots.dk_iterate(q, state, variant, exact_order)
+        zmag = float(torch.max(torch.hypot(state.re[0], state.im[0])).item())
+        if state.last_max_update <= tol * max(zmag, 1e-300):
+            return state, state.iteration
+    raise roots.NoConvergence("", state)
+
+
+@pytest.mark.parametrize("exact_order", [True, False])
+@pytest.mark.parametrize("k,deg", [(2, 8), (3, 16), (4, 12)])
+def test_dk_solve_chunked_equals_stepwise_loop(k, deg, exact_order):
+    """dk_solve's chunked device loop returns exactly the state and sweep
+    count of the sweep-by-sweep reference loop."""
+    q = roots.chebyshev_coeffs(deg, k)
+    tol = roots.default_tolerance(k)
+    want, wi = _dk_solve_stepwise(q, Variant.BRANCH_FREE, tol, 200, exact_order)
+    got, gi = roots.dk_solve(q, Variant.BRANCH_FREE, tol=tol, exact_order=exact_order)
+    assert gi == wi and got.converged
+    assert_bitwise(got.re.cpu().numpy(), want.re.cpu().numpy())
+    assert_bitwise(got.im.cpu().numpy(), want.im.cpu().numpy())
+    assert got.last_max_update == want.last_max_update
+    # a budget that ends mid-chunk: NoConvergence carries the last state
+    cut = max(1, wi - 2)
+    with pytest.raises(roots.NoConvergence) as info:
+        roots.dk_solve(q, Variant.BRANCH_FREE, tol=tol, max_iter=cut, exact_order=exact_order)
+    ref = roots.dk_sweeps(q, roots.aberth_init(q, Variant.BRANCH_FREE), cut, Variant.BRANCH_FREE, exact_order)
+    assert info.value.state.iteration == cut
+    assert_bitwise(info.value.state.re.cpu().numpy(), ref.re.cpu().numpy())
