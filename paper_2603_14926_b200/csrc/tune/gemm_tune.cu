@@ -145,6 +145,13 @@ static int gemv_wring_launch(const double* A, const double* x, double* y, int64_
   kern<<<grid, 128 * Q, smem, st>>>(A, n, m * n, x, n, y, m, m, n);
   return launch_status();
 }
+template <int K, int C, int D, int RPC>
+static int gemv_mc_launch(const double* A, const double* x, double* y, int64_t m, int64_t n,
+                          cudaStream_t st) {
+  gemv_mc_kernel<K, BRANCH_FREE, C, D, RPC><<<(unsigned)((m + RPC - 1) / RPC), 128 * RPC, 0, st>>>(
+      A, n, m * n, x, n, y, m, m, n);
+  return launch_status();
+}
 template <int K>
 static int gemv_run(int cfg, const double* A, const double* x, double* y, int64_t m, int64_t n,
                     cudaStream_t st) {
@@ -194,10 +201,16 @@ static int gemv_run(int cfg, const double* A, const double* x, double* y, int64_
     case 42: return gemv_wring_launch<K, 4, 4, 3>(A, x, y, m, n, st);
     case 43: return gemv_wring_launch<K, 8, 1, 6>(A, x, y, m, n, st);
     case 44: return gemv_wring_launch<K, 6, 2, 3>(A, x, y, m, n, st);
+    case 45: return gemv_mc_launch<K, 2, 2, 1>(A, x, y, m, n, st);
+    case 46: return gemv_mc_launch<K, 2, 1, 1>(A, x, y, m, n, st);
+    case 47: return gemv_mc_launch<K, 2, 2, 2>(A, x, y, m, n, st);
+    case 48: return gemv_mc_launch<K, 2, 1, 2>(A, x, y, m, n, st);
+    case 49: return gemv_mc_launch<K, 1, 4, 1>(A, x, y, m, n, st);
+    case 50: return gemv_mc_launch<K, 4, 1, 1>(A, x, y, m, n, st);
     default: return MW_ERR_INVALID;
   }
 }
-extern "C" int mwt_gemv_num_configs(void) { return 45; }
+extern "C" int mwt_gemv_num_configs(void) { return 51; }
 extern "C" const char* mwt_gemv_config_name(int cfg) {
   static const char* names[] = {"W4_R2_D4", "W1_R8_D8", "W1_R8_D4", "W2_R4_D4", "W2_R4_D8",
                                 "W4_R2_D2", "W4_R1_D4", "W8_R1_D2", "st_R2_D4_S2", "st_R2_D4_S3",
@@ -208,8 +221,9 @@ extern "C" const char* mwt_gemv_config_name(int cfg) {
                                 "rt1_D4", "rt1_D2_P", "rt1_D4_P", "rt2_D2", "rt2_D4", "rt2_D2_P",
                                 "rt2_D1_P", "rt1_D2_P_b8", "rt2_D2_P_b4", "rt1_D1_P_b12",
                                 "wr_Q8_J2_S4", "wr_Q8_J2_S3", "wr_Q6_J2_S4", "wr_Q6_J4_S2", "wr_Q4_J4_S3",
-                                "wr_Q8_J1_S6", "wr_Q6_J2_S3"};
-  return (cfg >= 0 && cfg < 45) ? names[cfg] : "?";
+                                "wr_Q8_J1_S6", "wr_Q6_J2_S3", "mc_C2_D2", "mc_C2_D1", "mc_C2_D2_R2",
+                                "mc_C2_D1_R2", "mc_C1_D4", "mc_C4_D1"};
+  return (cfg >= 0 && cfg < 51) ? names[cfg] : "?";
 }
 extern "C" int mwt_gemv(int cfg, int k, const double* A, const double* x, double* y, int64_t m,
                         int64_t n, void* stream) {

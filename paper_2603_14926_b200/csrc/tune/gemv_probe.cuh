@@ -147,3 +147,77 @@ __global__ void __launch_bounds__(128, MINB)
   }
 }
 }  // namespace mw
+
+namespace mw {
+// Experimental fold order (timing only): P = 128 * C partials per row, 128
+// threads per row, thread u folds the C partials u, u+128, ... (partial v
+// folds t = v, v + P, ...) as C independent chains stepped together, D
+// elements per chain loaded ahead; the partials combine by the pairwise
+// tree over P in shared memory.
+template <int K, int VAR, int C, int D, int RPC = 1>
+__global__ void __launch_bounds__(128 * RPC)
+    gemv_mc_kernel(const double* __restrict__ A, int64_t lda, int64_t sA,
+                   const double* __restrict__ x, int64_t sx, double* __restrict__ y, int64_t sy,
+                   int64_t m, int64_t n) {
+  constexpr int P = 128 * C;
+  const int u = threadIdx.x % 128, slot = threadIdx.x / 128;
+  const int64_t i = blockIdx.x * (int64_t)RPC + slot;
+  const bool live = i < m;
+  const double* row = A + (live ? i : 0) * lda;
+  V<K> acc[C];
+#pragma unroll
+  for (int c = 0; c < C; ++c) acc[c] = zero<K>();
+  int64_t t = u;
+  for (; t + (int64_t)(D - 1) * P + (C - 1) * 128 < n; t += (int64_t)D * P) {
+    V<K> a[D][C], xv[D][C];
+#pragma unroll
+    for (int d = 0; d < D; ++d)
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        a[d][c] = load<K>(row, sA, t + d * P + c * 128);
+        xv[d][c] = load<K>(x, sx, t + d * P + c * 128);
+      }
+#pragma unroll
+    for (int d = 0; d < D; ++d)
+#pragma unroll
+      for (int c = 0; c < C; ++c) acc[c] = Ops<K, VAR>::add(acc[c], Ops<K, VAR>::mul(a[d][c], xv[d][c]));
+  }
+  for (; t < n; t += P)
+#pragma unroll
+    for (int c = 0; c < C; ++c)
+      if (t + c * 128 < n)
+        acc[c] = Ops<K, VAR>::add(acc[c], Ops<K, VAR>::mul(load<K>(row, sA, t + c * 128), load<K>(x, sx, t + c * 128)));
+  __shared__ double part[RPC][K][P];
+#pragma unroll
+  for (int c = 0; c < C; ++c)
+#pragma unroll
+    for (int k = 0; k < K; ++k) part[slot][k][u + c * 128] = acc[c].c[k];
+  __syncthreads();
+  const int64_t valid = n < P ? n : P;
+#pragma unroll 1
+  for (int s = 1; s < P; s <<= 1) {
+    const int pairs = P / (2 * s);
+    for (int w = u; w < pairs; w += 128) {
+      const int idx = 2 * s * w;
+      if (idx + s < valid) {
+        V<K> l, r;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          l.c[k] = part[slot][k][idx];
+          r.c[k] = part[slot][k][idx + s];
+        }
+        const V<K> sum = Ops<K, VAR>::add(l, r);
+#pragma unroll
+        for (int k = 0; k < K; ++k) part[slot][k][idx] = sum.c[k];
+      }
+    }
+    __syncthreads();
+  }
+  if (u == 0 && live) {
+    V<K> r0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) r0.c[k] = part[slot][k][0];
+    store<K>(y, sy, i, r0);
+  }
+}
+}  // namespace mw
