@@ -221,3 +221,72 @@ __global__ void __launch_bounds__(128 * RPC)
   }
 }
 }  // namespace mw
+
+namespace mw {
+// Experimental fold order (timing only): 128 partials per row, partial u
+// folds the column PAIRS (2u + 256j, 2u + 1 + 256j), j ascending, so every
+// A and x access is one 16-byte load per lane (LDG.128); D pairs ahead.
+template <int K, int VAR, int D, int RPC = 2>
+__global__ void __launch_bounds__(128 * RPC)
+    gemv_v2_kernel(const double* __restrict__ A, int64_t lda, int64_t sA,
+                   const double* __restrict__ x, int64_t sx, double* __restrict__ y, int64_t sy,
+                   int64_t m, int64_t n) {
+  constexpr int P = 128;
+  const int u = threadIdx.x % P, slot = threadIdx.x / P;
+  const int64_t i = blockIdx.x * (int64_t)RPC + slot;
+  const bool live = i < m;
+  const double* row = A + (live ? i : 0) * lda;
+  V<K> acc = zero<K>();
+  auto ld2 = [&](const double* base, int64_t stride, int64_t t, V<K>& lo, V<K>& hi) {
+#pragma unroll
+    for (int c = 0; c < K; ++c) {
+      const double2 v = *reinterpret_cast<const double2*>(base + c * stride + t);
+      lo.c[c] = v.x;
+      hi.c[c] = v.y;
+    }
+  };
+  for (int64_t t = 2 * u; t < n; t += (int64_t)2 * P * D) {
+    V<K> a0[D], a1[D], x0[D], x1[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d)
+      if (t + (int64_t)2 * P * d < n) {
+        ld2(row, sA, t + (int64_t)2 * P * d, a0[d], a1[d]);
+        ld2(x, sx, t + (int64_t)2 * P * d, x0[d], x1[d]);
+      }
+#pragma unroll
+    for (int d = 0; d < D; ++d)
+      if (t + (int64_t)2 * P * d < n) {
+        acc = Ops<K, VAR>::add(acc, Ops<K, VAR>::mul(a0[d], x0[d]));
+        acc = Ops<K, VAR>::add(acc, Ops<K, VAR>::mul(a1[d], x1[d]));
+      }
+  }
+  __shared__ double part[RPC][K][P];
+#pragma unroll
+  for (int k = 0; k < K; ++k) part[slot][k][u] = acc.c[k];
+  __syncthreads();
+#pragma unroll 1
+  for (int s = 1; s < P; s <<= 1) {
+    const int per_row = P / (2 * s);
+    const int tid = threadIdx.x;
+    if (tid < RPC * per_row) {
+      const int r = tid / per_row, idx = 2 * s * (tid % per_row);
+      V<K> l, rr;
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        l.c[k] = part[r][k][idx];
+        rr.c[k] = part[r][k][idx + s];
+      }
+      const V<K> sum = Ops<K, VAR>::add(l, rr);
+#pragma unroll
+      for (int k = 0; k < K; ++k) part[r][k][idx] = sum.c[k];
+    }
+    __syncthreads();
+  }
+  if (u == 0 && live) {
+    V<K> r0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) r0.c[k] = part[slot][k][0];
+    store<K>(y, sy, i, r0);
+  }
+}
+}  // namespace mw
