@@ -109,3 +109,47 @@ def test_named_word_count_errors():
         mwm.dw_add_bf((1.0, 0.0, 0.0), (1.0, 0.0, 0.0))
     with pytest.raises(ValueError):
         mwm.normalize((1.0,) * 5)
+
+
+# --------------------------------------------- property tests (hypothesis)
+from hypothesis import given, settings  # noqa: E402
+from hypothesis import strategies as st  # noqa: E402
+
+
+@st.composite
+def _raw_expansions(draw):
+    """Decreasing raw expansions with random exponents, signs and zero
+    terms (every renormalisation branch), 1..64 lanes."""
+    k = draw(st.sampled_from([2, 3, 4]))
+    w = draw(st.integers(1, 64))
+    seed = draw(st.integers(0, 2**31 - 1))
+    rng = np.random.default_rng(seed)
+    m = {2: 2, 3: 4, 4: 5}[k]
+    raw = np.zeros((m, w))
+    raw[0] = rng.uniform(-1, 1, w) * np.exp2(rng.integers(-900, 900, w))
+    for j in range(1, m):
+        raw[j] = raw[j - 1] * np.exp2(-rng.integers(40, 60, w)) * rng.uniform(-1, 1, w)
+    raw[rng.random((m, w)) < 0.25] = 0.0
+    if k == 2:
+        raw[1] = np.where(np.abs(raw[1]) > np.abs(raw[0]), 0.0, raw[1])  # quick_two_sum contract
+    return k, raw
+
+
+@given(_raw_expansions())
+@settings(max_examples=120, deadline=None)
+def test_property_renormalize_matches_oracle(case):
+    k, raw = case
+    got = np.stack(mwm._renorm(k, tuple(raw)))
+    assert_bitwise(got, oracle.renormalize(k, raw))
+
+
+@given(st.integers(0, 2**31 - 1), st.integers(1, 300))
+@settings(max_examples=60, deadline=None)
+def test_property_sloppy_cleaned_fma_match_oracle(seed, w):
+    rng = np.random.default_rng(seed)
+    a2, b2 = rand_mw(rng, 2, w, -500, 500), rand_mw(rng, 2, w, -500, 500)
+    assert_bitwise(np.stack(mwm.dw_add_sloppy(tuple(a2), tuple(b2))), oracle.named("dw_add_sloppy", a2, b2))
+    a3, b3 = rand_mw(rng, 3, w, -300, 300), rand_mw(rng, 3, w, -300, 300)
+    assert_bitwise(np.stack(mwm.tw_mul_cleaned(tuple(a3), tuple(b3))), oracle.named("tw_mul_cleaned", a3, b3))
+    x, y, z = (rng.uniform(-1, 1, w) * np.exp2(rng.integers(-300, 300, w)) for _ in range(3))
+    assert_bitwise(eft.fma(x, y, z), oracle.fma(x, y, z))
