@@ -1017,3 +1017,35 @@ def test_dk_tree_powers_kernel_path_matches_in_warp_path(k, v):
     want_re, want_im, _, _ = oracle.dk_sweep(coeffs, zre, zim, v, exact=False, rows=(i0, i1))
     assert_bitwise(outs[1][0][:, i0:i1], want_re[:, i0:i1])
     assert_bitwise(outs[1][1][:, i0:i1], want_im[:, i0:i1])
+
+
+# ------------------------------------ Standard variant at benchmark sizes
+@pytest.mark.parametrize("k,n", [(2, 1024), (3, 1024), (4, 512)])
+def test_standard_gemm_sampled_rows_at_scale(k, n):
+    """The Standard (renormalising) GEMM at sizes where every warp sees
+    divergent renormalisation paths, sampled rows vs the oracle."""
+    a, b = gen.config3_gemm(k, n)
+    c = matmul(MWMatrix(a), MWMatrix(b), MatMulPlan(scheme="naive", variant="std")).numpy()
+    for r0 in (0, n // 2 + 1, n - 1):
+        assert_bitwise(c[:, r0], oracle.gemm(a, b, "std", rows=(r0, r0 + 1))[:, r0])
+
+
+def test_standard_horner_sampled_points_at_scale():
+    coeffs, x = gen.config4_horner(npts=1 << 20)
+    y = horner_eval_batched(MWPolynomial(coeffs), LaneBatch(x), Variant.STANDARD).numpy()
+    idx = np.r_[0:1024, (1 << 19):(1 << 19) + 1024, (1 << 20) - 1024:(1 << 20)]
+    assert_bitwise(y[:, idx], oracle.horner(coeffs, x[:, idx], "std"))
+
+
+@pytest.mark.parametrize("k", [3, 4])
+@pytest.mark.parametrize("exact", [True, False])
+def test_standard_dk_sweep_config5(k, exact):
+    """One Standard-variant sweep of the degree-512 config-5 problem, both
+    orders, vs the oracle (exact: reference order; tree: its restatement)."""
+    coeffs = gen.config5_poly(k)
+    zre, zim = gen.config5_init(k)
+    nxt = dk_iterate(MonicPoly(coeffs), RootState(re=zre, im=zim), Variant.STANDARD, exact_order=exact)
+    ore, oim, _, coll = oracle.dk_sweep(coeffs, zre, zim, "std", exact=exact)
+    assert coll is None
+    assert_bitwise(nxt.re.cpu().numpy(), ore)
+    assert_bitwise(nxt.im.cpu().numpy(), oim)
