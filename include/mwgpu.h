@@ -287,6 +287,12 @@ int mw_dk_exact_set_roots_per_cta(int roots);
  * ops, same order, identical results. */
 int mw_dk_exact_set_split(int on);
 
+/* Tuning knob of mw_gemm: 0 (default) picks the CTA tile per call from
+ * the shape (smaller tiles for row-block shards, where the large tile
+ * leaves SMs unevenly loaded), 1..3 force tile slot 0..2.  Every tile
+ * folds each C_ij in the same order: identical results. */
+int mw_gemm_set_tile_policy(int policy);
+
 /* Tuning knob of the tree-order sweep with a workspace (mw_dk_sweep_ws):
  * roots per CTA, 1, 2 or 4 = one chain per lane and the pairwise trees
  * packed level by level over the CTA's roots; -1 (default) = by shard

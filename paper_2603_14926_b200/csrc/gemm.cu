@@ -19,27 +19,99 @@
 
 namespace mw {
 
+// Tile configurations per K.  Slot 0 is the full-size optimum (tile sweep
+// on B200 with tune/gemm_tune.cu + scripts/tune_gemm.py: every
+// non-spilling configuration lands within 1-4 % of it; all are
+// bit-identical).  Slots 1 and 2 are smaller tiles for row-block shards:
+// a GEMM is FP64-pipe bound, so its time follows the busiest SM's share,
+// ceil(tiles / SMs) tiles, and at n/8 rows the big tiles leave SMs with one
+// tile fewer than others (DD 512 x 4096: 3.46 tiles per SM -> 4).
+// gemm_pick() chooses the slot minimising ceil(tiles / SMs) * tile area /
+// relative efficiency (measured, scripts/tune_gemm_shards.py: DD at 512
+// rows 16.55 -> 14.83 ms, TD at 256 rows 6.74 -> 6.15, QD at 512 rows
+// 28.96 -> 25.46 ms; full sizes keep slot 0).
+template <int bm, int bn, int tm, int tn, int minb>
+struct GemmTile {
+  static constexpr int BM = bm, BN = bn, BK = 16, TM = tm, TN = tn, MINB = minb;
+  static constexpr bool VEC = false;
+};
 template <int K>
-struct GemmCfg;
-// DD: 64x64 tile, 4x4 per thread, 256 threads.
+struct GemmCfgs;
 template <>
-struct GemmCfg<2> {
-  static constexpr int BM = 64, BN = 64, BK = 16, TM = 4, TN = 4, MINB = 2;
-  static constexpr bool VEC = false;
-};
-// TD and QD: 64x32 tile, 4x2 per thread, 256 threads.  (Tile sweep on
-// B200 with tune/gemm_tune.cu + scripts/tune_gemm.py: every non-spilling
-// configuration lands within 1-3 % of these; all are bit-identical.)
-template <>
-struct GemmCfg<3> {
-  static constexpr int BM = 64, BN = 32, BK = 16, TM = 4, TN = 2, MINB = 2;
-  static constexpr bool VEC = false;
+struct GemmCfgs<2> {
+  using C0 = GemmTile<64, 64, 4, 4, 2>;
+  using C1 = GemmTile<32, 64, 2, 4, 2>;
+  using C2 = GemmTile<32, 32, 2, 2, 2>;
+  static constexpr double REL[3] = {1.0, 0.979, 0.959};
 };
 template <>
-struct GemmCfg<4> {
-  static constexpr int BM = 64, BN = 32, BK = 16, TM = 4, TN = 2, MINB = 2;
-  static constexpr bool VEC = false;
+struct GemmCfgs<3> {
+  using C0 = GemmTile<64, 32, 4, 2, 2>;
+  using C1 = GemmTile<32, 32, 2, 2, 2>;
+  using C2 = GemmTile<32, 16, 2, 1, 4>;
+  static constexpr double REL[3] = {1.0, 0.989, 0.963};
 };
+template <>
+struct GemmCfgs<4> {
+  using C0 = GemmTile<64, 32, 4, 2, 2>;
+  using C1 = GemmTile<32, 32, 2, 2, 2>;
+  using C2 = GemmTile<32, 16, 2, 1, 4>;
+  static constexpr double REL[3] = {1.0, 0.993, 0.980};
+};
+template <int K>
+using GemmCfg = typename GemmCfgs<K>::C0;
+
+// 0: choose the tile per call (default); 1..3: always slot 0..2.
+static int g_gemm_tile_policy = 0;
+
+template <class Cf>
+static double gemm_cost(int64_t m, int64_t n, int sms, double rel) {
+  const int64_t tiles = ((n + Cf::BN - 1) / Cf::BN) * ((m + Cf::BM - 1) / Cf::BM);
+  const int64_t per_sm = (tiles + sms - 1) / sms;
+  return (double)per_sm * Cf::BM * Cf::BN / rel;
+}
+
+template <int K>
+static int gemm_pick(int64_t m, int64_t n) {
+  if (g_gemm_tile_policy > 0) return g_gemm_tile_policy - 1;
+  using Cs = GemmCfgs<K>;
+  const int sms = sm_count();
+  const double c0 = gemm_cost<typename Cs::C0>(m, n, sms, Cs::REL[0]);
+  const double c1 = gemm_cost<typename Cs::C1>(m, n, sms, Cs::REL[1]);
+  const double c2 = gemm_cost<typename Cs::C2>(m, n, sms, Cs::REL[2]);
+  return (c1 < c0 && c1 <= c2) ? 1 : (c2 < c0 && c2 < c1) ? 2 : 0;
+}
+
+template <int K, int VAR, class Cf>
+static int gemm_launch(const double* A, int64_t lda, int64_t sA, const double* B, int64_t ldb,
+                       int64_t sB, double* C, int64_t ldc, int64_t sC, int64_t m, int64_t n,
+                       int64_t kd, const double* Cin, int64_t ldci, int64_t sCi, int64_t batch,
+                       int64_t bsA, int64_t bsB, int64_t bsC, int64_t bsCi, cudaStream_t st) {
+  constexpr int NT = (Cf::BM / Cf::TM) * (Cf::BN / Cf::TN);
+  const size_t smem = GemmSmem<K, Cf>::BYTES;
+  // the dynamic-smem opt-in is per device; setting it twice is harmless
+  static bool attr_set[64] = {false};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64 || !attr_set[dev]) {
+    cudaFuncSetAttribute(gemm_kernel<K, VAR, false, Cf>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    cudaFuncSetAttribute(gemm_kernel<K, VAR, true, Cf>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    if (dev >= 0 && dev < 64) attr_set[dev] = true;
+  }
+  const int64_t tiles = ((n + Cf::BN - 1) / Cf::BN) * ((m + Cf::BM - 1) / Cf::BM);
+  if (tiles > 0x7fffffffLL) return MW_ERR_INVALID;
+  if (batch == 1 && Cin == nullptr) {
+    gemm_kernel<K, VAR, false, Cf><<<(unsigned)tiles, NT, smem, st>>>(
+        A, lda, sA, B, ldb, sB, C, ldc, sC, m, n, kd, nullptr, 0, 0, 1, 0, 0, 0, 0);
+  } else {
+    const unsigned gy = (unsigned)(batch < 65535 ? batch : 65535);
+    gemm_kernel<K, VAR, true, Cf><<<dim3((unsigned)tiles, gy), NT, smem, st>>>(
+        A, lda, sA, B, ldb, sB, C, ldc, sC, m, n, kd, Cin, ldci, sCi, batch, bsA, bsB, bsC, bsCi);
+  }
+  return launch_status();
+}
 
 template <int K, int VAR>
 struct GemmLaunch {
@@ -47,37 +119,31 @@ struct GemmLaunch {
                  int64_t sB, double* C, int64_t ldc, int64_t sC, int64_t m, int64_t n, int64_t kd,
                  const double* Cin, int64_t ldci, int64_t sCi, int64_t batch, int64_t bsA,
                  int64_t bsB, int64_t bsC, int64_t bsCi, cudaStream_t st) {
-    using Cf = GemmCfg<K>;
-    constexpr int NT = (Cf::BM / Cf::TM) * (Cf::BN / Cf::TN);
-    const size_t smem = GemmSmem<K, Cf>::BYTES;
-    // the dynamic-smem opt-in is per device; setting it twice is harmless
-    static bool attr_set[64] = {false};
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (dev < 0 || dev >= 64 || !attr_set[dev]) {
-      cudaFuncSetAttribute(gemm_kernel<K, VAR, false, Cf>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)smem);
-      cudaFuncSetAttribute(gemm_kernel<K, VAR, true, Cf>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)smem);
-      if (dev >= 0 && dev < 64) attr_set[dev] = true;
-    }
-    const int64_t tiles = ((n + Cf::BN - 1) / Cf::BN) * ((m + Cf::BM - 1) / Cf::BM);
-    if (tiles > 0x7fffffffLL) return MW_ERR_INVALID;
-    if (batch == 1 && Cin == nullptr) {
-      gemm_kernel<K, VAR, false, Cf><<<(unsigned)tiles, NT, smem, st>>>(
-          A, lda, sA, B, ldb, sB, C, ldc, sC, m, n, kd, nullptr, 0, 0, 1, 0, 0, 0, 0);
-    } else {
-      const unsigned gy = (unsigned)(batch < 65535 ? batch : 65535);
-      gemm_kernel<K, VAR, true, Cf><<<dim3((unsigned)tiles, gy), NT, smem, st>>>(
-          A, lda, sA, B, ldb, sB, C, ldc, sC, m, n, kd, Cin, ldci, sCi, batch, bsA, bsB, bsC, bsCi);
-    }
-    return launch_status();
+    using Cs = GemmCfgs<K>;
+    // batched products (the Strassen leaves) keep slot 0
+    const int slot = (batch == 1 && Cin == nullptr) ? gemm_pick<K>(m, n) : 0;
+    if (slot == 1)
+      return gemm_launch<K, VAR, typename Cs::C1>(A, lda, sA, B, ldb, sB, C, ldc, sC, m, n, kd, Cin,
+                                                  ldci, sCi, batch, bsA, bsB, bsC, bsCi, st);
+    if (slot == 2)
+      return gemm_launch<K, VAR, typename Cs::C2>(A, lda, sA, B, ldb, sB, C, ldc, sC, m, n, kd, Cin,
+                                                  ldci, sCi, batch, bsA, bsB, bsC, bsCi, st);
+    return gemm_launch<K, VAR, typename Cs::C0>(A, lda, sA, B, ldb, sB, C, ldc, sC, m, n, kd, Cin,
+                                                ldci, sCi, batch, bsA, bsB, bsC, bsCi, st);
   }
 };
 
 }  // namespace mw
 
 using namespace mw;
+
+// Tuning knob: GEMM tile choice (0 = per call by shape, default; 1..3 =
+// always slot 0..2).  Results are identical.
+extern "C" int mw_gemm_set_tile_policy(int policy) {
+  if (policy < 0 || policy > 3) return MW_ERR_INVALID;
+  g_gemm_tile_policy = policy;
+  return MW_OK;
+}
 
 extern "C" int mw_gemm_batched(int k, int variant, const double* A, int64_t lda, int64_t sA,
                                int64_t bsA, const double* B, int64_t ldb, int64_t sB, int64_t bsB,

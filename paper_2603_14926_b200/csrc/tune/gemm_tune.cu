@@ -33,15 +33,17 @@ CFGV(V64x32_42_2, 64, 32, 16, 4, 2, 2, true)
 CFGV(V32x32_22_2, 32, 32, 16, 2, 2, 2, true)
 CFGV(V64x64_44_2_bk8, 64, 64, 8, 4, 4, 2, true)
 
+static int64_t g_rows = 0;  // 0: square; else rows of A / C (row-block shard)
 template <int K, class Cf>
 static int launch(const double* A, const double* B, double* C, int64_t n, cudaStream_t st) {
   constexpr int NT = (Cf::BM / Cf::TM) * (Cf::BN / Cf::TN);
   const size_t smem = GemmSmem<K, Cf>::BYTES;
   cudaFuncSetAttribute(gemm_kernel<K, BRANCH_FREE, false, Cf>,
                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  const int64_t tiles = ((n + Cf::BN - 1) / Cf::BN) * ((n + Cf::BM - 1) / Cf::BM);
+  const int64_t m = g_rows ? g_rows : n;
+  const int64_t tiles = ((n + Cf::BN - 1) / Cf::BN) * ((m + Cf::BM - 1) / Cf::BM);
   gemm_kernel<K, BRANCH_FREE, false, Cf><<<(unsigned)tiles, NT, smem, st>>>(
-      A, n, n * n, B, n, n * n, C, n, n * n, n, n, n, nullptr, 0, 0, 1, 0, 0, 0, 0);
+      A, n, m * n, B, n, n * n, C, n, m * n, m, n, n, nullptr, 0, 0, 1, 0, 0, 0, 0);
   return launch_status();
 }
 
@@ -81,6 +83,7 @@ extern "C" const char* mwt_config_name(int cfg) {
                                 "V64x64_44_2", "V64x32_42_2", "V32x32_22_2", "V64x64_44_2_bk8"};
   return (cfg >= 0 && cfg < 16) ? names[cfg] : "?";
 }
+extern "C" void mwt_gemm_set_rows(int64_t rows) { g_rows = rows; }
 extern "C" int mwt_gemm(int cfg, int k, const double* A, const double* B, double* C, int64_t n,
                         void* stream) {
   cudaStream_t st = (cudaStream_t)stream;

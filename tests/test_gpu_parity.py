@@ -1049,3 +1049,29 @@ def test_standard_dk_sweep_config5(k, exact):
     assert coll is None
     assert_bitwise(nxt.re.cpu().numpy(), ore)
     assert_bitwise(nxt.im.cpu().numpy(), oim)
+
+
+@pytest.mark.parametrize("k,m,n", [(2, 512, 4096), (3, 256, 2048), (4, 512, 2048), (3, 67, 93)])
+def test_gemm_tile_slots_bit_identical(k, m, n):
+    """Every GEMM tile slot (and the per-shape choice) gives the same bits
+    on row-block shard shapes; a sampled row equals the oracle."""
+    from paper_2603_14926_b200 import _lib
+    from paper_2603_14926_b200.linalg import gemm_into
+
+    lib = _lib.load()
+    rng = np.random.default_rng(m + n + k)
+    a, b = gen.g_k(rng, k, (m, n)), gen.g_k(rng, k, (n, n))
+    A, B = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+    outs = []
+    try:
+        for policy in (0, 1, 2, 3):
+            assert lib.mw_gemm_set_tile_policy(policy) == 0
+            C = torch.empty((k, m, n), dtype=torch.float64, device="cuda")
+            gemm_into(A, B, C, Variant.BRANCH_FREE)
+            outs.append(C.cpu().numpy())
+    finally:
+        lib.mw_gemm_set_tile_policy(0)
+    for o in outs[1:]:
+        assert_bitwise(o, outs[0])
+    r = m // 3
+    assert_bitwise(outs[0][:, r], oracle.gemm(a, b, "bf", rows=(r, r + 1))[:, r])
