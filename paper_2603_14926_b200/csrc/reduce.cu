@@ -449,10 +449,17 @@ struct GemvLaunch {
       gemv_exact_kernel<K, VAR><<<(unsigned)ceil_div(m, 128), 128, 0, st>>>(A, lda, sA, x, sx, y,
                                                                             sy, m, n);
     } else {
-      // rows per CTA: 2 for DD/TD, 1 for QD (measured; same tree, same bits)
-      constexpr int R = K == 4 ? 1 : GEMV_ROWS_PER_CTA;
-      gemv_tree_kernel<K, VAR, GEMV_WARPS, R><<<(unsigned)ceil_div(m, R), 32 * GEMV_WARPS * R, 0, st>>>(
-          A, lda, sA, x, sx, y, sy, m, n);
+      // rows per CTA: 2 for DD/TD from 1536 rows, else 1 -- with fewer rows
+      // (a row-block shard at 4-8 GPUs) two-row CTAs leave SMs idle
+      // (scripts/gemv_msweep.py: TD 296 rows 10.0 -> 8.5 us); 1 for QD.
+      // Same partials and tree either way: same bits.
+      if (K != 4 && m >= 1536)
+        gemv_tree_kernel<K, VAR, GEMV_WARPS, GEMV_ROWS_PER_CTA>
+            <<<(unsigned)ceil_div(m, GEMV_ROWS_PER_CTA), 32 * GEMV_WARPS * GEMV_ROWS_PER_CTA, 0, st>>>(
+                A, lda, sA, x, sx, y, sy, m, n);
+      else
+        gemv_tree_kernel<K, VAR, GEMV_WARPS, 1><<<(unsigned)m, 32 * GEMV_WARPS, 0, st>>>(
+            A, lda, sA, x, sx, y, sy, m, n);
     }
     return launch_status();
   }
