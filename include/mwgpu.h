@@ -287,6 +287,12 @@ int mw_dk_exact_set_roots_per_cta(int roots);
  * ops, same order, identical results. */
 int mw_dk_exact_set_split(int on);
 
+/* Tuning knob of the tree dot: 1 (default) runs dots of 2..16 blocks of
+ * 4096 elements as one thread-block cluster (block roots folded through
+ * distributed shared memory), 0 always uses the single-launch ticket
+ * form.  Same partials and trees: identical results. */
+int mw_dot_set_cluster(int on);
+
 /* Tuning knob of mw_gemm: 0 (default) picks the CTA tile per call from
  * the shape (smaller tiles for row-block shards, where the large tile
  * leaves SMs unevenly loaded), 1..3 force tile slot 0..2.  Every tile

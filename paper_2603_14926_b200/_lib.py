@@ -59,6 +59,7 @@ _SIGS = {
     "mw_dk_exact_set_split": ([I], I),
     "mw_dk_tree_set_roots_per_cta": ([I], I),
     "mw_gemm_set_tile_policy": ([I], I),
+    "mw_dot_set_cluster": ([I], I),
     "mw_dk_sweep_peer": ([I, I, P, I64, I64, P, I64, I64, P, P, P, P, P, P, P, I, I, I, I, ctypes.c_longlong, P, P,
                           I, P, P], I),
     "mw_dk_sweep_workspace": ([I, I64, I64], I64),

@@ -146,6 +146,66 @@ __global__ void __launch_bounds__(DOT_BLOCK) dot_fused_kernel(
   }
 }
 
+// Single-launch tree dot for 1 < nb <= 16 blocks (n <= 65536, config 1)
+// as ONE thread-block cluster: each block's subtree root goes straight into
+// the leader block's shared memory (distributed shared memory), one
+// cluster barrier, and the leader folds the nb roots with the same
+// pairwise tree -- no global partials, fences or atomic ticket on the
+// latency path.  Same partials, same trees: bit-identical to
+// dot_fused_kernel.
+constexpr int DOT_CLUSTER_MAX = 16;
+static int g_dot_cluster = 1;
+__device__ __forceinline__ unsigned cluster_ctarank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}  // 0: always the ticket form (tuning / tests)
+template <int K, int VAR>
+__global__ void __launch_bounds__(DOT_BLOCK) dot_cluster_kernel(
+    const double* __restrict__ x, int64_t sx, const double* __restrict__ y, int64_t sy,
+    int64_t n, double* __restrict__ out) {
+  __shared__ double roots[K][DOT_CLUSTER_MAX];
+  const unsigned rank = cluster_ctarank();
+  const int64_t nb = gridDim.x;
+  const int64_t base = (int64_t)rank * DOT_PER_BLOCK + threadIdx.x;
+  V<K> acc = zero<K>();
+  if ((int64_t)rank * DOT_PER_BLOCK + DOT_PER_BLOCK <= n) {
+    V<K> xs[DOT_LEAF], ys[DOT_LEAF];
+#pragma unroll
+    for (int j = 0; j < DOT_LEAF; ++j) {
+      xs[j] = load<K>(x, sx, base + j * DOT_BLOCK);
+      ys[j] = load<K>(y, sy, base + j * DOT_BLOCK);
+    }
+#pragma unroll
+    for (int j = 0; j < DOT_LEAF; ++j)
+      acc = Ops<K, VAR>::add(acc, Ops<K, VAR>::mul(xs[j], ys[j]));
+  } else {
+    for (int64_t t = base; t < n; t += DOT_BLOCK)
+      acc = Ops<K, VAR>::add(acc, Ops<K, VAR>::mul(load<K>(x, sx, t), load<K>(y, sy, t)));
+  }
+  V<K> r = block_tree<K, VAR>(acc, (int64_t)rank * DOT_BLOCK, dot_partial_count(n));
+  if (threadIdx.x == 0) {
+    const unsigned local = static_cast<unsigned>(__cvta_generic_to_shared(&roots[0][rank]));
+    unsigned remote;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(remote) : "r"(local));
+#pragma unroll
+    for (int c = 0; c < K; ++c)
+      asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(remote + c * DOT_CLUSTER_MAX * 8u),
+                   "d"(r.c[c])
+                   : "memory");
+  }
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  if (rank != 0) return;
+  V<K> v = zero<K>();
+  if (threadIdx.x < nb) {
+#pragma unroll
+    for (int c = 0; c < K; ++c) v.c[c] = roots[c][threadIdx.x];
+  }
+  __syncthreads();  // block_tree reuses its shared buffer
+  V<K> root = block_tree<K, VAR>(v, 0, nb);
+  if (threadIdx.x == 0) store<K>(out, 1, 0, root);
+}
+
 // Tree stage above the leaves: groups of 256 values -> one subtree root.
 template <int K, int VAR>
 __global__ void __launch_bounds__(DOT_BLOCK) tree_fold_kernel(const double* __restrict__ in,
@@ -212,6 +272,29 @@ struct DotLaunch {
     // left zero by every call, never overwritten); partials start at ws + 1
     unsigned int* ticket = reinterpret_cast<unsigned int*>(ws);
     double* part = ws + 1;
+    if (nb <= DOT_CLUSTER_MAX && g_dot_cluster) {
+      auto kern = dot_cluster_kernel<K, VAR>;
+      static bool attr_set[64] = {false};
+      int dev = 0;
+      cudaGetDevice(&dev);
+      if (dev < 0 || dev >= 64 || !attr_set[dev]) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (dev >= 0 && dev < 64) attr_set[dev] = true;
+      }
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3((unsigned)nb);
+      cfg.blockDim = dim3(DOT_BLOCK);
+      cfg.stream = st;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = (unsigned)nb;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      if (cudaLaunchKernelEx(&cfg, kern, x, sx, y, sy, n, out) == cudaSuccess) return launch_status();
+      (void)cudaGetLastError();  // cluster shape not available: the ticket form below
+    }
     if (nb <= DOT_BLOCK) {
       dot_fused_kernel<K, VAR><<<(unsigned)nb, DOT_BLOCK, 0, st>>>(x, sx, y, sy, n, part, ticket,
                                                                   out);
@@ -472,6 +555,14 @@ using namespace mw;
 static int variant_ok(int k, int variant) {
   if (k < 2 || k > 4) return MW_ERR_INVALID;
   return (variant == 0 || variant == 1) ? MW_OK : MW_ERR_INVALID;
+}
+
+// Tuning knob: 1 (default) runs dots of 2..16 blocks as one thread-block
+// cluster, 0 always uses the single-launch ticket form.  Same results.
+extern "C" int mw_dot_set_cluster(int on) {
+  if (on != 0 && on != 1) return MW_ERR_INVALID;
+  g_dot_cluster = on;
+  return MW_OK;
 }
 
 extern "C" int64_t mw_dot_workspace(int k, int64_t n) {

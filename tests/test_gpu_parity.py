@@ -1075,3 +1075,27 @@ def test_gemm_tile_slots_bit_identical(k, m, n):
         assert_bitwise(o, outs[0])
     r = m // 3
     assert_bitwise(outs[0][:, r], oracle.gemm(a, b, "bf", rows=(r, r + 1))[:, r])
+
+
+@pytest.mark.parametrize("k", [2, 3, 4])
+@pytest.mark.parametrize("n", [4097, 8192, 40000, 65535, 65536, 65537])
+def test_dot_cluster_form_matches_ticket_form(k, n):
+    """Dots of 2..16 blocks as one thread-block cluster (block roots through
+    distributed shared memory) equal the single-launch ticket form and the
+    oracle's tree restatement bit for bit (65537 takes the ticket form)."""
+    from paper_2603_14926_b200 import _lib
+
+    lib = _lib.load()
+    rng = np.random.default_rng(3 * n + k)
+    x, y = gen.g_k(rng, k, n), gen.g_k(rng, k, n)
+    X, Y = LaneBatch(x), LaneBatch(y)
+    try:
+        outs = []
+        for on in (1, 0, 1):  # cluster, ticket, cluster again (repeat calls)
+            assert lib.mw_dot_set_cluster(on) == 0
+            outs.append(np.array(blas.dot(X, Y, Variant.BRANCH_FREE, order="tree")))
+    finally:
+        lib.mw_dot_set_cluster(1)
+    for o in outs[1:]:
+        assert_bitwise(o, outs[0])
+    assert_bitwise(outs[0], oracle.dot(x, y, "bf", order=1))
