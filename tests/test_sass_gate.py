@@ -107,13 +107,16 @@ def test_dd_standard_add_is_accurate_add(sass):
     assert lane_bodies(a, m, f, (20, 0, 0)) >= 1
 
 
-def test_gemm_inner_loop_has_no_contraction(sass):
-    """DD GEMM: the MAC body issues exactly one DFMA per product."""
-    hits = [f for f in sass if f.startswith("_ZN2mw11gemm_kernelILi2ELi1ELb0E") and "GemmCfg" in f]
-    assert len(hits) == 1
+@pytest.mark.parametrize("tile,macs", [("GemmTileILi64ELi64ELi4ELi4ELi2E", 16),
+                                       ("GemmTileILi32ELi64ELi2ELi4ELi2E", 8),
+                                       ("GemmTileILi32ELi32ELi2ELi2ELi2E", 4)])
+def test_gemm_inner_loop_has_no_contraction(sass, tile, macs):
+    """DD GEMM, every tile slot: the MAC body issues exactly one DFMA per
+    product (TM x TN MACs per k step: DFMA 1, DMUL 3, DADD 25 each)."""
+    hits = [f for f in sass if f.startswith("_ZN2mw11gemm_kernelILi2ELi1ELb0E") and tile in f]
+    assert len(hits) == 1, hits
     a, m, f, _, _ = mix(sass[hits[0]])
-    # 4x4 register tile per t step: 16 MACs -> 16 DFMA, 48 DMUL, 16*25 DADD
-    assert (a, m, f) == (400, 48, 16)
+    assert (a, m, f) == (25 * macs, 3 * macs, macs)
 
 
 @pytest.mark.parametrize("op,mix_expect", [(0, (3, 0, 0)), (1, (6, 0, 0)), (2, (0, 1, 1))])
