@@ -27,7 +27,8 @@ namespace mw {
 // ceil(tiles / SMs) tiles, and at n/8 rows the big tiles leave SMs with one
 // tile fewer than others (DD 512 x 4096: 3.46 tiles per SM -> 4).
 // gemm_pick() chooses the slot minimising ceil(tiles / SMs) * tile area /
-// relative efficiency (measured, scripts/tune_gemm_shards.py: DD at 512
+// relative efficiency per variant (measured, scripts/tune_gemm_shards.py
+// and scripts/time_gemm_std_tiles.py: DD at 512
 // rows 16.55 -> 14.83 ms, TD at 256 rows 6.74 -> 6.15, QD at 512 rows
 // 28.96 -> 25.46 ms; full sizes keep slot 0).
 template <int bm, int bn, int tm, int tn, int minb>
@@ -43,6 +44,7 @@ struct GemmCfgs<2> {
   using C1 = GemmTile<32, 64, 2, 4, 2>;
   using C2 = GemmTile<32, 32, 2, 2, 2>;
   static constexpr double REL[3] = {1.0, 0.979, 0.959};
+  static constexpr double REL_STD[3] = {1.0, 0.979, 0.959};  // DD Standard add is branch-free
 };
 template <>
 struct GemmCfgs<3> {
@@ -50,6 +52,7 @@ struct GemmCfgs<3> {
   using C1 = GemmTile<32, 32, 2, 2, 2>;
   using C2 = GemmTile<32, 16, 2, 1, 4>;
   static constexpr double REL[3] = {1.0, 0.989, 0.963};
+  static constexpr double REL_STD[3] = {0.990, 0.987, 1.0};
 };
 template <>
 struct GemmCfgs<4> {
@@ -57,6 +60,9 @@ struct GemmCfgs<4> {
   using C1 = GemmTile<32, 32, 2, 2, 2>;
   using C2 = GemmTile<32, 16, 2, 1, 4>;
   static constexpr double REL[3] = {1.0, 0.993, 0.980};
+  // Standard QD: the renormalisation's divergent branches serialise a
+  // thread's MACs, so small register tiles win (n = 2048: 373 / 254 / 234 ms)
+  static constexpr double REL_STD[3] = {0.628, 0.924, 1.0};
 };
 template <int K>
 using GemmCfg = typename GemmCfgs<K>::C0;
@@ -71,14 +77,15 @@ static double gemm_cost(int64_t m, int64_t n, int sms, double rel) {
   return (double)per_sm * Cf::BM * Cf::BN / rel;
 }
 
-template <int K>
+template <int K, int VAR>
 static int gemm_pick(int64_t m, int64_t n) {
   if (g_gemm_tile_policy > 0) return g_gemm_tile_policy - 1;
   using Cs = GemmCfgs<K>;
   const int sms = sm_count();
-  const double c0 = gemm_cost<typename Cs::C0>(m, n, sms, Cs::REL[0]);
-  const double c1 = gemm_cost<typename Cs::C1>(m, n, sms, Cs::REL[1]);
-  const double c2 = gemm_cost<typename Cs::C2>(m, n, sms, Cs::REL[2]);
+  const double* rel = VAR == BRANCH_FREE ? Cs::REL : Cs::REL_STD;
+  const double c0 = gemm_cost<typename Cs::C0>(m, n, sms, rel[0]);
+  const double c1 = gemm_cost<typename Cs::C1>(m, n, sms, rel[1]);
+  const double c2 = gemm_cost<typename Cs::C2>(m, n, sms, rel[2]);
   return (c1 < c0 && c1 <= c2) ? 1 : (c2 < c0 && c2 < c1) ? 2 : 0;
 }
 
@@ -121,7 +128,7 @@ struct GemmLaunch {
                  int64_t bsB, int64_t bsC, int64_t bsCi, cudaStream_t st) {
     using Cs = GemmCfgs<K>;
     // batched products (the Strassen leaves) keep slot 0
-    const int slot = (batch == 1 && Cin == nullptr) ? gemm_pick<K>(m, n) : 0;
+    const int slot = (batch == 1 && Cin == nullptr) ? gemm_pick<K, VAR>(m, n) : 0;
     if (slot == 1)
       return gemm_launch<K, VAR, typename Cs::C1>(A, lda, sA, B, ldb, sB, C, ldc, sC, m, n, kd, Cin,
                                                   ldci, sCi, batch, bsA, bsB, bsC, bsCi, st);
