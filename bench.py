@@ -287,12 +287,18 @@ def run_ours(args):
     e2e = None
     if not args.no_e2e:
         # pinned host buffers, pre-split into row / point chunks so each chunk
-        # streams in (and its result out) while the previous one computes
-        # GEMMs are not split (a row chunk would add a partial last wave per
-        # launch); the smallest-input product goes first so the others' inputs
-        # stream in behind it, and Horner's points are chunked 8 ways so its
-        # output drains while the later chunks compute.
-        NCH_G, NCH_H = 1, 8
+        # streams in (and its result out) while the previous one computes.
+        # Order: the first Horner point chunk (a small transfer) starts the
+        # step, so the GEMM inputs stream in behind its compute; the GEMMs
+        # follow smallest-input first (not split: a row chunk would add a
+        # partial last wave per launch); the remaining Horner chunks end the
+        # step, so only one small chunk's input and one small chunk's output
+        # are not hidden behind compute.
+        NCH_G = 1
+        # Horner chunks of whole waves (resident CTAs x 256 points; the QD
+        # kernel holds 8 CTAs per SM) so no chunk but the last ends on a
+        # partially filled wave
+        wave_pts = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count * 8 * 256
         a_pin, b_pin, c_pin = [], [], []
         for g in sorted(gdata, key=lambda g: g["k"] * g["n"] ** 2):
             lo, hi = g["lo"], g["hi"]
@@ -302,7 +308,7 @@ def run_ours(args):
             b_pin.append(torch.from_numpy(g["b_host"]).pin_memory())
             c_pin.append([torch.empty((g["k"], r1 - r0, g["n"]), dtype=torch.float64).pin_memory()
                           for r0, r1 in zip(cuts[:-1], cuts[1:]) if r1 > r0])
-        pcuts = np.linspace(plo, phi, NCH_H + 1).astype(int)
+        pcuts = np.unique(np.r_[np.arange(plo, phi, 4 * wave_pts), phi]).astype(int)
         x_pin = [torch.from_numpy(np.ascontiguousarray(xh[:, p0:p1])).pin_memory()
                  for p0, p1 in zip(pcuts[:-1], pcuts[1:]) if p1 > p0]
         y_pin = [torch.empty_like(t).pin_memory() for t in x_pin]
@@ -321,25 +327,25 @@ def run_ours(args):
             soon as it lands, and its result copied D2H on a second copy stream
             behind it, so transfers overlap compute."""
             cur = torch.cuda.current_stream()
-            h2d_stream.wait_stream(cur)
+            # no wait on `cur` here: the next step's inputs may stream in
+            # while this step still computes (the device buffers are fresh
+            # allocations, released to the allocator only after the compute
+            # stream's use: record_stream below)
+
+            def stage(host):
+                dev_t = host.to("cuda", non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record()
+                return dev_t, ev
+
             staged = []
             with torch.cuda.stream(h2d_stream):
+                cf = c_pin_coeffs.to("cuda", non_blocking=True)
+                xs = [stage(x_pin[0])] if x_pin else []
                 for bp, chunks in zip(b_pin, a_pin):
                     B = bp.to("cuda", non_blocking=True)
-                    parts = []
-                    for ap in chunks:
-                        A = ap.to("cuda", non_blocking=True)
-                        ev = torch.cuda.Event()
-                        ev.record()
-                        parts.append((A, ev))
-                    staged.append((B, parts))
-                cf = c_pin_coeffs.to("cuda", non_blocking=True)
-                xs = []
-                for xp in x_pin:
-                    X = xp.to("cuda", non_blocking=True)
-                    ev = torch.cuda.Event()
-                    ev.record()
-                    xs.append((X, ev))
+                    staged.append((B, [stage(ap) for ap in chunks]))
+                xs += [stage(xp) for xp in x_pin[1:]]
 
             def drain(dev_t, host_t):
                 d2h_stream.wait_stream(cur)
@@ -347,6 +353,20 @@ def run_ours(args):
                     host_t.copy_(dev_t, non_blocking=True)
                 dev_t.record_stream(d2h_stream)
 
+            P = None
+
+            def horner_chunk(i):
+                nonlocal P
+                X, ev = xs[i]
+                cur.wait_event(ev)
+                X.record_stream(cur)
+                if P is None:
+                    cf.record_stream(cur)
+                    P = mw.MWPolynomial(cf)
+                drain(mw.horner_eval_batched(P, mw.LaneBatch(X), BF).planes, y_pin[i])
+
+            if xs:
+                horner_chunk(0)
             for (B, parts), cps in zip(staged, c_pin):
                 Bm = None
                 for (A, ev), cp in zip(parts, cps):
@@ -356,14 +376,8 @@ def run_ours(args):
                         B.record_stream(cur)
                         Bm = mw.MWMatrix(B)
                     drain(mw.matmul(mw.MWMatrix(A), Bm, plan).planes, cp)
-            P = None
-            for (X, ev), yp in zip(xs, y_pin):
-                cur.wait_event(ev)
-                X.record_stream(cur)
-                if P is None:
-                    cf.record_stream(cur)
-                    P = mw.MWPolynomial(cf)
-                drain(mw.horner_eval_batched(P, mw.LaneBatch(X), BF).planes, yp)
+            for i in range(1, len(xs)):
+                horner_chunk(i)
             cur.wait_stream(d2h_stream)
 
         for _ in range(max(1, min(args.warmup, 2))):
