@@ -715,7 +715,7 @@ __device__ __forceinline__ Cx<K, VAR> cx_get(const double* base, int idx) {
 // scripts/time_dk_shard.py: TD 18.6 -> 17.2, QD 36.4 -> 32.5 us at 64
 // roots; with 2 roots per CTA the extra warps cost more than they save).
 template <int R>
-__host__ __device__ constexpr int dk_treem_warps() { return R == 1 ? 6 : 5 * R; }
+__host__ __device__ constexpr int dk_treem_warps() { return R == 1 ? 8 : 5 * R; }
 
 // Phase timestamps for the tuning harness only (csrc/tune/dk_phase.cu
 // defines MW_DK_PROFILE); compiled out of the product.
@@ -808,9 +808,14 @@ __global__ void __launch_bounds__(32 * dk_treem_warps<R>(), R == 2 ? 2 : 1)
   const int v32 = (int)(valid < 32 ? valid : 32);
   const int b32 = (int)(nblocks < 32 ? nblocks : 32);
   const int64_t rbase = i0 + (int64_t)blockIdx.x * R;
+  // role of this warp in the first phase; with one root per CTA the powers
+  // and w^32 warps sit on sub-partitions 2 and 3 (warps 6, 7; 4 and 5 idle)
+  // so the denominator warps (sub-partitions 0, 1: the longest chains)
+  // issue alone
+  const int rw = R == 1 ? (warp < 4 ? warp : warp == 6 ? 4 : warp == 7 ? 5 : 99) : warp;
   if (threadIdx.x == 0) MW_DK_MARK(0);
 
-  if (warp < 2 * R) {
+  if (rw < 2 * R) {
     // ---- denominator partial u = lane + 32h of root r
     const int r = warp >> 1, h = warp & 1;
     const int64_t i = rbase + r;
@@ -834,7 +839,7 @@ __global__ void __launch_bounds__(32 * dk_treem_warps<R>(), R == 2 ? 2 : 1)
     }
     cx_put<K, VAR>(den_s + (size_t)r * 2 * K * 64, u, v);
     if (threadIdx.x == 0) MW_DK_MARK(1);
-  } else if (warp < 4 * R) {
+  } else if (rw < 4 * R) {
     // ---- numerator block u = lane + 32h of root r (Horner from its top)
     const int r = (warp - 2 * R) >> 1, h = warp & 1;
     const int64_t i = rbase + r;
@@ -857,12 +862,12 @@ __global__ void __launch_bounds__(32 * dk_treem_warps<R>(), R == 2 ? 2 : 1)
     }
     cx_put<K, VAR>(num_s + (size_t)r * 2 * K * 64, u, p);
     if (threadIdx.x == 64 * R) MW_DK_MARK(2);
-  } else if (warp < 5 * R) {
+  } else if (rw < 5 * R) {
     // ---- powers of root r: x_l = w^l (Hillis-Steele scan), x_l * w^32
-    const int r = warp - 4 * R;
+    const int r = rw - 4 * R;
     const int64_t i = rbase + r;
     asm volatile("griddepcontrol.wait;" ::: "memory");
-    if (threadIdx.x == 128 * R) MW_DK_MARK(3);
+    if (rw == 4 * R && lane == 0) MW_DK_MARK(3);
     Cx<K, VAR> w = c_one<K, VAR>(), w32 = c_one<K, VAR>();
     if (i < i1) {
       const int64_t q = i - i0;
@@ -884,7 +889,7 @@ __global__ void __launch_bounds__(32 * dk_treem_warps<R>(), R == 2 ? 2 : 1)
       w32 = cx_get<K, VAR>(pw + (size_t)R * 2 * 2 * K * 32 + (size_t)r * 2 * K * 64, 0);
     }
     const Cx<K, VAR> xh = c_mul_ol(x, w32);
-    if (threadIdx.x == 128 * R) MW_DK_MARK(4);
+    if (rw == 4 * R && lane == 0) MW_DK_MARK(4);
     double* pr = pw + (size_t)r * 2 * 2 * K * 32;
 #pragma unroll
     for (int c = 0; c < K; ++c) {
@@ -893,9 +898,9 @@ __global__ void __launch_bounds__(32 * dk_treem_warps<R>(), R == 2 ? 2 : 1)
       pr[(1 * 2 * K + c) * 32 + lane] = xh.re.c[c];
       pr[(1 * 2 * K + K + c) * 32 + lane] = xh.im.c[c];
     }
-  } else if constexpr (R == 1) {
+  } else if (R == 1 && rw == 5) {
     // ---- w^32 of root r: five squarings of w (beside the scan)
-    const int r = warp - 5 * R;
+    const int r = rw - 5 * R;
     const int64_t i = rbase + r;
     asm volatile("griddepcontrol.wait;" ::: "memory");
     Cx<K, VAR> w32 = c_one<K, VAR>();
