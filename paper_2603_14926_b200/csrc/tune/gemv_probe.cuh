@@ -290,3 +290,79 @@ __global__ void __launch_bounds__(128 * RPC)
   }
 }
 }  // namespace mw
+
+namespace mw {
+// gemv_tree_kernel's partials and tree (bit-identical) with x staged in
+// shared memory once per CTA (RPC rows share it): the fold loads only A
+// from global memory; x comes from shared memory.
+template <int K, int VAR, int RPC, int D>
+__global__ void __launch_bounds__(128 * RPC, 1)
+    gemv_xs_kernel(const double* __restrict__ A, int64_t lda, int64_t sA,
+                   const double* __restrict__ x, int64_t sx, double* __restrict__ y, int64_t sy,
+                   int64_t m, int64_t n) {
+  constexpr int P = 128;
+  extern __shared__ double xs[];  // [K][n], then part [RPC][K][P]
+  double* part = xs + (size_t)K * n;
+  const int u = threadIdx.x % P, slot = threadIdx.x / P;
+  for (int64_t e = threadIdx.x; e < (int64_t)K * n; e += blockDim.x) {
+    const int64_t c = e / n, t = e % n;
+    xs[e] = x[c * sx + t];
+  }
+  __syncthreads();
+  for (int64_t i = blockIdx.x * (int64_t)RPC + slot; i - slot < m; i += (int64_t)gridDim.x * RPC) {
+    const bool live = i < m;
+    const double* row = A + (live ? i : 0) * lda;
+    V<K> acc = zero<K>();
+    int64_t t = u;
+    for (; t + (D - 1) * P < n; t += D * P) {
+      V<K> a[D];
+#pragma unroll
+      for (int d = 0; d < D; ++d) a[d] = load<K>(row, sA, t + d * P);
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        V<K> xv;
+#pragma unroll
+        for (int c = 0; c < K; ++c) xv.c[c] = xs[c * n + t + d * P];
+        acc = Ops<K, VAR>::add(acc, Ops<K, VAR>::mul(a[d], xv));
+      }
+    }
+    for (; t < n; t += P) {
+      V<K> xv;
+#pragma unroll
+      for (int c = 0; c < K; ++c) xv.c[c] = xs[c * n + t];
+      acc = Ops<K, VAR>::add(acc, Ops<K, VAR>::mul(load<K>(row, sA, t), xv));
+    }
+    const int64_t valid = n < P ? n : P;
+#pragma unroll
+    for (int c = 0; c < K; ++c) part[(slot * K + c) * P + u] = acc.c[c];
+    __syncthreads();
+#pragma unroll 1
+    for (int s = 1; s < P; s <<= 1) {
+      const int per_row = P / (2 * s);
+      const int tid = threadIdx.x;
+      if (tid < RPC * per_row) {
+        const int r = tid / per_row, idx = 2 * s * (tid % per_row);
+        if (idx + s < valid) {
+          V<K> l, rr;
+#pragma unroll
+          for (int c = 0; c < K; ++c) {
+            l.c[c] = part[(r * K + c) * P + idx];
+            rr.c[c] = part[(r * K + c) * P + idx + s];
+          }
+          const V<K> sum = Ops<K, VAR>::add(l, rr);
+#pragma unroll
+          for (int c = 0; c < K; ++c) part[(r * K + c) * P + idx] = sum.c[c];
+        }
+      }
+      __syncthreads();
+    }
+    if (u == 0 && live) {
+      V<K> r0;
+#pragma unroll
+      for (int c = 0; c < K; ++c) r0.c[c] = part[(slot * K + c) * P];
+      store<K>(y, sy, i, r0);
+    }
+    __syncthreads();
+  }
+}
+}  // namespace mw
