@@ -176,6 +176,13 @@ static int gemv_xs_launch(const double* A, const double* x, double* y, int64_t m
   kern<<<(unsigned)grid, 128 * RPC, smem, st>>>(A, n, m * n, x, n, y, m, m, n);
   return launch_status();
 }
+template <int K, int RPC, int D>
+static int gemv_cs_launch(const double* A, const double* x, double* y, int64_t m, int64_t n,
+                          cudaStream_t st) {
+  gemv_cs_kernel<K, BRANCH_FREE, RPC, D><<<(unsigned)((m + RPC - 1) / RPC), 128 * RPC, 0, st>>>(
+      A, n, m * n, x, n, y, m, m, n);
+  return launch_status();
+}
 template <int K>
 static int gemv_run(int cfg, const double* A, const double* x, double* y, int64_t m, int64_t n,
                     cudaStream_t st) {
@@ -239,10 +246,12 @@ static int gemv_run(int cfg, const double* A, const double* x, double* y, int64_
     case 56: return gemv_xs_launch<K, 6, 4, 1>(A, x, y, m, n, st);
     case 57: return gemv_xs_launch<K, 4, 4, 2>(A, x, y, m, n, st);
     case 58: return gemv_xs_launch<K, 8, 2, 1>(A, x, y, m, n, st);
+    case 59: return gemv_cs_launch<K, 2, 4>(A, x, y, m, n, st);
+    case 60: return gemv_cs_launch<K, 1, 4>(A, x, y, m, n, st);
     default: return MW_ERR_INVALID;
   }
 }
-extern "C" int mwt_gemv_num_configs(void) { return 59; }
+extern "C" int mwt_gemv_num_configs(void) { return 61; }
 extern "C" const char* mwt_gemv_config_name(int cfg) {
   static const char* names[] = {"W4_R2_D4", "W1_R8_D8", "W1_R8_D4", "W2_R4_D4", "W2_R4_D8",
                                 "W4_R2_D2", "W4_R1_D4", "W8_R1_D2", "st_R2_D4_S2", "st_R2_D4_S3",
@@ -255,8 +264,8 @@ extern "C" const char* mwt_gemv_config_name(int cfg) {
                                 "wr_Q8_J2_S4", "wr_Q8_J2_S3", "wr_Q6_J2_S4", "wr_Q6_J4_S2", "wr_Q4_J4_S3",
                                 "wr_Q8_J1_S6", "wr_Q6_J2_S3", "mc_C2_D2", "mc_C2_D1", "mc_C2_D2_R2",
                                 "mc_C2_D1_R2", "mc_C1_D4", "mc_C4_D1", "v2_D2_R2", "v2_D2_R1", "v2_D1_R2", "v2_D4_R1",
-                                "xs_R8_D4", "xs_R6_D4", "xs_R4_D4_c2", "xs_R8_D2"};
-  return (cfg >= 0 && cfg < 59) ? names[cfg] : "?";
+                                "xs_R8_D4", "xs_R6_D4", "xs_R4_D4_c2", "xs_R8_D2", "cs_R2_D4", "cs_R1_D4"};
+  return (cfg >= 0 && cfg < 61) ? names[cfg] : "?";
 }
 extern "C" int mwt_gemv(int cfg, int k, const double* A, const double* x, double* y, int64_t m,
                         int64_t n, void* stream) {

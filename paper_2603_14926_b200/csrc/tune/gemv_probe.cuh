@@ -366,3 +366,65 @@ __global__ void __launch_bounds__(128 * RPC, 1)
   }
 }
 }  // namespace mw
+
+namespace mw {
+// gemv_tree_kernel with A read through streaming loads (ld.global.cs:
+// evict-first, A is read exactly once); same partials and tree.
+template <int K, int VAR, int RPC, int D>
+__global__ void __launch_bounds__(128 * RPC)
+    gemv_cs_kernel(const double* __restrict__ A, int64_t lda, int64_t sA,
+                   const double* __restrict__ x, int64_t sx, double* __restrict__ y, int64_t sy,
+                   int64_t m, int64_t n) {
+  constexpr int P = 128;
+  const int u = threadIdx.x % P, slot = threadIdx.x / P;
+  const int64_t i = blockIdx.x * (int64_t)RPC + slot;
+  const bool live = i < m;
+  const double* row = A + (live ? i : 0) * lda;
+  V<K> acc = zero<K>();
+  int64_t t = u;
+  for (; t + (D - 1) * P < n; t += D * P) {
+    V<K> a[D], xv[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+#pragma unroll
+      for (int c = 0; c < K; ++c) a[d].c[c] = __ldcs(row + c * sA + t + d * P);
+      xv[d] = load<K>(x, sx, t + d * P);
+    }
+#pragma unroll
+    for (int d = 0; d < D; ++d) acc = Ops<K, VAR>::add(acc, Ops<K, VAR>::mul(a[d], xv[d]));
+  }
+  for (; t < n; t += P)
+    acc = Ops<K, VAR>::add(acc, Ops<K, VAR>::mul(load<K>(row, sA, t), load<K>(x, sx, t)));
+  __shared__ double part[RPC][K][P];
+#pragma unroll
+  for (int c = 0; c < K; ++c) part[slot][c][u] = acc.c[c];
+  __syncthreads();
+  const int64_t valid = n < P ? n : P;
+#pragma unroll 1
+  for (int s = 1; s < P; s <<= 1) {
+    const int per_row = P / (2 * s);
+    const int tid = threadIdx.x;
+    if (tid < RPC * per_row) {
+      const int r = tid / per_row, idx = 2 * s * (tid % per_row);
+      if (idx + s < valid) {
+        V<K> l, rr;
+#pragma unroll
+        for (int c = 0; c < K; ++c) {
+          l.c[c] = part[r][c][idx];
+          rr.c[c] = part[r][c][idx + s];
+        }
+        const V<K> sum = Ops<K, VAR>::add(l, rr);
+#pragma unroll
+        for (int c = 0; c < K; ++c) part[r][c][idx] = sum.c[c];
+      }
+    }
+    __syncthreads();
+  }
+  if (u == 0 && live) {
+    V<K> r0;
+#pragma unroll
+    for (int c = 0; c < K; ++c) r0.c[c] = part[slot][c][0];
+    store<K>(y, sy, i, r0);
+  }
+}
+}  // namespace mw
