@@ -1044,22 +1044,65 @@ __global__ void __launch_bounds__(32 * dk_treem_warps<R>(), R == 2 ? 2 : 1)
   __syncthreads();
 
   if (threadIdx.x == 0) MW_DK_MARK(7);
-  if (warp == 2 * R) {
-    if (lane < R) {
-      const int64_t i = rbase + lane;
-      if (i < i1) {
-        Cx<K, VAR> z;
-        z.re = load<K>(zre, sz, i);
-        z.im = load<K>(zim, sz, i);
-        const Cx<K, VAR> acc = cx_get<K, VAR>(num_s + (size_t)lane * 2 * K * 64, 0);
-        const Cx<K, VAR> den = cx_get<K, VAR>(den_s + (size_t)lane * 2 * K * 64, 0);
-        dk_tail<K, VAR, PEER>(acc, den, z, zre_out, zim_out, so, step_mag, i, &peers);
+  // Tail (dk_tail's ops, roots.py:297-308) split over two warps, lane r =
+  // root r: warp 2R forms |den|^2 and its Newton reciprocal (the dependent
+  // chain), warp 2R+1 meanwhile forms the numerator acc * conj(den); after
+  // one hand-off each applies the reciprocal to its half and stores it.
+  if (warp == 2 * R || warp == 2 * R + 1) {
+    const bool chain = warp == 2 * R;
+    const int64_t i = rbase + lane;
+    const bool act = lane < R && i < i1;
+    double* my = pw + (size_t)(lane < R ? lane : 0) * (3 * K + 1);  // num_re, num_im, rcp, step_im0
+    Cx<K, VAR> z, acc, den;
+    V<K> num, step;
+    if (act) {
+      z.re = load<K>(zre, sz, i);
+      z.im = load<K>(zim, sz, i);
+      acc = cx_get<K, VAR>(num_s + (size_t)lane * 2 * K * 64, 0);
+      den = cx_get<K, VAR>(den_s + (size_t)lane * 2 * K * 64, 0);
+      if (chain) {
+        const V<K> mag = O::add(O::mul(den.re, den.re), O::mul(den.im, den.im));
+        const V<K> rcp = recip_newton<K, VAR>(mag);
+#pragma unroll
+        for (int c = 0; c < K; ++c) my[2 * K + c] = rcp.c[c];
+      } else {
+        const V<K> num_re = O::add(O::mul(acc.re, den.re), O::mul(acc.im, den.im));
+        const V<K> num_im = O::add(O::mul(acc.im, den.re), neg(O::mul(acc.re, den.im)));
+#pragma unroll
+        for (int c = 0; c < K; ++c) {
+          my[c] = num_re.c[c];
+          my[K + c] = num_im.c[c];
+        }
       }
     }
-    if (lane == 0) MW_DK_MARK(8);
-    if constexpr (PEER) {
-      __syncwarp();
-      if (lane == 0) dk_peer_ticket(peers);
+    bar_sync_n(12, 64);
+    if (act) {
+      V<K> rcp;
+#pragma unroll
+      for (int c = 0; c < K; ++c) {
+        rcp.c[c] = my[2 * K + c];
+        num.c[c] = my[(chain ? 0 : K) + c];
+      }
+      step = O::mul(num, rcp);
+      const V<K> nz = O::add(chain ? z.re : z.im, neg(step));
+      double* outp = chain ? zre_out : zim_out;
+      store<K>(outp, so, i, nz);
+      if constexpr (PEER) {
+        for (int p = 0; p < peers.world; ++p) {
+          if (p == peers.rank) continue;
+          store<K>(peers.out[p] + (chain ? 0 : (int64_t)K * so), so, i, nz);
+        }
+      }
+      if (!chain) my[3 * K] = step.c[0];
+    }
+    bar_sync_n(12, 64);
+    if (chain) {
+      if (act) step_mag[i] = hypot(step.c[0], my[3 * K]);
+      if (lane == 0) MW_DK_MARK(8);
+      if constexpr (PEER) {
+        __syncwarp();
+        if (lane == 0) dk_peer_ticket(peers);
+      }
     }
   }
 }
