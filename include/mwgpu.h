@@ -276,7 +276,7 @@ int mw_dk_sweep_ws(int k, int variant, const double* coeffs, int64_t sc,
                    int64_t so, double* step_mag, int* flag_dev, int exact_order,
                    double* ws, void* stream);
 
-/* Tuning knob of the exact-order sweep: roots per CTA (1..32, default 16).
+/* Tuning knob of the exact-order sweep: roots per CTA (1..32, default 32).
  * Results do not depend on it (each root is one chain in reference order). */
 int mw_dk_exact_set_roots_per_cta(int roots);
 

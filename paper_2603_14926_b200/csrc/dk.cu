@@ -3,7 +3,7 @@
 
 namespace mw {
 
-int g_dk_exact_roots = 16;
+int g_dk_exact_roots = 32;
 int g_dk_exact_split = 1;
 int g_dk_tree_roots = -1;
 

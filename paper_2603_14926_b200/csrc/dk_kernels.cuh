@@ -143,7 +143,7 @@ __device__ __forceinline__ void dk_tail(const Cx<K, VAR>& acc, const Cx<K, VAR>&
 constexpr int DK_EXACT_ROOTS = 32;  // lanes per role warp (two warps: num + den)
 // Roots handled per CTA (<= 32; lanes beyond it idle).  Fewer roots per
 // CTA spread the 2n sequential chains over more SM sub-partitions.
-extern int g_dk_exact_roots;  // default 16 (dk.cu)
+extern int g_dk_exact_roots;  // default 32 (dk.cu; 16 and 8 measured 0.5-5 % slower)
 // 1: split-pair exact kernel (dk_exact2_kernel) for TD and QD, 0:
 // single-warp chains everywhere.  Measured (config 5, us/sweep, eager,
 // single -> split): TD 353 -> 295 (one hand-off per step), QD 745 -> 575

@@ -28,4 +28,4 @@ for k in (2, 3, 4):
             print(f"k={k} split={split} roots/CTA={r:2d}: {e0.elapsed_time(e1)/10*1e3:8.1f} us/sweep  "
                   f"bitwise_same={same}", flush=True)
     lib.mw_dk_exact_set_split(1)
-    lib.mw_dk_exact_set_roots_per_cta(16)
+    lib.mw_dk_exact_set_roots_per_cta(32)

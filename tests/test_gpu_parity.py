@@ -995,7 +995,7 @@ def test_dk_tree_powers_kernel_path_matches_in_warp_path(k, v):
     C, R, I = (torch.from_numpy(a).cuda() for a in (coeffs, zre, zim))
     i0, i1 = 7, 141
     outs = []
-    for use_ws, roots in ((False, 2), (True, 0), (True, 2), (True, 4)):
+    for use_ws, roots in ((False, 2), (True, 0), (True, 1), (True, 2), (True, 4)):
         lib.mw_dk_tree_set_roots_per_cta(roots)
         ore, oim = torch.zeros_like(R), torch.zeros_like(I)
         mag = torch.zeros(n, dtype=torch.float64, device="cuda")
@@ -1007,7 +1007,7 @@ def test_dk_tree_powers_kernel_path_matches_in_warp_path(k, v):
             rc = lib.mw_dk_sweep_ws(*args, ws.data_ptr(), _lib.stream_handle(R.device))
         else:
             rc = lib.mw_dk_sweep(*args, _lib.stream_handle(R.device))
-        lib.mw_dk_tree_set_roots_per_cta(4)
+        lib.mw_dk_tree_set_roots_per_cta(-1)  # back to the default (auto)
         _lib.check(rc, "sweep")
         outs.append((ore.cpu().numpy(), oim.cpu().numpy(), mag.cpu().numpy()))
     for o in outs[1:]:  # in-warp powers == powers kernel, for every roots-per-CTA form
