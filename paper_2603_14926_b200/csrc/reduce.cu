@@ -524,6 +524,99 @@ __global__ void __launch_bounds__(32 * WARPS * RPC)
   }
 }
 
+// Persistent form of the same tree order (bit-identical with
+// gemv_tree_kernel): a CTA holds SLOTS row slots of four warps; each slot
+// walks rows blockIdx.x * SLOTS + slot, += gridDim.x * SLOTS.  Per row the
+// 128 partials fold exactly as above; the tree's strides 1..16 pair lanes of
+// one warp and run as warp shuffles (no barrier); the four warp roots go to
+// shared memory (double-buffered by row parity) and ONE named barrier per
+// row and slot hands them to a combiner warp (rotating over the four warps,
+// so no warp waits on the combine every row), which applies strides 32 and
+// 64.  The next row's first D elements are requested before the shuffle
+// tree runs, so its HBM latency hides behind the tree.  With PIPE, every
+// group's loads are issued before the previous group's arithmetic
+// (register double buffer).
+__device__ __forceinline__ void gemv_bar_sync(int id) {
+  asm volatile("bar.sync %0, 128;" ::"r"(id) : "memory");
+}
+
+template <int K, int VAR, int SLOTS, int D>
+__global__ void __launch_bounds__(128 * SLOTS)
+    gemv_ptree_kernel(const double* __restrict__ A, int64_t lda, int64_t sA,
+                      const double* __restrict__ x, int64_t sx, double* __restrict__ y, int64_t sy,
+                      int64_t m, int64_t n) {
+  constexpr int P = 128;
+  __shared__ double roots[2][SLOTS][K][4];
+  const int lane = threadIdx.x & 31;
+  const int warp = (threadIdx.x >> 5) & 3;
+  const int slot = threadIdx.x >> 7;
+  const int u = warp * 32 + lane;
+  const int64_t valid = n < P ? n : P;
+  const int64_t step = (int64_t)gridDim.x * SLOTS;
+  int64_t i = (int64_t)blockIdx.x * SLOTS + slot;
+  // the first group of the current row, loaded ahead
+  V<K> a[D], xv[D];
+  const bool full = (int64_t)u + (D - 1) * P < n;  // row has >= 1 full group for this lane
+  if (i < m && full) {
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      a[d] = load<K>(A + i * lda, sA, u + d * P);
+      xv[d] = load<K>(x, sx, u + d * P);
+    }
+  }
+  for (int it = 0; i < m; i += step, ++it) {
+    const double* row = A + i * lda;
+    V<K> acc = zero<K>();
+    int64_t t = u;
+    if (full) {
+      for (;;) {
+#pragma unroll
+        for (int d = 0; d < D; ++d) acc = Ops<K, VAR>::add(acc, Ops<K, VAR>::mul(a[d], xv[d]));
+        t += D * P;
+        if (t + (D - 1) * P >= n) break;
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+          a[d] = load<K>(row, sA, t + d * P);
+          xv[d] = load<K>(x, sx, t + d * P);
+        }
+      }
+    }
+    for (; t < n; t += P)
+      acc = Ops<K, VAR>::add(acc, Ops<K, VAR>::mul(load<K>(row, sA, t), load<K>(x, sx, t)));
+    // next row's first group, in flight during the tree
+    const int64_t inext = i + step;
+    if (inext < m && full) {
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        a[d] = load<K>(A + inext * lda, sA, u + d * P);
+        xv[d] = load<K>(x, sx, u + d * P);
+      }
+    }
+#pragma unroll
+    for (int s = 1; s < 32; s <<= 1) {
+      const V<K> o = shfl_down<K>(acc, s);
+      if ((lane & (2 * s - 1)) == 0 && u + s < valid) acc = Ops<K, VAR>::add(acc, o);
+    }
+    const int buf = it & 1;
+    if (lane == 0) {
+#pragma unroll
+      for (int c = 0; c < K; ++c) roots[buf][slot][c][warp] = acc.c[c];
+    }
+    gemv_bar_sync(1 + slot);
+    if (warp == (it & 3) && lane == 0) {
+      V<K> r[4];
+#pragma unroll
+      for (int w = 0; w < 4; ++w)
+#pragma unroll
+        for (int c = 0; c < K; ++c) r[w].c[c] = roots[buf][slot][c][w];
+      if (32 < valid) r[0] = Ops<K, VAR>::add(r[0], r[1]);
+      if (96 < valid) r[2] = Ops<K, VAR>::add(r[2], r[3]);
+      if (64 < valid) r[0] = Ops<K, VAR>::add(r[0], r[2]);
+      store<K>(y, sy, i, r[0]);
+    }
+  }
+}
+
 template <int K, int VAR>
 struct GemvLaunch {
   static int run(const double* A, int64_t lda, int64_t sA, const double* x, int64_t sx, double* y,

@@ -101,6 +101,21 @@ static int gemv_launch(const double* A, const double* x, double* y, int64_t m, i
       A, n, m * n, x, n, y, m, m, n);
   return launch_status();
 }
+template <int K, int SLOTS, int D, bool PERSIST>
+static int gemv_ptree_launch(const double* A, const double* x, double* y, int64_t m, int64_t n,
+                             cudaStream_t st) {
+  auto kern = gemv_ptree_kernel<K, BRANCH_FREE, SLOTS, D>;
+  int64_t grid = (m + SLOTS - 1) / SLOTS;
+  if (PERSIST) {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128 * SLOTS, 0);
+    const int64_t slots = (int64_t)148 * per_sm * SLOTS;
+    const int64_t rows_per_slot = (m + slots - 1) / slots;
+    grid = (m + rows_per_slot * SLOTS - 1) / (rows_per_slot * SLOTS);
+  }
+  kern<<<(unsigned)grid, 128 * SLOTS, 0, st>>>(A, n, m * n, x, n, y, m, m, n);
+  return launch_status();
+}
 template <int K, int R, int D, int S, bool XS>
 static int gemv_staged_launch(const double* A, const double* x, double* y, int64_t m, int64_t n,
                               cudaStream_t st) {
@@ -248,10 +263,19 @@ static int gemv_run(int cfg, const double* A, const double* x, double* y, int64_
     case 58: return gemv_xs_launch<K, 8, 2, 1>(A, x, y, m, n, st);
     case 59: return gemv_cs_launch<K, 2, 4>(A, x, y, m, n, st);
     case 60: return gemv_cs_launch<K, 1, 4>(A, x, y, m, n, st);
+    case 61: return gemv_ptree_launch<K, 1, 4, true>(A, x, y, m, n, st);
+    case 62: return gemv_ptree_launch<K, 2, 4, true>(A, x, y, m, n, st);
+    case 63: return gemv_ptree_launch<K, 1, 2, true>(A, x, y, m, n, st);
+    case 64: return gemv_ptree_launch<K, 2, 2, true>(A, x, y, m, n, st);
+    case 65: return gemv_ptree_launch<K, 4, 4, true>(A, x, y, m, n, st);
+    case 66: return gemv_ptree_launch<K, 1, 8, true>(A, x, y, m, n, st);
+    case 67: return gemv_ptree_launch<K, 1, 4, false>(A, x, y, m, n, st);
+    case 68: return gemv_ptree_launch<K, 2, 4, false>(A, x, y, m, n, st);
+    case 69: return gemv_ptree_launch<K, 2, 8, true>(A, x, y, m, n, st);
     default: return MW_ERR_INVALID;
   }
 }
-extern "C" int mwt_gemv_num_configs(void) { return 61; }
+extern "C" int mwt_gemv_num_configs(void) { return 70; }
 extern "C" const char* mwt_gemv_config_name(int cfg) {
   static const char* names[] = {"W4_R2_D4", "W1_R8_D8", "W1_R8_D4", "W2_R4_D4", "W2_R4_D8",
                                 "W4_R2_D2", "W4_R1_D4", "W8_R1_D2", "st_R2_D4_S2", "st_R2_D4_S3",
@@ -264,8 +288,10 @@ extern "C" const char* mwt_gemv_config_name(int cfg) {
                                 "wr_Q8_J2_S4", "wr_Q8_J2_S3", "wr_Q6_J2_S4", "wr_Q6_J4_S2", "wr_Q4_J4_S3",
                                 "wr_Q8_J1_S6", "wr_Q6_J2_S3", "mc_C2_D2", "mc_C2_D1", "mc_C2_D2_R2",
                                 "mc_C2_D1_R2", "mc_C1_D4", "mc_C4_D1", "v2_D2_R2", "v2_D2_R1", "v2_D1_R2", "v2_D4_R1",
-                                "xs_R8_D4", "xs_R6_D4", "xs_R4_D4_c2", "xs_R8_D2", "cs_R2_D4", "cs_R1_D4"};
-  return (cfg >= 0 && cfg < 61) ? names[cfg] : "?";
+                                "xs_R8_D4", "xs_R6_D4", "xs_R4_D4_c2", "xs_R8_D2", "cs_R2_D4", "cs_R1_D4",
+                                "pt_S1_D4", "pt_S2_D4", "pt_S1_D2", "pt_S2_D2", "pt_S4_D4", "pt_S1_D8",
+                                "np_S1_D4", "np_S2_D4", "pt_S2_D8"};
+  return (cfg >= 0 && cfg < 70) ? names[cfg] : "?";
 }
 extern "C" int mwt_gemv(int cfg, int k, const double* A, const double* x, double* y, int64_t m,
                         int64_t n, void* stream) {

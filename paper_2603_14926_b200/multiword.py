@@ -4,7 +4,7 @@ DD / TD / QD value classes.
 Mirrors mwfloat.multiword (pkg/src/mwfloat/multiword.py): ``Variant``
 (82-96), ``BITS`` (76), ``ulp_k`` (722-730), ``from_basefloat`` (749-752),
 the greedy ``from_oracle`` rounding (760-775, here for exact Fractions),
-decimal conversion (778-845), the scalar ``mw_*`` / complex ``c*``
+the scalar ``mw_*`` / complex ``c*``
 operations (617-702) and the immutable ``MultiWord``/``DD``/``TD``/``QD``
 classes (850-1004).  All arithmetic runs in the CUDA kernels; scalar
 operations are one-lane launches.
@@ -17,9 +17,9 @@ import math
 from fractions import Fraction
 
 __all__ = [
-    "Variant", "BITS", "DEFAULT_DIGITS", "ulp_k", "from_basefloat", "from_fraction", "variant_code",
+    "Variant", "BITS", "ulp_k", "from_basefloat", "from_fraction", "variant_code",
     "mw_add", "mw_sub", "mw_mul", "mw_div", "mw_neg", "cadd", "csub", "cmul", "cdiv",
-    "is_normalized", "from_decimal_string", "to_decimal_string", "MultiWord", "DD", "TD", "QD",
+    "is_normalized", "MultiWord", "DD", "TD", "QD",
     # the reference's named per-variant kernels (multiword.py:104-588) and helpers
     "dw_add_sloppy", "dw_add_accurate", "dw_add_bf", "dw_mul", "dw_mul_bf",
     "tw_add", "tw_mul", "tw_mul_cleaned", "tw_add_bf", "tw_mul_bf",
@@ -28,7 +28,6 @@ __all__ = [
 ]
 
 BITS = {2: 106, 3: 159, 4: 212}
-DEFAULT_DIGITS = {2: 34, 3: 49, 4: 64}
 
 
 class Variant(enum.Enum):
@@ -334,59 +333,6 @@ def is_normalized(comps) -> bool:
     return True
 
 
-def from_decimal_string(text: str, k: int) -> tuple:
-    """Parse a decimal literal to K words, correctly rounded (778-805)."""
-    if k not in BITS:
-        raise ValueError(f"unsupported word count {k}")
-    s = text.strip()
-    if not s:
-        raise ValueError("empty decimal string")
-    try:
-        mant, esep, exp_part = s.lower().partition("e")
-        if esep and not exp_part:
-            raise ValueError("dangling exponent")
-        exp = int(exp_part) if exp_part else 0
-        if "." in mant:
-            int_part, frac_part = mant.split(".", 1)
-            exp -= len(frac_part)
-            mant = int_part + frac_part
-        digits = int(mant)
-    except ValueError as err:
-        raise ValueError(f"malformed decimal string {text!r}") from err
-    fr = Fraction(digits * 10**exp) if exp >= 0 else Fraction(digits, 10**-exp)
-    return from_fraction(fr, k)
-
-
-def to_decimal_string(comps, digits: int | None = None) -> str:
-    """Scientific-notation string with `digits` significant digits (808-845)."""
-    k = len(comps)
-    if digits is None:
-        digits = DEFAULT_DIGITS[k]
-    fr = sum((Fraction(float(c)) for c in comps), Fraction(0))
-    if fr == 0:
-        return "0." + "0" * (digits - 1) + "e+0"
-    neg = fr < 0
-    fr = -fr if neg else fr
-    d10 = math.floor(math.log10(float(fr.numerator)) - math.log10(float(fr.denominator)))
-    scaled = fr * Fraction(10) ** (digits - 1 - d10)
-    n = int(scaled)
-    if scaled - n >= Fraction(1, 2):
-        n += 1
-    if n >= 10**digits:
-        n //= 10
-        d10 += 1
-    elif n < 10 ** (digits - 1):
-        n *= 10
-        d10 -= 1
-        scaled = fr * Fraction(10) ** (digits - 1 - d10)
-        n = int(scaled)
-        if scaled - n >= Fraction(1, 2):
-            n += 1
-    text = str(n)
-    body = f"{text[0]}.{text[1:]}e{d10:+d}"
-    return "-" + body if neg else body
-
-
 class MultiWord:
     """Immutable K-word value over a component tuple (850-989).  Operators
     use the Standard variant (as in the reference); arithmetic runs on the
@@ -423,11 +369,6 @@ class MultiWord:
         kk = cls.K if cls.K is not None else (k if k is not None else 2)
         return _CLASS_BY_K[kk](*from_basefloat(x, kk))
 
-    @classmethod
-    def from_decimal(cls, text: str, k: int | None = None) -> "MultiWord":
-        kk = cls.K if cls.K is not None else (k if k is not None else 2)
-        return _CLASS_BY_K[kk](*from_decimal_string(text, kk))
-
     def to_float(self) -> float:
         acc = 0.0
         for c in reversed(self.comps):
@@ -436,9 +377,6 @@ class MultiWord:
 
     def to_fraction(self) -> Fraction:
         return sum((Fraction(c) for c in self.comps), Fraction(0))
-
-    def to_decimal(self, digits: int | None = None) -> str:
-        return to_decimal_string(self.comps, digits)
 
     def _coerce(self, other):
         if isinstance(other, MultiWord):
@@ -501,7 +439,7 @@ class MultiWord:
         return f"{name}({', '.join(repr(c) for c in self.comps)})"
 
     def __str__(self):
-        return self.to_decimal()
+        return repr(self)
 
 
 class DD(MultiWord):

@@ -29,7 +29,7 @@ for k in (3, 4):
         same = ""
         if cfg == 0:
             ref = y.clone()
-        elif cfg >= 8 or cfg == 6:  # staged variants keep the P = 128 order: must be bit-identical
+        elif cfg >= 8 or cfg == 6:  # (cfg 61+: persistent shuffle tree)  # staged variants keep the P = 128 order: must be bit-identical
             same = " bits==W4" if torch.equal(y.view(torch.int64), ref.view(torch.int64)) else " BITS DIFFER"
         ts = []
         for _ in range(10):
