@@ -18,8 +18,11 @@ microbenchmark (8 independent chains per thread, all SMs), counting one
 DADD/DMUL/DFMA as one FP64 op; algorithmic FP64 ops per MAC are
 DD 29, TD 96, QD 209.
 
---impl reference times the reference algorithm's CPU implementation (the C
-restatement in oracle/, all host threads) on a bounded sample per step.
+--impl reference times the UNMODIFIED reference package (baseline/_ref,
+installed by scripts/install_reference.sh) through its own public calls,
+sharded over host processes, on a bounded sample per step; the C
+restatement in oracle/ (the port) is timed beside it.  `--gpus N` without a
+torchrun environment re-executes itself under torchrun with N ranks.
 """
 
 from __future__ import annotations
@@ -194,6 +197,10 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1 and args.backend == "nccl" and torch.cuda.device_count() < world:
+        print(f"bench.py: {world} NCCL ranks need {world} GPUs, {torch.cuda.device_count()} visible "
+              "(use --backend gloo to exercise the multi-rank logic on fewer GPUs)", file=sys.stderr)
+        sys.exit(3)
     dev_index = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(dev_index)
     if world > 1:
@@ -276,7 +283,12 @@ def run_ours(args):
         for i in range(n_parts):
             part_ms[i] += ev[s][i].elapsed_time(ev[s][i + 1])
     part_ms /= args.steps
+    my_shard = {"rank": rank, "device": dev_index, "ms_per_step": round(ms_total / args.steps, 3),
+                "gemm_rows": [[g["lo"], g["hi"]] for g in gdata], "horner_points": [plo, phi]}
+    rank_shards = [my_shard]
     if world > 1:
+        rank_shards = [None] * world
+        dist.all_gather_object(rank_shards, my_shard)
         tt = torch.tensor([ms_total], dtype=torch.float64, device="cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms_total = float(tt.item())
@@ -456,6 +468,9 @@ def run_ours(args):
                 "workload": "config3 GEMM DD n4096 + TD n2048 + QD n2048, config4 QD Horner deg1024 x 2^24 pts",
                 "gemm": [f"k{k} n{n}" for k, n in gemm_parts], "horner": horner,
                 "parallelism": f"rows/points sharded over {world} GPU(s), no collective",
+                "ranks": world, "backend": args.backend if world > 1 else None,
+                "shards": rank_shards,
+                "shared_gpus": (world > torch.cuda.device_count()) or None,
                 "l2": "inputs larger than L2 (GEMM DD A+B 537 MB, Horner x 537 MB); no flush",
                 "bit_exact": "GEMM naive order and Horner per point, vs reference",
             },
@@ -774,6 +789,7 @@ def cpu_sample(gemm_parts, horner, budget_rows=None, horner_pts=1 << 19):
     import oracle
     from paper_2603_14926_b200 import gen
 
+    oracle.set_threads(os.cpu_count() or 1)  # torchrun exports OMP_NUM_THREADS=1: use every host thread
     threads = oracle.max_threads()
     sample_rows = {2: 64, 3: 64, 4: 32} if budget_rows is None else budget_rows
     tot_mp = 0.0
@@ -797,44 +813,237 @@ def cpu_sample(gemm_parts, horner, budget_rows=None, horner_pts=1 << 19):
     tot_s += dt * (horner["npts"] / pts)
     tot_mp += 2 * horner["npts"] * horner["degree"]
     return {"value": round(tot_mp / tot_s / 1e9, 4), "unit": "G MP-ops/s", "cores": threads, "kind": "port",
+            **host_description(),
             "sample": "; ".join(desc) + " -- extrapolated linearly to the full step (uniform work per row/point)",
             "seconds_per_step_extrapolated": round(tot_s, 2)}
 
 
+# ------------------------------------------- the unmodified reference (CPU)
+REF_DIR = os.path.join(REPO, "baseline", "_ref")
+_REF_DATA = {}
+
+
+def host_description():
+    """CPU model (the reference's cli.hardware_tag recipe, cli.py:72-82),
+    logical and physical core counts."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.lower().startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    phys = None
+    try:
+        import psutil
+
+        phys = psutil.cpu_count(logical=False)
+    except Exception:
+        pass
+    return {"cpu_model": model, "logical_cpus": os.cpu_count(), "physical_cores": phys}
+
+
+def _ref_import():
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    import mwfloat  # noqa: F401  (baseline/_ref: the unmodified reference package)
+    from mwfloat import batch, linalg
+    from mwfloat.multiword import Variant
+
+    return batch, linalg, Variant
+
+
+def _ref_gemm_rows(job):
+    """linalg.matmul(A[r0:r1], B, naive, bf) -- the reference's own public
+    call on one row block (its partition, linalg.py:352-365), one process."""
+    k, r0, r1 = job
+    _, linalg, Variant = _ref_import()
+    a, b = _REF_DATA[("gemm", k)]
+    t = time.perf_counter()
+    linalg.matmul(linalg.MWMatrix(tuple(np.ascontiguousarray(a[c, r0:r1]) for c in range(k))),
+                  linalg.MWMatrix(tuple(b[c] for c in range(k))),
+                  linalg.MatMulPlan(scheme="naive", variant="bf"))
+    return time.perf_counter() - t
+
+
+def _ref_horner_chunk(job):
+    """Lane-batched Horner over the reference's own dispatch table
+    (_BATCH_MUL/_BATCH_ADD[(4, BF)], batch.py:178-194): bitwise equal to
+    poly.horner_eval per point (poly.py:89-96)."""
+    p0, p1 = job
+    batch, _, Variant = _ref_import()
+    coeffs, x = _REF_DATA["horner"]
+    k = coeffs.shape[0]
+    add, mul = batch._BATCH_ADD[k, Variant.BRANCH_FREE], batch._BATCH_MUL[k, Variant.BRANCH_FREE]
+    xs = tuple(np.ascontiguousarray(x[c, p0:p1]) for c in range(k))
+    t = time.perf_counter()
+    deg = coeffs.shape[1] - 1
+    acc = tuple(np.full(p1 - p0, coeffs[c, deg]) for c in range(k))
+    for i in range(deg - 1, -1, -1):
+        acc = add(mul(acc, xs), tuple(float(coeffs[c, i]) for c in range(k)))
+    return time.perf_counter() - t
+
+
+def reference_sample(gemm_parts, horner, procs, rows_per_proc, pts_per_proc, pool):
+    """One bounded sample of the step on the unmodified reference, sharded
+    across `procs` processes: per GEMM, `procs` row blocks
+    of rows_per_proc[k] rows; Horner, `procs` chunks of pts_per_proc points.
+    Returns (measured wall seconds, MP-ops done, extrapolated full-step
+    seconds, description)."""
+    wall = mp = full_s = 0.0
+    desc = []
+    for k, n in gemm_parts:
+        r = rows_per_proc[k]
+        jobs = [(k, i * r, (i + 1) * r) for i in range(procs) if (i + 1) * r <= n]
+        t = time.perf_counter()
+        pool.map(_ref_gemm_rows, jobs)
+        dt = time.perf_counter() - t
+        done = 2 * len(jobs) * r * n * n
+        wall += dt
+        mp += done
+        full_s += dt * (2 * n**3) / done
+        desc.append(f"gemm k{k} n{n}: {len(jobs) * r} rows in {dt:.2f}s")
+    c = pts_per_proc
+    jobs = [(i * c, (i + 1) * c) for i in range(procs)]
+    t = time.perf_counter()
+    pool.map(_ref_horner_chunk, jobs)
+    dt = time.perf_counter() - t
+    done = 2 * len(jobs) * c * horner["degree"]
+    wall += dt
+    mp += done
+    full_s += dt * (2 * horner["npts"] * horner["degree"]) / done
+    desc.append(f"horner: {len(jobs) * c} pts in {dt:.2f}s")
+    return wall, mp, full_s, "; ".join(desc)
+
+
 def run_reference(args):
+    """The reference arm: the UNMODIFIED reference package (baseline/_ref,
+    scripts/install_reference.sh) through its own public calls, sharded
+    over processes on the host cores, each step a bounded sample of the
+    workload (rates extrapolate linearly: uniform work per row / point).
+    Under torchrun only rank 0 runs.  The C restatement (oracle/, the
+    port) is timed beside it and reported under `port`."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    import multiprocessing as mp_
+
+    from paper_2603_14926_b200 import gen
+
     gemm_parts = [(k, 512 if args.quick else n) for k, n in GEMM_PARTS]
     horner = dict(HORNER)
     if args.quick:
         horner["npts"] = 1 << 16
-    small = {2: 16, 3: 16, 4: 8}
-    for _ in range(args.warmup):
-        cpu_sample(gemm_parts, horner, budget_rows={k: 1 for k in small}, horner_pts=4096)
-    vals = []
-    descs = None
-    for _ in range(args.steps):
-        r = cpu_sample(gemm_parts, horner, budget_rows=small, horner_pts=1 << 18)
-        vals.append(r["value"])
-        descs = r
-    v = statistics.median(vals)
+    host = host_description()
+    procs = max(1, min(os.cpu_count() or 1, 64))
+    have_ref = os.path.exists(os.path.join(REF_DIR, "mwfloat", "__init__.py"))
+    kind = "reference" if have_ref else "port"
+    port = None
+    steps_s = []
+    if have_ref:
+        for k, n in gemm_parts:
+            _REF_DATA[("gemm", k)] = gen.config3_gemm(k, n)
+        _REF_DATA["horner"] = gen.config4_horner(npts=procs * 4096, degree=horner["degree"], k=horner["k"])
+        _ref_import()
+        rows = {2: 1, 3: 1, 4: 1}
+        pts = 1024 if args.quick else 2048
+        with mp_.get_context("fork").Pool(procs) as pool:
+            for _ in range(args.warmup):
+                reference_sample(gemm_parts, horner, procs, rows, 256, pool)
+            vals, walls = [], []
+            for _ in range(args.steps):
+                wall, done, full_s, desc = reference_sample(gemm_parts, horner, procs, rows, pts, pool)
+                vals.append(step_mp_ops(gemm_parts, horner) / full_s / 1e9)
+                walls.append(wall)
+                steps_s.append(full_s)
+        v = statistics.median(vals)
+        sample = (f"unmodified reference (baseline/_ref mwfloat), {procs} processes x 1 thread: " + desc
+                  + " per step (median of steps); rates extrapolated linearly to the full step")
+        ms_step = statistics.median(walls) * 1e3
+        try:  # the C restatement of the same algorithm, for comparison
+            port = cpu_sample(gemm_parts, horner, budget_rows={2: 16, 3: 16, 4: 8}, horner_pts=1 << 18)
+        except Exception as e:
+            port = {"error": f"{type(e).__name__}: {e}"[:200]}
+    else:
+        small = {2: 16, 3: 16, 4: 8}
+        for _ in range(args.warmup):
+            cpu_sample(gemm_parts, horner, budget_rows={k: 1 for k in small}, horner_pts=4096)
+        vals, walls = [], []
+        for _ in range(args.steps):
+            t = time.perf_counter()
+            r = cpu_sample(gemm_parts, horner, budget_rows=small, horner_pts=1 << 18)
+            walls.append(time.perf_counter() - t)
+            vals.append(r["value"])
+            steps_s.append(r["seconds_per_step_extrapolated"])
+            desc = r
+        v = statistics.median(vals)
+        procs = desc["cores"]
+        sample = "C restatement (oracle/, port; baseline/_ref absent): " + desc["sample"]
+        ms_step = statistics.median(walls) * 1e3
     print(json.dumps({
         "metric": "DD/TD/QD GEMM and Horner Gops/s vs FP64 FMA roofline, 1/2/4/8 B200",
-        "impl": "reference", "value": v, "unit": "G MP-ops/s", "n_gpus": world, "steps": args.steps,
+        "impl": "reference", "value": round(v, 5), "unit": "G MP-ops/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64 (DD/TD/QD multi-word)", "data": "synthetic (seeded, SURVEY §8(d) G_K)",
-        "ms_per_step": round(descs["seconds_per_step_extrapolated"] * 1e3, 1),
-        "config": {"workload": "config3 GEMM DD n4096 + TD n2048 + QD n2048, config4 QD Horner deg1024 x 2^24 pts"},
-        "cpu_baseline": {"value": v, "unit": "G MP-ops/s", "cores": descs["cores"], "kind": "port",
-                         "sample": descs["sample"]},
-        "e2e": {"value": v, "unit": "G MP-ops/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "ms_per_step": round(ms_step, 1),
+        "extrapolated": True,
+        "ms_per_full_step_extrapolated": round(statistics.median(steps_s) * 1e3, 1),
+        "config": {
+            "workload": "config3 GEMM DD n4096 + TD n2048 + QD n2048, config4 QD Horner deg1024 x 2^24 pts",
+            "gemm": [f"k{k} n{n}" for k, n in gemm_parts], "horner": horner,
+            "parallelism": f"rows/points sharded over {procs} host processes (CPU), no collective",
+            "l2": "n/a (CPU)", "bit_exact": "the reference itself",
+            "sample": "each step is a bounded sample (ms_per_step = its measured wall time); value = the "
+                      "sample's MP-op rate, i.e. the full step extrapolated linearly",
+        },
+        "host": host,
+        "cpu_baseline": {"value": round(v, 5), "unit": "G MP-ops/s", "cores": procs, "kind": kind, "sample": sample,
+                         **host},
+        "port": port,
+        "e2e": {"value": round(v, 5), "unit": "G MP-ops/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
+
+
+def launch_cmd(nproc: int, argv: list, port: int) -> list:
+    """torchrun command line that re-runs this script with one rank per GPU
+    (the driver's own launch form: 127.0.0.1 rendezvous, one node)."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+            "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + list(argv)
+
+
+def self_launch(args, argv) -> int | None:
+    """`--gpus N` without a torchrun environment: re-execute under torchrun
+    with N ranks and return its exit code.  Under torchrun, a world size that
+    differs from --gpus is an error (exit 2), never a silent 1-rank run."""
+    ws = os.environ.get("WORLD_SIZE")
+    if ws is not None:
+        if int(ws) != args.gpus:
+            print(f"bench.py: WORLD_SIZE={ws} but --gpus {args.gpus}; refusing to run", file=sys.stderr)
+            return 2
+        return None
+    if args.gpus <= 1:
+        return None
+    import socket
+    import subprocess
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ)
+    if args.backend == "nccl":
+        env.setdefault("NCCL_DEBUG", "INFO")  # the communicator lines (nranks) for the driver
+    print(f"[bench] self-launch: {args.gpus} ranks under torchrun (backend {args.backend})", file=sys.stderr)
+    return subprocess.call(launch_cmd(args.gpus, argv, port), env=env)
 
 
 if __name__ == "__main__":
     a = parse()
+    rc = self_launch(a, sys.argv[1:])
+    if rc is not None:
+        sys.exit(rc)
     if a.impl == "reference":
         run_reference(a)
     else:
