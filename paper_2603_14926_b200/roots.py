@@ -222,7 +222,12 @@ def aberth_init(q: MonicPoly, variant: Variant = Variant.STANDARD, radius=None) 
     cn = LaneBatch(q.planes[:, n - 1 : n].contiguous())
     nn = LaneBatch(np.array(from_basefloat(float(n), k)).reshape(k, 1), device=dev)
     center = tuple(-c for c in batch_div(cn, nn, variant).lane(0))
-    rad = radius_estimate(q, variant) if radius is None else tuple(getattr(radius, "comps", radius))
+    if radius is None:
+        rad = radius_estimate(q, variant)
+    elif isinstance(radius, (int, float)):
+        rad = from_basefloat(float(radius), k)
+    else:
+        rad = tuple(getattr(radius, "comps", radius))
     if len(rad) != k:
         rad = from_basefloat(float(rad[0]), k)
     cosv = np.zeros((k, n))

@@ -232,9 +232,12 @@ def test_gemm_identity_bitwise():
 def test_gemm_config3_sampled_rows(k, n):
     a, b = gen.config3_gemm(k, n)
     c = matmul(MWMatrix(a), MWMatrix(b), MatMulPlan(scheme="naive", variant="bf")).numpy()
-    for r0 in (0, n // 2 + 3, n - 1):
-        ref = oracle.gemm(a, b, "bf", rows=(r0, r0 + 1))
-        assert_bitwise(c[:, r0], ref[:, r0])
+    # one full row of C in every 64-row CTA tile band (64 DD rows, 32 TD/QD
+    # rows), at a varying offset inside the band, plus the last row: every
+    # tile row and, through the full rows, every tile column is checked
+    rows = np.unique(np.r_[[band * 64 + (band * 37) % 64 for band in range(n // 64)], n - 1])
+    ref = oracle.gemm(np.ascontiguousarray(a[:, rows]), b, "bf")
+    assert_bitwise(c[:, rows], ref)
 
 
 # ---------------------------------------------------------------- horner
@@ -261,8 +264,10 @@ def test_horner_vs_oracle(k, deg, npts):
 def test_horner_config4_full_with_sampled_check():
     coeffs, x = gen.config4_horner()
     y = horner_eval_batched(MWPolynomial(coeffs), LaneBatch(x), Variant.BRANCH_FREE).numpy()
-    idx = np.r_[0:2048, (1 << 23):(1 << 23) + 2048, (1 << 24) - 2048:(1 << 24)]
-    assert_bitwise(y[:, idx], oracle.horner(coeffs, x[:, idx], "bf"))
+    # 2^20 random points (every CTA's worth of points is sampled) + both ends
+    rng = np.random.default_rng(4)
+    idx = np.unique(np.r_[rng.choice(1 << 24, 1 << 20, replace=False), 0:256, (1 << 24) - 256:(1 << 24)])
+    assert_bitwise(y[:, idx], oracle.horner(coeffs, np.ascontiguousarray(x[:, idx]), "bf"))
     assert np.all(np.isfinite(y[0]))
 
 
@@ -341,18 +346,28 @@ def test_dk_solve_quadratic(k):
     assert abs(rs[0] + 1.0) <= 1e-30 and abs(rs[1] - 1.0) <= 1e-30
 
 
+@pytest.mark.parametrize("k,v", CASES, ids=IDS)
+def test_aberth_init_on_device_matches_reference(golden, k, v):
+    """aberth_init with the device lane ops (centre -c_{n-1}/n by the Newton
+    division kernel, rotations by the mul/add kernels) reproduces the
+    reference's initial state bit for bit (roots.py:188-221)."""
+    g = golden("dk")
+    p = f"k{k}_{v}"
+    st = roots.aberth_init(MonicPoly(g[p + "_coeffs"]), V(v))
+    assert st.re.is_cuda
+    assert_bitwise(st.re.cpu().numpy(), g[p + "_zre"])
+    assert_bitwise(st.im.cpu().numpy(), g[p + "_zim"])
+
+
 @pytest.mark.parametrize("k", [3, 4])
-def test_dk_config5_200_sweeps_exact_matches_oracle_trajectory(k):
-    """Exact-order kernel tracks the oracle for a burst of sweeps (the
-    trajectory is chaotic, so only the exact order stays bitwise)."""
-    coeffs = gen.config5_poly(k)
-    zre, zim = gen.config5_init(k)
-    st = dk_sweeps(MonicPoly(coeffs), RootState(re=zre, im=zim), 3, Variant.BRANCH_FREE, exact_order=True)
-    ore, oim = zre, zim
-    for _ in range(3):
-        ore, oim, _, _ = oracle.dk_sweep(coeffs, ore, oim, "bf", exact=True)
-    assert_bitwise(st.re.cpu().numpy(), ore)
-    assert_bitwise(st.im.cpu().numpy(), oim)
+def test_aberth_init_config5_circle_on_device(golden, k):
+    """The config-5 R0 = 1.5 Aberth circle (reference centre and angles,
+    SURVEY §8(d)) built on the device equals the reference's state."""
+    g = golden("dk")
+    p = f"c5_k{k}"
+    st = roots.aberth_init(MonicPoly(g[p + "_coeffs"]), Variant.BRANCH_FREE, radius=1.5)
+    assert_bitwise(st.re.cpu().numpy(), g[p + "_ab_zre"])
+    assert_bitwise(st.im.cpu().numpy(), g[p + "_ab_zim"])
 
 
 @pytest.mark.parametrize("exact", [True, False])

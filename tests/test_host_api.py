@@ -161,6 +161,18 @@ def test_aberth_init_host_logic_matches_reference(golden, monkeypatch, k, v):
     assert_bitwise(st.im.numpy(), g[p + "_zim"])
 
 
+@pytest.mark.parametrize("k", [3, 4])
+def test_aberth_init_config5_circle_host_logic(golden, monkeypatch, k):
+    """The R0 = 1.5 circle of config 5 (radius override) with the oracle for
+    the lane ops equals the reference's state (roots.py:199-217)."""
+    _oracle_batch(monkeypatch)
+    g = golden("dk")
+    p = f"c5_k{k}"
+    st = roots.aberth_init(MonicPoly(g[p + "_coeffs"], device="cpu"), Variant.BRANCH_FREE, radius=1.5)
+    assert_bitwise(st.re.numpy(), g[p + "_ab_zre"])
+    assert_bitwise(st.im.numpy(), g[p + "_ab_zim"])
+
+
 def test_aberth_init_collision_check(monkeypatch):
     _oracle_batch(monkeypatch)
     st = RootState(re=np.array([[0.5, 0.5], [0.0, 0.0]]), im=np.array([[0.1, 0.1], [0.0, 0.0]]))

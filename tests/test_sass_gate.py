@@ -130,3 +130,47 @@ def test_raw_eft_kernels(sass, op, mix_expect):
     da, dm, df = mix_expect
     u = max(a // da if da else 0, m // dm if dm else 0)
     assert u >= 1 and (a, m, f) == (u * da, u * dm, u * df)
+
+
+# ---- the kernels that carry the headline (config 3 GEMM, config 4 Horner)
+MAC_MIX = {2: (25, 3, 1), 3: (87, 6, 3), 4: (193, 10, 6)}  # add + mul per MAC (DADD, DMUL, DFMA)
+CTRL = ("BRA", "BSSY", "BSYNC", "WARPSYNC", "BAR", "CALL", "RET", "EXIT")
+
+
+def straight_line_fp64(body):
+    """Control-flow instructions between the first and last FP64
+    instruction: none means the unrolled MAC / step bodies form one basic
+    block (branch-free, as the reference's BF kernels are)."""
+    ops = [opcode(i) for i in body]
+    fp = [i for i, o in enumerate(ops) if o.split(".")[0] in ("DADD", "DMUL", "DFMA")]
+    return [ops[i] for i in range(fp[0], fp[-1] + 1) if ops[i].split(".")[0] in CTRL]
+
+
+def test_horner_qd_step_bodies(sass):
+    """horner_kernel<4, BF>: two points per thread, one Horner step each per
+    loop trip = exactly 2 x (mul + add) = 2 x (DADD 193, DMUL 10, DFMA 6);
+    no FP64 compare; no control flow inside the FP64 body."""
+    hits = [f for f in sass if f.startswith("_ZN2mw13horner_kernelILi4ELi1EEEv")]
+    assert len(hits) == 1, hits
+    body = sass[hits[0]]
+    a, m, f, _, dsetp = mix(body)
+    assert (a, m, f) == (2 * 193, 2 * 10, 2 * 6)
+    assert dsetp == 0
+    assert straight_line_fp64(body) == []
+
+
+@pytest.mark.parametrize("k", [2, 3, 4])
+def test_gemm_every_tile_slot_mac_mix(sass, k):
+    """gemm_kernel<K, BF>, every tile slot the per-call choice can pick:
+    TM x TN MACs per k step, each exactly one BF mul + one BF add (DD
+    25/3/1, TD 87/6/3, QD 193/10/6), no FP64 compare, one basic block."""
+    pat = re.compile(rf"_ZN2mw11gemm_kernelILi{k}ELi1ELb0ENS_8GemmTileILi(\d+)ELi(\d+)ELi(\d+)ELi(\d+)ELi(\d+)E")
+    slots = [(f, pat.match(f)) for f in sass if pat.match(f)]
+    assert len(slots) >= 3, [f for f, _ in slots]
+    for f, mt in slots:
+        tm, tn = int(mt.group(3)), int(mt.group(4))
+        a, m, d, _, dsetp = mix(sass[f])
+        da, dm, df = MAC_MIX[k]
+        assert (a, m, d) == (tm * tn * da, tm * tn * dm, tm * tn * df), (f, a, m, d)
+        assert dsetp == 0
+        assert straight_line_fp64(sass[f]) == [], f
