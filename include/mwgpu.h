@@ -38,6 +38,10 @@ extern "C" {
 #define MW_ERR_INVALID -1     /* bad k / size / stride / pointer            */
 #define MW_ERR_UNSUPPORTED -2 /* reserved: (k, variant) without a kernel     */
 
+/* Largest DK degree: the collision key j*n + i must stay below INT32_MAX
+ * (the "no collision" sentinel), so every collision is reported. */
+#define MW_DK_MAX_N 46340
+
 #define MW_ORDER_EXACT 0 /* reference fold order: bit-exact, one thread/output */
 #define MW_ORDER_TREE 1  /* fixed split + pairwise tree: within n*2^-p bound   */
 
@@ -196,7 +200,7 @@ int mw_poly_eval(int k, int variant, const double* coeffs, int64_t sc,
  * min over (j*n + i) of the colliding pairs, and the caller raises
  * CollisionError (roots.py:289-292).  exact_order = 1 replays the
  * reference order bit for bit; 0 splits the Horner and the ordered product
- * across a warp (within the stated bound). */
+ * across a warp (within the stated bound).  1 <= n <= MW_DK_MAX_N. */
 int mw_dk_sweep(int k, int variant, const double* coeffs, int64_t sc,
                 int64_t n, const double* zre, const double* zim, int64_t sz,
                 int64_t i0, int64_t i1, double* zre_out, double* zim_out,
@@ -276,35 +280,51 @@ int mw_dk_sweep_ws(int k, int variant, const double* coeffs, int64_t sc,
                    int64_t so, double* step_mag, int* flag_dev, int exact_order,
                    double* ws, void* stream);
 
-/* Tuning knob of the exact-order sweep: roots per CTA (1..32, default 32).
- * Results do not depend on it (each root is one chain in reference order). */
-int mw_dk_exact_set_roots_per_cta(int roots);
+/* Per-call tuning of the launch shape (no global state: the library is
+ * stateless and reentrant).  Results never depend on it:
+ * every choice runs the same ops in the same order.  NULL = defaults.
+ *   gemm_tile      0 (default) picks the CTA tile per call from the shape
+ *                  (smaller tiles for row-block shards, where the large
+ *                  tile leaves SMs unevenly loaded); 1..3 force slot 0..2.
+ *   dot_cluster    1 (default) runs dots of 2..16 blocks of 4096 elements
+ *                  as one thread-block cluster (block roots folded through
+ *                  distributed shared memory); 0 the single-launch ticket
+ *                  form.
+ *   dk_tree_roots  tree-order sweep with a workspace: roots per CTA, 1, 2
+ *                  or 4 (one chain per lane, trees packed level by level
+ *                  over the CTA's roots); -1 (default) by shard size (4
+ *                  from 512 roots, 2 from 256, else 1); 0 the 3-warp
+ *                  single-root kernel.
+ *   dk_exact_roots exact-order sweep: roots per CTA, 1..32 (default 32).
+ *   dk_exact_split exact-order sweep: 1 (default) splits each TD/QD
+ *                  root's chains over a pair of warps (real / imaginary
+ *                  halves of the 3M product), 0 one warp per chain.      */
+typedef struct mw_tuning {
+  int gemm_tile;
+  int dot_cluster;
+  int dk_tree_roots;
+  int dk_exact_roots;
+  int dk_exact_split;
+} mw_tuning;
 
-/* Tuning knob of the exact-order sweep: 1 (default) splits each TD/QD
- * root's numerator and denominator chains over a pair of warps (real and
- * imaginary halves of the 3M product, one hand-off per step); DD keeps one
- * warp per chain (measured faster); 0 runs every chain on one warp.  Same
- * ops, same order, identical results. */
-int mw_dk_exact_set_split(int on);
+/* Fills *t with the defaults; returns MW_OK (MW_ERR_INVALID for NULL). */
+int mw_tuning_defaults(mw_tuning* t);
 
-/* Tuning knob of the tree dot: 1 (default) runs dots of 2..16 blocks of
- * 4096 elements as one thread-block cluster (block roots folded through
- * distributed shared memory), 0 always uses the single-launch ticket
- * form.  Same partials and trees: identical results. */
-int mw_dot_set_cluster(int on);
-
-/* Tuning knob of mw_gemm: 0 (default) picks the CTA tile per call from
- * the shape (smaller tiles for row-block shards, where the large tile
- * leaves SMs unevenly loaded), 1..3 force tile slot 0..2.  Every tile
- * folds each C_ij in the same order: identical results. */
-int mw_gemm_set_tile_policy(int policy);
-
-/* Tuning knob of the tree-order sweep with a workspace (mw_dk_sweep_ws):
- * roots per CTA, 1, 2 or 4 = one chain per lane and the pairwise trees
- * packed level by level over the CTA's roots; -1 (default) = by shard
- * size (4 from 512 roots, 2 from 256, else 1); 0 = the 3-warp single-root
- * kernel.  Same tree order, identical results. */
-int mw_dk_tree_set_roots_per_cta(int roots);
+/* mw_gemm / mw_dot / mw_dk_sweep_ws with explicit tuning (NULL = the
+ * defaults the plain entry points use); MW_ERR_INVALID for a value out of
+ * range. */
+int mw_gemm_ex(int k, int variant, const double* A, int64_t lda, int64_t sA,
+               const double* B, int64_t ldb, int64_t sB, double* C, int64_t ldc,
+               int64_t sC, int64_t m, int64_t n, int64_t kd,
+               const mw_tuning* tune, void* stream);
+int mw_dot_ex(int k, int variant, const double* x, int64_t sx, const double* y,
+              int64_t sy, int64_t n, double* ws, double* out_dev, int order,
+              const mw_tuning* tune, void* stream);
+int mw_dk_sweep_ex(int k, int variant, const double* coeffs, int64_t sc,
+                   int64_t n, const double* zre, const double* zim, int64_t sz,
+                   int64_t i0, int64_t i1, double* zre_out, double* zim_out,
+                   int64_t so, double* step_mag, int* flag_dev, int exact_order,
+                   double* ws, const mw_tuning* tune, void* stream);
 
 /* FP64 pipe microbenchmark: 8 independent DFMA (op = 0) or DADD (op = 1)
  * chains per thread, 8 unrolled steps per iteration: executes

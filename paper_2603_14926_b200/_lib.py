@@ -55,11 +55,10 @@ _SIGS = {
     "mw_horner": ([I, I, P, I64, I64, P, I64, P, I64, I64, P], I),
     "mw_poly_eval": ([I, I, P, I64, I64, P, P, I64, P, P, I64, I64, I, P], I),
     "mw_dk_sweep": ([I, I, P, I64, I64, P, P, I64, I64, I64, P, P, I64, P, P, I, P], I),
-    "mw_dk_exact_set_roots_per_cta": ([I], I),
-    "mw_dk_exact_set_split": ([I], I),
-    "mw_dk_tree_set_roots_per_cta": ([I], I),
-    "mw_gemm_set_tile_policy": ([I], I),
-    "mw_dot_set_cluster": ([I], I),
+    "mw_tuning_defaults": ([P], I),
+    "mw_gemm_ex": ([I, I, P, I64, I64, P, I64, I64, P, I64, I64, I64, I64, I64, P, P], I),
+    "mw_dot_ex": ([I, I, P, I64, P, I64, I64, P, P, I, P, P], I),
+    "mw_dk_sweep_ex": ([I, I, P, I64, I64, P, P, I64, I64, I64, P, P, I64, P, P, I, P, P, P], I),
     "mw_dk_sweep_peer": ([I, I, P, I64, I64, P, I64, I64, P, P, P, P, P, P, P, I, I, I, I, ctypes.c_longlong, P, P,
                           I, P, P], I),
     "mw_dk_sweep_workspace": ([I, I64, I64], I64),
@@ -75,6 +74,30 @@ _SIGS = {
 }
 
 EXPORTS = tuple(_SIGS)
+
+
+class Tuning(ctypes.Structure):
+    """mw_tuning (include/mwgpu.h): per-call launch-shape choices; results
+    never depend on them.  Defaults as in the library."""
+
+    _fields_ = [("gemm_tile", I), ("dot_cluster", I), ("dk_tree_roots", I), ("dk_exact_roots", I),
+                ("dk_exact_split", I)]
+
+
+def tuning(**kw) -> Tuning:
+    """A Tuning with the library defaults, overridden by ``kw``."""
+    t = Tuning()
+    load().mw_tuning_defaults(ctypes.byref(t))
+    for key, val in kw.items():
+        if not hasattr(t, key):
+            raise TypeError(f"unknown tuning field {key!r}")
+        setattr(t, key, int(val))
+    return t
+
+
+def tuning_ptr(t):
+    """ctypes argument for an optional Tuning (None -> NULL = defaults)."""
+    return None if t is None else ctypes.cast(ctypes.byref(t), ctypes.c_void_p)
 
 
 def build(verbose: bool = False) -> str:
@@ -107,14 +130,42 @@ _raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
 
 def stream_handle(device: torch.device | None = None) -> int:
     """cudaStream_t of torch's current stream on ``device`` (as an int).
-    Uses torch's raw-handle accessor when present (no Stream object: this
-    is on every call's host path), else torch.cuda.current_stream."""
+    The C library launches on the CURRENT device, so an operand on another
+    device is an error here (wrap the call in ``torch.cuda.device(...)`` or
+    use ``on_device``) -- never a launch on the wrong GPU.  Uses torch's
+    raw-handle accessor when present (no Stream object: this is on every
+    call's host path), else torch.cuda.current_stream."""
+    cur = torch.cuda.current_device()
+    idx = getattr(device, "index", None)
+    if idx is None:
+        idx = cur
+    elif idx != cur:
+        raise ValueError(f"mwgpu: operands on cuda:{idx} but the current device is cuda:{cur}; "
+                         "launch under torch.cuda.device(...)")
     if _raw_stream is not None:
-        idx = getattr(device, "index", None)
-        if idx is None:
-            idx = torch.cuda.current_device()
         return _raw_stream(idx)
     return torch.cuda.current_stream(device).cuda_stream
+
+
+class on_device:
+    """Context manager: make ``t``'s device current for a launch (no-op
+    when it already is)."""
+
+    __slots__ = ("idx", "prev")
+
+    def __init__(self, t: torch.Tensor):
+        self.idx = t.device.index
+
+    def __enter__(self):
+        self.prev = torch.cuda.current_device()
+        if self.idx is not None and self.idx != self.prev:
+            torch.cuda.set_device(self.idx)
+        return self
+
+    def __exit__(self, *exc):
+        if self.idx is not None and self.idx != self.prev:
+            torch.cuda.set_device(self.prev)
+        return False
 
 
 def check(rc: int, what: str):
@@ -136,6 +187,21 @@ def require_cuda(*tensors: torch.Tensor):
             raise RuntimeError(
                 "mwgpu: operands must live on a CUDA device; the B200 path has no CPU fallback"
             )
+
+
+def require_planes(*tensors: torch.Tensor):
+    """CUDA, float64, C-contiguous, all on one device: what the plane
+    strides the wrappers pass to the C-ABI assume (a non-contiguous or
+    foreign tensor would otherwise turn into out-of-bounds device reads)."""
+    require_cuda(*tensors)
+    dev = tensors[0].device
+    for t in tensors:
+        if t.dtype != torch.float64:
+            raise ValueError(f"mwgpu: float64 planes required, got {t.dtype}")
+        if not t.is_contiguous():
+            raise ValueError("mwgpu: planes tensors must be contiguous")
+        if t.device != dev:
+            raise ValueError("mwgpu: operands on different devices")
 
 
 def ptr(t: torch.Tensor) -> int:

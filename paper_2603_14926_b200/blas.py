@@ -62,7 +62,7 @@ def _workspace(device, n: int, stream: int | None = None) -> torch.Tensor:
 
 
 def dot_tensor(x: LaneBatch, y: LaneBatch, variant: Variant = Variant.BRANCH_FREE, order: str = "tree",
-               out: torch.Tensor | None = None) -> torch.Tensor:
+               out: torch.Tensor | None = None, tuning=None) -> torch.Tensor:
     """dot(x, y) as a (K,) device tensor (no host synchronisation)."""
     _check_pair(x, y)
     o = _order(order)
@@ -75,14 +75,16 @@ def dot_tensor(x: LaneBatch, y: LaneBatch, variant: Variant = Variant.BRANCH_FRE
     wsn = lib.mw_dot_workspace(k, n) if o == _lib.ORDER_TREE else 0
     st = _lib.stream_handle(x.device)
     ws = _workspace(x.device, wsn, st)
-    rc = lib.mw_dot(k, v, x.planes.data_ptr(), n, y.planes.data_ptr(), n, n, ws.data_ptr(), out.data_ptr(), o, st)
+    rc = lib.mw_dot_ex(k, v, x.planes.data_ptr(), n, y.planes.data_ptr(), n, n, ws.data_ptr(), out.data_ptr(), o,
+                       _lib.tuning_ptr(tuning), st)
     _lib.check(rc, "mw_dot")
     return out
 
 
-def dot(x: LaneBatch, y: LaneBatch, variant: Variant = Variant.BRANCH_FREE, order: str = "tree") -> tuple:
+def dot(x: LaneBatch, y: LaneBatch, variant: Variant = Variant.BRANCH_FREE, order: str = "tree",
+        tuning=None) -> tuple:
     """dot(x, y) as a K-word tuple."""
-    return tuple(float(c) for c in dot_tensor(x, y, variant, order).cpu())
+    return tuple(float(c) for c in dot_tensor(x, y, variant, order, tuning=tuning).cpu())
 
 
 def axpy_(alpha, x: LaneBatch, y: LaneBatch, variant: Variant = Variant.BRANCH_FREE) -> LaneBatch:

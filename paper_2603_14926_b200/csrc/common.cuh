@@ -14,6 +14,22 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
 // Cached SM count of the current device (148 on B200).
 int sm_count();
 
+// Per-call tuning (include/mwgpu.h): NULL -> the defaults; out-of-range
+// values -> false (the entry point returns MW_ERR_INVALID).
+inline mw_tuning tuning_defaults() { return mw_tuning{0, 1, -1, 32, 1}; }
+inline bool tuning_resolve(const mw_tuning* in, mw_tuning* out) {
+  *out = in ? *in : tuning_defaults();
+  const mw_tuning& t = *out;
+  if (t.gemm_tile < 0 || t.gemm_tile > 3) return false;
+  if (t.dot_cluster != 0 && t.dot_cluster != 1) return false;
+  if (t.dk_tree_roots != -1 && t.dk_tree_roots != 0 && t.dk_tree_roots != 1 && t.dk_tree_roots != 2 &&
+      t.dk_tree_roots != 4)
+    return false;
+  if (t.dk_exact_roots < 1 || t.dk_exact_roots > 32) return false;
+  if (t.dk_exact_split != 0 && t.dk_exact_split != 1) return false;
+  return true;
+}
+
 inline int launch_status() {
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? MW_OK : static_cast<int>(e);

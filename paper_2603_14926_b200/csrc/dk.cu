@@ -3,10 +3,6 @@
 
 namespace mw {
 
-int g_dk_exact_roots = 32;
-int g_dk_exact_split = 1;
-int g_dk_tree_roots = -1;
-
 #define MW_DK_EXTERN(FN) \
   MW_DK_FOR_K(extern template, FN, 2) MW_DK_FOR_K(extern template, FN, 3) MW_DK_FOR_K(extern template, FN, 4)
 MW_DK_EXTERN(dk_exact_launch)
@@ -17,12 +13,12 @@ struct DkLaunch {
   static int run(const double* coeffs, int64_t sc, int64_t n, const double* zre,
                  const double* zim, int64_t sz, int64_t i0, int64_t i1, double* zre_out,
                  double* zim_out, int64_t so, double* step_mag, int* flag, int exact, double* ws,
-                 cudaStream_t st) {
+                 mw_tuning tune, cudaStream_t st) {
     if (exact)
       return dk_exact_launch<K, VAR, false>(coeffs, sc, n, zre, zim, sz, i0, i1, zre_out, zim_out,
-                                            so, step_mag, flag, DkPeers{}, ws, st);
+                                            so, step_mag, flag, DkPeers{}, ws, tune, st);
     return dk_tree_launch<K, VAR, false>(coeffs, sc, n, zre, zim, sz, i0, i1, zre_out, zim_out,
-                                         so, step_mag, flag, DkPeers{}, ws, st);
+                                         so, step_mag, flag, DkPeers{}, ws, tune, st);
   }
 };
 
@@ -37,9 +33,9 @@ struct DkPeerLaunch {
     double* oim = state_out + (int64_t)K * n;
     if (exact)
       return dk_exact_launch<K, VAR, true>(coeffs, sc, n, zre, zim, n, i0, i1, ore, oim, n,
-                                           step_mag, flag, peers, ws, st);
+                                           step_mag, flag, peers, ws, tuning_defaults(), st);
     return dk_tree_launch<K, VAR, true>(coeffs, sc, n, zre, zim, n, i0, i1, ore, oim, n,
-                                        step_mag, flag, peers, ws, st);
+                                        step_mag, flag, peers, ws, tuning_defaults(), st);
   }
 };
 
@@ -47,27 +43,9 @@ struct DkPeerLaunch {
 
 using namespace mw;
 
-// Tuning knob for the exact-order sweep: roots per CTA (1..32).
-extern "C" int mw_dk_exact_set_roots_per_cta(int r) {
-  if (r < 1 || r > 32) return MW_ERR_INVALID;
-  g_dk_exact_roots = r;
-  return MW_OK;
-}
-
-// Tuning knob for the tree-order sweep: roots per CTA (0 = the 3-warp
-// single-root kernel, 1, 2 or 4 = dk_treem_kernel, -1 = auto by shard
-// size).  Results are identical.
-extern "C" int mw_dk_tree_set_roots_per_cta(int r) {
-  if (r != -1 && r != 0 && r != 1 && r != 2 && r != 4) return MW_ERR_INVALID;
-  g_dk_tree_roots = r;
-  return MW_OK;
-}
-
-// Tuning knob: exact-order kernel form (1 = split warp pairs for TD/QD,
-// default; 0 = one warp per chain).  Results are identical.
-extern "C" int mw_dk_exact_set_split(int on) {
-  if (on != 0 && on != 1) return MW_ERR_INVALID;
-  g_dk_exact_split = on;
+extern "C" int mw_tuning_defaults(mw_tuning* t) {
+  if (!t) return MW_ERR_INVALID;
+  *t = tuning_defaults();
   return MW_OK;
 }
 
@@ -75,16 +53,8 @@ extern "C" int mw_dk_sweep(int k, int variant, const double* coeffs, int64_t sc,
                            const double* zre, const double* zim, int64_t sz, int64_t i0,
                            int64_t i1, double* zre_out, double* zim_out, int64_t so,
                            double* step_mag, int* flag_dev, int exact_order, void* stream) {
-  if (k < 2 || k > 4) return MW_ERR_INVALID;
-  if (variant != 0 && variant != 1) return MW_ERR_INVALID;
-  if (n < 1 || i0 < 0 || i1 < i0 || i1 > n) return MW_ERR_INVALID;
-  if (i1 == i0) return MW_OK;
-  if (!coeffs || !zre || !zim || !zre_out || !zim_out || !step_mag || !flag_dev)
-    return MW_ERR_INVALID;
-  if (sc < n || sz < n || so < n) return MW_ERR_INVALID;
-  return dispatch<DkLaunch>(k, variant, coeffs, sc, n, zre, zim, sz, i0, i1, zre_out, zim_out,
-                            so, step_mag, flag_dev, exact_order ? 1 : 0, (double*)nullptr,
-                            as_stream(stream));
+  return mw_dk_sweep_ex(k, variant, coeffs, sc, n, zre, zim, sz, i0, i1, zre_out, zim_out, so,
+                        step_mag, flag_dev, exact_order, nullptr, nullptr, stream);
 }
 
 extern "C" int64_t mw_dk_sweep_workspace(int k, int64_t i0, int64_t i1) {
@@ -100,15 +70,29 @@ extern "C" int mw_dk_sweep_ws(int k, int variant, const double* coeffs, int64_t 
                               int64_t i1, double* zre_out, double* zim_out, int64_t so,
                               double* step_mag, int* flag_dev, int exact_order, double* ws,
                               void* stream) {
+  return mw_dk_sweep_ex(k, variant, coeffs, sc, n, zre, zim, sz, i0, i1, zre_out, zim_out, so,
+                        step_mag, flag_dev, exact_order, ws, nullptr, stream);
+}
+
+// The sweep with explicit per-call tuning (NULL = defaults).  The collision
+// key j*n + i is an int: n above 46340 would overflow it, so such sizes are
+// rejected instead of silently losing a collision.
+extern "C" int mw_dk_sweep_ex(int k, int variant, const double* coeffs, int64_t sc, int64_t n,
+                              const double* zre, const double* zim, int64_t sz, int64_t i0,
+                              int64_t i1, double* zre_out, double* zim_out, int64_t so,
+                              double* step_mag, int* flag_dev, int exact_order, double* ws,
+                              const mw_tuning* tune, void* stream) {
+  mw_tuning t;
+  if (!tuning_resolve(tune, &t)) return MW_ERR_INVALID;
   if (k < 2 || k > 4) return MW_ERR_INVALID;
   if (variant != 0 && variant != 1) return MW_ERR_INVALID;
-  if (n < 1 || i0 < 0 || i1 < i0 || i1 > n) return MW_ERR_INVALID;
+  if (n < 1 || n > MW_DK_MAX_N || i0 < 0 || i1 < i0 || i1 > n) return MW_ERR_INVALID;
   if (i1 == i0) return MW_OK;
   if (!coeffs || !zre || !zim || !zre_out || !zim_out || !step_mag || !flag_dev)
     return MW_ERR_INVALID;
   if (sc < n || sz < n || so < n) return MW_ERR_INVALID;
   return dispatch<DkLaunch>(k, variant, coeffs, sc, n, zre, zim, sz, i0, i1, zre_out, zim_out,
-                            so, step_mag, flag_dev, exact_order ? 1 : 0, ws,
+                            so, step_mag, flag_dev, exact_order ? 1 : 0, ws, t,
                             as_stream(stream));
 }
 
@@ -127,7 +111,7 @@ extern "C" int mw_dk_sweep_peer(int k, int variant, const double* coeffs, int64_
                                 void* stream) {
   if (k < 2 || k > 4) return MW_ERR_INVALID;
   if (variant != 0 && variant != 1) return MW_ERR_INVALID;
-  if (n < 1 || i0 < 0 || i1 <= i0 || i1 > n) return MW_ERR_INVALID;
+  if (n < 1 || n > MW_DK_MAX_N || i0 < 0 || i1 <= i0 || i1 > n) return MW_ERR_INVALID;
   if (world < 1 || rank < 0 || rank >= world || sweeps < 1 || sweep < 0 || sweep >= sweeps)
     return MW_ERR_INVALID;
   if (spin_limit < 1) return MW_ERR_INVALID;

@@ -141,14 +141,14 @@ __device__ __forceinline__ void dk_tail(const Cx<K, VAR>& acc, const Cx<K, VAR>&
 }
 
 constexpr int DK_EXACT_ROOTS = 32;  // lanes per role warp (two warps: num + den)
-// Roots handled per CTA (<= 32; lanes beyond it idle).  Fewer roots per
+// Roots handled per CTA (mw_tuning.dk_exact_roots, <= 32; lanes beyond it
+// idle; default 32, 16 and 8 measured 0.5-5 % slower).  Fewer roots per
 // CTA spread the 2n sequential chains over more SM sub-partitions.
-extern int g_dk_exact_roots;  // default 32 (dk.cu; 16 and 8 measured 0.5-5 % slower)
-// 1: split-pair exact kernel (dk_exact2_kernel) for TD and QD, 0:
-// single-warp chains everywhere.  Measured (config 5, us/sweep, eager,
-// single -> split): TD 353 -> 295 (one hand-off per step), QD 745 -> 575
-// (XP: p1, p2 handed over too); DD 165 -> 173, so DD stays single-warp.
-extern int g_dk_exact_split;  // default 1 (dk.cu)
+// mw_tuning.dk_exact_split = 1: split-pair exact kernel (dk_exact2_kernel)
+// for TD and QD, 0: single-warp chains everywhere.  Measured (config 5,
+// us/sweep, eager, single -> split): TD 353 -> 295 (one hand-off per step),
+// QD 745 -> 575 (XP: p1, p2 handed over too); DD 165 -> 173, so DD stays
+// single-warp.
 constexpr int DK_SPLIT_MIN_K = 3;
 constexpr int DK_CH = 128;          // roots staged in smem per chunk
 
@@ -1107,10 +1107,10 @@ __global__ void __launch_bounds__(32 * dk_treem_warps<R>(), R == 2 ? 2 : 1)
   }
 }
 
-// Roots per CTA of the tree sweep: 0 = the 3-warp single-root kernel
-// (dk_tree_kernel), 1, 2 or 4 = dk_treem_kernel<R>, -1 = by shard size
-// (4 from 512 roots, 2 from 256, else 1).  Results are identical.
-extern int g_dk_tree_roots;  // default 2 (dk.cu)
+// Roots per CTA of the tree sweep (mw_tuning.dk_tree_roots): 0 = the
+// 3-warp single-root kernel (dk_tree_kernel), 1, 2 or 4 =
+// dk_treem_kernel<R>, -1 (default) = by shard size (4 from 512 roots, 2
+// from 256, else 1).  Results are identical.
 
 // dk_treem_kernel<R> as a programmatic dependent launch after dk_pow_kernel
 // (plain stream order where that is unsupported).
@@ -1160,7 +1160,7 @@ template <int K, int VAR, bool PEER>
 int dk_tree_launch(const double* coeffs, int64_t sc, int64_t n, const double* zre,
                           const double* zim, int64_t sz, int64_t i0, int64_t i1, double* zre_out,
                           double* zim_out, int64_t so, double* step_mag, int* flag, DkPeers peers,
-                          double* ws, cudaStream_t st) {
+                          double* ws, mw_tuning tune, cudaStream_t st) {
   const int64_t cnt = i1 - i0;
   if (!ws) {
     dk_tree_kernel<K, VAR, PEER, false><<<(unsigned)cnt, 96, 0, st>>>(
@@ -1168,7 +1168,7 @@ int dk_tree_launch(const double* coeffs, int64_t sc, int64_t n, const double* zr
         (const double*)nullptr, (int64_t)0);
     return launch_status();
   }
-  int roots = g_dk_tree_roots;
+  int roots = tune.dk_tree_roots;
   if (roots < 0) roots = cnt >= 512 ? 4 : cnt >= 256 ? 2 : 1;  // auto: ~128+ CTAs when possible
   // R = 1 squares w -> w^32 inside the sweep (beside the scan)
   dk_pow_kernel<K, VAR><<<(unsigned)((cnt + 127) / 128), 128, 0, st>>>(zre, zim, sz, n, i0, i1, ws,
@@ -1210,12 +1210,12 @@ template <int K, int VAR, bool PEER>
 int dk_exact_launch(const double* coeffs, int64_t sc, int64_t n, const double* zre,
                     const double* zim, int64_t sz, int64_t i0, int64_t i1, double* zre_out,
                     double* zim_out, int64_t so, double* step_mag, int* flag, DkPeers peers,
-                    double* ws, cudaStream_t st) {
+                    double* ws, mw_tuning tune, cudaStream_t st) {
   (void)ws;
   const int64_t cnt = i1 - i0;
-  const int r = g_dk_exact_roots;
+  const int r = tune.dk_exact_roots;
   const int64_t blocks = (cnt + r - 1) / r;
-  if (g_dk_exact_split && K >= DK_SPLIT_MIN_K)
+  if (tune.dk_exact_split && K >= DK_SPLIT_MIN_K)
     dk_exact2_kernel<K, VAR, PEER><<<(unsigned)blocks, 128, 0, st>>>(
         coeffs, sc, n, zre, zim, sz, i0, i1, zre_out, zim_out, so, step_mag, flag, r, peers);
   else
@@ -1230,7 +1230,7 @@ int dk_exact_launch(const double* coeffs, int64_t sc, int64_t n, const double* z
 #define MW_DK_LAUNCH_SIG(FN, K, VAR, PEER)                                                    \
   int FN<K, VAR, PEER>(const double*, int64_t, int64_t, const double*, const double*, int64_t, \
                        int64_t, int64_t, double*, double*, int64_t, double*, int*, DkPeers,    \
-                       double*, cudaStream_t)
+                       double*, mw_tuning, cudaStream_t)
 #define MW_DK_FOR_K(PREFIX, FN, K)             \
   PREFIX MW_DK_LAUNCH_SIG(FN, K, 0, false);    \
   PREFIX MW_DK_LAUNCH_SIG(FN, K, 1, false);    \

@@ -67,9 +67,6 @@ struct GemmCfgs<4> {
 template <int K>
 using GemmCfg = typename GemmCfgs<K>::C0;
 
-// 0: choose the tile per call (default); 1..3: always slot 0..2.
-static int g_gemm_tile_policy = 0;
-
 template <class Cf>
 static double gemm_cost(int64_t m, int64_t n, int sms, double rel) {
   const int64_t tiles = ((n + Cf::BN - 1) / Cf::BN) * ((m + Cf::BM - 1) / Cf::BM);
@@ -78,8 +75,9 @@ static double gemm_cost(int64_t m, int64_t n, int sms, double rel) {
 }
 
 template <int K, int VAR>
-static int gemm_pick(int64_t m, int64_t n) {
-  if (g_gemm_tile_policy > 0) return g_gemm_tile_policy - 1;
+static int gemm_pick(int64_t m, int64_t n, int policy) {
+  // policy (mw_tuning.gemm_tile): 0 = choose per call, 1..3 = slot 0..2
+  if (policy > 0) return policy - 1;
   using Cs = GemmCfgs<K>;
   const int sms = sm_count();
   const double* rel = VAR == BRANCH_FREE ? Cs::REL : Cs::REL_STD;
@@ -125,10 +123,10 @@ struct GemmLaunch {
   static int run(const double* A, int64_t lda, int64_t sA, const double* B, int64_t ldb,
                  int64_t sB, double* C, int64_t ldc, int64_t sC, int64_t m, int64_t n, int64_t kd,
                  const double* Cin, int64_t ldci, int64_t sCi, int64_t batch, int64_t bsA,
-                 int64_t bsB, int64_t bsC, int64_t bsCi, cudaStream_t st) {
+                 int64_t bsB, int64_t bsC, int64_t bsCi, int policy, cudaStream_t st) {
     using Cs = GemmCfgs<K>;
     // batched products (the Strassen leaves) keep slot 0
-    const int slot = (batch == 1 && Cin == nullptr) ? gemm_pick<K, VAR>(m, n) : 0;
+    const int slot = (batch == 1 && Cin == nullptr) ? gemm_pick<K, VAR>(m, n, policy) : 0;
     if (slot == 1)
       return gemm_launch<K, VAR, typename Cs::C1>(A, lda, sA, B, ldb, sB, C, ldc, sC, m, n, kd, Cin,
                                                   ldci, sCi, batch, bsA, bsB, bsC, bsCi, st);
@@ -144,14 +142,6 @@ struct GemmLaunch {
 
 using namespace mw;
 
-// Tuning knob: GEMM tile choice (0 = per call by shape, default; 1..3 =
-// always slot 0..2).  Results are identical.
-extern "C" int mw_gemm_set_tile_policy(int policy) {
-  if (policy < 0 || policy > 3) return MW_ERR_INVALID;
-  g_gemm_tile_policy = policy;
-  return MW_OK;
-}
-
 extern "C" int mw_gemm_batched(int k, int variant, const double* A, int64_t lda, int64_t sA,
                                int64_t bsA, const double* B, int64_t ldb, int64_t sB, int64_t bsB,
                                double* C, int64_t ldc, int64_t sC, int64_t bsC, const double* Cin,
@@ -166,12 +156,21 @@ extern "C" int mw_gemm_batched(int k, int variant, const double* A, int64_t lda,
   if (Cin && ldci < n) return MW_ERR_INVALID;
   if (batch > 1 && (bsA < 0 || bsB < 0 || bsC < 0 || (Cin && bsCi < 0))) return MW_ERR_INVALID;
   return dispatch<GemmLaunch>(k, variant, A, lda, sA, B, ldb, sB, C, ldc, sC, m, n, kd, Cin, ldci,
-                              sCi, batch, bsA, bsB, bsC, bsCi, as_stream(stream));
+                              sCi, batch, bsA, bsB, bsC, bsCi, 0, as_stream(stream));
 }
 
 extern "C" int mw_gemm(int k, int variant, const double* A, int64_t lda, int64_t sA,
                        const double* B, int64_t ldb, int64_t sB, double* C, int64_t ldc,
                        int64_t sC, int64_t m, int64_t n, int64_t kd, void* stream) {
+  return mw_gemm_ex(k, variant, A, lda, sA, B, ldb, sB, C, ldc, sC, m, n, kd, nullptr, stream);
+}
+
+extern "C" int mw_gemm_ex(int k, int variant, const double* A, int64_t lda, int64_t sA,
+                          const double* B, int64_t ldb, int64_t sB, double* C, int64_t ldc,
+                          int64_t sC, int64_t m, int64_t n, int64_t kd, const mw_tuning* tune,
+                          void* stream) {
+  mw_tuning t;
+  if (!tuning_resolve(tune, &t)) return MW_ERR_INVALID;
   if (k < 2 || k > 4) return MW_ERR_INVALID;
   if (variant != 0 && variant != 1) return MW_ERR_INVALID;
   if (m < 0 || n < 0 || kd < 0) return MW_ERR_INVALID;
@@ -183,5 +182,6 @@ extern "C" int mw_gemm(int k, int variant, const double* A, int64_t lda, int64_t
   }
   return dispatch<GemmLaunch>(k, variant, A, lda, sA, B, ldb, sB, C, ldc, sC, m, n, kd,
                               (const double*)nullptr, (int64_t)0, (int64_t)0, (int64_t)1,
-                              (int64_t)0, (int64_t)0, (int64_t)0, (int64_t)0, as_stream(stream));
+                              (int64_t)0, (int64_t)0, (int64_t)0, (int64_t)0, t.gemm_tile,
+                              as_stream(stream));
 }

@@ -154,12 +154,11 @@ __global__ void __launch_bounds__(DOT_BLOCK) dot_fused_kernel(
 // latency path.  Same partials, same trees: bit-identical to
 // dot_fused_kernel.
 constexpr int DOT_CLUSTER_MAX = 16;
-static int g_dot_cluster = 1;
 __device__ __forceinline__ unsigned cluster_ctarank() {
   unsigned r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
   return r;
-}  // 0: always the ticket form (tuning / tests)
+}
 template <int K, int VAR>
 __global__ void __launch_bounds__(DOT_BLOCK) dot_cluster_kernel(
     const double* __restrict__ x, int64_t sx, const double* __restrict__ y, int64_t sy,
@@ -258,7 +257,7 @@ static int fold_levels(const double* in, int64_t istride, int64_t count, double*
 template <int K, int VAR>
 struct DotLaunch {
   static int run(const double* x, int64_t sx, const double* y, int64_t sy, int64_t n, double* ws,
-                 double* out, int order, cudaStream_t st) {
+                 double* out, int order, int cluster, cudaStream_t st) {
     if (order == MW_ORDER_EXACT || n == 0) {
       dot_exact_kernel<K, VAR><<<1, 1, 0, st>>>(x, sx, y, sy, n, out);
       return launch_status();
@@ -272,7 +271,7 @@ struct DotLaunch {
     // left zero by every call, never overwritten); partials start at ws + 1
     unsigned int* ticket = reinterpret_cast<unsigned int*>(ws);
     double* part = ws + 1;
-    if (nb <= DOT_CLUSTER_MAX && g_dot_cluster) {
+    if (nb <= DOT_CLUSTER_MAX && cluster) {
       auto kern = dot_cluster_kernel<K, VAR>;
       static bool attr_set[64] = {false};
       int dev = 0;
@@ -650,14 +649,6 @@ static int variant_ok(int k, int variant) {
   return (variant == 0 || variant == 1) ? MW_OK : MW_ERR_INVALID;
 }
 
-// Tuning knob: 1 (default) runs dots of 2..16 blocks as one thread-block
-// cluster, 0 always uses the single-launch ticket form.  Same results.
-extern "C" int mw_dot_set_cluster(int on) {
-  if (on != 0 && on != 1) return MW_ERR_INVALID;
-  g_dot_cluster = on;
-  return MW_OK;
-}
-
 extern "C" int64_t mw_dot_workspace(int k, int64_t n) {
   if (k < 2 || k > 4 || n < 0) return 0;
   int64_t nb = ceil_div(n, DOT_PER_BLOCK);
@@ -678,12 +669,21 @@ extern "C" int64_t mw_dot_num_partials(int64_t n) { return n <= 0 ? 0 : ceil_div
 
 extern "C" int mw_dot(int k, int variant, const double* x, int64_t sx, const double* y, int64_t sy,
                       int64_t n, double* ws, double* out_dev, int order, void* stream) {
+  return mw_dot_ex(k, variant, x, sx, y, sy, n, ws, out_dev, order, nullptr, stream);
+}
+
+extern "C" int mw_dot_ex(int k, int variant, const double* x, int64_t sx, const double* y,
+                         int64_t sy, int64_t n, double* ws, double* out_dev, int order,
+                         const mw_tuning* tune, void* stream) {
   int rc = variant_ok(k, variant);
   if (rc) return rc;
+  mw_tuning t;
+  if (!tuning_resolve(tune, &t)) return MW_ERR_INVALID;
   if (n < 0 || !out_dev || (n > 0 && (!x || !y || sx < n || sy < n))) return MW_ERR_INVALID;
   if (order != MW_ORDER_EXACT && order != MW_ORDER_TREE) return MW_ERR_INVALID;
   if (order == MW_ORDER_TREE && mw_dot_workspace(k, n) > 0 && !ws) return MW_ERR_INVALID;
-  return dispatch<DotLaunch>(k, variant, x, sx, y, sy, n, ws, out_dev, order, as_stream(stream));
+  return dispatch<DotLaunch>(k, variant, x, sx, y, sy, n, ws, out_dev, order, t.dot_cluster,
+                             as_stream(stream));
 }
 
 extern "C" int mw_dot_partials(int k, int variant, const double* x, int64_t sx, const double* y,

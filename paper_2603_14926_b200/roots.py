@@ -250,10 +250,11 @@ def aberth_init(q: MonicPoly, variant: Variant = Variant.STANDARD, radius=None) 
 # ---------------------------------------------------------------- sweep
 def sweep_into(coeffs: torch.Tensor, zre: torch.Tensor, zim: torch.Tensor, out_re: torch.Tensor,
                out_im: torch.Tensor, step_mag: torch.Tensor, flag: torch.Tensor, variant,
-               exact_order: bool = True, i0: int = 0, i1: int | None = None) -> None:
+               exact_order: bool = True, i0: int = 0, i1: int | None = None, tuning=None) -> None:
     """Raw launch: roots [i0, i1) of the frozen state -> out planes at the
     same indices (plane stride n).  ``flag`` (int32 device scalar) must hold
-    INT32_MAX beforehand; it is lowered to min(j*n + i) on a collision."""
+    INT32_MAX beforehand; it is lowered to min(j*n + i) on a collision.
+    ``tuning``: an optional _lib.Tuning (launch shape only; same bits)."""
     k, n = zre.shape
     i1 = n if i1 is None else i1
     lib = _lib.load()
@@ -261,10 +262,11 @@ def sweep_into(coeffs: torch.Tensor, zre: torch.Tensor, zim: torch.Tensor, out_r
     if not exact_order and i1 > i0:
         # stream-ordered scratch for the lane-per-root powers kernel
         ws = torch.empty(lib.mw_dk_sweep_workspace(k, i0, i1), dtype=torch.float64, device=zre.device)
-    rc = lib.mw_dk_sweep_ws(
+    rc = lib.mw_dk_sweep_ex(
         k, variant_code(variant), coeffs.data_ptr(), coeffs.shape[1], n, zre.data_ptr(), zim.data_ptr(), n,
         i0, i1, out_re.data_ptr(), out_im.data_ptr(), n, step_mag.data_ptr(), flag.data_ptr(),
-        1 if exact_order else 0, None if ws is None else ws.data_ptr(), _lib.stream_handle(zre.device),
+        1 if exact_order else 0, None if ws is None else ws.data_ptr(), _lib.tuning_ptr(tuning),
+        _lib.stream_handle(zre.device),
     )
     _lib.check(rc, "mw_dk_sweep")
 
@@ -300,7 +302,7 @@ def dk_iterate(q: MonicPoly, state: RootState, variant: Variant = Variant.STANDA
 
 
 def dk_sweeps(q: MonicPoly, state: RootState, sweeps: int, variant: Variant = Variant.BRANCH_FREE,
-              exact_order: bool = True, check: bool = True) -> RootState:
+              exact_order: bool = True, check: bool = True, tuning=None) -> RootState:
     """``sweeps`` sweeps back to back on the device (ping-pong buffers, no
     host synchronisation in between).  Collision flags are kept per sweep
     and checked once at the end (first colliding sweep reported)."""
@@ -311,7 +313,8 @@ def dk_sweeps(q: MonicPoly, state: RootState, sweeps: int, variant: Variant = Va
     flags = torch.full((max(sweeps, 1),), INT32_MAX, dtype=torch.int32, device=dev)
     for s in range(sweeps):
         src, dst = bufs[s & 1], bufs[(s + 1) & 1]
-        sweep_into(q.planes, src[0], src[1], dst[0], dst[1], mag, flags[s : s + 1], variant, exact_order)
+        sweep_into(q.planes, src[0], src[1], dst[0], dst[1], mag, flags[s : s + 1], variant, exact_order,
+                   tuning=tuning)
     fin = bufs[sweeps & 1]
     if check and sweeps > 0:
         f = flags.cpu().numpy()
@@ -335,7 +338,7 @@ class DKSweepGraph:
     """
 
     def __init__(self, q: MonicPoly, state: RootState, sweeps: int, variant: Variant = Variant.BRANCH_FREE,
-                 exact_order: bool = True):
+                 exact_order: bool = True, tuning=None):
         _lib.require_cuda(q.planes, state.re, state.im)
         if sweeps < 1:
             raise ValueError("sweeps must be >= 1")
@@ -354,7 +357,7 @@ class DKSweepGraph:
             for s_ in range(sweeps):
                 a, b = self.bufs[s_ & 1], self.bufs[(s_ + 1) & 1]
                 sweep_into(q.planes, a[0], a[1], b[0], b[1], self.mag, self.flags[s_ : s_ + 1], variant,
-                           exact_order)
+                           exact_order, tuning=tuning)
 
         side = torch.cuda.Stream(device=dev)
         side.wait_stream(torch.cuda.current_stream(dev))

@@ -7,13 +7,12 @@ from paper_2603_14926_b200 import gen
 from paper_2603_14926_b200.roots import DKSweepGraph
 orders = sys.argv[1:] or ["tree", "exact"]
 from paper_2603_14926_b200 import _lib
-if os.environ.get("DK_TREE_ROOTS"):
-    _lib.load().mw_dk_tree_set_roots_per_cta(int(os.environ["DK_TREE_ROOTS"]))
+tune = _lib.tuning(dk_tree_roots=int(os.environ["DK_TREE_ROOTS"])) if os.environ.get("DK_TREE_ROOTS") else None
 for k in (3, 4):
     q = mw.MonicPoly(torch.from_numpy(gen.config5_poly(k)).cuda())
     zre, zim = (torch.from_numpy(t).cuda() for t in gen.config5_init(k))
     for order in orders:
-        g = DKSweepGraph(q, mw.RootState(re=zre, im=zim), 200, mw.Variant.BRANCH_FREE, exact_order=order == "exact")
+        g = DKSweepGraph(q, mw.RootState(re=zre, im=zim), 200, mw.Variant.BRANCH_FREE, exact_order=order == "exact", tuning=tune)
         g.replay(); torch.cuda.synchronize()
         ts = []
         for _ in range(5):

@@ -21,13 +21,13 @@ for k in (3, 4):
         i1 = n // G
         row = []
         for r in (0, 1, 2, 4, -1):
-            lib.mw_dk_tree_set_roots_per_cta(r)
-            sweep_into(coeffs, zre, zim, ore, oim, mag, flag, BF, False, 0, i1)
+            tune = _lib.tuning(dk_tree_roots=r)
+            sweep_into(coeffs, zre, zim, ore, oim, mag, flag, BF, False, 0, i1, tuning=tune)
             torch.cuda.synchronize()
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g):
                 for _ in range(50):
-                    sweep_into(coeffs, zre, zim, ore, oim, mag, flag, BF, False, 0, i1)
+                    sweep_into(coeffs, zre, zim, ore, oim, mag, flag, BF, False, 0, i1, tuning=tune)
             g.replay(); torch.cuda.synchronize()
             ts = []
             for _ in range(5):
@@ -36,5 +36,4 @@ for k in (3, 4):
                 ts.append(e0.elapsed_time(e1) / 50 * 1e3)
             ts.sort()
             row.append(f"R={r:2d} {ts[2]:6.2f}us")
-        lib.mw_dk_tree_set_roots_per_cta(-1)
         print(f"k={k} G={G} roots={i1:3d}: " + " | ".join(row), flush=True)

@@ -12,16 +12,15 @@ for k in (2, 3, 4):
     X, Y = mw.LaneBatch(gen.g_k(rng, k, 65536)), mw.LaneBatch(gen.g_k(rng, k, 65536))
     out = torch.empty(k, dtype=torch.float64, device="cuda")
     for on in (0, 1):
-        lib.mw_dot_set_cluster(on)
-        blas.dot_tensor(X, Y, BF, out=out); torch.cuda.synchronize()
+        tune = _lib.tuning(dot_cluster=on)
+        blas.dot_tensor(X, Y, BF, out=out, tuning=tune); torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
             for _ in range(100):
-                blas.dot_tensor(X, Y, BF, out=out)
+                blas.dot_tensor(X, Y, BF, out=out, tuning=tune)
         g.replay(); torch.cuda.synchronize()
         ts = []
         for _ in range(5):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(); g.replay(); e1.record(); torch.cuda.synchronize(); ts.append(e0.elapsed_time(e1) * 10)
         print(f"k={k} {'cluster' if on else 'ticket '}: {sorted(ts)[2]:.2f} us per dot", flush=True)
-    lib.mw_dot_set_cluster(1)

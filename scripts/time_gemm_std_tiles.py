@@ -12,10 +12,9 @@ for var in (mw.Variant.STANDARD, mw.Variant.BRANCH_FREE):
         C = torch.empty_like(A)
         row = []
         for pol in (1, 2, 3, 0):
-            lib.mw_gemm_set_tile_policy(pol)
-            gemm_into(A, B, C, var); torch.cuda.synchronize()
+            tune = _lib.tuning(gemm_tile=pol)
+            gemm_into(A, B, C, var, tuning=tune); torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(); gemm_into(A, B, C, var); e1.record(); torch.cuda.synchronize()
+            e0.record(); gemm_into(A, B, C, var, tuning=tune); e1.record(); torch.cuda.synchronize()
             row.append(f"{['auto','slot0','slot1','slot2'][pol]} {e0.elapsed_time(e1):7.2f}ms")
-        lib.mw_gemm_set_tile_policy(0)
         print(f"{var.value} k={k} n={n}: " + " | ".join(row), flush=True)

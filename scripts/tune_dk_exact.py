@@ -13,19 +13,16 @@ for k in (2, 3, 4):
     st = mw.RootState(*[torch.from_numpy(t).cuda() for t in gen.config5_init(k)])
     ref = None
     for split in (0, 1):
-        lib.mw_dk_exact_set_split(split)
         for r in (32, 16, 8):
-            lib.mw_dk_exact_set_roots_per_cta(r)
-            out = mw.dk_sweeps(q, st, 2, mw.Variant.BRANCH_FREE, exact_order=True)
+            tune = _lib.tuning(dk_exact_split=split, dk_exact_roots=r)
+            out = mw.dk_sweeps(q, st, 2, mw.Variant.BRANCH_FREE, exact_order=True, tuning=tune)
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            out = mw.dk_sweeps(q, st, 10, mw.Variant.BRANCH_FREE, exact_order=True)
+            out = mw.dk_sweeps(q, st, 10, mw.Variant.BRANCH_FREE, exact_order=True, tuning=tune)
             e1.record(); torch.cuda.synchronize()
             bits = np.stack([out.re.cpu().numpy(), out.im.cpu().numpy()]).view(np.int64)
             same = ref is None or np.array_equal(bits, ref)
             ref = bits if ref is None else ref
             print(f"k={k} split={split} roots/CTA={r:2d}: {e0.elapsed_time(e1)/10*1e3:8.1f} us/sweep  "
                   f"bitwise_same={same}", flush=True)
-    lib.mw_dk_exact_set_split(1)
-    lib.mw_dk_exact_set_roots_per_cta(32)

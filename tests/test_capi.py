@@ -83,10 +83,24 @@ def test_other_entry_checks():
     assert lib.mw_renormalize(3, None, 8, p, 8, 8, None) == _lib.MW_ERR_INVALID
     assert lib.mw_fma(p, p, None, p, 8, None) == _lib.MW_ERR_INVALID
     assert lib.mw_fma(p, p, p, p, -1, None) == _lib.MW_ERR_INVALID
-    for bad in (3, 5, -2):
-        assert lib.mw_dk_tree_set_roots_per_cta(bad) == _lib.MW_ERR_INVALID
-    for good in (0, 1, 2, 4, -1):
-        assert lib.mw_dk_tree_set_roots_per_cta(good) == _lib.MW_OK
+    # per-call tuning (no global knobs): defaults, and out-of-range values
+    # rejected before anything is launched
+    t = _lib.tuning()
+    assert (t.gemm_tile, t.dot_cluster, t.dk_tree_roots, t.dk_exact_roots, t.dk_exact_split) == (0, 1, -1, 32, 1)
+    tp = _lib.tuning_ptr
+    for bad in (dict(gemm_tile=4), dict(gemm_tile=-1), dict(dot_cluster=2), dict(dk_tree_roots=3),
+                dict(dk_tree_roots=-2), dict(dk_exact_roots=0), dict(dk_exact_roots=33), dict(dk_exact_split=2)):
+        bt = _lib.tuning(**bad)
+        assert lib.mw_gemm_ex(2, 1, p, 8, 64, p, 8, 64, p, 8, 64, 8, 8, 8, tp(bt), None) == _lib.MW_ERR_INVALID, bad
+        assert lib.mw_dot_ex(2, 1, p, 8, p, 8, 8, p, p, 1, tp(bt), None) == _lib.MW_ERR_INVALID, bad
+        assert lib.mw_dk_sweep_ex(3, 1, p, 8, 8, p, p, 8, 0, 8, p, p, 8, p, p, 0, p, tp(bt), None) == \
+            _lib.MW_ERR_INVALID, bad
+    # the DK collision key j*n + i must fit an int: larger degrees are refused
+    assert lib.mw_dk_sweep(3, 1, p, 46341, 46341, p, p, 46341, 0, 1, p, p, 46341, p, p, 1, None) == \
+        _lib.MW_ERR_INVALID
+    for name in ("mw_dk_tree_set_roots_per_cta", "mw_gemm_set_tile_policy", "mw_dot_set_cluster",
+                 "mw_dk_exact_set_split", "mw_dk_exact_set_roots_per_cta"):
+        assert not hasattr(lib, name), f"{name}: the C-ABI keeps no global tuning state"
 
 
 def test_peer_sweep_checks():

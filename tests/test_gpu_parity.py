@@ -744,20 +744,17 @@ def test_no_out_of_bounds_writes(k):
     assert _guards_intact(fre, g2, nr) and _guards_intact(fim, g2, nr) and _guards_intact(mag, gm, nr)
     # tree sweeps with a workspace: every roots-per-CTA form, ragged last CTA
     i0, i1 = 3, 37  # 34 roots: 4 per CTA leaves 2 in the last
-    try:
-        for roots in (0, 1, 2, 4):
-            assert lib.mw_dk_tree_set_roots_per_cta(roots) == 0
-            wsn = lib.mw_dk_sweep_workspace(k, i0, i1)
-            wsf, gw, _ = _guarded((1, wsn))
-            assert lib.mw_dk_sweep_ws(k, 1, coeffs.data_ptr(), nr, nr, zr_t.data_ptr(), zi_t.data_ptr(), nr, i0,
-                                      i1, fre.data_ptr() + g2 * 8, fim.data_ptr() + g2 * 8, ps2,
-                                      mag.data_ptr() + gm * 8, flag.data_ptr(), 0, wsf.data_ptr() + gw * 8,
-                                      st) == 0
-            torch.cuda.synchronize()
-            assert _guards_intact(fre, g2, nr) and _guards_intact(fim, g2, nr) and _guards_intact(mag, gm, nr)
-            assert _guards_intact(wsf, gw, wsn)
-    finally:
-        lib.mw_dk_tree_set_roots_per_cta(-1)
+    for roots in (0, 1, 2, 4):
+        tune = _lib.tuning(dk_tree_roots=roots)
+        wsn = lib.mw_dk_sweep_workspace(k, i0, i1)
+        wsf, gw, _ = _guarded((1, wsn))
+        assert lib.mw_dk_sweep_ex(k, 1, coeffs.data_ptr(), nr, nr, zr_t.data_ptr(), zi_t.data_ptr(), nr, i0,
+                                  i1, fre.data_ptr() + g2 * 8, fim.data_ptr() + g2 * 8, ps2,
+                                  mag.data_ptr() + gm * 8, flag.data_ptr(), 0, wsf.data_ptr() + gw * 8,
+                                  _lib.tuning_ptr(tune), st) == 0
+        torch.cuda.synchronize()
+        assert _guards_intact(fre, g2, nr) and _guards_intact(fim, g2, nr) and _guards_intact(mag, gm, nr)
+        assert _guards_intact(wsf, gw, wsn)
     # kernels outside the dispatch tables, renormalisation, fma
     full, g, ps = _guarded((k, w))
     if k in (2, 3):
@@ -979,14 +976,11 @@ def test_dk_exact_split_and_single_warp_forms_agree(k, v):
     zre = np.zeros((k, n)); zim = np.zeros((k, n))
     zre[0] = 1.3 * np.cos(ang); zim[0] = 1.3 * np.sin(ang)
     want_re, want_im, _, _ = oracle.dk_sweep(coeffs, zre, zim, v, exact=True)
-    try:
-        for split in (0, 1):
-            lib.mw_dk_exact_set_split(split)
-            out = dk_sweeps(MonicPoly(coeffs), RootState(re=zre, im=zim), 1, V(v), exact_order=True)
-            assert_bitwise(out.re.cpu().numpy(), want_re)
-            assert_bitwise(out.im.cpu().numpy(), want_im)
-    finally:
-        lib.mw_dk_exact_set_split(1)
+    for split in (0, 1):
+        out = dk_sweeps(MonicPoly(coeffs), RootState(re=zre, im=zim), 1, V(v), exact_order=True,
+                        tuning=_lib.tuning(dk_exact_split=split))
+        assert_bitwise(out.re.cpu().numpy(), want_re)
+        assert_bitwise(out.im.cpu().numpy(), want_im)
 
 
 @pytest.mark.parametrize("k", [2, 3, 4])
@@ -1011,7 +1005,7 @@ def test_dk_tree_powers_kernel_path_matches_in_warp_path(k, v):
     i0, i1 = 7, 141
     outs = []
     for use_ws, roots in ((False, 2), (True, 0), (True, 1), (True, 2), (True, 4)):
-        lib.mw_dk_tree_set_roots_per_cta(roots)
+        tune = _lib.tuning(dk_tree_roots=roots)
         ore, oim = torch.zeros_like(R), torch.zeros_like(I)
         mag = torch.zeros(n, dtype=torch.float64, device="cuda")
         flag = torch.full((1,), 2**31 - 1, dtype=torch.int32, device="cuda")
@@ -1019,10 +1013,9 @@ def test_dk_tree_powers_kernel_path_matches_in_warp_path(k, v):
                 oim.data_ptr(), n, mag.data_ptr(), flag.data_ptr(), 0]
         if use_ws:
             ws = torch.empty(lib.mw_dk_sweep_workspace(k, i0, i1), dtype=torch.float64, device="cuda")
-            rc = lib.mw_dk_sweep_ws(*args, ws.data_ptr(), _lib.stream_handle(R.device))
+            rc = lib.mw_dk_sweep_ex(*args, ws.data_ptr(), _lib.tuning_ptr(tune), _lib.stream_handle(R.device))
         else:
             rc = lib.mw_dk_sweep(*args, _lib.stream_handle(R.device))
-        lib.mw_dk_tree_set_roots_per_cta(-1)  # back to the default (auto)
         _lib.check(rc, "sweep")
         outs.append((ore.cpu().numpy(), oim.cpu().numpy(), mag.cpu().numpy()))
     for o in outs[1:]:  # in-warp powers == powers kernel, for every roots-per-CTA form
@@ -1078,14 +1071,10 @@ def test_gemm_tile_slots_bit_identical(k, m, n):
     a, b = gen.g_k(rng, k, (m, n)), gen.g_k(rng, k, (n, n))
     A, B = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
     outs = []
-    try:
-        for policy in (0, 1, 2, 3):
-            assert lib.mw_gemm_set_tile_policy(policy) == 0
-            C = torch.empty((k, m, n), dtype=torch.float64, device="cuda")
-            gemm_into(A, B, C, Variant.BRANCH_FREE)
-            outs.append(C.cpu().numpy())
-    finally:
-        lib.mw_gemm_set_tile_policy(0)
+    for policy in (0, 1, 2, 3):
+        C = torch.empty((k, m, n), dtype=torch.float64, device="cuda")
+        gemm_into(A, B, C, Variant.BRANCH_FREE, tuning=_lib.tuning(gemm_tile=policy))
+        outs.append(C.cpu().numpy())
     for o in outs[1:]:
         assert_bitwise(o, outs[0])
     r = m // 3
@@ -1104,13 +1093,9 @@ def test_dot_cluster_form_matches_ticket_form(k, n):
     rng = np.random.default_rng(3 * n + k)
     x, y = gen.g_k(rng, k, n), gen.g_k(rng, k, n)
     X, Y = LaneBatch(x), LaneBatch(y)
-    try:
-        outs = []
-        for on in (1, 0, 1):  # cluster, ticket, cluster again (repeat calls)
-            assert lib.mw_dot_set_cluster(on) == 0
-            outs.append(np.array(blas.dot(X, Y, Variant.BRANCH_FREE, order="tree")))
-    finally:
-        lib.mw_dot_set_cluster(1)
+    outs = []
+    for on in (1, 0, 1):  # cluster, ticket, cluster again (repeat calls)
+        outs.append(np.array(blas.dot(X, Y, Variant.BRANCH_FREE, order="tree", tuning=_lib.tuning(dot_cluster=on))))
     for o in outs[1:]:
         assert_bitwise(o, outs[0])
     assert_bitwise(outs[0], oracle.dot(x, y, "bf", order=1))
