@@ -95,6 +95,11 @@ def tuning(**kw) -> Tuning:
     return t
 
 
+def tune_kw(t, *fields) -> dict:
+    """Keyword arguments for the extension from an optional Tuning."""
+    return {} if t is None else {f: int(getattr(t, f)) for f in fields}
+
+
 def tuning_ptr(t):
     """ctypes argument for an optional Tuning (None -> NULL = defaults)."""
     return None if t is None else ctypes.cast(ctypes.byref(t), ctypes.c_void_p)
@@ -105,6 +110,33 @@ def build(verbose: bool = False) -> str:
     out = None if verbose else subprocess.DEVNULL
     subprocess.run(["make", "-s", "-j8", "-C", CSRC], check=True, stdout=out)
     return LIB_PATH
+
+
+EXT_PATH = os.path.join(_HERE, "_mwext.so")
+_ext = None
+
+
+def ext():
+    """The PyTorch extension over the C-ABI (csrc/ext/mwext.cpp): the hot
+    entry points take torch tensors directly (validation, device guard and
+    torch's current stream in C++).  Raises if it has not been built."""
+    global _ext
+    if _ext is None:
+        if not os.path.exists(EXT_PATH):
+            raise RuntimeError(
+                f"mwgpu: extension missing at {EXT_PATH}; build it with "
+                "`make -C paper_2603_14926_b200/csrc` (no CPU fallback exists)"
+            )
+        import importlib.machinery
+        import importlib.util
+
+        load()  # libmwgpu.so first (the extension links it)
+        loader = importlib.machinery.ExtensionFileLoader("_mwext", EXT_PATH)
+        spec = importlib.util.spec_from_file_location("_mwext", EXT_PATH, loader=loader)
+        mod = importlib.util.module_from_spec(spec)
+        loader.exec_module(mod)
+        _ext = mod
+    return _ext
 
 
 def load() -> ctypes.CDLL:

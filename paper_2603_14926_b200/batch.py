@@ -153,20 +153,14 @@ def _check_pair(a: LaneBatch, b: LaneBatch):
         raise ValueError("mixed lane widths")
 
 
+_OPS = {"mw_ew_add": 0, "mw_ew_sub": 1, "mw_ew_mul": 2, "mw_ew_div": 3}
+
+
 def _binary(fn_name: str, a: LaneBatch, b: LaneBatch, variant) -> LaneBatch:
+    """One lane kernel through the extension (csrc/ext/mwext.cpp -> the
+    C-ABI mw_ew_*): validation, device guard and stream in C++."""
     _check_pair(a, b)
-    v = variant_code(variant)
-    _lib.require_cuda(a.planes, b.planes)
-    if a.device != b.device:
-        raise ValueError("operands on different devices")
-    k, w = a.k, a.width
-    out = torch.empty((k, w), dtype=torch.float64, device=a.device)
-    lib = _lib.load()
-    rc = getattr(lib, fn_name)(
-        k, v, _lib.ptr(a.planes), w, _lib.ptr(b.planes), w, _lib.ptr(out), w, w,
-        _lib.stream_handle(a.device),
-    )
-    _lib.check(rc, fn_name)
+    out = _lib.ext().ew(_OPS[fn_name], variant_code(variant), a.planes, b.planes)
     return LaneBatch(out, count=max(a.count, b.count))
 
 

@@ -46,39 +46,15 @@ def _check_pair(x: LaneBatch, y: LaneBatch):
         raise ValueError("mixed lane widths")
 
 
-_WS: dict = {}
-
-
-def _workspace(device, n: int, stream: int | None = None) -> torch.Tensor:
-    """Zero-initialised dot workspace, cached per (device, stream) and grown
-    on demand (the single-launch dot re-arms its ticket itself).  Calls on
-    one stream are serialised, so reuse is safe."""
-    key = (str(device), _lib.stream_handle(device) if stream is None else stream)
-    ws = _WS.get(key)
-    if ws is None or ws.numel() < max(n, 1):
-        ws = torch.zeros(max(n, 1), dtype=torch.float64, device=device)
-        _WS[key] = ws
-    return ws
-
-
 def dot_tensor(x: LaneBatch, y: LaneBatch, variant: Variant = Variant.BRANCH_FREE, order: str = "tree",
                out: torch.Tensor | None = None, tuning=None) -> torch.Tensor:
-    """dot(x, y) as a (K,) device tensor (no host synchronisation)."""
+    """dot(x, y) as a (K,) device tensor (no host synchronisation).  The
+    tree order's workspace lives in the extension: one zeroed buffer per
+    (device, stream) for eager calls, a private one per call captured into
+    a CUDA graph (csrc/ext/mwext.cpp)."""
     _check_pair(x, y)
-    o = _order(order)
-    v = variant_code(variant)
-    _lib.require_cuda(x.planes, y.planes)
-    k, n = x.k, x.width
-    lib = _lib.load()
-    if out is None:
-        out = torch.empty(k, dtype=torch.float64, device=x.device)
-    wsn = lib.mw_dot_workspace(k, n) if o == _lib.ORDER_TREE else 0
-    st = _lib.stream_handle(x.device)
-    ws = _workspace(x.device, wsn, st)
-    rc = lib.mw_dot_ex(k, v, x.planes.data_ptr(), n, y.planes.data_ptr(), n, n, ws.data_ptr(), out.data_ptr(), o,
-                       _lib.tuning_ptr(tuning), st)
-    _lib.check(rc, "mw_dot")
-    return out
+    return _lib.ext().dot(variant_code(variant), x.planes, y.planes, _order(order), out,
+                          **_lib.tune_kw(tuning, "dot_cluster"))
 
 
 def dot(x: LaneBatch, y: LaneBatch, variant: Variant = Variant.BRANCH_FREE, order: str = "tree",
@@ -93,14 +69,7 @@ def axpy_(alpha, x: LaneBatch, y: LaneBatch, variant: Variant = Variant.BRANCH_F
     alpha = tuple(float(a) for a in getattr(alpha, "comps", alpha))
     if len(alpha) != x.k:
         raise ValueError("mixed word counts")
-    _lib.require_cuda(x.planes, y.planes)
-    import ctypes
-
-    al = (ctypes.c_double * x.k)(*alpha)
-    n = x.width
-    rc = _lib.load().mw_axpy(x.k, variant_code(variant), ctypes.cast(al, ctypes.c_void_p), x.planes.data_ptr(), n,
-                             y.planes.data_ptr(), n, n, _lib.stream_handle(x.device))
-    _lib.check(rc, "mw_axpy")
+    _lib.ext().axpy_(variant_code(variant), alpha, x.planes, y.planes)
     y.count = max(x.count, y.count)
     return y
 
@@ -119,16 +88,6 @@ def gemv(a: MWMatrix, x: LaneBatch, variant: Variant = Variant.BRANCH_FREE, orde
         raise ValueError("mixed word counts")
     if a.cols != x.width:
         raise ValueError(f"shape mismatch: {a.rows}x{a.cols} @ {x.width}")
-    o = _order(order)
-    _lib.require_cuda(a.planes, x.planes)
-    k, m, n = a.k, a.rows, a.cols
-    row1 = m if row1 is None else row1
-    rows = row1 - row0
-    if out is None:
-        out = torch.empty((k, rows), dtype=torch.float64, device=a.device)
-    es = a.planes.element_size()
-    rc = _lib.load().mw_gemv(k, variant_code(variant), a.planes.data_ptr() + row0 * n * es, n, m * n,
-                             x.planes.data_ptr(), n, out.data_ptr(), out.shape[1], rows, n, o,
-                             _lib.stream_handle(a.device))
-    _lib.check(rc, "mw_gemv")
+    out = _lib.ext().gemv(variant_code(variant), a.planes, x.planes, row0, a.rows if row1 is None else row1,
+                          _order(order), out)
     return LaneBatch(out)

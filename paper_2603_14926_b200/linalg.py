@@ -267,31 +267,10 @@ def gemm_into(a: torch.Tensor, b: torch.Tensor, c: torch.Tensor, variant, row0: 
     """C[row0:row1] = A[row0:row1] B on the planes tensors (K, m, kd),
     (K, kd, n), (K, m, n) -- the row-block form the multi-GPU path shards.
     ``tuning``: an optional _lib.Tuning (launch shape only; same bits)."""
-    if a.dim() != 3 or b.dim() != 3 or c.dim() != 3:
-        raise ValueError("gemm_into: planes tensors (K, rows, cols) expected")
-    k, m, kd = a.shape
-    n = b.shape[2]
-    if b.shape[0] != k or c.shape[0] != k:
-        raise ValueError("mixed word counts")
-    if b.shape[1] != kd or tuple(c.shape[1:]) != (m, n):
-        raise ValueError(f"shape mismatch: {m}x{kd} @ {b.shape[1]}x{n} -> {c.shape[1]}x{c.shape[2]}")
-    _lib.require_planes(a, b, c)
-    row1 = m if row1 is None else row1
-    if not 0 <= row0 <= row1 <= m:
-        raise ValueError(f"row range [{row0}, {row1}) outside 0..{m}")
-    rows = row1 - row0
-    if rows <= 0:
-        return
-    es = a.element_size()
-    with _lib.on_device(a):
-        rc = _lib.load().mw_gemm_ex(
-            k, variant_code(variant),
-            a.data_ptr() + row0 * kd * es, kd, m * kd,
-            b.data_ptr(), n, kd * n,
-            c.data_ptr() + row0 * n * es, n, m * n,
-            rows, n, kd, _lib.tuning_ptr(tuning), _lib.stream_handle(a.device),
-        )
-    _lib.check(rc, "mw_gemm")
+    # validation (shapes, K, float64, contiguity, one device), the device
+    # guard and torch's current stream are in the extension
+    _lib.ext().gemm(variant_code(variant), a, b, c, row0, -1 if row1 is None else row1,
+                    **_lib.tune_kw(tuning, "gemm_tile"))
 
 
 def _ew_planes(name: str, a: torch.Tensor, b: torch.Tensor, variant) -> torch.Tensor:

@@ -94,28 +94,7 @@ def horner_into(coeffs: torch.Tensor, x: torch.Tensor, y: torch.Tensor, variant,
                 p1: int | None = None) -> None:
     """y[:, p0:p1] = Horner(coeffs, x[:, p0:p1]) on planes tensors -- the
     point-shard form the multi-GPU path uses."""
-    if coeffs.dim() != 2 or x.dim() != 2 or y.dim() != 2:
-        raise ValueError("horner_into: planes tensors (K, n) expected")
-    k, npts = x.shape
-    if coeffs.shape[0] != k or y.shape[0] != k:
-        raise ValueError("mixed word counts")
-    if y.shape[1] != npts:
-        raise ValueError("mixed lane widths")
-    _lib.require_planes(coeffs, x, y)
-    p1 = npts if p1 is None else p1
-    if not 0 <= p0 <= p1 <= npts:
-        raise ValueError(f"point range [{p0}, {p1}) outside 0..{npts}")
-    cnt = p1 - p0
-    if cnt <= 0:
-        return
-    es = x.element_size()
-    with _lib.on_device(x):
-        rc = _lib.load().mw_horner(
-            k, variant_code(variant), coeffs.data_ptr(), coeffs.shape[1], coeffs.shape[1] - 1,
-            x.data_ptr() + p0 * es, x.shape[1], y.data_ptr() + p0 * es, y.shape[1], cnt,
-            _lib.stream_handle(x.device),
-        )
-    _lib.check(rc, "mw_horner")
+    _lib.ext().horner(variant_code(variant), coeffs, x, y, p0, -1 if p1 is None else p1)
 
 
 def horner_eval_batched(p: MWPolynomial, xs: LaneBatch, variant: Variant = Variant.STANDARD) -> LaneBatch:

@@ -255,20 +255,11 @@ def sweep_into(coeffs: torch.Tensor, zre: torch.Tensor, zim: torch.Tensor, out_r
     same indices (plane stride n).  ``flag`` (int32 device scalar) must hold
     INT32_MAX beforehand; it is lowered to min(j*n + i) on a collision.
     ``tuning``: an optional _lib.Tuning (launch shape only; same bits)."""
-    k, n = zre.shape
-    i1 = n if i1 is None else i1
-    lib = _lib.load()
-    ws = None
-    if not exact_order and i1 > i0:
-        # stream-ordered scratch for the lane-per-root powers kernel
-        ws = torch.empty(lib.mw_dk_sweep_workspace(k, i0, i1), dtype=torch.float64, device=zre.device)
-    rc = lib.mw_dk_sweep_ex(
-        k, variant_code(variant), coeffs.data_ptr(), coeffs.shape[1], n, zre.data_ptr(), zim.data_ptr(), n,
-        i0, i1, out_re.data_ptr(), out_im.data_ptr(), n, step_mag.data_ptr(), flag.data_ptr(),
-        1 if exact_order else 0, None if ws is None else ws.data_ptr(), _lib.tuning_ptr(tuning),
-        _lib.stream_handle(zre.device),
-    )
-    _lib.check(rc, "mw_dk_sweep")
+    # the tree order's stream-ordered scratch (lane-per-root powers kernel)
+    # is allocated in the extension from torch's caching allocator
+    _lib.ext().dk_sweep(variant_code(variant), coeffs, zre, zim, out_re, out_im, step_mag, flag, bool(exact_order),
+                        i0, -1 if i1 is None else i1,
+                        **_lib.tune_kw(tuning, "dk_tree_roots", "dk_exact_roots", "dk_exact_split"))
 
 
 def _raise_collision(code: int, n: int):

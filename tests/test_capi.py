@@ -149,3 +149,22 @@ def test_workspace_sizes():
     assert lib.mw_dot_workspace(2, 1 << 28) == 1 + 65536 * 2 + 256 * 2
     assert lib.mw_tree_fold_workspace(3, 256) == 0
     assert lib.mw_tree_fold_workspace(3, 257) == 2 * 3
+
+
+def test_extension_loads_and_refuses_cpu_tensors():
+    """The PyTorch extension over the C-ABI (csrc/ext/mwext.cpp) loads on a
+    CPU-only host, exposes the hot entry points, and refuses host tensors
+    (no CPU fallback) before anything is launched."""
+    import torch
+
+    e = _lib.ext()
+    for name in ("ew", "axpy_", "dot", "gemv", "gemm", "horner", "dk_sweep", "version"):
+        assert hasattr(e, name), name
+    assert e.version() == _lib.version()
+    x = torch.zeros(2, 8, dtype=torch.float64)
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        e.ew(0, 1, x, x)
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        e.dot(1, x, x, 1)
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        e.gemm(1, x.reshape(2, 2, 4), x.reshape(2, 4, 2), x.reshape(2, 2, 4)[:, :, :2].contiguous())

@@ -1099,3 +1099,61 @@ def test_dot_cluster_form_matches_ticket_form(k, n):
     for o in outs[1:]:
         assert_bitwise(o, outs[0])
     assert_bitwise(outs[0], oracle.dot(x, y, "bf", order=1))
+
+
+# ------------------------------------------- the extension's host boundary
+def test_extension_validates_operands():
+    """Wrong dtype, overlapping / strided lanes, mixed K, wrong out shapes
+    -> ValueError before any launch (no silent out-of-bounds access)."""
+    from paper_2603_14926_b200 import _lib
+
+    e = _lib.ext()
+    a = torch.zeros(3, 64, dtype=torch.float64, device="cuda")
+    with pytest.raises(ValueError):
+        e.ew(0, 1, a.float(), a.float())
+    with pytest.raises(ValueError):
+        e.ew(0, 1, a, torch.zeros(2, 64, dtype=torch.float64, device="cuda"))  # mixed K
+    with pytest.raises(ValueError):
+        e.ew(0, 1, a[:, ::2], a[:, ::2])  # strided lanes
+    with pytest.raises(ValueError):
+        e.ew(0, 1, a, a, torch.zeros(3, 63, dtype=torch.float64, device="cuda"))
+    A = torch.zeros(3, 8, 8, dtype=torch.float64, device="cuda")
+    with pytest.raises(ValueError):
+        e.gemm(1, A, A.transpose(1, 2), A)  # non-contiguous B
+    with pytest.raises(ValueError):
+        e.gemm(1, A, A, A, 0, 9)  # rows outside C
+    with pytest.raises(ValueError):
+        e.horner(1, torch.zeros(3, 5, dtype=torch.float64, device="cuda"), a, a, 10, 5)
+    # column slices of a wider batch are fine (plane stride = full width)
+    w = torch.from_numpy(gen.g_k(np.random.default_rng(1), 3, 256)).cuda()
+    out = e.ew(2, 1, w[:, 10:74], w[:, 100:164])
+    assert_bitwise(out.cpu().numpy(), oracle.ew("mul", w[:, 10:74].cpu().numpy(), w[:, 100:164].cpu().numpy(), "bf"))
+
+
+def test_dot_graphs_on_two_streams_keep_private_workspaces():
+    """Two CUDA graphs of the ticket-form tree dot (n = 2^20: 256 blocks,
+    workspace ticket + partials) replayed concurrently on two streams give
+    the eager result: graph captures get their own workspace."""
+    k, n = 3, 1 << 20
+    rng = np.random.default_rng(11)
+    X, Y = LaneBatch(gen.g_k(rng, k, n)), LaneBatch(gen.g_k(rng, k, n))
+    X2, Y2 = LaneBatch(gen.g_k(rng, k, n)), LaneBatch(gen.g_k(rng, k, n))
+    want1 = blas.dot_tensor(X, Y, Variant.BRANCH_FREE).cpu().numpy()
+    want2 = blas.dot_tensor(X2, Y2, Variant.BRANCH_FREE).cpu().numpy()
+    o1 = torch.empty(k, dtype=torch.float64, device="cuda")
+    o2 = torch.empty(k, dtype=torch.float64, device="cuda")
+    g1, g2 = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g1):
+        blas.dot_tensor(X, Y, Variant.BRANCH_FREE, out=o1)
+    with torch.cuda.graph(g2):
+        blas.dot_tensor(X2, Y2, Variant.BRANCH_FREE, out=o2)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    torch.cuda.synchronize()
+    for _ in range(20):
+        with torch.cuda.stream(s1):
+            g1.replay()
+        with torch.cuda.stream(s2):
+            g2.replay()
+    torch.cuda.synchronize()
+    assert_bitwise(o1.cpu().numpy(), want1)
+    assert_bitwise(o2.cpu().numpy(), want2)
