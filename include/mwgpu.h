@@ -312,7 +312,11 @@ int mw_tuning_defaults(mw_tuning* t);
 
 /* mw_gemm / mw_dot / mw_dk_sweep_ws with explicit tuning (NULL = the
  * defaults the plain entry points use); MW_ERR_INVALID for a value out of
- * range. */
+ * range.  mw_dk_sweep_ex: if max_mag_bits != NULL (a device u64 the caller
+ * zeroes first) it is atomically raised to the bit pattern of every
+ * step_mag written, so after the sweep it holds the sweep's max update
+ * (RootState.last_max_update, roots.py:308) with no separate reduction;
+ * step_mag >= 0, so the bit order is the value order. */
 int mw_gemm_ex(int k, int variant, const double* A, int64_t lda, int64_t sA,
                const double* B, int64_t ldb, int64_t sB, double* C, int64_t ldc,
                int64_t sC, int64_t m, int64_t n, int64_t kd,
@@ -324,7 +328,8 @@ int mw_dk_sweep_ex(int k, int variant, const double* coeffs, int64_t sc,
                    int64_t n, const double* zre, const double* zim, int64_t sz,
                    int64_t i0, int64_t i1, double* zre_out, double* zim_out,
                    int64_t so, double* step_mag, int* flag_dev, int exact_order,
-                   double* ws, const mw_tuning* tune, void* stream);
+                   double* ws, unsigned long long* max_mag_bits,
+                   const mw_tuning* tune, void* stream);
 
 /* FP64 pipe microbenchmark: 8 independent DFMA (op = 0) or DADD (op = 1)
  * chains per thread, 8 unrolled steps per iteration: executes

@@ -58,7 +58,7 @@ _SIGS = {
     "mw_tuning_defaults": ([P], I),
     "mw_gemm_ex": ([I, I, P, I64, I64, P, I64, I64, P, I64, I64, I64, I64, I64, P, P], I),
     "mw_dot_ex": ([I, I, P, I64, P, I64, I64, P, P, I, P, P], I),
-    "mw_dk_sweep_ex": ([I, I, P, I64, I64, P, P, I64, I64, I64, P, P, I64, P, P, I, P, P, P], I),
+    "mw_dk_sweep_ex": ([I, I, P, I64, I64, P, P, I64, I64, I64, P, P, I64, P, P, I, P, P, P, P], I),
     "mw_dk_sweep_peer": ([I, I, P, I64, I64, P, I64, I64, P, P, P, P, P, P, P, I, I, I, I, ctypes.c_longlong, P, P,
                           I, P, P], I),
     "mw_dk_sweep_workspace": ([I, I64, I64], I64),

@@ -13,12 +13,14 @@ struct DkLaunch {
   static int run(const double* coeffs, int64_t sc, int64_t n, const double* zre,
                  const double* zim, int64_t sz, int64_t i0, int64_t i1, double* zre_out,
                  double* zim_out, int64_t so, double* step_mag, int* flag, int exact, double* ws,
-                 mw_tuning tune, cudaStream_t st) {
+                 mw_tuning tune, unsigned long long* max_bits, cudaStream_t st) {
+    DkPeers none{};
+    none.max_bits = max_bits;
     if (exact)
       return dk_exact_launch<K, VAR, false>(coeffs, sc, n, zre, zim, sz, i0, i1, zre_out, zim_out,
-                                            so, step_mag, flag, DkPeers{}, ws, tune, st);
+                                            so, step_mag, flag, none, ws, tune, st);
     return dk_tree_launch<K, VAR, false>(coeffs, sc, n, zre, zim, sz, i0, i1, zre_out, zim_out,
-                                         so, step_mag, flag, DkPeers{}, ws, tune, st);
+                                         so, step_mag, flag, none, ws, tune, st);
   }
 };
 
@@ -54,7 +56,7 @@ extern "C" int mw_dk_sweep(int k, int variant, const double* coeffs, int64_t sc,
                            int64_t i1, double* zre_out, double* zim_out, int64_t so,
                            double* step_mag, int* flag_dev, int exact_order, void* stream) {
   return mw_dk_sweep_ex(k, variant, coeffs, sc, n, zre, zim, sz, i0, i1, zre_out, zim_out, so,
-                        step_mag, flag_dev, exact_order, nullptr, nullptr, stream);
+                        step_mag, flag_dev, exact_order, nullptr, nullptr, nullptr, stream);
 }
 
 extern "C" int64_t mw_dk_sweep_workspace(int k, int64_t i0, int64_t i1) {
@@ -71,7 +73,7 @@ extern "C" int mw_dk_sweep_ws(int k, int variant, const double* coeffs, int64_t 
                               double* step_mag, int* flag_dev, int exact_order, double* ws,
                               void* stream) {
   return mw_dk_sweep_ex(k, variant, coeffs, sc, n, zre, zim, sz, i0, i1, zre_out, zim_out, so,
-                        step_mag, flag_dev, exact_order, ws, nullptr, stream);
+                        step_mag, flag_dev, exact_order, ws, nullptr, nullptr, stream);
 }
 
 // The sweep with explicit per-call tuning (NULL = defaults).  The collision
@@ -81,7 +83,8 @@ extern "C" int mw_dk_sweep_ex(int k, int variant, const double* coeffs, int64_t 
                               const double* zre, const double* zim, int64_t sz, int64_t i0,
                               int64_t i1, double* zre_out, double* zim_out, int64_t so,
                               double* step_mag, int* flag_dev, int exact_order, double* ws,
-                              const mw_tuning* tune, void* stream) {
+                              unsigned long long* max_mag_bits, const mw_tuning* tune,
+                              void* stream) {
   mw_tuning t;
   if (!tuning_resolve(tune, &t)) return MW_ERR_INVALID;
   if (k < 2 || k > 4) return MW_ERR_INVALID;
@@ -92,7 +95,7 @@ extern "C" int mw_dk_sweep_ex(int k, int variant, const double* coeffs, int64_t 
     return MW_ERR_INVALID;
   if (sc < n || sz < n || so < n) return MW_ERR_INVALID;
   return dispatch<DkLaunch>(k, variant, coeffs, sc, n, zre, zim, sz, i0, i1, zre_out, zim_out,
-                            so, step_mag, flag_dev, exact_order ? 1 : 0, ws, t,
+                            so, step_mag, flag_dev, exact_order ? 1 : 0, ws, t, max_mag_bits,
                             as_stream(stream));
 }
 

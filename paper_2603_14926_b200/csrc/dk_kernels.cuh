@@ -99,7 +99,16 @@ struct DkPeers {
   int* timeout;                    // set to 1 when a wait gave up
   long long spin_limit;
   int world, rank, sweep, sweeps;
+  // optional (any sweep, not only the peer form): atomically raised to the
+  // bit pattern of every step_mag written -- the sweep's max update
+  // (roots.py:308) without a separate reduction; step_mag >= 0, so the
+  // unsigned bit order is the value order (NaN, as np.max, dominates)
+  unsigned long long* max_bits;
 };
+
+__device__ __forceinline__ void dk_note_max(unsigned long long* max_bits, double m) {
+  if (max_bits) atomicMax(max_bits, (unsigned long long)__double_as_longlong(m));
+}
 
 // Called by exactly one thread per CTA, after a sync over the CTA's
 // storing threads.
@@ -130,7 +139,9 @@ __device__ __forceinline__ void dk_tail(const Cx<K, VAR>& acc, const Cx<K, VAR>&
   const V<K> nim = O::add(z.im, neg(step_im));
   store<K>(zre_out, so, i, nre);
   store<K>(zim_out, so, i, nim);
-  step_mag[i] = hypot(step_re.c[0], step_im.c[0]);
+  const double smag = hypot(step_re.c[0], step_im.c[0]);
+  step_mag[i] = smag;
+  if (P) dk_note_max(P->max_bits, smag);
   if constexpr (PEER) {
     for (int p = 0; p < P->world; ++p) {
       if (p == P->rank) continue;
@@ -1097,7 +1108,11 @@ __global__ void __launch_bounds__(32 * dk_treem_warps<R>(), R == 2 ? 2 : 1)
     }
     bar_sync_n(12, 64);
     if (chain) {
-      if (act) step_mag[i] = hypot(step.c[0], my[3 * K]);
+      if (act) {
+        const double smag = hypot(step.c[0], my[3 * K]);
+        step_mag[i] = smag;
+        dk_note_max(peers.max_bits, smag);
+      }
       if (lane == 0) MW_DK_MARK(8);
       if constexpr (PEER) {
         __syncwarp();

@@ -264,7 +264,7 @@ void horner(int64_t variant, const at::Tensor& coeffs, const at::Tensor& x, cons
 void dk_sweep(int64_t variant, const at::Tensor& coeffs, const at::Tensor& zre, const at::Tensor& zim,
               const at::Tensor& out_re, const at::Tensor& out_im, const at::Tensor& step_mag,
               const at::Tensor& flag, bool exact_order, int64_t i0, int64_t i1, int64_t dk_tree_roots,
-              int64_t dk_exact_roots, int64_t dk_exact_split) {
+              int64_t dk_exact_roots, int64_t dk_exact_split, c10::optional<at::Tensor> max_bits) {
   const c10::Device dev = zre.device();
   const int64_t k = zre.dim() > 0 ? zre.size(0) : 0;
   for (auto* p : {&coeffs, &zre, &zim, &out_re, &out_im}) contiguous_planes(*p, "dk planes", k, dev);
@@ -277,6 +277,13 @@ void dk_sweep(int64_t variant, const at::Tensor& coeffs, const at::Tensor& zre, 
   if (!flag.is_cuda() || flag.scalar_type() != at::kInt || flag.numel() < 1 || flag.device() != dev)
     throw py::value_error("flag: int32 device scalar expected");
   if (i1 < 0) i1 = n;
+  unsigned long long* maxp = nullptr;
+  if (max_bits.has_value()) {
+    const at::Tensor& mb = *max_bits;
+    if (!mb.is_cuda() || mb.scalar_type() != at::kLong || mb.numel() < 1 || mb.device() != dev)
+      throw py::value_error("max_bits: int64 device scalar expected");
+    maxp = reinterpret_cast<unsigned long long*>(mb.data_ptr<int64_t>());
+  }
   c10::cuda::CUDAGuard guard(dev);
   void* st = stream_of(dev);
   at::Tensor ws;
@@ -287,7 +294,8 @@ void dk_sweep(int64_t variant, const at::Tensor& coeffs, const at::Tensor& zre, 
   }
   const mw_tuning t = tuning_from(INT64_MIN, INT64_MIN, dk_tree_roots, dk_exact_roots, dk_exact_split);
   check(mw_dk_sweep_ex((int)k, (int)variant, dptr(coeffs), n, n, dptr(zre), dptr(zim), n, i0, i1, dptr(out_re),
-                       dptr(out_im), n, dptr(step_mag), flag.data_ptr<int>(), exact_order ? 1 : 0, wsp, &t, st),
+                       dptr(out_im), n, dptr(step_mag), flag.data_ptr<int>(), exact_order ? 1 : 0, wsp, maxp, &t,
+                       st),
         "mw_dk_sweep");
 }
 
@@ -309,6 +317,6 @@ PYBIND11_MODULE(TORCH_EXTENSION_NAME, m) {
   m.def("dk_sweep", &dk_sweep, py::arg("variant"), py::arg("coeffs"), py::arg("zre"), py::arg("zim"),
         py::arg("out_re"), py::arg("out_im"), py::arg("step_mag"), py::arg("flag"), py::arg("exact_order"),
         py::arg("i0") = 0, py::arg("i1") = -1, py::arg("dk_tree_roots") = D, py::arg("dk_exact_roots") = D,
-        py::arg("dk_exact_split") = D);
+        py::arg("dk_exact_split") = D, py::arg("max_bits") = py::none());
   m.def("version", []() { return std::string(mw_version()); });
 }

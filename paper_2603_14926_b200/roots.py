@@ -250,16 +250,20 @@ def aberth_init(q: MonicPoly, variant: Variant = Variant.STANDARD, radius=None) 
 # ---------------------------------------------------------------- sweep
 def sweep_into(coeffs: torch.Tensor, zre: torch.Tensor, zim: torch.Tensor, out_re: torch.Tensor,
                out_im: torch.Tensor, step_mag: torch.Tensor, flag: torch.Tensor, variant,
-               exact_order: bool = True, i0: int = 0, i1: int | None = None, tuning=None) -> None:
+               exact_order: bool = True, i0: int = 0, i1: int | None = None, tuning=None,
+               max_bits: torch.Tensor | None = None) -> None:
     """Raw launch: roots [i0, i1) of the frozen state -> out planes at the
     same indices (plane stride n).  ``flag`` (int32 device scalar) must hold
     INT32_MAX beforehand; it is lowered to min(j*n + i) on a collision.
-    ``tuning``: an optional _lib.Tuning (launch shape only; same bits)."""
+    ``tuning``: an optional _lib.Tuning (launch shape only; same bits).
+    ``max_bits`` (int64 device scalar, zero beforehand) receives the bit
+    pattern of the largest step_mag written (the sweep's max update)."""
     # the tree order's stream-ordered scratch (lane-per-root powers kernel)
     # is allocated in the extension from torch's caching allocator
     _lib.ext().dk_sweep(variant_code(variant), coeffs, zre, zim, out_re, out_im, step_mag, flag, bool(exact_order),
                         i0, -1 if i1 is None else i1,
-                        **_lib.tune_kw(tuning, "dk_tree_roots", "dk_exact_roots", "dk_exact_split"))
+                        **_lib.tune_kw(tuning, "dk_tree_roots", "dk_exact_roots", "dk_exact_split"),
+                        max_bits=max_bits)
 
 
 def _raise_collision(code: int, n: int):
@@ -281,14 +285,19 @@ def dk_iterate(q: MonicPoly, state: RootState, variant: Variant = Variant.STANDA
     out_re = torch.empty_like(state.re)
     out_im = torch.empty_like(state.im)
     mag = torch.empty(state.n, dtype=torch.float64, device=dev)
-    flag = torch.full((1,), INT32_MAX, dtype=torch.int32, device=dev)
-    sweep_into(q.planes, state.re, state.im, out_re, out_im, mag, flag, variant, exact_order)
-    code = int(flag.item())
+    # one int64 pair, uploaded by a copy (no fill kernel): [0] low word =
+    # the collision flag (INT32_MAX = none), [1] = the max-update bits the
+    # sweep kernel raises atomically (no torch reduction per sweep)
+    status = torch.tensor([INT32_MAX, 0], dtype=torch.int64).to(dev, non_blocking=True)
+    sweep_into(q.planes, state.re, state.im, out_re, out_im, mag, status.view(torch.int32)[0:1], variant,
+               exact_order, max_bits=status[1:2])
+    host = status.cpu().numpy()  # one read-back per sweep
+    code = int(host[0])
     if code != INT32_MAX:
         _raise_collision(code, state.n)
     return RootState(
         re=out_re, im=out_im, iteration=state.iteration + 1, converged=False,
-        last_max_update=float(mag.max().item()),
+        last_max_update=float(host[1:2].view(np.float64)[0]),
     )
 
 

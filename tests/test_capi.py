@@ -93,7 +93,7 @@ def test_other_entry_checks():
         bt = _lib.tuning(**bad)
         assert lib.mw_gemm_ex(2, 1, p, 8, 64, p, 8, 64, p, 8, 64, 8, 8, 8, tp(bt), None) == _lib.MW_ERR_INVALID, bad
         assert lib.mw_dot_ex(2, 1, p, 8, p, 8, 8, p, p, 1, tp(bt), None) == _lib.MW_ERR_INVALID, bad
-        assert lib.mw_dk_sweep_ex(3, 1, p, 8, 8, p, p, 8, 0, 8, p, p, 8, p, p, 0, p, tp(bt), None) == \
+        assert lib.mw_dk_sweep_ex(3, 1, p, 8, 8, p, p, 8, 0, 8, p, p, 8, p, p, 0, p, None, tp(bt), None) == \
             _lib.MW_ERR_INVALID, bad
     # the DK collision key j*n + i must fit an int: larger degrees are refused
     assert lib.mw_dk_sweep(3, 1, p, 46341, 46341, p, p, 46341, 0, 1, p, p, 46341, p, p, 1, None) == \

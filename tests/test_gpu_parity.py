@@ -751,7 +751,7 @@ def test_no_out_of_bounds_writes(k):
         assert lib.mw_dk_sweep_ex(k, 1, coeffs.data_ptr(), nr, nr, zr_t.data_ptr(), zi_t.data_ptr(), nr, i0,
                                   i1, fre.data_ptr() + g2 * 8, fim.data_ptr() + g2 * 8, ps2,
                                   mag.data_ptr() + gm * 8, flag.data_ptr(), 0, wsf.data_ptr() + gw * 8,
-                                  _lib.tuning_ptr(tune), st) == 0
+                                  None, _lib.tuning_ptr(tune), st) == 0
         torch.cuda.synchronize()
         assert _guards_intact(fre, g2, nr) and _guards_intact(fim, g2, nr) and _guards_intact(mag, gm, nr)
         assert _guards_intact(wsf, gw, wsn)
@@ -1013,7 +1013,7 @@ def test_dk_tree_powers_kernel_path_matches_in_warp_path(k, v):
                 oim.data_ptr(), n, mag.data_ptr(), flag.data_ptr(), 0]
         if use_ws:
             ws = torch.empty(lib.mw_dk_sweep_workspace(k, i0, i1), dtype=torch.float64, device="cuda")
-            rc = lib.mw_dk_sweep_ex(*args, ws.data_ptr(), _lib.tuning_ptr(tune), _lib.stream_handle(R.device))
+            rc = lib.mw_dk_sweep_ex(*args, ws.data_ptr(), None, _lib.tuning_ptr(tune), _lib.stream_handle(R.device))
         else:
             rc = lib.mw_dk_sweep(*args, _lib.stream_handle(R.device))
         _lib.check(rc, "sweep")
