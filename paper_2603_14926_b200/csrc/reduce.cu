@@ -539,8 +539,8 @@ __device__ __forceinline__ void gemv_bar_sync(int id) {
   asm volatile("bar.sync %0, 128;" ::"r"(id) : "memory");
 }
 
-template <int K, int VAR, int SLOTS, int D>
-__global__ void __launch_bounds__(128 * SLOTS)
+template <int K, int VAR, int SLOTS, int D, bool XPF = true, int MINB = 1>
+__global__ void __launch_bounds__(128 * SLOTS, MINB)
     gemv_ptree_kernel(const double* __restrict__ A, int64_t lda, int64_t sA,
                       const double* __restrict__ x, int64_t sx, double* __restrict__ y, int64_t sy,
                       int64_t m, int64_t n) {
@@ -553,10 +553,9 @@ __global__ void __launch_bounds__(128 * SLOTS)
   const int64_t valid = n < P ? n : P;
   const int64_t step = (int64_t)gridDim.x * SLOTS;
   int64_t i = (int64_t)blockIdx.x * SLOTS + slot;
-  // the first group of the current row, loaded ahead
-  V<K> a[D], xv[D];
   const bool full = (int64_t)u + (D - 1) * P < n;  // row has >= 1 full group for this lane
-  if (i < m && full) {
+  V<K> a[D], xv[D];
+  if (XPF && i < m && full) {  // the first group of the first row, loaded ahead
 #pragma unroll
     for (int d = 0; d < D; ++d) {
       a[d] = load<K>(A + i * lda, sA, u + d * P);
@@ -567,28 +566,41 @@ __global__ void __launch_bounds__(128 * SLOTS)
     const double* row = A + i * lda;
     V<K> acc = zero<K>();
     int64_t t = u;
-    if (full) {
-      for (;;) {
+    if (XPF) {
+      if (full) {
+        for (;;) {
 #pragma unroll
-        for (int d = 0; d < D; ++d) acc = Ops<K, VAR>::add(acc, Ops<K, VAR>::mul(a[d], xv[d]));
-        t += D * P;
-        if (t + (D - 1) * P >= n) break;
+          for (int d = 0; d < D; ++d) acc = Ops<K, VAR>::add(acc, Ops<K, VAR>::mul(a[d], xv[d]));
+          t += D * P;
+          if (t + (D - 1) * P >= n) break;
+#pragma unroll
+          for (int d = 0; d < D; ++d) {
+            a[d] = load<K>(row, sA, t + d * P);
+            xv[d] = load<K>(x, sx, t + d * P);
+          }
+        }
+      }
+    } else {
+      for (; t + (D - 1) * P < n; t += D * P) {
 #pragma unroll
         for (int d = 0; d < D; ++d) {
           a[d] = load<K>(row, sA, t + d * P);
           xv[d] = load<K>(x, sx, t + d * P);
         }
+#pragma unroll
+        for (int d = 0; d < D; ++d) acc = Ops<K, VAR>::add(acc, Ops<K, VAR>::mul(a[d], xv[d]));
       }
     }
     for (; t < n; t += P)
       acc = Ops<K, VAR>::add(acc, Ops<K, VAR>::mul(load<K>(row, sA, t), load<K>(x, sx, t)));
-    // next row's first group, in flight during the tree
-    const int64_t inext = i + step;
-    if (inext < m && full) {
+    if (XPF) {  // next row's first group, in flight during the tree
+      const int64_t inext = i + step;
+      if (inext < m && full) {
 #pragma unroll
-      for (int d = 0; d < D; ++d) {
-        a[d] = load<K>(A + inext * lda, sA, u + d * P);
-        xv[d] = load<K>(x, sx, u + d * P);
+        for (int d = 0; d < D; ++d) {
+          a[d] = load<K>(A + inext * lda, sA, u + d * P);
+          xv[d] = load<K>(x, sx, u + d * P);
+        }
       }
     }
 #pragma unroll

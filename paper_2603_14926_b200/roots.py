@@ -401,7 +401,14 @@ def dk_solve(q: MonicPoly, variant: Variant = Variant.STANDARD, tol: float | Non
     and returns the first converged sweep's state (a collision raises at
     its own sweep, before that sweep's convergence test, as in the
     reference loop).  The up to 31 sweeps computed past convergence cost
-    device time only."""
+    device time only.
+
+    The iterates are bit-identical to the reference's sweep by sweep (exact
+    order).  The convergence TEST is not bit-identical: the reference
+    compares np.hypot magnitudes (roots.py:308, 334-336), here |step| is
+    CUDA's hypot in the sweep kernel (<= 2 ulp) and max|z| torch.hypot, so
+    when the largest update lands within a few ulp of tol * max|z| the
+    first converged sweep can differ from the reference loop's by one."""
     if tol is None:
         tol = default_tolerance(q.k)
     if tol <= 0:

@@ -11,10 +11,20 @@ lib.mwt_gemv_config_name.restype = ctypes.c_char_p
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 NOFLUSH = "--noflush" in sys.argv
 MAC = {3: 96, 4: 209}
+PAD = int(os.environ.get("PAD", "0"))  # extra elements between A's planes (layout experiment)
+lib.mwt_gemv_set_sa.argtypes = [ctypes.c_int64]
 for k in (3, 4):
     a, x = gen.config2_gemv(k)
-    A, X = torch.from_numpy(a).cuda(), torch.from_numpy(x).cuda()
     m, n = a.shape[1], a.shape[2]
+    if PAD:
+        buf = torch.empty((k, m * n + PAD), dtype=torch.float64, device="cuda")
+        buf[:, : m * n] = torch.from_numpy(a.reshape(k, m * n)).cuda()
+        A = buf
+        lib.mwt_gemv_set_sa(m * n + PAD)
+    else:
+        A = torch.from_numpy(a).cuda()
+        lib.mwt_gemv_set_sa(0)
+    X = torch.from_numpy(x).cuda()
     y = torch.empty((k, m), dtype=torch.float64, device="cuda")
     ref = None
     sel = [int(c) for c in os.environ.get("CFGS", "").split(",") if c]
@@ -39,4 +49,4 @@ for k in (3, 4):
             e0.record(); lib.mwt_gemv(cfg, k, A.data_ptr(), X.data_ptr(), y.data_ptr(), m, n, st); e1.record()
             torch.cuda.synchronize(); ts.append(e0.elapsed_time(e1))
         ms = sorted(ts)[len(ts) // 2]
-        print(f"k={k} {lib.mwt_gemv_config_name(cfg).decode():10s} {ms*1e3:8.1f} us  {MAC[k]*m*n/(ms/1e3)/1e12:6.2f} T/s{same}", flush=True)
+        print(f"k={k} pad={PAD} {lib.mwt_gemv_config_name(cfg).decode():10s} {ms*1e3:8.1f} us  {MAC[k]*m*n/(ms/1e3)/1e12:6.2f} T/s{same}", flush=True)
