@@ -60,6 +60,8 @@ def parse():
                     help="N > 1: also time the dot and the DK sweep with the exchange fused into the kernel "
                          "(DotPeer / DKPeerGraph, cudaIpc peer memory); off by default until it has been run "
                          "on a multi-GPU node")
+    ap.add_argument("--secondary-timeout", type=float, default=480.0,
+                    help="seconds the secondary rows may take before the line is printed without the rest")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="process-group backend for N > 1 (gloo only to exercise the multi-rank "
                          "logic where fewer GPUs than ranks exist; never for timing)")
@@ -204,10 +206,13 @@ def run_ours(args):
     dev_index = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(dev_index)
     if world > 1:
+        from datetime import timedelta
+
+        # bounded collectives: a lost peer ends the run instead of hanging it
         if args.backend == "nccl":
-            dist.init_process_group("nccl", device_id=torch.device("cuda", dev_index))
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev_index), timeout=timedelta(seconds=300))
         else:
-            dist.init_process_group("gloo")
+            dist.init_process_group("gloo", timeout=timedelta(seconds=300))
     lib = _lib.load()
     stream = lambda: torch.cuda.current_stream().cuda_stream  # noqa: E731
 
@@ -446,49 +451,74 @@ def run_ours(args):
         "peak_source": "measured live: DFMA microbenchmark, 8 chains/thread, all SMs (mw_fp64_peak_kernel)",
     }
 
-    sec = None
-    if not args.no_secondary:
-        try:
-            sec = secondary(args, torch, dist, mw, world, rank, peak)
-        except Exception as e:  # reported in the line; the headline stands on its own
-            sec = {"error": f"{type(e).__name__}: {e}"[:300]}
-
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_sample(gemm_parts, horner)
 
-    if rank == 0:
-        line = {
-            "metric": "DD/TD/QD GEMM and Horner Gops/s vs FP64 FMA roofline, 1/2/4/8 B200",
-            "value": round(value, 3), "unit": "G MP-ops/s",
-            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": round(ms_step, 3), "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f64 (DD/TD/QD multi-word)", "data": "synthetic (seeded, SURVEY §8(d) G_K)",
-            "config": {
-                "workload": "config3 GEMM DD n4096 + TD n2048 + QD n2048, config4 QD Horner deg1024 x 2^24 pts",
-                "gemm": [f"k{k} n{n}" for k, n in gemm_parts], "horner": horner,
-                "parallelism": f"rows/points sharded over {world} GPU(s), no collective",
-                "ranks": world, "backend": args.backend if world > 1 else None,
-                "shards": rank_shards,
-                "shared_gpus": (world > torch.cuda.device_count()) or None,
-                "l2": "inputs larger than L2 (GEMM DD A+B 537 MB, Horner x 537 MB); no flush",
-                "bit_exact": "GEMM naive order and Horner per point, vs reference",
-            },
-            "parts": [{"name": p["name"], "ms": round(p["ms"], 3), "G_MPops": round(p["gmpops"], 2),
-                       "fp64_Tops": round(p["fp64_tops"], 3), "frac": round(p["frac_of_fp64_peak"], 4)}
-                      for p in parts],
-            "fp64_peak_measured": {"dfma_Tops": round(peak["dfma"] / 1e12, 3), "dadd_Tops": round(peak["dadd"] / 1e12, 3),
-                                   "method": "8 independent DFMA / DADD chains per thread, 8 CTAs x 256 threads per SM, "
-                                             "~0.75 s per op (best of 3)",
-                                   "clocks": peak_clk.summary()},
-            "roofline": roofline,
-            "cpu_baseline": cpu,
-            "e2e": e2e,
-            "gpu_launches": args.steps * (len(dev) + 1),
-            "clocks": clk.summary(),
-            "secondary": sec,
-        }
-        print(json.dumps(line))
+    sec = {}
+    line = {
+        "metric": "DD/TD/QD GEMM and Horner Gops/s vs FP64 FMA roofline, 1/2/4/8 B200",
+        "value": round(value, 3), "unit": "G MP-ops/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(ms_step, 3), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64 (DD/TD/QD multi-word)", "data": "synthetic (seeded, SURVEY §8(d) G_K)",
+        "config": {
+            "workload": "config3 GEMM DD n4096 + TD n2048 + QD n2048, config4 QD Horner deg1024 x 2^24 pts",
+            "gemm": [f"k{k} n{n}" for k, n in gemm_parts], "horner": horner,
+            "parallelism": f"rows/points sharded over {world} GPU(s), no collective",
+            "ranks": world, "backend": args.backend if world > 1 else None,
+            "shards": rank_shards,
+            "shared_gpus": (world > torch.cuda.device_count()) or None,
+            "l2": "inputs larger than L2 (GEMM DD A+B 537 MB, Horner x 537 MB); no flush",
+            "bit_exact": "GEMM naive order and Horner per point, vs reference",
+        },
+        "parts": [{"name": p["name"], "ms": round(p["ms"], 3), "G_MPops": round(p["gmpops"], 2),
+                   "fp64_Tops": round(p["fp64_tops"], 3), "frac": round(p["frac_of_fp64_peak"], 4)}
+                  for p in parts],
+        "fp64_peak_measured": {"dfma_Tops": round(peak["dfma"] / 1e12, 3), "dadd_Tops": round(peak["dadd"] / 1e12, 3),
+                               "method": "8 independent DFMA / DADD chains per thread, 8 CTAs x 256 threads per SM, "
+                                         "~0.75 s per op (best of 3)",
+                               "clocks": peak_clk.summary()},
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": args.steps * (len(dev) + 1),
+        "clocks": clk.summary(),
+        "secondary": sec if not args.no_secondary else None,
+    }
+
+    # The headline is complete here.  The secondary rows run under a
+    # watchdog: if they have not finished in time (a stuck collective at
+    # N > 1, say), the line is printed with what was measured and the
+    # process exits -- the headline is never lost to a secondary row.
+    import threading
+
+    printed = threading.Event()
+
+    def emit(note=None):
+        if printed.is_set():
+            return
+        printed.set()
+        if note:
+            line["secondary_note"] = note
+        if rank == 0:
+            print(json.dumps(line), flush=True)
+
+    def on_timeout():
+        emit(f"secondary rows stopped by the {args.secondary_timeout:.0f} s watchdog")
+        sys.stdout.flush()
+        os._exit(0)
+
+    if not args.no_secondary:
+        dog = threading.Timer(args.secondary_timeout, on_timeout)
+        dog.daemon = True
+        dog.start()
+        try:
+            secondary(args, torch, dist, mw, world, rank, peak, out=sec)
+        except Exception as e:  # reported in the line; the headline stands on its own
+            sec["error"] = f"{type(e).__name__}: {e}"[:300]
+        dog.cancel()
+    emit()
     if world > 1:
         dist.destroy_process_group()
 
@@ -498,7 +528,7 @@ ADD_OPS = {2: 20, 3: 57, 4: 103}
 MUL_OPS = {2: 9, 3: 39, 4: 106}
 
 
-def secondary(args, torch, dist, mw, world, rank, peak):
+def secondary(args, torch, dist, mw, world, rank, peak, out=None):
     """The other §8 rows, measured on the same run (not the headline):
     config 1 dot/axpy (DD n=65536), config 2 GEMV (TD/QD 2048^2),
     config 5 DK (TD/QD n=512, 200 sweeps; roots sharded + one all-gather
@@ -513,7 +543,7 @@ def secondary(args, torch, dist, mw, world, rank, peak):
         hbm = json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json")))["hbm_gbs"] * 1e9
     except (OSError, ValueError, KeyError):
         pass
-    out = {}
+    out = {} if out is None else out  # filled in place: a watchdog may print it early
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > L2 (126 MB)
 
     def timed(fn, reps, flush_l2=False):
@@ -554,10 +584,20 @@ def secondary(args, torch, dist, mw, world, rank, peak):
         torch.cuda.synchronize()
         return statistics.median(e0.elapsed_time(e1) for e0, e1 in evs) / calls
 
-    def timed_graph_flushed(fn, reps=20):
+    flush_rd = None
+
+    def timed_graph_flushed(fn, reps=20, clean=False):
         """Device time of ONE call (captured alone in a CUDA graph, so the
         host-side API cost cannot leave the GPU idle inside the timed
-        region), L2 flushed before every replay; median over replays."""
+        region), L2 flushed before every replay; median over replays.
+        The flush writes a 256 MB buffer, which leaves L2 full of DIRTY
+        lines: the timed call then pays their write-back as it streams its
+        operand in.  clean=True also reads a second 256 MB buffer after
+        the write, so the call starts from a cold but clean L2 (the state
+        ncu's cache control leaves)."""
+        nonlocal flush_rd
+        if clean and flush_rd is None:
+            flush_rd = torch.ones(256 << 20, dtype=torch.uint8, device="cuda")
         fn()
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
@@ -566,8 +606,11 @@ def secondary(args, torch, dist, mw, world, rank, peak):
         g.replay()
         torch.cuda.synchronize()
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+        sink = torch.empty((), dtype=torch.int64, device="cuda")
         for e0, e1 in evs:
             flush.fill_(1)
+            if clean:
+                torch.sum(flush_rd, dtype=torch.int64, out=sink)
             e0.record()
             g.replay()
             e1.record()
@@ -610,15 +653,36 @@ def secondary(args, torch, dist, mw, world, rank, peak):
     ms_axpy = timed(lambda: blas.axpy_(tuple(alpha), Xs, Ys, BF), 200)
     if world == 1:
         ms_axpy_graph = timed_graph(lambda: blas.axpy_(tuple(alpha), Xs, Ys, BF))
+    def host_us(fn, calls=2000):
+        """Host cost of the public API per call: wall time of back-to-back
+        calls (the device work queues behind them), synchronised at the end."""
+        for _ in range(50):
+            fn()
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        for _ in range(calls):
+            fn()
+        torch.cuda.synchronize()
+        return (time.perf_counter() - t) / calls * 1e6
+
+    if world == 1:
+        host_dot = host_us(lambda: blas.dot_tensor(X, Y, BF, out=dres))
+        host_axpy = host_us(lambda: blas.axpy_(tuple(alpha), Xs, Ys, BF))
+    else:
+        host_dot = host_axpy = None
     out["config1_dot_dd_n65536"] = {
+        "host_us_per_call": None if host_dot is None else round(host_dot, 2),
         "us_per_call": round(ms_dot * 1e3, 2), "G_MPops": round(2 * n1 / (ms_dot / 1e3) / 1e9, 3),
         "us_per_call_graph": None if ms_dot_graph is None else round(ms_dot_graph * 1e3, 2),
         "G_MPops_graph": None if ms_dot_graph is None else round(2 * n1 / (ms_dot_graph / 1e3) / 1e9, 3),
         "hbm_frac": round(2 * 2 * n1 * 8 / (ms_dot / 1e3) / hbm, 4),
         "order": "tree (256 strided partials per 4096-element block + pairwise tree)" + (", all-gather-then-sum over ranks" if world > 1 else ""),
-        "note": "2 MiB input is L2-resident and launch-bound; hbm_frac is bytes/time vs HBM copy peak",
+        "note": "2 MiB input is L2-resident and launch-bound; hbm_frac is bytes/time vs HBM copy peak; "
+                "us_per_call = one eager API call between CUDA events (launch latency included), "
+                "host_us_per_call = host cost per call issued back to back (PyTorch extension path)",
         "fused_peer_exchange": peer_dot}
     out["config1_axpy_dd_n65536"] = {
+        "host_us_per_call": None if host_axpy is None else round(host_axpy, 2),
         "us_per_call": round(ms_axpy * 1e3, 2), "G_MPops": round(2 * n1 / (ms_axpy / 1e3) / 1e9, 3),
         "us_per_call_graph": None if ms_axpy_graph is None else round(ms_axpy_graph * 1e3, 2),
         "hbm_frac": round(3 * 2 * (hi - lo) * 8 * world / (ms_axpy / 1e3) / hbm, 4)}
@@ -663,6 +727,8 @@ def secondary(args, torch, dist, mw, world, rank, peak):
         yb = torch.empty((k, rhi - rlo), dtype=torch.float64, device="cuda")
         ms_eager = timed(lambda: blas.gemv(A, XV, BF, "tree", rlo, rhi, out=yb), 20, flush_l2=True)
         ms = timed_graph_flushed(lambda: blas.gemv(A, XV, BF, "tree", rlo, rhi, out=yb))
+        ms_clean = timed_graph_flushed(lambda: blas.gemv(A, XV, BF, "tree", rlo, rhi, out=yb), clean=True)
+        ms_warm = timed_graph(lambda: blas.gemv(A, XV, BF, "tree", rlo, rhi, out=yb), calls=20)
         fp = MAC_OPS[k] * m * m
         out[f"config2_gemv_{'td' if k == 3 else 'qd'}_n2048"] = {
             "ms": round(ms, 4), "G_MPops": round(2 * m * m / (ms / 1e3) / 1e9, 2),
@@ -672,7 +738,11 @@ def secondary(args, torch, dist, mw, world, rank, peak):
             "hbm_bound_us": round(k * m * m * 8 / hbm / world * 1e6, 1),
             "l2": "flushed before each call",
             "timing": "one call per CUDA-graph replay (device time, no host API gap); ms_eager = the same call launched eagerly through the Python API",
-            "ms_eager": round(ms_eager, 4)}
+            "ms_eager": round(ms_eager, 4),
+            "ms_clean_flush": round(ms_clean, 4),
+            "ms_back_to_back": round(ms_warm, 4),
+            "flush_note": "ms: after a 256 MB write (dirty L2: the call pays the write-backs); ms_clean_flush: "
+                          "write then a 256 MB read (cold, clean L2); ms_back_to_back: 20 calls per graph"}
         del A
 
     # ---- config 3 with the reference's benchmark scheme (Strassen; 1 GPU):

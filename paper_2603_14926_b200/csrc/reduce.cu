@@ -628,6 +628,97 @@ __global__ void __launch_bounds__(128 * SLOTS, MINB)
   }
 }
 
+// Tree-order GEMV with A streamed through a per-WARP shared-memory ring by
+// 16-byte cp.async.cg (L2 only: A never enters L1, so x stays L1-resident):
+// every warp keeps S-1 chunks of D elements x K planes in flight while it
+// folds the current chunk from shared memory, so the loads of chunk c+1..
+// never wait behind the arithmetic of chunk c (the register-prefetch forms
+// get their next loads sunk below the fold by the compiler).  Same partials
+// (partial u folds t = u, u+128, ...), same tree: bit-identical.
+// Requires n % (128 D) == 0 and 16-byte aligned rows/planes (else the caller
+// uses gemv_tree_kernel).
+template <int K, int VAR, int D, int S>
+__global__ void __launch_bounds__(128)
+    gemv_cg_kernel(const double* __restrict__ A, int64_t lda, int64_t sA,
+                   const double* __restrict__ x, int64_t sx, double* __restrict__ y, int64_t sy,
+                   int64_t m, int64_t n) {
+  constexpr int P = 128;
+  constexpr int SEG = K * D;  // 256-byte segments per chunk per warp
+  extern __shared__ double gcg_ring[];  // [warp][S][K*D][32]
+  __shared__ double roots[K][4];
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int u = warp * 32 + lane;
+  const int64_t i = blockIdx.x;
+  const double* row = A + i * lda;
+  double* ring = gcg_ring + (size_t)warp * S * SEG * 32;
+  const int64_t nch = n / (D * P);
+  auto issue = [&](int64_t ch) {
+    double* st = ring + (size_t)(ch % S) * SEG * 32;
+    // SEG segments of 32 doubles; each lane copies 16 bytes of two of them
+#pragma unroll
+    for (int q = 0; q < SEG / 2; ++q) {
+      const int seg = 2 * q + (lane >> 4);
+      const int c = seg / D, d = seg % D;
+      const int off = (lane & 15) * 2;
+      const double* src = row + c * sA + ch * (D * P) + d * P + warp * 32 + off;
+      cp_async16(st + seg * 32 + off, src, 16);
+    }
+    if (SEG & 1) {
+      const int seg = SEG - 1;
+      const int c = seg / D, d = seg % D;
+      if (lane < 16)
+        cp_async16(st + seg * 32 + lane * 2, row + c * sA + ch * (D * P) + d * P + warp * 32 + lane * 2, 16);
+    }
+  };
+#pragma unroll
+  for (int p = 0; p < S - 1; ++p) {
+    if (p < nch) issue(p);
+    cp_async_commit();
+  }
+  V<K> acc = zero<K>();
+  for (int64_t ch = 0; ch < nch; ++ch) {
+    V<K> xv[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) xv[d] = load<K>(x, sx, ch * (D * P) + d * P + u);
+    cp_async_wait<S - 2>();
+    __syncwarp();
+    const double* st = ring + (size_t)(ch % S) * SEG * 32;
+    V<K> a[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d)
+#pragma unroll
+      for (int c = 0; c < K; ++c) a[d].c[c] = st[(c * D + d) * 32 + lane];
+    __syncwarp();  // every lane has read the stage before it is refilled
+    if (ch + S - 1 < nch) issue(ch + S - 1);
+    cp_async_commit();
+#pragma unroll
+    for (int d = 0; d < D; ++d) acc = Ops<K, VAR>::add(acc, Ops<K, VAR>::mul(a[d], xv[d]));
+  }
+  const int64_t valid = n < P ? n : P;
+#pragma unroll
+  for (int s = 1; s < 32; s <<= 1) {
+    const V<K> o = shfl_down<K>(acc, s);
+    if ((lane & (2 * s - 1)) == 0 && u + s < valid) acc = Ops<K, VAR>::add(acc, o);
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int c = 0; c < K; ++c) roots[c][warp] = acc.c[c];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    V<K> r[4];
+#pragma unroll
+    for (int w = 0; w < 4; ++w)
+#pragma unroll
+      for (int c = 0; c < K; ++c) r[w].c[c] = roots[c][w];
+    if (32 < valid) r[0] = Ops<K, VAR>::add(r[0], r[1]);
+    if (96 < valid) r[2] = Ops<K, VAR>::add(r[2], r[3]);
+    if (64 < valid) r[0] = Ops<K, VAR>::add(r[0], r[2]);
+    store<K>(y, sy, i, r[0]);
+  }
+}
+
 template <int K, int VAR>
 struct GemvLaunch {
   static int run(const double* A, int64_t lda, int64_t sA, const double* x, int64_t sx, double* y,

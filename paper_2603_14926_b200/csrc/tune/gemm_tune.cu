@@ -97,12 +97,16 @@ extern "C" int mwt_gemm(int cfg, int k, const double* A, const double* B, double
 // plane stride of A (elements): m * n unless set (padding experiments)
 static int64_t g_gemv_sa = 0;
 static inline int64_t gemv_sa(int64_t m, int64_t n) { return g_gemv_sa > 0 ? g_gemv_sa : m * n; }
+// row stride override (0 = n; -1 = every row reads row 0: A stays L2-resident)
+static int64_t g_gemv_lda = 0;
+static inline int64_t gemv_lda(int64_t n) { return g_gemv_lda == 0 ? n : (g_gemv_lda < 0 ? 0 : g_gemv_lda); }
+extern "C" void mwt_gemv_set_lda(int64_t v) { g_gemv_lda = v; }
 extern "C" void mwt_gemv_set_sa(int64_t sa) { g_gemv_sa = sa; }
 template <int K, int W, int R, int D>
 static int gemv_launch(const double* A, const double* x, double* y, int64_t m, int64_t n,
                        cudaStream_t st) {
   gemv_tree_kernel<K, BRANCH_FREE, W, R, D><<<(unsigned)((m + R - 1) / R), 32 * W * R, 0, st>>>(
-      A, n, gemv_sa(m, n), x, n, y, m, m, n);
+      A, gemv_lda(n), gemv_sa(m, n), x, n, y, m, m, n);
   return launch_status();
 }
 template <int K, int SLOTS, int D, bool PERSIST, bool XPF = true, int MINB = 1>
@@ -117,7 +121,17 @@ static int gemv_ptree_launch(const double* A, const double* x, double* y, int64_
     const int64_t rows_per_slot = (m + slots - 1) / slots;
     grid = (m + rows_per_slot * SLOTS - 1) / (rows_per_slot * SLOTS);
   }
-  kern<<<(unsigned)grid, 128 * SLOTS, 0, st>>>(A, n, gemv_sa(m, n), x, n, y, m, m, n);
+  kern<<<(unsigned)grid, 128 * SLOTS, 0, st>>>(A, gemv_lda(n), gemv_sa(m, n), x, n, y, m, m, n);
+  return launch_status();
+}
+template <int K, int D, int S>
+static int gemv_cg_launch(const double* A, const double* x, double* y, int64_t m, int64_t n,
+                          cudaStream_t st) {
+  if (n % (128 * D)) return MW_ERR_INVALID;
+  auto kern = gemv_cg_kernel<K, BRANCH_FREE, D, S>;
+  const int smem = 4 * S * K * D * 32 * (int)sizeof(double);
+  if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  kern<<<(unsigned)m, 128, smem, st>>>(A, gemv_lda(n), gemv_sa(m, n), x, n, y, m, m, n);
   return launch_status();
 }
 template <int K, int R, int D, int S, bool XS>
@@ -126,7 +140,7 @@ static int gemv_staged_launch(const double* A, const double* x, double* y, int64
   constexpr size_t smem = gemv_staged_smem<K, R, D, S, XS>();
   auto kern = gemv_staged_kernel<K, BRANCH_FREE, R, D, S, XS>;
   if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  kern<<<(unsigned)((m + R - 1) / R), 128 * R, smem, st>>>(A, n, gemv_sa(m, n), x, n, y, m, m, n);
+  kern<<<(unsigned)((m + R - 1) / R), 128 * R, smem, st>>>(A, gemv_lda(n), gemv_sa(m, n), x, n, y, m, m, n);
   return launch_status();
 }
 template <int K, int G, int CH, int S>
@@ -138,20 +152,20 @@ static int gemv_bulk_launch(const double* A, const double* x, double* y, int64_t
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int grid = sm_count();
   if ((int64_t)grid * G > m) grid = (int)((m + G - 1) / G);
-  kern<<<grid, 128 * G, smem, st>>>(A, n, gemv_sa(m, n), x, n, y, m, m, n);
+  kern<<<grid, 128 * G, smem, st>>>(A, gemv_lda(n), gemv_sa(m, n), x, n, y, m, m, n);
   return launch_status();
 }
 template <int K, int MODE>
 static int gemv_probe_launch(const double* A, const double* x, double* y, int64_t m, int64_t n,
                              cudaStream_t st) {
-  gemv_probe_kernel<K, BRANCH_FREE, MODE><<<(unsigned)((m + 1) / 2), 256, 0, st>>>(A, n, gemv_sa(m, n), x, n, y, m, m, n);
+  gemv_probe_kernel<K, BRANCH_FREE, MODE><<<(unsigned)((m + 1) / 2), 256, 0, st>>>(A, gemv_lda(n), gemv_sa(m, n), x, n, y, m, m, n);
   return launch_status();
 }
 template <int K, int RT, int D, bool PIPE, int MINB = 1>
 static int gemv_rt_launch(const double* A, const double* x, double* y, int64_t m, int64_t n,
                           cudaStream_t st) {
   gemv_rt_kernel<K, BRANCH_FREE, RT, D, PIPE, MINB><<<(unsigned)((m + RT - 1) / RT), 128, 0, st>>>(
-      A, n, gemv_sa(m, n), x, n, y, m, m, n);
+      A, gemv_lda(n), gemv_sa(m, n), x, n, y, m, m, n);
   return launch_status();
 }
 template <int K, int Q, int J, int S>
@@ -164,14 +178,14 @@ static int gemv_wring_launch(const double* A, const double* x, double* y, int64_
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int grid = sm_count();
   if ((int64_t)grid * Q > m) grid = (int)((m + Q - 1) / Q);
-  kern<<<grid, 128 * Q, smem, st>>>(A, n, gemv_sa(m, n), x, n, y, m, m, n);
+  kern<<<grid, 128 * Q, smem, st>>>(A, gemv_lda(n), gemv_sa(m, n), x, n, y, m, m, n);
   return launch_status();
 }
 template <int K, int C, int D, int RPC>
 static int gemv_mc_launch(const double* A, const double* x, double* y, int64_t m, int64_t n,
                           cudaStream_t st) {
   gemv_mc_kernel<K, BRANCH_FREE, C, D, RPC><<<(unsigned)((m + RPC - 1) / RPC), 128 * RPC, 0, st>>>(
-      A, n, gemv_sa(m, n), x, n, y, m, m, n);
+      A, gemv_lda(n), gemv_sa(m, n), x, n, y, m, m, n);
   return launch_status();
 }
 template <int K, int D, int RPC>
@@ -179,7 +193,7 @@ static int gemv_v2_launch(const double* A, const double* x, double* y, int64_t m
                           cudaStream_t st) {
   if (n % 256) return MW_ERR_INVALID;
   gemv_v2_kernel<K, BRANCH_FREE, D, RPC><<<(unsigned)((m + RPC - 1) / RPC), 128 * RPC, 0, st>>>(
-      A, n, gemv_sa(m, n), x, n, y, m, m, n);
+      A, gemv_lda(n), gemv_sa(m, n), x, n, y, m, m, n);
   return launch_status();
 }
 template <int K, int RPC, int D, int CPS>
@@ -192,14 +206,14 @@ static int gemv_xs_launch(const double* A, const double* x, double* y, int64_t m
   int64_t grid = (int64_t)148 * CPS;
   const int64_t need = (m + RPC - 1) / RPC;
   if (grid > need) grid = need;
-  kern<<<(unsigned)grid, 128 * RPC, smem, st>>>(A, n, gemv_sa(m, n), x, n, y, m, m, n);
+  kern<<<(unsigned)grid, 128 * RPC, smem, st>>>(A, gemv_lda(n), gemv_sa(m, n), x, n, y, m, m, n);
   return launch_status();
 }
 template <int K, int RPC, int D>
 static int gemv_cs_launch(const double* A, const double* x, double* y, int64_t m, int64_t n,
                           cudaStream_t st) {
   gemv_cs_kernel<K, BRANCH_FREE, RPC, D><<<(unsigned)((m + RPC - 1) / RPC), 128 * RPC, 0, st>>>(
-      A, n, gemv_sa(m, n), x, n, y, m, m, n);
+      A, gemv_lda(n), gemv_sa(m, n), x, n, y, m, m, n);
   return launch_status();
 }
 template <int K>
@@ -286,10 +300,18 @@ static int gemv_run(int cfg, const double* A, const double* x, double* y, int64_
     case 77: return gemv_ptree_launch<K, 2, 4, false, false, 4>(A, x, y, m, n, st);
     case 78: return gemv_ptree_launch<K, 1, 2, false, false, 8>(A, x, y, m, n, st);
     case 79: return gemv_ptree_launch<K, 1, 2, true, false, 8>(A, x, y, m, n, st);
+    case 80: return gemv_cg_launch<K, 4, 3>(A, x, y, m, n, st);
+    case 81: return gemv_cg_launch<K, 4, 4>(A, x, y, m, n, st);
+    case 82: return gemv_cg_launch<K, 2, 4>(A, x, y, m, n, st);
+    case 83: return gemv_cg_launch<K, 2, 6>(A, x, y, m, n, st);
+    case 84: return gemv_cg_launch<K, 2, 3>(A, x, y, m, n, st);
+    case 85: return gemv_cg_launch<K, 1, 8>(A, x, y, m, n, st);
+    case 86: return gemv_cg_launch<K, 4, 2>(A, x, y, m, n, st);
+    case 87: return gemv_cg_launch<K, 8, 2>(A, x, y, m, n, st);
     default: return MW_ERR_INVALID;
   }
 }
-extern "C" int mwt_gemv_num_configs(void) { return 80; }
+extern "C" int mwt_gemv_num_configs(void) { return 88; }
 extern "C" const char* mwt_gemv_config_name(int cfg) {
   static const char* names[] = {"W4_R2_D4", "W1_R8_D8", "W1_R8_D4", "W2_R4_D4", "W2_R4_D8",
                                 "W4_R2_D2", "W4_R1_D4", "W8_R1_D2", "st_R2_D4_S2", "st_R2_D4_S3",
@@ -305,8 +327,9 @@ extern "C" const char* mwt_gemv_config_name(int cfg) {
                                 "xs_R8_D4", "xs_R6_D4", "xs_R4_D4_c2", "xs_R8_D2", "cs_R2_D4", "cs_R1_D4",
                                 "pt_S1_D4", "pt_S2_D4", "pt_S1_D2", "pt_S2_D2", "pt_S4_D4", "pt_S1_D8",
                                 "np_S1_D4", "np_S2_D4", "pt_S2_D8", "pn_S1_D4", "pn_S2_D4", "pn_S1_D4_m8",
-                                "pn_S2_D4_m4", "nn_S1_D4", "nn_S2_D4", "nn_S1_D4_m8", "nn_S2_D4_m4", "nn_S1_D2_m8", "pn_S1_D2_m8"};
-  return (cfg >= 0 && cfg < 80) ? names[cfg] : "?";
+                                "pn_S2_D4_m4", "nn_S1_D4", "nn_S2_D4", "nn_S1_D4_m8", "nn_S2_D4_m4", "nn_S1_D2_m8", "pn_S1_D2_m8",
+                                "cg_D4_S3", "cg_D4_S4", "cg_D2_S4", "cg_D2_S6", "cg_D2_S3", "cg_D1_S8", "cg_D4_S2", "cg_D8_S2"};
+  return (cfg >= 0 && cfg < 88) ? names[cfg] : "?";
 }
 extern "C" int mwt_gemv(int cfg, int k, const double* A, const double* x, double* y, int64_t m,
                         int64_t n, void* stream) {

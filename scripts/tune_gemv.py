@@ -13,6 +13,8 @@ NOFLUSH = "--noflush" in sys.argv
 MAC = {3: 96, 4: 209}
 PAD = int(os.environ.get("PAD", "0"))  # extra elements between A's planes (layout experiment)
 lib.mwt_gemv_set_sa.argtypes = [ctypes.c_int64]
+lib.mwt_gemv_set_lda.argtypes = [ctypes.c_int64]
+lib.mwt_gemv_set_lda(int(os.environ.get("LDA", "0")))  # -1: every row reads row 0 (A L2-resident; timing probe)
 for k in (3, 4):
     a, x = gen.config2_gemv(k)
     m, n = a.shape[1], a.shape[2]
@@ -39,7 +41,7 @@ for k in (3, 4):
         same = ""
         if cfg == 0:
             ref = y.clone()
-        elif cfg >= 8 or cfg == 6:  # (cfg 61+: persistent shuffle tree)  # staged variants keep the P = 128 order: must be bit-identical
+        elif (cfg >= 8 or cfg == 6) and not os.environ.get("LDA"):  # (cfg 61+: persistent shuffle tree)  # staged variants keep the P = 128 order: must be bit-identical
             same = " bits==W4" if torch.equal(y.view(torch.int64), ref.view(torch.int64)) else " BITS DIFFER"
         ts = []
         for _ in range(10):
