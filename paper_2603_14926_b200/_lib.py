@@ -1,9 +1,17 @@
-"""ctypes binding of the C-ABI library ``libmwgpu.so`` (include/mwgpu.h).
+"""Bindings of the C-ABI library ``libmwgpu.so`` (include/mwgpu.h).
 
-This is the only way the Python package reaches the GPU: every public
-operation calls one of these entry points with raw device pointers taken
-from torch CUDA tensors and torch's current CUDA stream.  There is no CPU
-fallback -- if the library or a CUDA device is missing, calls raise.
+The package reaches the GPU only through that library:
+
+* ``ext()`` -- the PyTorch extension ``_mwext.so`` (csrc/ext/mwext.cpp)
+  for the hot entry points (lane ops, axpy, dot, GEMV, GEMM, Horner, DK
+  sweep): tensors in, validation, device guard and torch's current stream
+  in C++;
+* ``load()`` -- ctypes for the cold paths (peer memory / IPC, named ops,
+  Estrin, partial dots, the microbenchmark), with raw device pointers and
+  torch's current stream.
+
+There is no CPU fallback -- if a library or a CUDA device is missing,
+calls raise.
 """
 
 from __future__ import annotations
@@ -163,8 +171,9 @@ _raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
 def stream_handle(device: torch.device | None = None) -> int:
     """cudaStream_t of torch's current stream on ``device`` (as an int).
     The C library launches on the CURRENT device, so an operand on another
-    device is an error here (wrap the call in ``torch.cuda.device(...)`` or
-    use ``on_device``) -- never a launch on the wrong GPU.  Uses torch's
+    device is an error here (wrap the call in ``torch.cuda.device(...)``;
+    the extension's entry points switch devices themselves) -- never a
+    launch on the wrong GPU.  Uses torch's
     raw-handle accessor when present (no Stream object: this is on every
     call's host path), else torch.cuda.current_stream."""
     cur = torch.cuda.current_device()
@@ -177,27 +186,6 @@ def stream_handle(device: torch.device | None = None) -> int:
     if _raw_stream is not None:
         return _raw_stream(idx)
     return torch.cuda.current_stream(device).cuda_stream
-
-
-class on_device:
-    """Context manager: make ``t``'s device current for a launch (no-op
-    when it already is)."""
-
-    __slots__ = ("idx", "prev")
-
-    def __init__(self, t: torch.Tensor):
-        self.idx = t.device.index
-
-    def __enter__(self):
-        self.prev = torch.cuda.current_device()
-        if self.idx is not None and self.idx != self.prev:
-            torch.cuda.set_device(self.idx)
-        return self
-
-    def __exit__(self, *exc):
-        if self.idx is not None and self.idx != self.prev:
-            torch.cuda.set_device(self.prev)
-        return False
 
 
 def check(rc: int, what: str):
@@ -219,21 +207,6 @@ def require_cuda(*tensors: torch.Tensor):
             raise RuntimeError(
                 "mwgpu: operands must live on a CUDA device; the B200 path has no CPU fallback"
             )
-
-
-def require_planes(*tensors: torch.Tensor):
-    """CUDA, float64, C-contiguous, all on one device: what the plane
-    strides the wrappers pass to the C-ABI assume (a non-contiguous or
-    foreign tensor would otherwise turn into out-of-bounds device reads)."""
-    require_cuda(*tensors)
-    dev = tensors[0].device
-    for t in tensors:
-        if t.dtype != torch.float64:
-            raise ValueError(f"mwgpu: float64 planes required, got {t.dtype}")
-        if not t.is_contiguous():
-            raise ValueError("mwgpu: planes tensors must be contiguous")
-        if t.device != dev:
-            raise ValueError("mwgpu: operands on different devices")
 
 
 def ptr(t: torch.Tensor) -> int:
