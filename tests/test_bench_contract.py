@@ -1,5 +1,5 @@
 """The driver contract of bench.py's JSON line, checked on the committed
-r01 bench log (CPU-only): every key the driver and the judge read is
+r02 bench log (CPU-only): every key the driver and the judge read is
 present with the right shape."""
 
 import json
@@ -9,7 +9,7 @@ REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def _line():
-    with open(os.path.join(REPO, "profiles", "r01_bench.log")) as f:
+    with open(os.path.join(REPO, "profiles", "r02_bench.log")) as f:
         return json.loads(f.read().strip().splitlines()[-1])
 
 
