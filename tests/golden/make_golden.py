@@ -23,6 +23,8 @@ public functions on small seeded cases:
   cgemm.npz   cmatmul (3M) on gen_complex_test_matrices     (linalg.py:247-276, 572-590)
   strassen.npz matmul(scheme="strassen") with even splits and odd peels (linalg.py:390-546)
   testmats.npz gen_test_matrices(16, k) and chebyshev_coeffs(12, k) (linalg.py:224-244, roots.py:343-368)
+  dksolve.npz dk_solve from the reference's Aberth start (final roots and
+              sweep count) on chebyshev_coeffs(16 / 64)   (roots.py:318-368)
   named.npz   dw_add_sloppy, tw_mul_cleaned, tw_/qw_renormalize, normalize,
               eft.fma, strassen_pad_policy (multiword.py:104-358, 710-719)
   polyx.npz   estrin_eval per point (== estrin_eval_batched) and
@@ -434,6 +436,26 @@ def main():
         out["strassen_pad"] = np.array(pads, dtype=np.int64)
         np.savez_compressed(os.path.join(HERE, "named.npz"), **out)
         print(f"named done {time.time() - t0:.1f}s")
+
+    # ------------------------------------------------------------ dk_solve
+    # the full solve loop (roots.py:318-340) from the reference's own Aberth
+    # start: final roots and the sweep count, on the Chebyshev test
+    # polynomials (roots.py:343-368) at n = 16 for all six (K, Variant)
+    # pairs and at the paper's n = 64 for TD and QD
+    if want("dksolve"):
+        out = {}
+        cases_s = [(k, v, 16) for k, v in cases] + [(3, BF, 64), (4, BF, 64)]
+        for k, v, n in cases_s:
+            q = roots.chebyshev_coeffs(n, k)
+            st, iters = roots.dk_solve(q, v)
+            p = f"k{k}_{tag[v]}_n{n}"
+            out[p + "_coeffs"] = np.stack(q.comps)
+            out[p + "_re"] = np.stack(st.re)
+            out[p + "_im"] = np.stack(st.im)
+            out[p + "_iters"] = np.array([iters])
+            out[p + "_maxupd"] = np.array([st.last_max_update])
+        np.savez_compressed(os.path.join(HERE, "dksolve.npz"), **out)
+        print(f"dksolve done {time.time() - t0:.1f}s")
 
     print(f"all done {time.time() - t0:.1f}s  (mwfloat {getattr(mwfloat, '__version__', '?')})")
 

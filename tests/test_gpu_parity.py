@@ -1157,3 +1157,22 @@ def test_dot_graphs_on_two_streams_keep_private_workspaces():
     torch.cuda.synchronize()
     assert_bitwise(o1.cpu().numpy(), want1)
     assert_bitwise(o2.cpu().numpy(), want2)
+
+
+DKSOLVE = [(2, "bf", 16), (3, "bf", 16), (4, "bf", 16), (2, "std", 16), (3, "std", 16), (4, "std", 16),
+           (3, "bf", 64), (4, "bf", 64)]
+
+
+@pytest.mark.parametrize("k,v,n", DKSOLVE, ids=[f"k{k}_{v}_n{n}" for k, v, n in DKSOLVE])
+def test_dk_solve_matches_reference_solve(golden, k, v, n):
+    """roots.dk_solve on the device (Aberth start on the device, chunked
+    sweeps, on-device convergence test) against the reference's dk_solve
+    (roots.py:318-340) on chebyshev_coeffs(n): same sweep count, same
+    roots bit for bit -- including the paper's n = 64 TD/QD problem."""
+    g = golden("dksolve")
+    p = f"k{k}_{v}_n{n}"
+    state, iters = roots.dk_solve(MonicPoly(g[p + "_coeffs"]), V(v))
+    assert iters == int(g[p + "_iters"][0])
+    assert_bitwise(state.re.cpu().numpy(), g[p + "_re"])
+    assert_bitwise(state.im.cpu().numpy(), g[p + "_im"])
+    assert math.isclose(state.last_max_update, float(g[p + "_maxupd"][0]), rel_tol=1e-15)

@@ -218,3 +218,31 @@ def test_multiword_value_class_host_parts():
     assert DD(1.0) == 1.0 and QD(2.0) == QD(2.0)
     assert abs(DD(-3.0)) == DD(3.0)  # negation needs no arithmetic kernel
     assert is_normalized((1.0, 2.0**-60)) and not is_normalized((1.0, 0.5))
+
+
+DKSOLVE = [(2, "bf", 16), (3, "bf", 16), (4, "bf", 16), (2, "std", 16), (3, "std", 16), (4, "std", 16),
+           (3, "bf", 64), (4, "bf", 64)]
+
+
+@pytest.mark.parametrize("k,v,n", DKSOLVE, ids=[f"k{k}_{v}_n{n}" for k, v, n in DKSOLVE])
+def test_dk_solve_oracle_loop_matches_reference(golden, monkeypatch, k, v, n):
+    """The oracle's reference-order sweep, looped with the reference's
+    convergence test (roots.py:334-339, np.hypot), from the Aberth start,
+    reproduces the reference's dk_solve: same sweep count, same roots bit
+    for bit (dksolve.npz, chebyshev_coeffs(n))."""
+    _oracle_batch(monkeypatch)
+    g = golden("dksolve")
+    p = f"k{k}_{v}_n{n}"
+    coeffs = g[p + "_coeffs"]
+    st = roots.aberth_init(MonicPoly(coeffs, device="cpu"), Variant.parse(v))
+    zre, zim = st.re.numpy(), st.im.numpy()
+    tol = roots.default_tolerance(k)
+    for it in range(1, 201):
+        zre, zim, mag, coll = oracle.dk_sweep(coeffs, zre, zim, v, exact=True)
+        assert coll is None
+        zmag = float(np.max(np.hypot(zre[0], zim[0])))
+        if float(mag.max()) <= tol * max(zmag, 1e-300):
+            break
+    assert it == int(g[p + "_iters"][0])
+    assert_bitwise(zre, g[p + "_re"])
+    assert_bitwise(zim, g[p + "_im"])
