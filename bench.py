@@ -803,6 +803,32 @@ def secondary(args, torch, dist, mw, world, rank, peak, out=None):
             "horner_G_MPops": round(hor_mp / (ms_bf / 1e3) / 1e9, 1),
             "estrin_G_MPops": round(est_mp / (ms_est / 1e3) / 1e9, 1),
             "note": "the reference's Estrin zero-pads 1025 coefficients to 2048 and evaluates every node: 2x Horner's K-word ops per point; per-op rates compare the kernels"}
+        # the paper's root-finding benchmark: Durand-Kerner
+        # on the Chebyshev test polynomial of degree 64, to convergence from
+        # the Aberth start, NoBF (Standard) vs BF; the reference order (bit-
+        # exact with mwfloat's dk_solve, sweep count included) and the tree order
+        from paper_2603_14926_b200 import roots as mwroots
+
+        for k in (3, 4):
+            q = mwroots.chebyshev_coeffs(64, k)
+            row = {}
+            for vname, var in (("std", STD), ("bf", BF)):
+                for order, exact in (("exact", True), ("tree", False)):
+                    st0 = mwroots.aberth_init(q, var)
+                    mwroots.dk_solve(q, var, state=st0, exact_order=exact)  # warm-up
+                    torch.cuda.synchronize()
+                    ts = []
+                    for _ in range(3):
+                        t = time.perf_counter()
+                        _, iters = mwroots.dk_solve(q, var, state=st0, exact_order=exact)
+                        torch.cuda.synchronize()
+                        ts.append(time.perf_counter() - t)
+                    row[f"{vname}_{order}_ms"] = round(statistics.median(ts) * 1e3, 2)
+                    row[f"{vname}_{order}_sweeps"] = iters
+            row["paper_epyc_s"] = {"nobf": 0.306 if k == 3 else 0.989, "bf_simd": 0.156 if k == 3 else 0.415}
+            row["note"] = ("wall time of dk_solve from the Aberth start (host loop over device sweeps, one read-back "
+                           "per chunk); paper: EPYC 9354P, its own C library (PAPER.md:443-447)")
+            cmp[f"dk_chebyshev_n64_{'td' if k == 3 else 'qd'}"] = row
         out["paper_comparisons"] = cmp
         del c4, xd4, y4, P4, X4
 
