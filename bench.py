@@ -582,7 +582,12 @@ def secondary(args, torch, dist, mw, world, rank, peak, out=None):
             g.replay()
             e1.record()
         torch.cuda.synchronize()
-        return statistics.median(e0.elapsed_time(e1) for e0, e1 in evs) / calls
+        ms = statistics.median(e0.elapsed_time(e1) for e0, e1 in evs) / calls
+        if world > 1:
+            t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
 
     flush_rd = None
 
