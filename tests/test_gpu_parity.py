@@ -1176,3 +1176,46 @@ def test_dk_solve_matches_reference_solve(golden, k, v, n):
     assert_bitwise(state.re.cpu().numpy(), g[p + "_re"])
     assert_bitwise(state.im.cpu().numpy(), g[p + "_im"])
     assert math.isclose(state.last_max_update, float(g[p + "_maxupd"][0]), rel_tol=1e-15)
+
+
+def test_extension_edge_cases_and_column_slices():
+    """Empty operands launch nothing and return exact zeros / untouched
+    outputs; column slices of wider batches (plane stride > width) go
+    through dot, axpy and Horner without a copy and match the oracle."""
+    from paper_2603_14926_b200 import _lib
+    from paper_2603_14926_b200.poly import horner_into
+
+    e = _lib.ext()
+    rng = np.random.default_rng(21)
+    for k in (2, 3, 4):
+        z = torch.zeros((k, 0), dtype=torch.float64, device="cuda")
+        assert e.ew(2, 1, z, z).shape == (k, 0)
+        d = e.dot(1, z, z, 1)
+        torch.cuda.synchronize()
+        assert_bitwise(d.cpu().numpy(), np.zeros(k))  # fold from an exact zero
+        e.axpy_(1, [1.0] + [0.0] * (k - 1), z, z)
+        wide_x, wide_y = gen.g_k(rng, k, 10000), gen.g_k(rng, k, 10000)
+        X, Y = torch.from_numpy(wide_x).cuda(), torch.from_numpy(wide_y).cuda()
+        lo, hi = 1234, 1234 + 5000
+        got = e.dot(1, X[:, lo:hi], Y[:, lo:hi], 1).cpu().numpy()
+        assert_bitwise(got, oracle.dot(wide_x[:, lo:hi], wide_y[:, lo:hi], "bf", order=1))
+        got = e.dot(1, X[:, lo:hi], Y[:, lo:hi], 0).cpu().numpy()
+        assert_bitwise(got, oracle.dot(wide_x[:, lo:hi], wide_y[:, lo:hi], "bf", order=0))
+        alpha = tuple(gen.g_k(rng, k, 1)[:, 0])
+        Yc = Y.clone()
+        e.axpy_(1, list(alpha), X[:, lo:hi], Yc[:, lo:hi])
+        want = oracle.ew("add", oracle.ew("mul", np.tile(np.array(alpha)[:, None], (1, hi - lo)),
+                                          wide_x[:, lo:hi], "bf"), wide_y[:, lo:hi], "bf")
+        out = Yc.cpu().numpy()
+        assert_bitwise(out[:, lo:hi], want)
+        assert_bitwise(out[:, :lo], wide_y[:, :lo])  # outside the slice: untouched
+        assert_bitwise(out[:, hi:], wide_y[:, hi:])
+        coeffs = gen.g_k(rng, k, 17)
+        C = torch.from_numpy(coeffs).cuda()
+        yv = torch.full_like(X, 7.0)
+        horner_into(C, X, yv, Variant.BRANCH_FREE, 300, 300)  # empty range: nothing written
+        assert torch.all(yv == 7.0)
+        horner_into(C, X, yv, Variant.BRANCH_FREE, 300, 1300)
+        hv = yv.cpu().numpy()
+        assert_bitwise(hv[:, 300:1300], oracle.horner(coeffs, np.ascontiguousarray(wide_x[:, 300:1300]), "bf"))
+        assert np.all(hv[:, :300] == 7.0) and np.all(hv[:, 1300:] == 7.0)
