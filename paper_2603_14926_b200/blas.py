@@ -52,7 +52,6 @@ def dot_tensor(x: LaneBatch, y: LaneBatch, variant: Variant = Variant.BRANCH_FRE
     tree order's workspace lives in the extension: one zeroed buffer per
     (device, stream) for eager calls, a private one per call captured into
     a CUDA graph (csrc/ext/mwext.cpp)."""
-    _check_pair(x, y)
     return _lib.ext().dot(variant_code(variant), x.planes, y.planes, _order(order), out,
                           **_lib.tune_kw(tuning, "dot_cluster"))
 
@@ -64,12 +63,9 @@ def dot(x: LaneBatch, y: LaneBatch, variant: Variant = Variant.BRANCH_FREE, orde
 
 
 def axpy_(alpha, x: LaneBatch, y: LaneBatch, variant: Variant = Variant.BRANCH_FREE) -> LaneBatch:
-    """y <- alpha x + y in place; alpha is a K-word tuple."""
-    _check_pair(x, y)
-    alpha = tuple(float(a) for a in getattr(alpha, "comps", alpha))
-    if len(alpha) != x.k:
-        raise ValueError("mixed word counts")
-    _lib.ext().axpy_(variant_code(variant), alpha, x.planes, y.planes)
+    """y <- alpha x + y in place; alpha is a K-word tuple.  (K, widths and
+    devices are checked by the extension: ValueError on a mismatch.)"""
+    _lib.ext().axpy_(variant_code(variant), getattr(alpha, "comps", alpha), x.planes, y.planes)
     y.count = max(x.count, y.count)
     return y
 

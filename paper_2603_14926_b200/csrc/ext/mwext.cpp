@@ -57,6 +57,13 @@ void require_planes(const at::Tensor& t, const char* name, int64_t k, const c10:
   if (k >= 0 && t.size(0) != k) throw py::value_error("mixed word counts");
 }
 
+// The reference's argument errors come first, whatever the device
+// (batch.py:197-201): mixed word counts, then mixed lane widths.
+void check_pair(const at::Tensor& a, const at::Tensor& b) {
+  if (a.dim() >= 1 && b.dim() >= 1 && a.size(0) != b.size(0)) throw py::value_error("mixed word counts");
+  if (a.dim() == 2 && b.dim() == 2 && a.size(1) != b.size(1)) throw py::value_error("mixed lane widths");
+}
+
 // (K, W) planes with unit lane stride; returns the plane stride.
 int64_t lane_planes(const at::Tensor& t, const char* name, int64_t k, const c10::Device& dev) {
   require_planes(t, name, k, dev);
@@ -94,6 +101,7 @@ mw_tuning tuning_from(int64_t gemm_tile, int64_t dot_cluster, int64_t dk_tree_ro
 // op: 0 add, 1 sub, 2 mul, 3 div (batch.py:204-231, linalg._ew_sub).
 at::Tensor ew(int64_t op, int64_t variant, const at::Tensor& a, const at::Tensor& b,
               c10::optional<at::Tensor> out) {
+  check_pair(a, b);
   const c10::Device dev = a.device();
   const int64_t k = a.dim() > 0 ? a.size(0) : 0;
   const int64_t sa = lane_planes(a, "a", k, dev);
@@ -120,6 +128,7 @@ at::Tensor ew(int64_t op, int64_t variant, const at::Tensor& a, const at::Tensor
 
 // y <- alpha x + y (batch_mul then batch_add, batch.py:204-213).
 void axpy_(int64_t variant, const std::vector<double>& alpha, const at::Tensor& x, const at::Tensor& y) {
+  check_pair(x, y);
   const c10::Device dev = x.device();
   const int64_t k = x.dim() > 0 ? x.size(0) : 0;
   if ((int64_t)alpha.size() != k) throw py::value_error("mixed word counts");
@@ -159,6 +168,7 @@ at::Tensor dot_workspace(int64_t need, const c10::Device& dev, void* st, bool ca
 
 at::Tensor dot(int64_t variant, const at::Tensor& x, const at::Tensor& y, int64_t order,
                c10::optional<at::Tensor> out, int64_t dot_cluster) {
+  check_pair(x, y);
   const c10::Device dev = x.device();
   const int64_t k = x.dim() > 0 ? x.size(0) : 0;
   const int64_t sx = lane_planes(x, "x", k, dev);

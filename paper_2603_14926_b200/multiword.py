@@ -50,6 +50,10 @@ class Variant(enum.Enum):
 
 def variant_code(v) -> int:
     """C-ABI code: MW_VARIANT_STANDARD = 0, MW_VARIANT_BRANCH_FREE = 1."""
+    if v is Variant.BRANCH_FREE:  # fast path: on every call's host path
+        return 1
+    if v is Variant.STANDARD:
+        return 0
     return 1 if Variant.parse(v) is Variant.BRANCH_FREE else 0
 
 
