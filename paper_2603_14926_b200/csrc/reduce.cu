@@ -719,6 +719,78 @@ __global__ void __launch_bounds__(128)
   }
 }
 
+// Same partials and tree as gemv_tree_kernel (bit-identical), 64 threads per
+// row: thread t folds partials t and t + 64 as two interleaved independent
+// chains (ILP 2 within a row; each thread lives twice as long, half as many
+// threads per row).  D elements of each chain loaded ahead.  RPC rows per CTA.
+template <int K, int VAR, int D, int RPC>
+__global__ void __launch_bounds__(64 * RPC)
+    gemv_u2_kernel(const double* __restrict__ A, int64_t lda, int64_t sA,
+                   const double* __restrict__ x, int64_t sx, double* __restrict__ y, int64_t sy,
+                   int64_t m, int64_t n) {
+  constexpr int P = 128;
+  __shared__ double part[RPC][K][P];
+  const int t = threadIdx.x & 63;
+  const int slot = threadIdx.x >> 6;
+  const int64_t i = blockIdx.x * (int64_t)RPC + slot;
+  const bool live = i < m;
+  const double* row = A + (live ? i : 0) * lda;
+  V<K> acc0 = zero<K>(), acc1 = zero<K>();
+  int64_t e = t;  // chain 0 at e, chain 1 at e + 64
+  for (; e + 64 + (D - 1) * P < n; e += D * P) {
+    V<K> a0[D], x0[D], a1[D], x1[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      a0[d] = load<K>(row, sA, e + d * P);
+      x0[d] = load<K>(x, sx, e + d * P);
+      a1[d] = load<K>(row, sA, e + 64 + d * P);
+      x1[d] = load<K>(x, sx, e + 64 + d * P);
+    }
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      acc0 = Ops<K, VAR>::add(acc0, Ops<K, VAR>::mul(a0[d], x0[d]));
+      acc1 = Ops<K, VAR>::add(acc1, Ops<K, VAR>::mul(a1[d], x1[d]));
+    }
+  }
+  for (int64_t f = e; f < n; f += P)
+    acc0 = Ops<K, VAR>::add(acc0, Ops<K, VAR>::mul(load<K>(row, sA, f), load<K>(x, sx, f)));
+  for (int64_t f = e + 64; f < n; f += P)
+    acc1 = Ops<K, VAR>::add(acc1, Ops<K, VAR>::mul(load<K>(row, sA, f), load<K>(x, sx, f)));
+  const int64_t valid = n < P ? n : P;
+#pragma unroll
+  for (int c = 0; c < K; ++c) {
+    part[slot][c][t] = acc0.c[c];
+    part[slot][c][t + 64] = acc1.c[c];
+  }
+  __syncthreads();
+  const int tid = threadIdx.x;
+#pragma unroll 1
+  for (int s = 1; s < P; s <<= 1) {
+    const int per_row = P / (2 * s);
+    for (int w = tid; w < RPC * per_row; w += 64 * RPC) {
+      const int r = w / per_row, idx = 2 * s * (w % per_row);
+      if (idx + s < valid) {
+        V<K> a, b;
+#pragma unroll
+        for (int c = 0; c < K; ++c) {
+          a.c[c] = part[r][c][idx];
+          b.c[c] = part[r][c][idx + s];
+        }
+        const V<K> sum = Ops<K, VAR>::add(a, b);
+#pragma unroll
+        for (int c = 0; c < K; ++c) part[r][c][idx] = sum.c[c];
+      }
+    }
+    __syncthreads();
+  }
+  if (t == 0 && live) {
+    V<K> r0;
+#pragma unroll
+    for (int c = 0; c < K; ++c) r0.c[c] = part[slot][c][0];
+    store<K>(y, sy, i, r0);
+  }
+}
+
 template <int K, int VAR>
 struct GemvLaunch {
   static int run(const double* A, int64_t lda, int64_t sA, const double* x, int64_t sx, double* y,
