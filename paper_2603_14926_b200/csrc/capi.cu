@@ -1,5 +1,6 @@
 // capi.cu — library metadata, device helpers and the FP64 pipe
 // microbenchmark used as the roofline denominator.
+#include <atomic>
 #include "common.cuh"
 
 namespace mw {
@@ -7,10 +8,10 @@ namespace mw {
 // Per-device cache (one process may drive several GPUs); a benign race
 // only repeats the query.
 int sm_count() {
-  static int cached[64] = {0};
+  static std::atomic<int> cached[64];  // zero-initialised; racing first calls store the same value
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
-  if (cached[dev] == 0) {
+  if (cached[dev].load(std::memory_order_relaxed) == 0) {
     int v = 0;
     cached[dev] = (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess &&
                    v > 0)

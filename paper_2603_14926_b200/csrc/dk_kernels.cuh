@@ -27,6 +27,7 @@
 // by level across the CTA's roots; dk_tree_kernel (3 warps per root) is the
 // workspace-free form.  Both give the same bits.
 #pragma once
+#include <atomic>
 #include <climits>
 #include <cstring>
 
@@ -1137,7 +1138,7 @@ static int dk_treem_launch(const double* coeffs, int64_t sc, int64_t n, const do
   const int64_t cnt = i1 - i0;
   const size_t smem = dk_treem_smem<K>(R);
   auto kern = dk_treem_kernel<K, VAR, R, PEER>;
-  static bool attr_set[64] = {false};  // per instantiation and device
+  static std::atomic<bool> attr_set[64];  // per instantiation and device; idempotent, race-free
   int dev = -1;
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= 64 || !attr_set[dev]) {

@@ -15,6 +15,7 @@
 // intensity is ~29/96/209 FP64 ops per (2K x 8 B) of smem traffic, so the
 // kernel is bound by FP64 issue, not memory; the only overhead on the
 // pipe is the exact-zero start (one add per output).
+#include <atomic>
 #include "gemm_kernel.cuh"
 
 namespace mw {
@@ -95,7 +96,7 @@ static int gemm_launch(const double* A, int64_t lda, int64_t sA, const double* B
   constexpr int NT = (Cf::BM / Cf::TM) * (Cf::BN / Cf::TN);
   const size_t smem = GemmSmem<K, Cf>::BYTES;
   // the dynamic-smem opt-in is per device; setting it twice is harmless
-  static bool attr_set[64] = {false};
+  static std::atomic<bool> attr_set[64];  // lazy per-device init; idempotent, race-free
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= 64 || !attr_set[dev]) {

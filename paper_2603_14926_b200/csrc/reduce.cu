@@ -17,6 +17,7 @@
 //         for i % 2s == 0 when i+s < count; an unpaired tail passes through).
 //   gemv: 128 partials per row; partial u folds t = u, u+128, ... ascending
 //         from exact zero; the partials combine by the same pairwise tree.
+#include <atomic>
 #include "common.cuh"
 #include "peer.cuh"
 
@@ -273,7 +274,7 @@ struct DotLaunch {
     double* part = ws + 1;
     if (nb <= DOT_CLUSTER_MAX && cluster) {
       auto kern = dot_cluster_kernel<K, VAR>;
-      static bool attr_set[64] = {false};
+      static std::atomic<bool> attr_set[64];  // lazy per-device init; idempotent, race-free
       int dev = 0;
       cudaGetDevice(&dev);
       if (dev < 0 || dev >= 64 || !attr_set[dev]) {
