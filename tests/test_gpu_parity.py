@@ -1219,3 +1219,49 @@ def test_extension_edge_cases_and_column_slices():
         hv = yv.cpu().numpy()
         assert_bitwise(hv[:, 300:1300], oracle.horner(coeffs, np.ascontiguousarray(wide_x[:, 300:1300]), "bf"))
         assert np.all(hv[:, :300] == 7.0) and np.all(hv[:, 1300:] == 7.0)
+
+
+def test_concurrent_callers_with_different_tuning():
+    """The C-ABI is stateless: two host threads on their own streams, one
+    forcing GEMM tile slot 0 and the tree dot's ticket form, the other
+    slot 2 and the cluster form, issue interleaved calls; every result is
+    bitwise the default one (no shared tuning state to race on)."""
+    import threading
+
+    from paper_2603_14926_b200 import _lib
+    from paper_2603_14926_b200.linalg import gemm_into
+
+    rng = np.random.default_rng(33)
+    k, m, n = 3, 160, 96
+    A = torch.from_numpy(gen.g_k(rng, k, (m, n))).cuda()
+    B = torch.from_numpy(gen.g_k(rng, k, (n, n))).cuda()
+    X, Y = LaneBatch(gen.g_k(rng, k, 40000)), LaneBatch(gen.g_k(rng, k, 40000))
+    C0 = torch.empty((k, m, n), dtype=torch.float64, device="cuda")
+    gemm_into(A, B, C0, Variant.BRANCH_FREE)
+    d0 = blas.dot_tensor(X, Y, Variant.BRANCH_FREE).clone()
+    torch.cuda.synchronize()
+    errors = []
+
+    def worker(tile, cluster):
+        try:
+            s = torch.cuda.Stream()
+            tune = _lib.tuning(gemm_tile=tile, dot_cluster=cluster)
+            with torch.cuda.stream(s):
+                for _ in range(30):
+                    C = torch.empty_like(C0)
+                    gemm_into(A, B, C, Variant.BRANCH_FREE, tuning=tune)
+                    d = blas.dot_tensor(X, Y, Variant.BRANCH_FREE, tuning=tune)
+                    s.synchronize()
+                    if not (torch.equal(C.view(torch.int64), C0.view(torch.int64))
+                            and torch.equal(d.view(torch.int64), d0.view(torch.int64))):
+                        errors.append((tile, cluster))
+                        return
+        except Exception as e:  # surfaced below
+            errors.append(repr(e))
+
+    ts = [threading.Thread(target=worker, args=(1, 0)), threading.Thread(target=worker, args=(3, 1))]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errors, errors
