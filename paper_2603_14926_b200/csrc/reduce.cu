@@ -792,6 +792,61 @@ __global__ void __launch_bounds__(64 * RPC)
   }
 }
 
+// Same 128 partials and tree (bit-identical), ONE warp per row: lane l folds
+// partials l, l + 32, l + 64, l + 96 as four interleaved independent chains
+// (ILP 4), so 2048 rows are 2048 warps -- one resident wave on 148 SMs, no
+// CTA turnover.  Tree: strides 1..16 by shuffles inside each chain, stride
+// 32 pairs chains (0,1) and (2,3), stride 64 pairs the results -- all in
+// registers of one lane.  D elements of every chain loaded ahead.
+template <int K, int VAR, int D, int WPC>
+__global__ void __launch_bounds__(32 * WPC)
+    gemv_w1_kernel(const double* __restrict__ A, int64_t lda, int64_t sA,
+                   const double* __restrict__ x, int64_t sx, double* __restrict__ y, int64_t sy,
+                   int64_t m, int64_t n) {
+  constexpr int P = 128;
+  const int lane = threadIdx.x & 31;
+  const int64_t i = blockIdx.x * (int64_t)WPC + (threadIdx.x >> 5);
+  if (i >= m) return;
+  const double* row = A + i * lda;
+  V<K> acc[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) acc[c] = zero<K>();
+  int64_t t = lane;  // chain c at t + 32c
+  for (; t + 96 + (D - 1) * P < n; t += D * P) {
+    V<K> a[D][4], xv[D][4];
+#pragma unroll
+    for (int d = 0; d < D; ++d)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        a[d][c] = load<K>(row, sA, t + 32 * c + d * P);
+        xv[d][c] = load<K>(x, sx, t + 32 * c + d * P);
+      }
+#pragma unroll
+    for (int d = 0; d < D; ++d)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc[c] = Ops<K, VAR>::add(acc[c], Ops<K, VAR>::mul(a[d][c], xv[d][c]));
+  }
+#pragma unroll
+  for (int c = 0; c < 4; ++c)
+    for (int64_t f = t + 32 * c; f < n; f += P)
+      acc[c] = Ops<K, VAR>::add(acc[c], Ops<K, VAR>::mul(load<K>(row, sA, f), load<K>(x, sx, f)));
+  const int64_t valid = n < P ? n : P;
+#pragma unroll
+  for (int s = 1; s < 32; s <<= 1) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const V<K> o = shfl_down<K>(acc[c], s);
+      if ((lane & (2 * s - 1)) == 0 && 32 * c + lane + s < valid) acc[c] = Ops<K, VAR>::add(acc[c], o);
+    }
+  }
+  if (lane == 0) {
+    if (32 < valid) acc[0] = Ops<K, VAR>::add(acc[0], acc[1]);
+    if (96 < valid) acc[2] = Ops<K, VAR>::add(acc[2], acc[3]);
+    if (64 < valid) acc[0] = Ops<K, VAR>::add(acc[0], acc[2]);
+    store<K>(y, sy, i, acc[0]);
+  }
+}
+
 template <int K, int VAR>
 struct GemvLaunch {
   static int run(const double* A, int64_t lda, int64_t sA, const double* x, int64_t sx, double* y,

@@ -141,6 +141,13 @@ static int gemv_u2_launch(const double* A, const double* x, double* y, int64_t m
       A, gemv_lda(n), gemv_sa(m, n), x, n, y, m, m, n);
   return launch_status();
 }
+template <int K, int D, int WPC>
+static int gemv_w1_launch(const double* A, const double* x, double* y, int64_t m, int64_t n,
+                          cudaStream_t st) {
+  gemv_w1_kernel<K, BRANCH_FREE, D, WPC><<<(unsigned)((m + WPC - 1) / WPC), 32 * WPC, 0, st>>>(
+      A, gemv_lda(n), gemv_sa(m, n), x, n, y, m, m, n);
+  return launch_status();
+}
 template <int K, int R, int D, int S, bool XS>
 static int gemv_staged_launch(const double* A, const double* x, double* y, int64_t m, int64_t n,
                               cudaStream_t st) {
@@ -321,10 +328,16 @@ static int gemv_run(int cfg, const double* A, const double* x, double* y, int64_
     case 91: return gemv_u2_launch<K, 4, 2>(A, x, y, m, n, st);
     case 92: return gemv_u2_launch<K, 1, 2>(A, x, y, m, n, st);
     case 93: return gemv_u2_launch<K, 2, 4>(A, x, y, m, n, st);
+    case 94: return gemv_w1_launch<K, 1, 1>(A, x, y, m, n, st);
+    case 95: return gemv_w1_launch<K, 2, 1>(A, x, y, m, n, st);
+    case 96: return gemv_w1_launch<K, 1, 2>(A, x, y, m, n, st);
+    case 97: return gemv_w1_launch<K, 2, 2>(A, x, y, m, n, st);
+    case 98: return gemv_w1_launch<K, 1, 4>(A, x, y, m, n, st);
+    case 99: return gemv_w1_launch<K, 4, 1>(A, x, y, m, n, st);
     default: return MW_ERR_INVALID;
   }
 }
-extern "C" int mwt_gemv_num_configs(void) { return 94; }
+extern "C" int mwt_gemv_num_configs(void) { return 100; }
 extern "C" const char* mwt_gemv_config_name(int cfg) {
   static const char* names[] = {"W4_R2_D4", "W1_R8_D8", "W1_R8_D4", "W2_R4_D4", "W2_R4_D8",
                                 "W4_R2_D2", "W4_R1_D4", "W8_R1_D2", "st_R2_D4_S2", "st_R2_D4_S3",
@@ -342,8 +355,9 @@ extern "C" const char* mwt_gemv_config_name(int cfg) {
                                 "np_S1_D4", "np_S2_D4", "pt_S2_D8", "pn_S1_D4", "pn_S2_D4", "pn_S1_D4_m8",
                                 "pn_S2_D4_m4", "nn_S1_D4", "nn_S2_D4", "nn_S1_D4_m8", "nn_S2_D4_m4", "nn_S1_D2_m8", "pn_S1_D2_m8",
                                 "cg_D4_S3", "cg_D4_S4", "cg_D2_S4", "cg_D2_S6", "cg_D2_S3", "cg_D1_S8", "cg_D4_S2", "cg_D8_S2",
-                                "u2_D2_R1", "u2_D2_R2", "u2_D4_R1", "u2_D4_R2", "u2_D1_R2", "u2_D2_R4"};
-  return (cfg >= 0 && cfg < 94) ? names[cfg] : "?";
+                                "u2_D2_R1", "u2_D2_R2", "u2_D4_R1", "u2_D4_R2", "u2_D1_R2", "u2_D2_R4",
+                                "w1_D1_W1", "w1_D2_W1", "w1_D1_W2", "w1_D2_W2", "w1_D1_W4", "w1_D4_W1"};
+  return (cfg >= 0 && cfg < 100) ? names[cfg] : "?";
 }
 extern "C" int mwt_gemv(int cfg, int k, const double* A, const double* x, double* y, int64_t m,
                         int64_t n, void* stream) {
