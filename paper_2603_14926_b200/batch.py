@@ -93,6 +93,15 @@ class LaneBatch:
         self.planes = as_planes(comps, 1, device)
         self.count = self.width if count is None else int(count)
 
+    @classmethod
+    def _wrap(cls, planes: torch.Tensor, count: int) -> "LaneBatch":
+        """A batch around planes a kernel just wrote (contiguous float64
+        (K, W) on the device): no conversion on the host path."""
+        b = object.__new__(cls)
+        b.planes = planes
+        b.count = count
+        return b
+
     @property
     def comps(self) -> tuple:
         return tuple(self.planes[c] for c in range(self.k))
@@ -158,10 +167,10 @@ _OPS = {"mw_ew_add": 0, "mw_ew_sub": 1, "mw_ew_mul": 2, "mw_ew_div": 3}
 
 def _binary(fn_name: str, a: LaneBatch, b: LaneBatch, variant) -> LaneBatch:
     """One lane kernel through the extension (csrc/ext/mwext.cpp -> the
-    C-ABI mw_ew_*): validation, device guard and stream in C++."""
-    _check_pair(a, b)
+    C-ABI mw_ew_*): validation (K, then widths, as batch.py:197-201),
+    device guard and stream in C++."""
     out = _lib.ext().ew(_OPS[fn_name], variant_code(variant), a.planes, b.planes)
-    return LaneBatch(out, count=max(a.count, b.count))
+    return LaneBatch._wrap(out, max(a.count, b.count))
 
 
 def batch_add(a: LaneBatch, b: LaneBatch, variant: Variant = Variant.STANDARD) -> LaneBatch:
