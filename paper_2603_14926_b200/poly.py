@@ -104,7 +104,7 @@ def horner_eval_batched(p: MWPolynomial, xs: LaneBatch, variant: Variant = Varia
     _lib.require_cuda(p.planes, xs.planes)
     y = torch.empty_like(xs.planes)
     horner_into(p.planes, xs.planes, y, variant)
-    return LaneBatch(y, count=xs.count)
+    return LaneBatch._wrap(y, xs.count)
 
 
 def horner_eval(p: MWPolynomial, x, variant: Variant = Variant.STANDARD) -> tuple:
