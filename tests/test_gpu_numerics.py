@@ -275,3 +275,59 @@ def test_dk_solve_chunked_equals_stepwise_loop(k, deg, exact_order):
     ref = roots.dk_sweeps(q, roots.aberth_init(q, Variant.BRANCH_FREE), cut, Variant.BRANCH_FREE, exact_order)
     assert info.value.state.iteration == cut
     assert_bitwise(info.value.state.re.cpu().numpy(), ref.re.cpu().numpy())
+
+
+def _scaled_ints(planes: np.ndarray, scale_bits: int) -> list:
+    """Each lane's K-word value times 2^scale_bits as an exact Python int."""
+    k, n = planes.shape
+    m, e = np.frexp(planes)
+    mant = (m * 2.0**53).astype(np.int64)  # exact: |m| < 1, 53-bit significands
+    out = [0] * n
+    for c in range(k):
+        for i in range(n):
+            if mant[c, i]:
+                sh = scale_bits + int(e[c, i]) - 53
+                out[i] += (int(mant[c, i]) << sh) if sh >= 0 else (int(mant[c, i]) >> -sh)
+    return out
+
+
+@pytest.mark.parametrize("k", [2, 3, 4])
+def test_tree_reductions_vs_exact_sum(k):
+    """The throughput (tree) orders of dot and GEMV against the EXACT
+    result (integer arithmetic on a common power-of-two scale -- an
+    exact oracle, stronger than a fixed-precision mpmath one): within
+    n 2^(-p+4) sum|x||y| (the |A||B|-scale bound of verify.py:369-381), and
+    normwise (error / sum|x||y|) no worse than 8x the reference order's
+    worst own error over the same samples (or 2^-p)."""
+    from paper_2603_14926_b200 import blas, gen
+
+    S = 1400
+    p = BITS[k]
+    rng = np.random.default_rng(700 + k)
+    n = 65536
+    x, y = gen.g_k(rng, k, n), gen.g_k(rng, k, n)
+    X, Y = LaneBatch(x), LaneBatch(y)
+    xi, yi = _scaled_ints(x, S), _scaled_ints(y, S)
+    ex = Fraction(sum(a * b for a, b in zip(xi, yi)), 1 << (2 * S))
+    mag = Fraction(sum(abs(a * b) for a, b in zip(xi, yi)), 1 << (2 * S))
+    tree = exact(np.array(blas.dot(X, Y, Variant.BRANCH_FREE, order="tree")))
+    ref = exact(np.array(blas.dot(X, Y, Variant.BRANCH_FREE, order="exact")))
+    bound = n * Fraction(2) ** (-p + 4) * mag
+    assert abs(tree - ex) <= bound
+    assert abs(tree - ex) / mag <= 8 * max(abs(ref - ex) / mag, Fraction(2) ** (-p))
+    # GEMV rows (config-2 shape, sampled rows) the same way
+    m = 2048
+    a, xv = gen.g_k(rng, k, (64, m)), gen.g_k(rng, k, m)
+    A, XV = linalg.MWMatrix(a), LaneBatch(xv)
+    yt = blas.gemv(A, XV, Variant.BRANCH_FREE, "tree").numpy()
+    ye = blas.gemv(A, XV, Variant.BRANCH_FREE, "exact").numpy()
+    xs = _scaled_ints(xv, S)
+    worst_t = worst_r = Fraction(0)
+    for r in range(0, 64, 3):
+        ar = _scaled_ints(np.ascontiguousarray(a[:, r]), S)
+        e_r = Fraction(sum(u * v for u, v in zip(ar, xs)), 1 << (2 * S))
+        g_r = Fraction(sum(abs(u * v) for u, v in zip(ar, xs)), 1 << (2 * S))
+        t_err, r_err = abs(exact(yt[:, r]) - e_r), abs(exact(ye[:, r]) - e_r)
+        assert t_err <= m * Fraction(2) ** (-p + 4) * g_r
+        worst_t, worst_r = max(worst_t, t_err / g_r), max(worst_r, r_err / g_r)
+    assert worst_t <= 8 * max(worst_r, Fraction(2) ** (-p))
