@@ -210,6 +210,9 @@ def run_ours(args):
 
         # bounded collectives: a lost peer ends the run instead of hanging it
         if args.backend == "nccl":
+            # the communicator's INIT lines (nranks / rank / device) stay visible to the driver
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=torch.device("cuda", dev_index), timeout=timedelta(seconds=300))
         else:
             dist.init_process_group("gloo", timeout=timedelta(seconds=300))
