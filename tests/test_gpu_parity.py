@@ -1265,3 +1265,29 @@ def test_concurrent_callers_with_different_tuning():
     for t in ts:
         t.join()
     assert not errors, errors
+
+
+@pytest.mark.parametrize("k,v", CASES, ids=IDS)
+def test_lane_ops_special_values_vs_oracle(k, v):
+    """Signed zeros, subnormal and near-overflow components, infinities and
+    NaNs in every lane op, both variants: bitwise equal to the oracle
+    (NaN positions compared, payloads not -- CUDA and x86 canonical NaNs
+    differ).  Non-finite values propagate, never trap
+    (multiword.py:18-20)."""
+    rng = np.random.default_rng(500 + k)
+    specials = [0.0, -0.0, 5e-324, -5e-324, 2.2250738585072014e-308, 1e-300, 1.0, -1.0, 1e300,
+                1.7976931348623157e308, -1.7976931348623157e308, np.inf, -np.inf, np.nan]
+    s = np.array(specials)
+    w = len(s) ** 2
+    a = np.zeros((k, w))
+    b = np.zeros((k, w))
+    a[0] = np.repeat(s, len(s))
+    b[0] = np.tile(s, len(s))
+    with np.errstate(all="ignore"):
+        for c in range(1, k):  # small trailing components where the leading one is finite
+            a[c] = np.where(np.isfinite(a[0]), a[c - 1] * 2.0**-53 * rng.uniform(-0.49, 0.49, w), 0.0)
+            b[c] = np.where(np.isfinite(b[0]), b[c - 1] * 2.0**-53 * rng.uniform(-0.49, 0.49, w), 0.0)
+    la, lb = LaneBatch(a), LaneBatch(b)
+    with np.errstate(all="ignore"):
+        for op, fn in (("add", batch_add), ("sub", batch_sub), ("mul", batch_mul), ("div", batch_div)):
+            assert_bitwise(fn(la, lb, V(v)).numpy(), oracle.ew(op, a, b, v), nan_ok=True)
