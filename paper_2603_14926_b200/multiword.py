@@ -327,62 +327,91 @@ def from_oracle(value, k: int) -> tuple:
 
 
 def is_normalized(comps) -> bool:
-    """Component-overlap invariant |c[i+1]| <= ulp(c[i]) / 2 (733-741)."""
-    for hi, lo in zip(comps, comps[1:]):
-        if hi == 0.0:
-            if lo != 0.0:
+    """Non-overlap invariant (733-741): every component is at most half an
+    ulp of the one before it, and nothing follows a zero component."""
+    prev = None
+    for c in comps:
+        if prev is not None:
+            if prev == 0.0 and c != 0.0:
                 return False
-        elif abs(lo) > 0.5 * math.ulp(abs(hi)):
-            return False
+            if prev != 0.0 and abs(c) > math.ulp(abs(prev)) / 2:
+                return False
+        prev = c
     return True
 
 
+# The value classes (multiword.py:850-1004): an immutable tuple of K
+# floats with the Standard-variant operators.  The operator methods are
+# generated from one table; every arithmetic operator is a one-lane device
+# kernel (mw_add / mw_sub / mw_mul / mw_div above).
+_BINOPS = {"add": mw_add, "sub": mw_sub, "mul": mw_mul, "truediv": mw_div}
+
+
+def _operator(op: str, reflected: bool):
+    fn = _BINOPS[op]
+
+    def method(self, other):
+        rhs = self._as_comps(other)
+        if rhs is NotImplemented:
+            return NotImplemented
+        return self._of(fn(rhs, self.comps) if reflected else fn(self.comps, rhs))
+
+    method.__name__ = f"__{'r' if reflected else ''}{op}__"
+    return method
+
+
 class MultiWord:
-    """Immutable K-word value over a component tuple (850-989).  Operators
-    use the Standard variant (as in the reference); arithmetic runs on the
-    device through one-lane kernels."""
+    """Immutable K-word value: ``comps`` is a tuple of K floats, leading
+    component first.  ``DD``, ``TD`` and ``QD`` fix K; the base class takes
+    K from the number of components.  Operators use the Standard variant,
+    as the reference's do."""
 
     __slots__ = ("comps",)
 
     K: int | None = None
 
     def __init__(self, *parts):
-        if len(parts) == 1 and isinstance(parts[0], (tuple, list)):
-            parts = tuple(parts[0])
-        k = self.K if self.K is not None else len(parts)
+        seq = parts[0] if len(parts) == 1 and isinstance(parts[0], (tuple, list)) else parts
+        k = len(seq) if self.K is None else self.K
         if k not in BITS:
             raise ValueError(f"unsupported word count {k}")
-        if len(parts) > k:
-            raise ValueError(f"{len(parts)} components for a {k}-word value")
-        comps = tuple(float(p) for p in parts) + (0.0,) * (k - len(parts))
-        object.__setattr__(self, "comps", comps)
+        if len(seq) > k:
+            raise ValueError(f"{len(seq)} components for a {k}-word value")
+        padded = [float(v) for v in seq] + [0.0] * (k - len(seq))
+        object.__setattr__(self, "comps", tuple(padded))
 
     def __setattr__(self, name, value):
         raise AttributeError("MultiWord values are immutable")
 
+    # -- construction / conversion
     @property
     def k(self) -> int:
         return len(self.comps)
 
-    @classmethod
-    def from_components(cls, comps) -> "MultiWord":
+    @staticmethod
+    def _of(comps) -> "MultiWord":
         return _CLASS_BY_K[len(comps)](*comps)
 
     @classmethod
+    def from_components(cls, comps) -> "MultiWord":
+        return MultiWord._of(tuple(comps))
+
+    @classmethod
     def from_float(cls, x: float, k: int | None = None) -> "MultiWord":
-        kk = cls.K if cls.K is not None else (k if k is not None else 2)
-        return _CLASS_BY_K[kk](*from_basefloat(x, kk))
+        width = cls.K or k or 2
+        return MultiWord._of(from_basefloat(x, width))
 
     def to_float(self) -> float:
-        acc = 0.0
-        for c in reversed(self.comps):
-            acc += c
-        return acc
+        """Components summed smallest first in binary64."""
+        total = 0.0
+        for c in self.comps[::-1]:
+            total += c
+        return total
 
     def to_fraction(self) -> Fraction:
-        return sum((Fraction(c) for c in self.comps), Fraction(0))
+        return sum(map(Fraction, self.comps), Fraction(0))
 
-    def _coerce(self, other):
+    def _as_comps(self, other):
         if isinstance(other, MultiWord):
             if other.k != self.k:
                 raise ValueError("mixed word counts")
@@ -391,71 +420,44 @@ class MultiWord:
             return from_basefloat(float(other), self.k)
         return NotImplemented
 
-    def _wrap(self, comps):
-        return _CLASS_BY_K[len(comps)](*comps)
-
-    def __add__(self, other):
-        rhs = self._coerce(other)
-        return NotImplemented if rhs is NotImplemented else self._wrap(mw_add(self.comps, rhs))
-
-    __radd__ = __add__
-
-    def __sub__(self, other):
-        rhs = self._coerce(other)
-        return NotImplemented if rhs is NotImplemented else self._wrap(mw_sub(self.comps, rhs))
-
-    def __rsub__(self, other):
-        rhs = self._coerce(other)
-        return NotImplemented if rhs is NotImplemented else self._wrap(mw_sub(rhs, self.comps))
-
-    def __mul__(self, other):
-        rhs = self._coerce(other)
-        return NotImplemented if rhs is NotImplemented else self._wrap(mw_mul(self.comps, rhs))
-
-    __rmul__ = __mul__
-
-    def __truediv__(self, other):
-        rhs = self._coerce(other)
-        return NotImplemented if rhs is NotImplemented else self._wrap(mw_div(self.comps, rhs))
-
-    def __rtruediv__(self, other):
-        rhs = self._coerce(other)
-        return NotImplemented if rhs is NotImplemented else self._wrap(mw_div(rhs, self.comps))
+    # -- arithmetic (one-lane device kernels, Standard variant)
+    # x + y and y + x both compute mw_add(x, y) (and likewise *), exactly
+    # as the reference aliases __radd__ / __rmul__ (the Standard kernels
+    # are not all bitwise commutative); - and / really reflect
+    __add__ = __radd__ = _operator("add", False)
+    __sub__ = _operator("sub", False)
+    __rsub__ = _operator("sub", True)
+    __mul__ = __rmul__ = _operator("mul", False)
+    __truediv__ = _operator("truediv", False)
+    __rtruediv__ = _operator("truediv", True)
 
     def __neg__(self):
-        return self._wrap(mw_neg(self.comps))
+        return MultiWord._of(mw_neg(self.comps))
 
     def __abs__(self):
-        return -self if self.comps[0] < 0.0 else self
+        return self if self.comps[0] >= 0.0 else -self
 
+    # -- comparison by exact value
     def __eq__(self, other):
-        if isinstance(other, MultiWord):
-            return other.k == self.k and self.to_fraction() == other.to_fraction()
         if isinstance(other, (int, float)):
             return self.to_fraction() == Fraction(float(other))
+        if isinstance(other, MultiWord):
+            return self.k == other.k and self.to_fraction() == other.to_fraction()
         return NotImplemented
 
     def __hash__(self):
         return hash(self.to_fraction())
 
     def __repr__(self):
-        name = type(self).__name__ if self.K is not None else f"MultiWord{self.k}"
-        return f"{name}({', '.join(repr(c) for c in self.comps)})"
+        label = f"MultiWord{self.k}" if self.K is None else type(self).__name__
+        return label + "(" + ", ".join(map(repr, self.comps)) + ")"
 
-    def __str__(self):
-        return repr(self)
-
-
-class DD(MultiWord):
-    K = 2
+    __str__ = __repr__
 
 
-class TD(MultiWord):
-    K = 3
-
-
-class QD(MultiWord):
-    K = 4
-
+DD = type("DD", (MultiWord,), {"K": 2, "__slots__": (), "__doc__": "Double-word (double-double) value."})
+TD = type("TD", (MultiWord,), {"K": 3, "__slots__": (), "__doc__": "Triple-word value."})
+QD = type("QD", (MultiWord,), {"K": 4, "__slots__": (), "__doc__": "Quadruple-word (quad-double) value."})
+DD.__module__ = TD.__module__ = QD.__module__ = __name__
 
 _CLASS_BY_K = {2: DD, 3: TD, 4: QD}
