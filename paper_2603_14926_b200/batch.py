@@ -79,6 +79,23 @@ def as_planes(comps, ndim: int, device=None) -> torch.Tensor:
     return t.to(device=dev, dtype=torch.float64).contiguous()
 
 
+def coefficient_planes(values, k: int | None = None) -> np.ndarray:
+    """(K, n) float64 planes from a list of K-word values -- tuples / lists,
+    objects with ``.comps``, or bare floats (which need ``k``: the value
+    becomes (x, 0, ..., 0)) -- in list order (coefficient i at column i)."""
+    def words(v):
+        if hasattr(v, "comps"):
+            return tuple(v.comps)
+        if isinstance(v, (tuple, list)):
+            return tuple(v)
+        if k is None:
+            raise ValueError("k required for bare float coefficients")
+        return (float(v),) + (0.0,) * (k - 1)
+
+    cols = [words(v) for v in values]
+    return np.array(cols, dtype=np.float64).T.copy()
+
+
 class LaneBatch:
     """W K-word values in component-planar layout (batch.py:61-93).
 

@@ -35,23 +35,33 @@ __all__ = ["Scheme", "MatMulPlan", "MWMatrix", "CMWMatrix", "matmul", "cmatmul",
 
 
 class Scheme(enum.Enum):
+    """Product scheme (linalg.py:59-72): the naive t-ascending fold, the
+    blocked form of the same fold, or Strassen's recursion."""
+
     NAIVE = "naive"
     BLOCKED = "blocked"
     STRASSEN = "strassen"
 
     @classmethod
     def parse(cls, name) -> "Scheme":
+        """A Scheme, its value or name (any case), or the reference's own
+        enum member."""
         if isinstance(name, cls):
             return name
-        key = str(getattr(name, "value", name)).lower()
-        for s in cls:
-            if s.value == key or s.name.lower() == key:
-                return s
-        raise ValueError(f"unknown scheme {name!r}")
+        wanted = str(getattr(name, "value", name)).lower()
+        found = {m.value: m for m in cls} | {m.name.lower(): m for m in cls}
+        if wanted not in found:
+            raise ValueError(f"unknown scheme {name!r}")
+        return found[wanted]
 
 
 @dataclass(frozen=True)
 class MatMulPlan:
+    """How ``matmul`` multiplies (linalg.py:75-89): scheme, kernel variant,
+    and the reference's ``simd`` / ``threads`` / ``strassen_cutoff`` knobs
+    (accepted and validated; the device kernels need no threads, and
+    results never depend on them)."""
+
     scheme: Scheme = Scheme.STRASSEN
     variant: Variant = Variant.STANDARD
     simd: bool = True
@@ -59,12 +69,12 @@ class MatMulPlan:
     strassen_cutoff: int = 32
 
     def __post_init__(self):
-        object.__setattr__(self, "scheme", Scheme.parse(self.scheme))
-        object.__setattr__(self, "variant", Variant.parse(self.variant))
-        if self.strassen_cutoff < 2:
-            raise ValueError("strassen_cutoff must be >= 2")
-        if self.threads < 1:
-            raise ValueError("threads must be >= 1")
+        for field, parse in (("scheme", Scheme.parse), ("variant", Variant.parse)):
+            object.__setattr__(self, field, parse(getattr(self, field)))
+        checks = (("strassen_cutoff", 2), ("threads", 1))
+        for field, least in checks:
+            if getattr(self, field) < least:
+                raise ValueError(f"{field} must be >= {least}")
 
 
 class MWMatrix:
@@ -129,28 +139,20 @@ class MWMatrix:
 
 
 class CMWMatrix:
-    """Complex matrix as a (re, im) pair of equally shaped MWMatrix
-    (linalg.py:161-193)."""
+    """Complex matrix: real and imaginary parts as two MWMatrix of one
+    shape and word count (linalg.py:161-193)."""
 
     __slots__ = ("re", "im")
 
     def __init__(self, re: MWMatrix, im: MWMatrix):
-        if (re.rows, re.cols, re.k) != (im.rows, im.cols, im.k):
+        same = re.rows == im.rows and re.cols == im.cols and re.k == im.k
+        if not same:
             raise ValueError("re/im shape mismatch")
-        self.re = re
-        self.im = im
+        self.re, self.im = re, im
 
-    @property
-    def rows(self):
-        return self.re.rows
-
-    @property
-    def cols(self):
-        return self.re.cols
-
-    @property
-    def k(self):
-        return self.re.k
+    rows = property(lambda self: self.re.rows)
+    cols = property(lambda self: self.re.cols)
+    k = property(lambda self: self.re.k)
 
     def bitwise_equal(self, other: "CMWMatrix") -> bool:
         return self.re.bitwise_equal(other.re) and self.im.bitwise_equal(other.im)

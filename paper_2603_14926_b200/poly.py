@@ -19,7 +19,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .batch import LaneBatch, as_planes
+from .batch import LaneBatch, as_planes, coefficient_planes
 from .multiword import BITS, Variant, from_basefloat, variant_code
 
 __all__ = [
@@ -66,18 +66,7 @@ class MWPolynomial:
     @classmethod
     def from_coeffs(cls, coeffs, k: int | None = None, device=None) -> "MWPolynomial":
         """coeffs: K-word tuples / objects with .comps / floats, low to high."""
-        rows = []
-        for c in coeffs:
-            if hasattr(c, "comps"):
-                rows.append(tuple(c.comps))
-            elif isinstance(c, (tuple, list)):
-                rows.append(tuple(c))
-            else:
-                if k is None:
-                    raise ValueError("k required for bare float coefficients")
-                rows.append(from_basefloat(float(c), k))
-        kk = len(rows[0])
-        return cls(np.array([[r[c] for r in rows] for c in range(kk)], dtype=np.float64), device=device)
+        return cls(coefficient_planes(coeffs, k), device=device)
 
     def coeff(self, i: int) -> tuple:
         return tuple(float(v) for v in self.planes[:, i].cpu())

@@ -29,7 +29,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .batch import LaneBatch, as_planes, batch_add, batch_div, batch_mul
+from .batch import LaneBatch, as_planes, batch_add, batch_div, batch_mul, coefficient_planes
 from .multiword import BITS, Variant, from_basefloat, from_fraction, variant_code
 
 __all__ = [
@@ -91,18 +91,7 @@ class MonicPoly:
 
     @classmethod
     def from_coeffs(cls, coeffs, k: int | None = None, device=None) -> "MonicPoly":
-        rows = []
-        for c in coeffs:
-            if hasattr(c, "comps"):
-                rows.append(tuple(c.comps))
-            elif isinstance(c, (tuple, list)):
-                rows.append(tuple(c))
-            else:
-                if k is None:
-                    raise ValueError("k required for bare float coefficients")
-                rows.append(from_basefloat(float(c), k))
-        kk = len(rows[0])
-        return cls(np.array([[r[c] for r in rows] for c in range(kk)], dtype=np.float64), device=device)
+        return cls(coefficient_planes(coeffs, k), device=device)
 
     @classmethod
     def from_polynomial(cls, p, variant: Variant = Variant.STANDARD) -> "MonicPoly":
