@@ -148,20 +148,17 @@ class LaneBatch:
 def pack(values, width: int | None = None, device=None) -> LaneBatch:
     """Pack K-word values (tuples or objects with ``.comps``) into a batch;
     tail lanes are zero padded (batch.py:96-112)."""
-    vals = [tuple(getattr(v, "comps", v)) for v in values]
-    if not vals:
+    words = [tuple(getattr(v, "comps", v)) for v in values]
+    if len(words) == 0:
         raise ValueError("cannot pack an empty value list")
-    k = len(vals[0])
-    for v in vals:
-        if len(v) != k:
-            raise ValueError("mixed word counts in pack")
-    w = width if width is not None else len(vals)
-    if w < len(vals):
-        raise ValueError(f"width {w} below value count {len(vals)}")
-    arr = np.zeros((k, w))
-    for i, v in enumerate(vals):
-        arr[:, i] = v
-    return LaneBatch(arr, count=len(vals), device=device)
+    if len({len(w) for w in words}) != 1:
+        raise ValueError("mixed word counts in pack")
+    lanes = len(words) if width is None else width
+    if lanes < len(words):
+        raise ValueError(f"width {lanes} below value count {len(words)}")
+    arr = np.zeros((len(words[0]), lanes))
+    arr[:, : len(words)] = np.array(words, dtype=np.float64).T
+    return LaneBatch(arr, count=len(words), device=device)
 
 
 def unpack(batch: LaneBatch) -> list:

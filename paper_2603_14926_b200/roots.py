@@ -52,11 +52,13 @@ INT32_MAX = 2**31 - 1
 
 
 class CollisionError(ValueError):
-    """Two root approximations coincided; the update is undefined."""
+    """A denominator factor z_i - z_j vanished: two approximations are equal
+    and the simultaneous update is undefined (roots.py:61-64)."""
 
 
 class NoConvergence(RuntimeError):
-    """Iteration budget exhausted; carries the best state reached."""
+    """The sweep budget ran out before the tolerance was met; ``state``
+    holds the last iterate (roots.py:67-74)."""
 
     def __init__(self, message, state):
         super().__init__(message)
