@@ -847,6 +847,76 @@ __global__ void __launch_bounds__(32 * WPC)
   }
 }
 
+// Tree-order GEMV (bit-identical) with DYNAMIC row assignment: a
+// persistent grid of 4-warp CTAs takes rows from a global ticket
+// (atomicAdd), the next ticket fetched while the current row folds, so CTAs
+// that finish early take more rows (no wave tail) and drift out of phase
+// (no convoy of load bursts).  ctr[0] is the row ticket, ctr[1] counts
+// finished CTAs; the last CTA re-arms both (graph-replay safe).
+template <int K, int VAR, int D, int MINB>
+__global__ void __launch_bounds__(128, MINB)
+    gemv_dyn_kernel(const double* __restrict__ A, int64_t lda, int64_t sA,
+                    const double* __restrict__ x, int64_t sx, double* __restrict__ y, int64_t sy,
+                    int64_t m, int64_t n, unsigned int* __restrict__ ctr) {
+  constexpr int P = 128;
+  __shared__ double roots[2][K][4];
+  __shared__ unsigned int nxt[2];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int u = tid;
+  const int64_t valid = n < P ? n : P;
+  if (tid == 0) nxt[0] = atomicAdd(&ctr[0], 1u);
+  __syncthreads();
+  int64_t i = nxt[0];
+  for (int it = 0; i < m; ++it) {
+    if (tid == 0) nxt[(it + 1) & 1] = atomicAdd(&ctr[0], 1u);
+    const double* row = A + i * lda;
+    V<K> acc = zero<K>();
+    int64_t t = u;
+    for (; t + (D - 1) * P < n; t += D * P) {
+      V<K> a[D], xv[D];
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        a[d] = load<K>(row, sA, t + d * P);
+        xv[d] = load<K>(x, sx, t + d * P);
+      }
+#pragma unroll
+      for (int d = 0; d < D; ++d) acc = Ops<K, VAR>::add(acc, Ops<K, VAR>::mul(a[d], xv[d]));
+    }
+    for (; t < n; t += P)
+      acc = Ops<K, VAR>::add(acc, Ops<K, VAR>::mul(load<K>(row, sA, t), load<K>(x, sx, t)));
+#pragma unroll
+    for (int s = 1; s < 32; s <<= 1) {
+      const V<K> o = shfl_down<K>(acc, s);
+      if ((lane & (2 * s - 1)) == 0 && u + s < valid) acc = Ops<K, VAR>::add(acc, o);
+    }
+    const int buf = it & 1;
+    if (lane == 0) {
+#pragma unroll
+      for (int c = 0; c < K; ++c) roots[buf][c][warp] = acc.c[c];
+    }
+    __syncthreads();
+    if (warp == (it & 3) && lane == 0) {
+      V<K> r[4];
+#pragma unroll
+      for (int w = 0; w < 4; ++w)
+#pragma unroll
+        for (int c = 0; c < K; ++c) r[w].c[c] = roots[buf][c][w];
+      if (32 < valid) r[0] = Ops<K, VAR>::add(r[0], r[1]);
+      if (96 < valid) r[2] = Ops<K, VAR>::add(r[2], r[3]);
+      if (64 < valid) r[0] = Ops<K, VAR>::add(r[0], r[2]);
+      store<K>(y, sy, i, r[0]);
+    }
+    i = nxt[(it + 1) & 1];
+  }
+  if (tid == 0) {
+    __threadfence();
+    if (atomicAdd(&ctr[1], 1u) == gridDim.x - 1) {
+      ctr[0] = 0u;
+      ctr[1] = 0u;
+    }
+  }
+}
+
 template <int K, int VAR>
 struct GemvLaunch {
   static int run(const double* A, int64_t lda, int64_t sA, const double* x, int64_t sx, double* y,

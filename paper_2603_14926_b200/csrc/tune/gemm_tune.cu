@@ -148,6 +148,24 @@ static int gemv_w1_launch(const double* A, const double* x, double* y, int64_t m
       A, gemv_lda(n), gemv_sa(m, n), x, n, y, m, m, n);
   return launch_status();
 }
+template <int K, int D, int MINB, int CPS>
+static int gemv_dyn_launch(const double* A, const double* x, double* y, int64_t m, int64_t n,
+                           cudaStream_t st) {
+  static unsigned int* ctr = nullptr;
+  if (!ctr) {
+    cudaMalloc(&ctr, 2 * sizeof(unsigned int));
+    cudaMemset(ctr, 0, 2 * sizeof(unsigned int));
+    cudaDeviceSynchronize();
+  }
+  auto kern = gemv_dyn_kernel<K, BRANCH_FREE, D, MINB>;
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, 0);
+  if (CPS > 0 && CPS < per_sm) per_sm = CPS;
+  int64_t grid = (int64_t)148 * per_sm;
+  if (grid > m) grid = m;
+  kern<<<(unsigned)grid, 128, 0, st>>>(A, gemv_lda(n), gemv_sa(m, n), x, n, y, m, m, n, ctr);
+  return launch_status();
+}
 template <int K, int R, int D, int S, bool XS>
 static int gemv_staged_launch(const double* A, const double* x, double* y, int64_t m, int64_t n,
                               cudaStream_t st) {
@@ -334,10 +352,16 @@ static int gemv_run(int cfg, const double* A, const double* x, double* y, int64_
     case 97: return gemv_w1_launch<K, 2, 2>(A, x, y, m, n, st);
     case 98: return gemv_w1_launch<K, 1, 4>(A, x, y, m, n, st);
     case 99: return gemv_w1_launch<K, 4, 1>(A, x, y, m, n, st);
+    case 100: return gemv_dyn_launch<K, 4, 1, 0>(A, x, y, m, n, st);
+    case 101: return gemv_dyn_launch<K, 4, 8, 0>(A, x, y, m, n, st);
+    case 102: return gemv_dyn_launch<K, 2, 8, 0>(A, x, y, m, n, st);
+    case 103: return gemv_dyn_launch<K, 4, 6, 0>(A, x, y, m, n, st);
+    case 104: return gemv_dyn_launch<K, 4, 8, 4>(A, x, y, m, n, st);
+    case 105: return gemv_dyn_launch<K, 4, 8, 6>(A, x, y, m, n, st);
     default: return MW_ERR_INVALID;
   }
 }
-extern "C" int mwt_gemv_num_configs(void) { return 100; }
+extern "C" int mwt_gemv_num_configs(void) { return 106; }
 extern "C" const char* mwt_gemv_config_name(int cfg) {
   static const char* names[] = {"W4_R2_D4", "W1_R8_D8", "W1_R8_D4", "W2_R4_D4", "W2_R4_D8",
                                 "W4_R2_D2", "W4_R1_D4", "W8_R1_D2", "st_R2_D4_S2", "st_R2_D4_S3",
@@ -356,8 +380,9 @@ extern "C" const char* mwt_gemv_config_name(int cfg) {
                                 "pn_S2_D4_m4", "nn_S1_D4", "nn_S2_D4", "nn_S1_D4_m8", "nn_S2_D4_m4", "nn_S1_D2_m8", "pn_S1_D2_m8",
                                 "cg_D4_S3", "cg_D4_S4", "cg_D2_S4", "cg_D2_S6", "cg_D2_S3", "cg_D1_S8", "cg_D4_S2", "cg_D8_S2",
                                 "u2_D2_R1", "u2_D2_R2", "u2_D4_R1", "u2_D4_R2", "u2_D1_R2", "u2_D2_R4",
-                                "w1_D1_W1", "w1_D2_W1", "w1_D1_W2", "w1_D2_W2", "w1_D1_W4", "w1_D4_W1"};
-  return (cfg >= 0 && cfg < 100) ? names[cfg] : "?";
+                                "w1_D1_W1", "w1_D2_W1", "w1_D1_W2", "w1_D2_W2", "w1_D1_W4", "w1_D4_W1",
+                                "dy_D4", "dy_D4_m8", "dy_D2_m8", "dy_D4_m6", "dy_D4_m8_c4", "dy_D4_m8_c6"};
+  return (cfg >= 0 && cfg < 106) ? names[cfg] : "?";
 }
 extern "C" int mwt_gemv(int cfg, int k, const double* A, const double* x, double* y, int64_t m,
                         int64_t n, void* stream) {
