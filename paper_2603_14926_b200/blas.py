@@ -65,7 +65,10 @@ def dot(x: LaneBatch, y: LaneBatch, variant: Variant = Variant.BRANCH_FREE, orde
 def axpy_(alpha, x: LaneBatch, y: LaneBatch, variant: Variant = Variant.BRANCH_FREE) -> LaneBatch:
     """y <- alpha x + y in place; alpha is a K-word tuple.  (K, widths and
     devices are checked by the extension: ValueError on a mismatch.)"""
-    _lib.ext().axpy_(variant_code(variant), getattr(alpha, "comps", alpha), x.planes, y.planes)
+    words = getattr(alpha, "comps", alpha)
+    if not isinstance(words, (tuple, list)):  # numpy / torch vectors of K words
+        words = [float(v) for v in words]
+    _lib.ext().axpy_(variant_code(variant), words, x.planes, y.planes)
     y.count = max(x.count, y.count)
     return y
 
