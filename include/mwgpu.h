@@ -312,11 +312,13 @@ int mw_tuning_defaults(mw_tuning* t);
 
 /* mw_gemm / mw_dot / mw_dk_sweep_ws with explicit tuning (NULL = the
  * defaults the plain entry points use); MW_ERR_INVALID for a value out of
- * range.  mw_dk_sweep_ex: if max_mag_bits != NULL (a device u64 the caller
- * zeroes first) it is atomically raised to the bit pattern of every
- * step_mag written, so after the sweep it holds the sweep's max update
- * (RootState.last_max_update, roots.py:308) with no separate reduction;
- * step_mag >= 0, so the bit order is the value order. */
+ * range.  mw_dk_sweep_ex: if max_mag_bits != NULL (two device u64 the
+ * caller zeroes first), [0] is atomically raised to the bit pattern of
+ * every step_mag written and [1] to that of every new root's
+ * hypot(re0, im0), so after the sweep they hold the sweep's max update
+ * (RootState.last_max_update, roots.py:308) and the max |z| of dk_solve's
+ * convergence test (roots.py:336) with no separate reduction; both are
+ * >= 0, so the bit order is the value order. */
 int mw_gemm_ex(int k, int variant, const double* A, int64_t lda, int64_t sA,
                const double* B, int64_t ldb, int64_t sB, double* C, int64_t ldc,
                int64_t sC, int64_t m, int64_t n, int64_t kd,

@@ -100,9 +100,11 @@ struct DkPeers {
   int* timeout;                    // set to 1 when a wait gave up
   long long spin_limit;
   int world, rank, sweep, sweeps;
-  // optional (any sweep, not only the peer form): atomically raised to the
-  // bit pattern of every step_mag written -- the sweep's max update
-  // (roots.py:308) without a separate reduction; step_mag >= 0, so the
+  // optional (any sweep, not only the peer form): max_bits[0] is raised
+  // atomically to the bit pattern of every step_mag written -- the sweep's
+  // max update (roots.py:308) -- and max_bits[1] to that of every new
+  // root's |z'| = hypot(re0, im0) (the max |z| of dk_solve's test,
+  // roots.py:336), with no separate reduction; both are >= 0, so the
   // unsigned bit order is the value order (NaN, as np.max, dominates)
   unsigned long long* max_bits;
 };
@@ -142,7 +144,10 @@ __device__ __forceinline__ void dk_tail(const Cx<K, VAR>& acc, const Cx<K, VAR>&
   store<K>(zim_out, so, i, nim);
   const double smag = hypot(step_re.c[0], step_im.c[0]);
   step_mag[i] = smag;
-  if (P) dk_note_max(P->max_bits, smag);
+  if (P && P->max_bits) {
+    dk_note_max(P->max_bits, smag);
+    dk_note_max(P->max_bits + 1, hypot(nre.c[0], nim.c[0]));
+  }
   if constexpr (PEER) {
     for (int p = 0; p < P->world; ++p) {
       if (p == P->rank) continue;
@@ -1064,7 +1069,8 @@ __global__ void __launch_bounds__(32 * dk_treem_warps<R>(), R == 2 ? 2 : 1)
     const bool chain = warp == 2 * R;
     const int64_t i = rbase + lane;
     const bool act = lane < R && i < i1;
-    double* my = pw + (size_t)(lane < R ? lane : 0) * (3 * K + 1);  // num_re, num_im, rcp, step_im0
+    double* my = pw + (size_t)(lane < R ? lane : 0) * (3 * K + 2);  // num_re, num_im, rcp, step_im0, z'_im0
+    double nz0 = 0.0;
     Cx<K, VAR> z, acc, den;
     V<K> num, step;
     if (act) {
@@ -1097,6 +1103,7 @@ __global__ void __launch_bounds__(32 * dk_treem_warps<R>(), R == 2 ? 2 : 1)
       }
       step = O::mul(num, rcp);
       const V<K> nz = O::add(chain ? z.re : z.im, neg(step));
+      nz0 = nz.c[0];
       double* outp = chain ? zre_out : zim_out;
       store<K>(outp, so, i, nz);
       if constexpr (PEER) {
@@ -1105,14 +1112,20 @@ __global__ void __launch_bounds__(32 * dk_treem_warps<R>(), R == 2 ? 2 : 1)
           store<K>(peers.out[p] + (chain ? 0 : (int64_t)K * so), so, i, nz);
         }
       }
-      if (!chain) my[3 * K] = step.c[0];
+      if (!chain) {
+        my[3 * K] = step.c[0];
+        my[3 * K + 1] = nz0;
+      }
     }
     bar_sync_n(12, 64);
     if (chain) {
       if (act) {
         const double smag = hypot(step.c[0], my[3 * K]);
         step_mag[i] = smag;
-        dk_note_max(peers.max_bits, smag);
+        if (peers.max_bits) {
+          dk_note_max(peers.max_bits, smag);
+          dk_note_max(peers.max_bits + 1, hypot(nz0, my[3 * K + 1]));
+        }
       }
       if (lane == 0) MW_DK_MARK(8);
       if constexpr (PEER) {

@@ -290,8 +290,9 @@ void dk_sweep(int64_t variant, const at::Tensor& coeffs, const at::Tensor& zre, 
   unsigned long long* maxp = nullptr;
   if (max_bits.has_value()) {
     const at::Tensor& mb = *max_bits;
-    if (!mb.is_cuda() || mb.scalar_type() != at::kLong || mb.numel() < 1 || mb.device() != dev)
-      throw py::value_error("max_bits: int64 device scalar expected");
+    if (!mb.is_cuda() || mb.scalar_type() != at::kLong || mb.numel() < 2 || !mb.is_contiguous() ||
+        mb.device() != dev)
+      throw py::value_error("max_bits: two contiguous int64 on the state's device expected");
     maxp = reinterpret_cast<unsigned long long*>(mb.data_ptr<int64_t>());
   }
   c10::cuda::CUDAGuard guard(dev);

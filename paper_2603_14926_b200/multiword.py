@@ -188,6 +188,15 @@ def _to_planes(*tuples):
     else:
         kind = "float"
     dev = next((c.device for c in comps if isinstance(c, torch.Tensor) and c.is_cuda), torch.device("cuda"))
+    if kind != "torch":
+        # host operands: broadcast and stack on the host, one copy up (no
+        # device-side stack kernel on this path)
+        arrs = np.broadcast_arrays(*[np.asarray(c, dtype=np.float64) for c in comps])
+        shape = arrs[0].shape
+        host = np.ascontiguousarray(np.stack([a.reshape(-1) for a in arrs]))
+        planes = torch.from_numpy(host).to(dev)
+        _lib.require_cuda(planes)
+        return planes, kind, tuple(shape)
     ts = [torch.as_tensor(c, dtype=torch.float64).to(dev) if isinstance(c, torch.Tensor)
           else torch.as_tensor(np.asarray(c, dtype=np.float64), device=dev) for c in comps]
     shape = torch.broadcast_shapes(*(t.shape for t in ts))

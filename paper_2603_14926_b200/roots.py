@@ -247,8 +247,9 @@ def sweep_into(coeffs: torch.Tensor, zre: torch.Tensor, zim: torch.Tensor, out_r
     same indices (plane stride n).  ``flag`` (int32 device scalar) must hold
     INT32_MAX beforehand; it is lowered to min(j*n + i) on a collision.
     ``tuning``: an optional _lib.Tuning (launch shape only; same bits).
-    ``max_bits`` (int64 device scalar, zero beforehand) receives the bit
-    pattern of the largest step_mag written (the sweep's max update)."""
+    ``max_bits`` (two int64 on the device, zero beforehand) receive the bit
+    patterns of the largest step_mag written (the sweep's max update) and
+    of the largest new |z| = hypot(re0, im0)."""
     # the tree order's stream-ordered scratch (lane-per-root powers kernel)
     # is allocated in the extension from torch's caching allocator
     _lib.ext().dk_sweep(variant_code(variant), coeffs, zre, zim, out_re, out_im, step_mag, flag, bool(exact_order),
@@ -276,12 +277,12 @@ def dk_iterate(q: MonicPoly, state: RootState, variant: Variant = Variant.STANDA
     out_re = torch.empty_like(state.re)
     out_im = torch.empty_like(state.im)
     mag = torch.empty(state.n, dtype=torch.float64, device=dev)
-    # one int64 pair, uploaded by a copy (no fill kernel): [0] low word =
-    # the collision flag (INT32_MAX = none), [1] = the max-update bits the
-    # sweep kernel raises atomically (no torch reduction per sweep)
-    status = torch.tensor([INT32_MAX, 0], dtype=torch.int64).to(dev, non_blocking=True)
+    # three int64, uploaded by a copy (no fill kernel): [0] low word = the
+    # collision flag (INT32_MAX = none), [1] / [2] = the max-update and
+    # max-|z| bits the sweep kernel raises atomically (no torch reduction)
+    status = torch.tensor([INT32_MAX, 0, 0], dtype=torch.int64).to(dev, non_blocking=True)
     sweep_into(q.planes, state.re, state.im, out_re, out_im, mag, status.view(torch.int32)[0:1], variant,
-               exact_order, max_bits=status[1:2])
+               exact_order, max_bits=status[1:3])
     host = status.cpu().numpy()  # one read-back per sweep
     code = int(host[0])
     if code != INT32_MAX:
@@ -395,11 +396,12 @@ def dk_solve(q: MonicPoly, variant: Variant = Variant.STANDARD, tol: float | Non
     device time only.
 
     The iterates are bit-identical to the reference's sweep by sweep (exact
-    order).  The convergence TEST is not bit-identical: the reference
-    compares np.hypot magnitudes (roots.py:308, 334-336), here |step| is
-    CUDA's hypot in the sweep kernel (<= 2 ulp) and max|z| torch.hypot, so
-    when the largest update lands within a few ulp of tol * max|z| the
-    first converged sweep can differ from the reference loop's by one."""
+    order), and the test is the reference's comparison evaluated on the
+    host in binary64; its two magnitudes, however, are CUDA's hypot (<= 2
+    ulp, taken inside the sweep kernel) where the reference uses np.hypot
+    (roots.py:308, 336), so when the largest update lands within a few ulp
+    of tol * max|z| the first converged sweep can differ from the
+    reference loop's by one."""
     if tol is None:
         tol = default_tolerance(q.k)
     if tol <= 0:
@@ -421,25 +423,29 @@ def dk_solve(q: MonicPoly, variant: Variant = Variant.STANDARD, tol: float | Non
         res_re = torch.empty((m, k, n), dtype=torch.float64, device=dev)
         res_im = torch.empty_like(res_re)
         mag = torch.empty((m, n), dtype=torch.float64, device=dev)
-        flags = torch.full((m,), INT32_MAX, dtype=torch.int32, device=dev)
+        # per sweep: [collision flag (low word), max-update bits, max-|z|
+        # bits], raised by the sweep kernels themselves; uploaded and read
+        # back once per chunk (no torch kernels on this path)
+        status = torch.from_numpy(np.tile(np.array([INT32_MAX, 0, 0], dtype=np.int64), (m, 1))).to(dev)
+        flags32 = status.view(torch.int32)  # (m, 6): column 0 is each row's low word
         src_re, src_im = cur_re, cur_im
         for s in range(m):
-            sweep_into(q.planes, src_re, src_im, res_re[s], res_im[s], mag[s], flags[s:s + 1], variant,
-                       exact_order)
+            sweep_into(q.planes, src_re, src_im, res_re[s], res_im[s], mag[s], flags32[s, 0:1], variant,
+                       exact_order, max_bits=status[s, 1:3])
             src_re, src_im = res_re[s], res_im[s]
-        upd = mag.max(dim=1).values
-        zmag = torch.hypot(res_re[:, 0], res_im[:, 0]).max(dim=1).values
-        conv = upd <= tol * torch.clamp(zmag, min=1e-300)
-        host = torch.stack([flags.to(torch.float64), conv.to(torch.float64), upd]).cpu().numpy()
+        host = status.cpu().numpy()
+        upd_all = host[:, 1].copy().view(np.float64)
+        zmag_all = host[:, 2].copy().view(np.float64)
         for s in range(m):
-            if int(host[0, s]) != INT32_MAX:
-                _raise_collision(int(host[0, s]), n)
-            if host[1, s]:
+            if int(host[s, 0]) != INT32_MAX:
+                _raise_collision(int(host[s, 0]), n)
+            upd, zmag = float(upd_all[s]), float(zmag_all[s])
+            if upd <= tol * max(zmag, 1e-300):  # the reference's test, on the host (roots.py:336-337)
                 st = RootState(re=res_re[s], im=res_im[s], iteration=it + s + 1, converged=True,
-                               last_max_update=float(host[2, s]))
+                               last_max_update=upd)
                 return st, st.iteration
         last = RootState(re=res_re[m - 1], im=res_im[m - 1], iteration=it + m, converged=False,
-                         last_max_update=float(host[2, m - 1]))
+                         last_max_update=float(upd_all[m - 1]))
         cur_re, cur_im, it = last.re, last.im, last.iteration
         done += m
         chunk = min(2 * chunk, 32)
