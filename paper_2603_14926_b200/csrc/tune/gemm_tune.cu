@@ -8,6 +8,7 @@
 #include "gemv_bulk.cuh"
 #include "gemv_probe.cuh"
 #include "gemv_wring.cuh"
+#include "gemv_pin.cuh"
 
 namespace mw {
 #define CFGV(NAME, bm, bn, bk, tm, tn, minb, vec)                             \
@@ -248,6 +249,13 @@ static int gemv_cs_launch(const double* A, const double* x, double* y, int64_t m
       A, gemv_lda(n), gemv_sa(m, n), x, n, y, m, m, n);
   return launch_status();
 }
+template <int K, int RPC, int D, int PIN, int MINB = 1>
+static int gemv_pin_launch(const double* A, const double* x, double* y, int64_t m, int64_t n,
+                           cudaStream_t st) {
+  gemv_pin_kernel<K, BRANCH_FREE, RPC, D, PIN, MINB>
+      <<<(unsigned)((m + RPC - 1) / RPC), 128 * RPC, 0, st>>>(A, gemv_lda(n), gemv_sa(m, n), x, n, y, m, m, n);
+  return launch_status();
+}
 template <int K>
 static int gemv_run(int cfg, const double* A, const double* x, double* y, int64_t m, int64_t n,
                     cudaStream_t st) {
@@ -358,10 +366,20 @@ static int gemv_run(int cfg, const double* A, const double* x, double* y, int64_
     case 103: return gemv_dyn_launch<K, 4, 6, 0>(A, x, y, m, n, st);
     case 104: return gemv_dyn_launch<K, 4, 8, 4>(A, x, y, m, n, st);
     case 105: return gemv_dyn_launch<K, 4, 8, 6>(A, x, y, m, n, st);
+    case 106: return gemv_pin_launch<K, 2, 4, 1>(A, x, y, m, n, st);
+    case 107: return gemv_pin_launch<K, 2, 2, 1>(A, x, y, m, n, st);
+    case 108: return gemv_pin_launch<K, 1, 4, 1>(A, x, y, m, n, st);
+    case 109: return gemv_pin_launch<K, 1, 2, 1>(A, x, y, m, n, st);
+    case 110: return gemv_pin_launch<K, 2, 4, 0>(A, x, y, m, n, st);
+    case 111: return gemv_pin_launch<K, 4, 2, 1>(A, x, y, m, n, st);
+    case 112: return gemv_pin_launch<K, 2, 8, 1>(A, x, y, m, n, st);
+    case 113: return gemv_pin_launch<K, 1, 8, 1>(A, x, y, m, n, st);
+    case 114: return gemv_pin_launch<K, 2, 4, 3>(A, x, y, m, n, st);
+    case 115: return gemv_pin_launch<K, 4, 4, 1>(A, x, y, m, n, st);
     default: return MW_ERR_INVALID;
   }
 }
-extern "C" int mwt_gemv_num_configs(void) { return 106; }
+extern "C" int mwt_gemv_num_configs(void) { return 116; }
 extern "C" const char* mwt_gemv_config_name(int cfg) {
   static const char* names[] = {"W4_R2_D4", "W1_R8_D8", "W1_R8_D4", "W2_R4_D4", "W2_R4_D8",
                                 "W4_R2_D2", "W4_R1_D4", "W8_R1_D2", "st_R2_D4_S2", "st_R2_D4_S3",
@@ -381,8 +399,10 @@ extern "C" const char* mwt_gemv_config_name(int cfg) {
                                 "cg_D4_S3", "cg_D4_S4", "cg_D2_S4", "cg_D2_S6", "cg_D2_S3", "cg_D1_S8", "cg_D4_S2", "cg_D8_S2",
                                 "u2_D2_R1", "u2_D2_R2", "u2_D4_R1", "u2_D4_R2", "u2_D1_R2", "u2_D2_R4",
                                 "w1_D1_W1", "w1_D2_W1", "w1_D1_W2", "w1_D2_W2", "w1_D1_W4", "w1_D4_W1",
-                                "dy_D4", "dy_D4_m8", "dy_D2_m8", "dy_D4_m6", "dy_D4_m8_c4", "dy_D4_m8_c6"};
-  return (cfg >= 0 && cfg < 106) ? names[cfg] : "?";
+                                "dy_D4", "dy_D4_m8", "dy_D2_m8", "dy_D4_m6", "dy_D4_m8_c4", "dy_D4_m8_c6",
+                                "pin_R2_D4", "pin_R2_D2", "pin_R1_D4", "pin_R1_D2", "pin0_R2_D4", "pin_R4_D2",
+                                "pin_R2_D8", "pin_R1_D8", "pin3_R2_D4", "pin_R4_D4"};
+  return (cfg >= 0 && cfg < 116) ? names[cfg] : "?";
 }
 extern "C" int mwt_gemv(int cfg, int k, const double* A, const double* x, double* y, int64_t m,
                         int64_t n, void* stream) {
