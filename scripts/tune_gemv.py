@@ -4,7 +4,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import paper_2603_14926_b200 as mw
 from paper_2603_14926_b200 import gen
-lib = ctypes.CDLL(os.path.join(os.path.dirname(mw._lib.LIB_PATH), "csrc", "tune", "libmwtune.so"))
+lib = ctypes.CDLL(os.path.join(os.path.dirname(mw._lib.LIB_PATH), "csrc", "tune", os.environ.get("TUNELIB", "libmwtune.so")))
 lib.mwt_gemv.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                          ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p]
 lib.mwt_gemv_config_name.restype = ctypes.c_char_p
@@ -41,7 +41,7 @@ for k in (3, 4):
         same = ""
         if cfg == 0:
             ref = y.clone()
-        elif (cfg >= 8 or cfg == 6) and not os.environ.get("LDA"):  # (cfg 61+: persistent shuffle tree)  # staged variants keep the P = 128 order: must be bit-identical
+        elif (cfg >= 8 or cfg == 6 or os.environ.get("TUNELIB")) and not os.environ.get("LDA"):  # (cfg 61+: persistent shuffle tree)  # staged variants keep the P = 128 order: must be bit-identical
             same = " bits==W4" if torch.equal(y.view(torch.int64), ref.view(torch.int64)) else " BITS DIFFER"
         ts = []
         for _ in range(10):
