@@ -5,9 +5,6 @@
 #include "../dk_kernels.cuh"
 
 namespace mw {
-int g_dk_exact_roots = 16;
-int g_dk_exact_split = 1;
-int g_dk_tree_roots = -1;
 int sm_count() { return 148; }
 }  // namespace mw
 using namespace mw;
@@ -16,14 +13,15 @@ extern "C" int dkp_sweep(int k, const double* coeffs, int64_t n, const double* z
                          const double* zim, int64_t i0, int64_t i1, double* zre_out,
                          double* zim_out, double* step_mag, int* flag, double* ws, int roots,
                          void* stream) {
-  g_dk_tree_roots = roots;
+  mw_tuning tune = tuning_defaults();
+  tune.dk_tree_roots = roots;
   cudaStream_t st = (cudaStream_t)stream;
   if (k == 3)
     return dk_tree_launch<3, BRANCH_FREE, false>(coeffs, n, n, zre, zim, n, i0, i1, zre_out, zim_out,
-                                                 n, step_mag, flag, DkPeers{}, ws, st);
+                                                 n, step_mag, flag, DkPeers{}, ws, tune, st);
   if (k == 4)
     return dk_tree_launch<4, BRANCH_FREE, false>(coeffs, n, n, zre, zim, n, i0, i1, zre_out, zim_out,
-                                                 n, step_mag, flag, DkPeers{}, ws, st);
+                                                 n, step_mag, flag, DkPeers{}, ws, tune, st);
   return MW_ERR_INVALID;
 }
 

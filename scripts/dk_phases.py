@@ -38,3 +38,5 @@ for k in (3, 4):
         span = (t[:, 8].max() - t[:, 0].min()) / 1e3
         print(f"k={k} roots={i1} R={roots} CTAs={ctas}: span {span:.2f} us; start spread {(t[:,0].max()-t[:,0].min())/1e3:.2f} us")
         print("   " + "  ".join(f"{nm}={v:.2f}" for nm, v in zip(NAMES, med)), flush=True)
+        if os.environ.get("DKP_DUMP"):
+            np.save(os.path.join(os.environ["DKP_DUMP"], f"dkp_k{k}_n{i1}_r{roots}.npy"), t)
