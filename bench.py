@@ -847,6 +847,11 @@ def secondary(args, torch, dist, mw, world, rank, peak, out=None):
         n5 = zre0.shape[1]
         mp_sweep = n5 * (20 * n5 + 31)
         fp_sweep = n5 * (n5 * (6 * MUL_OPS[k] + 14 * ADD_OPS[k]) + 20 * MUL_OPS[k] + 11 * ADD_OPS[k])
+        # the tree order executes fewer FP64 instructions per (i, j) than the
+        # reference's op sequence: its complex products are 4 mul + 2 add
+        # instead of 3 mul + 5 add and the Horner step adds the real
+        # coefficient to the real part only -- 8 mul + 7 add per pair
+        fp_sweep_tree = n5 * (n5 * (8 * MUL_OPS[k] + 7 * ADD_OPS[k]) + 20 * MUL_OPS[k] + 11 * ADD_OPS[k])
         for exact in (False, True):
             sweeps = 200
             if world == 1:
@@ -877,6 +882,11 @@ def secondary(args, torch, dist, mw, world, rank, peak, out=None):
                 "ms_200_sweeps": round(ms, 3), "us_per_sweep": round(ms * 1e3 / sweeps, 2),
                 "G_MPops": round(mp_sweep * sweeps / (ms / 1e3) / 1e9, 3),
                 "fp64_frac": round(fp_sweep * sweeps / (ms / 1e3) / peak["dfma"] / world, 4),
+                "fp64_frac_executed": round((fp_sweep if exact else fp_sweep_tree) * sweeps / (ms / 1e3)
+                                            / peak["dfma"] / world, 4),
+                "ops_note": ("fp64_frac counts the reference's op sequence per sweep (6 mul + 14 add per (i, j), "
+                             "SURVEY 8(d)); fp64_frac_executed what this order issues"
+                             + ("" if exact else " (8 mul + 7 add per (i, j): four-multiplication complex products)")),
                 "collective": ("all_gather of (re, im) K-planes per sweep"
                                + (", sweeps + NCCL captured in one CUDA graph" if args.backend == "nccl" else ""))
                 if world > 1 else None,

@@ -777,14 +777,6 @@ __device__ unsigned long long g_dk_prof[4096][12];
   } while (0)
 #endif
 
-// One denominator tree level (stride s over 32 values per root) on the
-// 2R denominator warps with FOUR lanes per complex product: lane roles
-// 0 / 1 / 2 / 3 hold p1 = a.re b.re, p2 = a.im b.im, p3 = a.re b.im, p4 =
-// a.im b.re of c_mul4 (one SIMD mul), then role 0 forms re = p1 - p2 and
-// role 2 forms im = p3 + p4 (one SIMD add).  The same operations on the
-// same operands as c_mul4, so the same bits, at a quarter of the
-// instructions a warp issues per product (a level's few products are
-// latency/issue bound on one warp each).
 __device__ __forceinline__ void bar_sync_n(int id, int threads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
@@ -802,23 +794,31 @@ __device__ __forceinline__ V<K> sel(bool t, const V<K>& a, const V<K>& b) {
   for (int c = 0; c < K; ++c) r.c[c] = t ? a.c[c] : b.c[c];
   return r;
 }
-template <int K, int VAR, int R>
-__device__ __forceinline__ void dk_den_level_split(double* den_s, int s, int v32) {
+// One complex product of a denominator tree level on FOUR adjacent lanes:
+// b[idx] <- b[idx] * b[idx + s] with idx = 2 s pair (pair < 0: lanes idle;
+// pairs whose partner index is >= v32 pass through).  Lane roles 0..3 form
+// p1 = a.re c.re, p2 = a.im c.im, p3 = a.re c.im, p4 = a.im c.re (one SIMD
+// mul), then role 0 forms re = p1 - p2 and role 2 im = p3 + p4 (one SIMD
+// add): c_mul4's operations on c_mul4's operands.
+template <int K, int VAR>
+__device__ __forceinline__ void dk_den_pair4(double* b, int s, int pair, int v32) {
   using O = Ops<K, VAR>;
-  const int lane = threadIdx.x & 31, wd = threadIdx.x >> 5;  // wd < 2R
-  const int per = 16 / s;                                    // pairs per root
-  const int pair = wd * 8 + lane / 4, role = lane & 3;
-  const bool have = pair < R * per;
-  const int r = have ? pair / per : 0;
-  const int idx = have ? 2 * s * (pair % per) : 0;
-  const bool act = have && idx + s < v32;
-  double* b = den_s + (size_t)r * 2 * K * 64;
-  const Cx<K, VAR> x = cx_get<K, VAR>(b, idx), y = cx_get<K, VAR>(b, idx + s);
-  // roles 0..3: x.re y.re, x.im y.im, x.re y.im, x.im y.re
-  const V<K> p = O::mul(sel<K>((role & 1) == 0, x.re, x.im), sel<K>(role == 0 || role == 3, y.re, y.im));
+  const int lane = threadIdx.x & 31, role = lane & 3;
+  const int idx = pair < 0 ? 0 : 2 * s * pair;
+  const bool act = pair >= 0 && idx + s < v32;
+  // this role's factor of a (re for roles 0, 2) and of c (re for roles 0, 3)
+  const double* pa = b + ((role & 1) ? K : 0) * 64 + idx;
+  const double* pc = b + ((role == 0 || role == 3) ? 0 : K) * 64 + idx + s;
+  V<K> fa, fc;
+#pragma unroll
+  for (int c = 0; c < K; ++c) {
+    fa.c[c] = pa[c * 64];
+    fc.c[c] = pc[c * 64];
+  }
+  const V<K> p = O::mul(fa, fc);
   const V<K> nxt = shfl_v<K, VAR>(p, lane + 1);
-  // role 0: re = p1 - p2; role 2: im = p3 + p4
   const V<K> q = O::add(p, sel<K>(role == 0, neg(nxt), nxt));
+  __syncwarp();  // every lane has read its operands before b[idx] is replaced
   if (act && (role == 0 || role == 2)) {
 #pragma unroll
     for (int c = 0; c < K; ++c) b[((role >> 1) * K + c) * 64 + idx] = q.c[c];
@@ -982,98 +982,51 @@ __global__ void __launch_bounds__(32 * dk_treem_warps<R>(), R == 2 ? 2 : 1)
   __syncthreads();
 
   if (threadIdx.x == 0) MW_DK_MARK(6);
-  // The two trees run decoupled, each under its own named barrier (so the
-  // denominator's levels -- the longer path -- never wait for numerator
-  // levels): numerator warps the levels A, 1, 2, 4, 8, 16 (complex adds);
-  // denominator warps the levels 1..16 (level A is done above).  With >= 2
-  // roots per CTA each denominator level's products are split over four
-  // warp groups (roles p1 = a.re b.re, p2 = a.im b.im, p3 = a.re b.im, p4 =
-  // a.im b.re of c_mul4), then roles 0 / 1 form re = p1 - p2 and im = p3 +
-  // p4: the ops and operands of c_mul4, so the same bits, at one mul + one
-  // add of latency per level.  The powers area (free after the barrier
-  // above) holds the role products.
+  // The two trees run decoupled and almost barrier-free.
+  //  denominator (32 values per root after level A): every complex product
+  //    runs on FOUR adjacent lanes (dk_den_pair4: the muls p1..p4 of c_mul4
+  //    as one SIMD mul, then re = p1 - p2 and im = p3 + p4 as one SIMD add
+  //    -- the same operations on the same operands, so the same bits).
+  //    Stride 1 has 16 pairs per root = 64 lanes = the root's two
+  //    denominator warps; one named barrier over the denominator warps;
+  //    strides 2..16 have <= 8 pairs = one warp per root, so they follow
+  //    each other under warp-level syncs only.
+  //  numerator (64 terms per root): one warp per root adds t_l + t_{l+32}
+  //    from shared memory and runs strides 1..16 as warp shuffles.
   if (warp < 2 * R) {
+    const int r = warp >> 1;
+    double* b = den_s + (size_t)r * 2 * K * 64;
+    dk_den_pair4<K, VAR>(b, 1, (warp & 1) * 8 + (lane >> 2), v32);
+    bar_sync_n(14, 64 * R);
+    // (the one warp per root is picked so that the CTA's tree warps --
+    // denominator and numerator -- spread over the four sub-partitions:
+    // they are latency bound and would otherwise share two of them)
+    if ((warp & 1) == ((r >> 1) & 1)) {
 #pragma unroll 1
-    for (int lev = 0; lev < 5; ++lev) {
-      const int s = 1 << lev, per = 16 >> lev;  // pairs per root
-      if constexpr (R >= 2) {
-        const int pairs = R * per;
-        const int wpr = (pairs + 31) >> 5;  // warps per role (4 * wpr <= 2R)
-        const int role = warp / wpr;
-        const int pair = (warp % wpr) * 32 + lane;
-        int r = 0, idx = 0;
-        bool act = false;
-        if (role < 4 && pair < pairs) {
-          r = pair / per;
-          idx = 2 * s * (pair % per);
-          act = idx + s < v32;
-        }
-        double* b = den_s + (size_t)r * 2 * K * 64;
-        double* xs = pw;  // [4][K][64]
-        if (act) {
-          const Cx<K, VAR> a = cx_get<K, VAR>(b, idx), c = cx_get<K, VAR>(b, idx + s);
-          // roles 0..3: p1 = a.re c.re, p2 = a.im c.im, p3 = a.re c.im, p4 = a.im c.re
-          const V<K> p = O::mul((role & 1) == 0 ? a.re : a.im, (role == 0 || role == 3) ? c.re : c.im);
-#pragma unroll
-          for (int cc = 0; cc < K; ++cc) xs[(role * K + cc) * 64 + pair] = p.c[cc];
-        }
-        bar_sync_n(14, 64 * R);
-        if (act && role < 2) {
-          // role 0: re = p1 - p2; role 1: im = p3 + p4
-          V<K> pa, pb;
-#pragma unroll
-          for (int cc = 0; cc < K; ++cc) {
-            pa.c[cc] = xs[((2 * role) * K + cc) * 64 + pair];
-            pb.c[cc] = xs[((2 * role + 1) * K + cc) * 64 + pair];
-          }
-          const V<K> q = O::add(pa, role == 0 ? neg(pb) : pb);
-#pragma unroll
-          for (int cc = 0; cc < K; ++cc) b[(role * K + cc) * 64 + idx] = q.c[cc];
-        }
-      } else if constexpr (K == 4) {
-        // one root: four lanes per product
-        dk_den_level_split<K, VAR, R>(den_s, s, v32);
-      } else {
-        const int tau = threadIdx.x;
-        if (tau < R * per) {
-          const int r = tau / per, idx = 2 * s * (tau % per);
-          if (idx + s < v32) {
-            double* b = den_s + (size_t)r * 2 * K * 64;
-            cx_put<K, VAR>(b, idx, c_mul4_ol(cx_get<K, VAR>(b, idx), cx_get<K, VAR>(b, idx + s)));
-          }
-        }
+      for (int s = 2; s < 32; s <<= 1) {
+        dk_den_pair4<K, VAR>(b, s, (lane >> 2) < 16 / s ? (lane >> 2) : -1, v32);
+        __syncwarp();
       }
-      bar_sync_n(14, 64 * R);
     }
-  } else if (warp < 4 * R) {
+  } else if (warp < 4 * R && (warp & 1) == 1 - ((((warp - 2 * R) >> 1) >> 1) & 1)) {
+    const int r = (warp - 2 * R) >> 1;
+    double* b = num_s + (size_t)r * 2 * K * 64;
+    const int lim = (int)(nblocks < 64 ? nblocks : 64);
+    Cx<K, VAR> t = cx_get<K, VAR>(b, lane);
+    if (lane + 32 < lim) {
+      const Cx<K, VAR> o = cx_get<K, VAR>(b, lane + 32);
+      t.re = O::add(t.re, o.re);
+      t.im = O::add(t.im, o.im);
+    }
 #pragma unroll 1
-    for (int lev = 0; lev < 6; ++lev) {
-      const int tau = threadIdx.x - 64 * R;
-      int r, idx, s, lim;
-      bool act;
-      if (lev == 0) {
-        r = tau >> 5;
-        idx = tau & 31;
-        s = 32;
-        lim = (int)(nblocks < 64 ? nblocks : 64);
-        act = tau < 32 * R;
-      } else {
-        s = 1 << (lev - 1);
-        const int per = 16 >> (lev - 1);
-        r = tau / per;
-        idx = 2 * s * (tau % per);
-        lim = b32;
-        act = tau < R * per;
+    for (int s = 1; s < 32; s <<= 1) {
+      const Cx<K, VAR> o = shfl_cx(t, s, false);
+      if ((lane & (2 * s - 1)) == 0 && lane + s < b32) {
+        t.re = O::add(t.re, o.re);
+        t.im = O::add(t.im, o.im);
       }
-      if (act && idx + s < lim) {
-        double* b = num_s + (size_t)r * 2 * K * 64;
-        Cx<K, VAR> a = cx_get<K, VAR>(b, idx), o = cx_get<K, VAR>(b, idx + s);
-        a.re = O::add(a.re, o.re);
-        a.im = O::add(a.im, o.im);
-        cx_put<K, VAR>(b, idx, a);
-      }
-      bar_sync_n(13, 64 * R);
     }
+    if (lane == 0) cx_put<K, VAR>(b, 0, t);
   }
   __syncthreads();
 
