@@ -7,10 +7,11 @@ The contract (tests/dk_accuracy.py): per root,
     |z_tree - z_ref| <= C_TREE * B_i + 2^(1-p) |z_i|,
     B_i = n 2^-p sum_j |c_j| |z_i|^j / |prod_{j != i}(z_i - z_j)|,
 
-C_TREE = 2 (measured worst 0.65, TD Aberth circle).  Against the mpmath
+C_TREE = 2 (measured worst 0.39, TD Aberth circle; the tree order's complex
+products are the four-multiplication form, oracle c_mul4).  Against the mpmath
 step on the worst roots (largest B_i and largest tree-vs-reference
 difference) the tree's largest error is within 10x the reference's largest
-error (measured <= 4x).  SURVEY's size-only bound n 2^(-p+4)|step| +
+error (measured <= 3.5x).  SURVEY's size-only bound n 2^(-p+4)|step| +
 2^-p|z| is missed by the reference's own step on the ill-conditioned roots
 -- recorded by a test below -- which is why the contract is
 condition-aware.
