@@ -430,9 +430,17 @@ def run_ours(args):
                           ms=part_ms[i], fp64_ops=ops,
                           mp_ops=2 * rows * n * n))
     hp = phi - plo
+    # config 4's points are plain doubles (x, 0, 0, 0): the kernel's product
+    # for such points issues 63 FP64 instructions instead of qw_mul_bf's 106
+    # (the operations +0 low words determine are removed; bit-identical,
+    # csrc/mw_eft.cuh qd_mul_bf_d), so a step EXECUTES 63 + 103 = 166, not
+    # 209.  The roofline counts what is executed; MP-ops count the K-word
+    # operations of the reference sequence (one mul + one add per step).
+    horner_step_ops = (63 + ADD_OPS[4]) if horner["k"] == 4 else MAC_OPS[horner["k"]]
     parts.append(dict(name=f"horner_qd_deg{horner['degree']}_pts{horner['npts']}", kernel="horner_kernel<4,1>",
                       ms=part_ms[-1],
-                      fp64_ops=MAC_OPS[4] * hp * horner["degree"], mp_ops=2 * hp * horner["degree"]))
+                      fp64_ops=horner_step_ops * hp * horner["degree"], mp_ops=2 * hp * horner["degree"],
+                      fp64_ops_reference=MAC_OPS[horner["k"]] * hp * horner["degree"]))
     for p in parts:
         p["fp64_tops"] = p["fp64_ops"] / (p["ms"] / 1e3) / 1e12 if p["ms"] > 0 else 0.0
         p["frac_of_fp64_peak"] = p["fp64_tops"] * 1e12 / peak["dfma"]
@@ -453,6 +461,12 @@ def run_ours(args):
         "algorithmic_bytes": dom["alg_bytes"],
         "peak_source": "measured live: DFMA microbenchmark, 8 chains/thread, all SMs (mw_fp64_peak_kernel)",
     }
+    if "fp64_ops_reference" in dom:
+        roofline["ops_note"] = (
+            "achieved counts the FP64 instructions the kernel issues: 166 per Horner step for double-valued QD "
+            "points (63-instruction product qd_mul_bf_d + 103-instruction add; bit-identical with the reference's "
+            "106 + 103 = 209, whose rate would be "
+            f"{dom['fp64_ops_reference'] / (dom['ms'] / 1e3) / 1e12:.3f} T/s)")
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:

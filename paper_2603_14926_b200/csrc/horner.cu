@@ -11,6 +11,15 @@
 // The coefficients are staged through shared memory in chunks of CH words
 // (uniform across the CTA: every read is a broadcast), highest chunk first.
 // Points are loaded/stored once, coalesced per plane.
+//
+// QD points that are plain doubles (x = (x0, +0, +0, +0): the usual case,
+// and the benchmark's config 4) take qd_mul_bf_d, the branch-free product
+// with the operations removed that +0 low words determine (63 instead of
+// 106 FP64 instructions, mw_eft.cuh) -- bit-identical for finite values; a
+// thread whose result has a non-finite component (overflow, or a NaN / inf
+// in the inputs) re-runs its points through the full product, so the result
+// is the reference's in every case.  The choice is per thread from the
+// point's own words: no flag, no pre-pass, nothing stored between calls.
 #include "common.cuh"
 
 namespace mw {
@@ -41,24 +50,67 @@ __global__ void __launch_bounds__(HORNER_THREADS)
     acc[j] = load<K>(coeffs, sc, degree);
   }
 
-  // coefficients deg-1 .. 0, in chunks [lo, hi) walked downward
-  for (int64_t hi = degree; hi > 0; hi -= HORNER_CH) {
-    const int64_t lo = hi > HORNER_CH ? hi - HORNER_CH : 0;
-    const int cnt = (int)(hi - lo);
-    __syncthreads();
-    for (int e = threadIdx.x; e < K * cnt; e += HORNER_THREADS) {
-      const int c = e / cnt, i = e % cnt;
-      cs[c][i] = coeffs[c * sc + lo + i];
-    }
-    __syncthreads();
+  // double-valued QD points: every low word is +0.0 (bit pattern 0)
+  bool dbl = false;
+  if constexpr (K == 4 && VAR == BRANCH_FREE) {
+    dbl = true;
+#pragma unroll
+    for (int j = 0; j < PPT; ++j)
+#pragma unroll
+      for (int c = 1; c < K; ++c) dbl = dbl && __double_as_longlong(xv[j].c[c]) == 0;
+  }
+
+  // coefficients deg-1 .. 0, in chunks [lo, hi) walked downward; pass 1 is
+  // the full-product re-run of a CTA in which some double-valued thread saw
+  // a non-finite result (never taken on finite data)
+  for (int pass = 0; pass < 2; ++pass) {
+    for (int64_t hi = degree; hi > 0; hi -= HORNER_CH) {
+      const int64_t lo = hi > HORNER_CH ? hi - HORNER_CH : 0;
+      const int cnt = (int)(hi - lo);
+      __syncthreads();
+      for (int e = threadIdx.x; e < K * cnt; e += HORNER_THREADS) {
+        const int c = e / cnt, i = e % cnt;
+        cs[c][i] = coeffs[c * sc + lo + i];
+      }
+      __syncthreads();
+      if constexpr (K == 4 && VAR == BRANCH_FREE) {
+        if (dbl) {
 #pragma unroll 1
-    for (int i = cnt - 1; i >= 0; --i) {
-      V<K> a;
+          for (int i = cnt - 1; i >= 0; --i) {
+            V<K> a;
 #pragma unroll
-      for (int c = 0; c < K; ++c) a.c[c] = cs[c][i];
+            for (int c = 0; c < K; ++c) a.c[c] = cs[c][i];
 #pragma unroll
-      for (int j = 0; j < PPT; ++j) acc[j] = Ops<K, VAR>::add(Ops<K, VAR>::mul(acc[j], xv[j]), a);
+            for (int j = 0; j < PPT; ++j) acc[j] = qd_add_bf(qd_mul_bf_d(acc[j], xv[j].c[0]), a);
+          }
+          continue;
+        }
+      }
+#pragma unroll 1
+      for (int i = cnt - 1; i >= 0; --i) {
+        V<K> a;
+#pragma unroll
+        for (int c = 0; c < K; ++c) a.c[c] = cs[c][i];
+#pragma unroll
+        for (int j = 0; j < PPT; ++j) acc[j] = Ops<K, VAR>::add(Ops<K, VAR>::mul(acc[j], xv[j]), a);
+      }
     }
+    bool redo = false;
+    if constexpr (K == 4 && VAR == BRANCH_FREE) {
+      if (pass == 0 && dbl) {
+#pragma unroll
+        for (int j = 0; j < PPT; ++j)
+#pragma unroll
+          for (int c = 0; c < K; ++c) redo = redo || !isfinite(acc[j].c[c]);
+      }
+      redo = __syncthreads_or(redo) != 0;  // uniform: the chunk loop has CTA barriers
+    }
+    if (!redo) break;
+    // every thread of the CTA runs again on the full product (those already
+    // on it recompute the same bits)
+    dbl = false;
+#pragma unroll
+    for (int j = 0; j < PPT; ++j) acc[j] = load<K>(coeffs, sc, degree);
   }
 
 #pragma unroll

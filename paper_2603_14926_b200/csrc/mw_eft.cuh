@@ -233,6 +233,44 @@ MW_HD V<4> qd_mul_bf(const V<4>& A, const V<4>& B) {
   return r;
 }
 
+// qd_mul_bf(A, (x, +0, +0, +0)) with the operations removed whose results
+// are determined when every operand is finite: a two_prod with +0 gives
+// (sign(a) 0, +0), a two_sum with a zero operand has the error term +0, and
+// two_sum(c4, e4) of an already error-free pair returns it unchanged.  The
+// three signed zeros sign(A_i) 0 and the sums they enter are kept, because
+// they decide the sign of a zero result (63 instead of 106 FP64
+// instructions).  Bit-identical with qd_mul_bf for finite operands,
+// signed zeros and subnormals included (checked against the reference's
+// qw_mul_bf, tests/test_oracle_golden.py, and on the device,
+// tests/test_gpu_parity.py); with a non-finite operand or an overflow the
+// removed operations would have produced NaNs, so callers must fall back
+// to qd_mul_bf whenever a result component is not finite (horner.cu does).
+MW_HD V<4> qd_mul_bf_d(const V<4>& A, double x) {
+  double a0, b0, d0, f0, i0, l0, b2, c2, a3, b3, e3, g3, c4, e4, b7, c7, b8, c8, d8, c9;
+  two_prod(A.c[0], x, a0, b0);
+  two_prod(A.c[1], x, d0, f0);
+  two_prod(A.c[2], x, i0, l0);
+  const double p0 = MW_MUL(A.c[3], x);
+  const double z0 = MW_MUL(A.c[0], 0.0), z1 = MW_MUL(A.c[1], 0.0), z2 = MW_MUL(A.c[2], 0.0);
+  const double c1 = MW_ADD(z0, d0);
+  const double g1 = MW_ADD(z0, i0);
+  const double m2 = MW_ADD(MW_ADD(z0, p0), MW_ADD(z1, z2));
+  two_sum(b0, c1, b2, c2);
+  quick_two_sum(a0, b2, a3, b3);
+  two_sum(f0, g1, e3, g3);
+  const double f3 = MW_ADD(l0, m2);
+  two_sum(c2, e3, c4, e4);
+  const double f4 = MW_ADD(f3, g3);
+  two_sum(b3, c4, b7, c7);
+  const double d7 = MW_ADD(e4, f4);
+  V<4> r;
+  quick_two_sum(a3, b7, r.c[0], b8);
+  two_sum(c7, d7, c8, d8);
+  two_sum(b8, c8, r.c[1], c9);
+  quick_two_sum(c9, d8, r.c[2], r.c[3]);
+  return r;
+}
+
 // ------------------------------------------- Standard (renormalising) TD/QD
 // The reference's conventional kernels, branches and all: a branch-free
 // core followed by a value-dependent renormalisation (multiword.py:

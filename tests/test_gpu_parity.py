@@ -261,6 +261,48 @@ def test_horner_vs_oracle(k, deg, npts):
     assert_bitwise(got, oracle.horner(coeffs, x, "bf"))
 
 
+@pytest.mark.parametrize("case", ["doubles", "zeros", "mixed", "nonfinite", "overflow"])
+def test_horner_qd_double_points_fast_path(case):
+    """QD points that are plain doubles take the shortened product
+    (qd_mul_bf_d); the result must be the reference's bit for bit: for
+    ordinary points, for exact / negative zeros in coefficients and points,
+    for warps that mix double-valued and full QD points (both loop bodies
+    in one CTA), and -- through the full-product re-run -- when inf / NaN
+    coefficients or an overflow make a result non-finite."""
+    rng = np.random.default_rng(77)
+    deg, npts = 300, 5000
+    coeffs = gen.g_k(rng, 4, deg + 1)
+    x = np.zeros((4, npts))
+    x[0] = rng.uniform(-1.1, 1.1, npts)
+    if case == "zeros":
+        for c in range(4):
+            m = rng.random(deg + 1) < 0.2
+            coeffs[c] = np.where(m, np.where(rng.random(deg + 1) < 0.5, 0.0, -0.0), coeffs[c])
+        m = rng.random(npts) < 0.2
+        x[0] = np.where(m, np.where(rng.random(npts) < 0.5, 0.0, -0.0), x[0])
+    if case == "mixed":  # every third point a full QD value, some low words -0.0
+        full = gen.g_k(rng, 4, npts)
+        sel = (np.arange(npts) % 3) == 0
+        x[:, sel] = full[:, sel]
+        x[1, (np.arange(npts) % 7) == 1] = -0.0
+    if case == "nonfinite":
+        coeffs[0, 17] = np.inf
+        coeffs[2, 120] = np.nan
+        x[0, 5] = np.inf
+        x[0, 77] = np.nan
+    if case == "overflow":  # |x| > 1 with huge coefficients: overflows part of the way down
+        coeffs = coeffs * 2.0 ** 1000
+        x[0] = rng.uniform(-40, 40, npts)
+    got = horner_eval_batched(MWPolynomial(coeffs), LaneBatch(x), Variant.BRANCH_FREE).numpy()
+    with np.errstate(all="ignore"):
+        want = oracle.horner(coeffs, x, "bf")
+    if case in ("nonfinite", "overflow"):
+        assert not np.all(np.isfinite(want))
+    if case == "overflow":
+        assert np.any(np.isfinite(want[0])) and not np.all(np.isfinite(want[0]))
+    assert_bitwise(got, want, nan_ok=True)
+
+
 def test_horner_config4_full_with_sampled_check():
     coeffs, x = gen.config4_horner()
     y = horner_eval_batched(MWPolynomial(coeffs), LaneBatch(x), Variant.BRANCH_FREE).numpy()
