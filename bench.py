@@ -488,6 +488,9 @@ def run_ours(args):
             "shared_gpus": (world > torch.cuda.device_count()) or None,
             "l2": "inputs larger than L2 (GEMM DD A+B 537 MB, Horner x 537 MB); no flush",
             "bit_exact": "GEMM naive order and Horner per point, vs reference",
+            "horner_points": "double-valued QD points (x, 0, 0, 0) as SURVEY 8(d) config 4 specifies; the kernel "
+                             "takes its bit-identical 63-instruction product for them (secondary."
+                             "paper_comparisons.horner_qd_deg1024_pts2p20_full_qd_points times full QD points)",
         },
         "parts": [{"name": p["name"], "ms": round(p["ms"], 3), "G_MPops": round(p["gmpops"], 2),
                    "fp64_Tops": round(p["fp64_tops"], 3), "frac": round(p["frac_of_fp64_peak"], 4)}
@@ -813,6 +816,21 @@ def secondary(args, torch, dist, mw, world, rank, peak, out=None):
         ms_std = timed(lambda: horner_into(c4, xd4, y4, STD), 3)
         cmp["horner_qd_deg1024_pts2p20"] = {
             "bf_ms": round(ms_bf, 3), "std_ms": round(ms_std, 3), "bf_speedup": round(ms_std / ms_bf, 3)}
+        # the same Horner at points with non-zero low words (full QD points):
+        # the kernel then issues the reference's 209 FP64 instructions per
+        # step instead of the 166 of the double-point product the headline's
+        # config 4 takes -- reported so both rates are on record
+        xf = gen.g_k(np.random.default_rng(44), 4, 1 << 20)
+        xfd = torch.from_numpy(xf).cuda()
+        ms_full = timed(lambda: horner_into(c4, xfd, y4, BF), 3)
+        hops = (1 << 20) * (c4.shape[1] - 1)
+        cmp["horner_qd_deg1024_pts2p20_full_qd_points"] = {
+            "ms": round(ms_full, 3), "ms_double_points": round(ms_bf, 3),
+            "G_MPops": round(2 * hops / (ms_full / 1e3) / 1e9, 1),
+            "fp64_frac": round(MAC_OPS[4] * hops / (ms_full / 1e3) / peak["dfma"], 4),
+            "fp64_frac_double_points": round((63 + ADD_OPS[4]) * hops / (ms_bf / 1e3) / peak["dfma"], 4),
+            "note": "full product 106 + add 103 = 209 FP64 instructions per step; double-valued points 63 + 103 = 166 (bit-identical)"}
+        del xfd
         P4, X4 = mw.MWPolynomial(c4), mw.LaneBatch(xd4)
         ms_est = timed(lambda: mw.estrin_eval_batched(P4, X4, BF), 3)
         npts4, deg4 = xd4.shape[1], c4.shape[1] - 1
