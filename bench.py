@@ -1141,6 +1141,8 @@ def run_reference(args):
             "gemm": [f"k{k} n{n}" for k, n in gemm_parts], "horner": horner,
             "parallelism": f"rows/points sharded over {procs} host processes (CPU), no collective",
             "l2": "n/a (CPU)", "bit_exact": "the reference itself",
+            "horner_points": "double-valued QD points (x, 0, 0, 0) as SURVEY 8(d) config 4 specifies; the reference "
+                             "runs its full qw_mul_bf on them",
             "sample": "each step is a bounded sample (ms_per_step = its measured wall time); value = the "
                       "sample's MP-op rate, i.e. the full step extrapolated linearly",
         },
