@@ -4,6 +4,7 @@
 // check their output is bit-identical to the product kernel.
 #include "../gemm_kernel.cuh"
 #include "../reduce.cu"  // GEMV kernel template (its C-ABI symbols stay private to this .so)
+#include "gemv_forms.cuh"
 #include "gemv_staged.cuh"
 #include "gemv_bulk.cuh"
 #include "gemv_probe.cuh"
