@@ -174,7 +174,11 @@ int mw_gemm_batched(int k, int variant, const double* A, int64_t lda,
 
 /* y_p = Horner(coeffs, x_p) for npts points: acc = a_deg; acc = acc (*) x
  * (+) a_i for i = deg-1..0 (poly.py:89-96).  coeffs: k planes of deg+1
- * doubles (a_i multiplies x^i).  Bit-exact with horner_eval per point. */
+ * doubles (a_i multiplies x^i).  Bit-exact with horner_eval per point.
+ * QD branch-free points whose low words are all +0.0 (plain doubles) take a
+ * shortened product (63 instead of 106 FP64 instructions) that is
+ * bit-identical for finite values; a non-finite result re-runs the full
+ * product, so the result is horner_eval's in every case. */
 int mw_horner(int k, int variant, const double* coeffs, int64_t sc,
               int64_t degree, const double* x, int64_t sx, double* y,
               int64_t sy, int64_t npts, void* stream);
@@ -199,8 +203,11 @@ int mw_poly_eval(int k, int variant, const double* coeffs, int64_t sc,
  * *flag_dev = INT32_MAX first; a vanishing denominator factor lowers it to
  * min over (j*n + i) of the colliding pairs, and the caller raises
  * CollisionError (roots.py:289-292).  exact_order = 1 replays the
- * reference order bit for bit; 0 splits the Horner and the ordered product
- * across a warp (within the stated bound).  1 <= n <= MW_DK_MAX_N. */
+ * reference order bit for bit; 0 is the tree order: 64 partial products and
+ * 64 Horner blocks per root combined by pairwise trees, complex products
+ * in the four-multiplication form -- within the stated accuracy contract
+ * of the reference, not bitwise.  1 <= n <=
+ * MW_DK_MAX_N. */
 int mw_dk_sweep(int k, int variant, const double* coeffs, int64_t sc,
                 int64_t n, const double* zre, const double* zim, int64_t sz,
                 int64_t i0, int64_t i1, double* zre_out, double* zim_out,
