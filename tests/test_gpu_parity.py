@@ -303,6 +303,43 @@ def test_horner_qd_double_points_fast_path(case):
     assert_bitwise(got, want, nan_ok=True)
 
 
+def test_horner_qd_special_values_fuzz():
+    """Randomised special values through the QD Horner kernel (both step
+    bodies and the non-finite re-run): coefficients and points drawn from
+    ordinary values mixed with +-0, subnormals, huge and tiny magnitudes,
+    inf and NaN, in any word; points double-valued or full QD.  Bitwise equal
+    to the oracle (NaN positions compared, payloads not)."""
+    rng = np.random.default_rng(4242)
+    special = np.array([0.0, -0.0, 5e-324, -2.2e-308, 1e-300, -1e300, 1.7e308, np.inf, -np.inf, np.nan,
+                        1.0, -1.0, 2.0 ** -53, 2.0 ** 52 + 1])
+
+    def draw(shape, p_special):
+        v = gen.g_k(rng, 4, shape)
+        m = rng.random(v.shape) < p_special
+        return np.where(m, rng.choice(special, v.shape), v)
+
+    for case in range(120):
+        deg = int(rng.integers(0, 48))
+        npts = int(rng.integers(1, 300))
+        ps = (0.0, 0.02, 0.3)[case % 3]
+        coeffs = draw(deg + 1, ps)
+        x = draw(npts, ps)
+        mode = case % 4
+        if mode in (0, 1):      # all double-valued
+            x[1:] = 0.0
+        elif mode == 2:         # a mix inside every warp
+            dblm = rng.random(npts) < 0.6
+            x[1:, dblm] = 0.0
+        if mode == 1:           # grow: |x| > 1 with large coefficients overflows part of the way
+            with np.errstate(all="ignore"):
+                coeffs = coeffs * 2.0 ** 900
+                x[0] = np.where(np.isfinite(x[0]), x[0] * 50.0, x[0])
+        got = horner_eval_batched(MWPolynomial(coeffs), LaneBatch(x), Variant.BRANCH_FREE).numpy()
+        with np.errstate(all="ignore"):
+            want = oracle.horner(coeffs, x, "bf")
+        assert_bitwise(got, want, nan_ok=True)
+
+
 def test_horner_config4_full_with_sampled_check():
     coeffs, x = gen.config4_horner()
     y = horner_eval_batched(MWPolynomial(coeffs), LaneBatch(x), Variant.BRANCH_FREE).numpy()
