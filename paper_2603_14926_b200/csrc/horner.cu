@@ -12,10 +12,11 @@
 // (uniform across the CTA: every read is a broadcast), highest chunk first.
 // Points are loaded/stored once, coalesced per plane.
 //
-// QD points that are plain doubles (x = (x0, +0, +0, +0): the usual case,
-// and the benchmark's config 4) take qd_mul_bf_d, the branch-free product
-// with the operations removed that +0 low words determine (63 instead of
-// 106 FP64 instructions, mw_eft.cuh) -- bit-identical for finite values; a
+// TD / QD points that are plain doubles (x = (x0, +0, ...): the usual case,
+// and the benchmark's config 4) take td_/qd_mul_bf_d, the branch-free
+// product with the operations removed that +0 low words determine (QD 63
+// instead of 106 FP64 instructions, TD 30 instead of 39; mw_eft.cuh; the DD
+// product has none to remove) -- bit-identical for finite values; a
 // thread whose result has a non-finite component (overflow, or a NaN / inf
 // in the inputs) re-runs its points through the full product, so the result
 // is the reference's in every case.  The choice is per thread from the
@@ -50,9 +51,10 @@ __global__ void __launch_bounds__(HORNER_THREADS)
     acc[j] = load<K>(coeffs, sc, degree);
   }
 
-  // double-valued QD points: every low word is +0.0 (bit pattern 0)
+  // double-valued points: every low word is +0.0 (bit pattern 0)
+  constexpr bool FAST = VAR == BRANCH_FREE && MulByDouble<K>::available;
   bool dbl = false;
-  if constexpr (K == 4 && VAR == BRANCH_FREE) {
+  if constexpr (FAST) {
     dbl = true;
 #pragma unroll
     for (int j = 0; j < PPT; ++j)
@@ -73,7 +75,7 @@ __global__ void __launch_bounds__(HORNER_THREADS)
         cs[c][i] = coeffs[c * sc + lo + i];
       }
       __syncthreads();
-      if constexpr (K == 4 && VAR == BRANCH_FREE) {
+      if constexpr (FAST) {
         if (dbl) {
 #pragma unroll 1
           for (int i = cnt - 1; i >= 0; --i) {
@@ -81,7 +83,8 @@ __global__ void __launch_bounds__(HORNER_THREADS)
 #pragma unroll
             for (int c = 0; c < K; ++c) a.c[c] = cs[c][i];
 #pragma unroll
-            for (int j = 0; j < PPT; ++j) acc[j] = qd_add_bf(qd_mul_bf_d(acc[j], xv[j].c[0]), a);
+            for (int j = 0; j < PPT; ++j)
+              acc[j] = MulByDouble<K>::add(MulByDouble<K>::mul(acc[j], xv[j].c[0]), a);
           }
           continue;
         }
@@ -96,7 +99,7 @@ __global__ void __launch_bounds__(HORNER_THREADS)
       }
     }
     bool redo = false;
-    if constexpr (K == 4 && VAR == BRANCH_FREE) {
+    if constexpr (FAST) {
       if (pass == 0 && dbl) {
 #pragma unroll
         for (int j = 0; j < PPT; ++j)

@@ -271,6 +271,48 @@ MW_HD V<4> qd_mul_bf_d(const V<4>& A, double x) {
   return r;
 }
 
+// td_mul_bf(A, (x, +0, +0)), shortened the same way (tw_mul_bf,
+// multiword.py:381-402): 30 instead of 39 FP64 instructions.  (The DD
+// product has nothing to remove: its a0 * b1 term is a single multiply
+// whose signed zero must be kept.)
+MW_HD V<3> td_mul_bf_d(const V<3>& A, double x) {
+  double a0, b0, d0, f0, b2, c2, a3, b3, b5, c5, b6;
+  two_prod(A.c[0], x, a0, b0);
+  two_prod(A.c[1], x, d0, f0);
+  const double i0 = MW_MUL(A.c[2], x);
+  const double z0 = MW_MUL(A.c[0], 0.0), z1 = MW_MUL(A.c[1], 0.0);
+  const double c1 = MW_ADD(z0, d0);
+  const double g2 = MW_ADD(MW_ADD(z0, i0), z1);
+  two_sum(b0, c1, b2, c2);
+  quick_two_sum(a0, b2, a3, b3);
+  const double e3 = MW_ADD(f0, g2);
+  const double c4 = MW_ADD(c2, e3);
+  quick_two_sum(b3, c4, b5, c5);
+  V<3> r;
+  quick_two_sum(a3, b5, r.c[0], b6);
+  quick_two_sum(b6, c5, r.c[1], r.c[2]);
+  return r;
+}
+
+// Product by a double-valued K-word point for the branch-free kernels that
+// have a shortened form (K = 3, 4).
+template <int K>
+struct MulByDouble {
+  static constexpr bool available = false;
+};
+template <>
+struct MulByDouble<3> {
+  static constexpr bool available = true;
+  static MW_HD V<3> mul(const V<3>& a, double x) { return td_mul_bf_d(a, x); }
+  static MW_HD V<3> add(const V<3>& a, const V<3>& b) { return td_add_bf(a, b); }
+};
+template <>
+struct MulByDouble<4> {
+  static constexpr bool available = true;
+  static MW_HD V<4> mul(const V<4>& a, double x) { return qd_mul_bf_d(a, x); }
+  static MW_HD V<4> add(const V<4>& a, const V<4>& b) { return qd_add_bf(a, b); }
+};
+
 // ------------------------------------------- Standard (renormalising) TD/QD
 // The reference's conventional kernels, branches and all: a branch-free
 // core followed by a value-dependent renormalisation (multiword.py:

@@ -261,27 +261,28 @@ def test_horner_vs_oracle(k, deg, npts):
     assert_bitwise(got, oracle.horner(coeffs, x, "bf"))
 
 
+@pytest.mark.parametrize("k", [3, 4])
 @pytest.mark.parametrize("case", ["doubles", "zeros", "mixed", "nonfinite", "overflow"])
-def test_horner_qd_double_points_fast_path(case):
-    """QD points that are plain doubles take the shortened product
-    (qd_mul_bf_d); the result must be the reference's bit for bit: for
+def test_horner_qd_double_points_fast_path(case, k):
+    """TD / QD points that are plain doubles take the shortened product
+    (td_/qd_mul_bf_d); the result must be the reference's bit for bit: for
     ordinary points, for exact / negative zeros in coefficients and points,
     for warps that mix double-valued and full QD points (both loop bodies
     in one CTA), and -- through the full-product re-run -- when inf / NaN
     coefficients or an overflow make a result non-finite."""
     rng = np.random.default_rng(77)
     deg, npts = 300, 5000
-    coeffs = gen.g_k(rng, 4, deg + 1)
-    x = np.zeros((4, npts))
+    coeffs = gen.g_k(rng, k, deg + 1)
+    x = np.zeros((k, npts))
     x[0] = rng.uniform(-1.1, 1.1, npts)
     if case == "zeros":
-        for c in range(4):
+        for c in range(k):
             m = rng.random(deg + 1) < 0.2
             coeffs[c] = np.where(m, np.where(rng.random(deg + 1) < 0.5, 0.0, -0.0), coeffs[c])
         m = rng.random(npts) < 0.2
         x[0] = np.where(m, np.where(rng.random(npts) < 0.5, 0.0, -0.0), x[0])
     if case == "mixed":  # every third point a full QD value, some low words -0.0
-        full = gen.g_k(rng, 4, npts)
+        full = gen.g_k(rng, k, npts)
         sel = (np.arange(npts) % 3) == 0
         x[:, sel] = full[:, sel]
         x[1, (np.arange(npts) % 7) == 1] = -0.0
@@ -303,18 +304,19 @@ def test_horner_qd_double_points_fast_path(case):
     assert_bitwise(got, want, nan_ok=True)
 
 
-def test_horner_qd_special_values_fuzz():
-    """Randomised special values through the QD Horner kernel (both step
+@pytest.mark.parametrize("k", [3, 4])
+def test_horner_qd_special_values_fuzz(k):
+    """Randomised special values through the TD / QD Horner kernel (both step
     bodies and the non-finite re-run): coefficients and points drawn from
     ordinary values mixed with +-0, subnormals, huge and tiny magnitudes,
     inf and NaN, in any word; points double-valued or full QD.  Bitwise equal
     to the oracle (NaN positions compared, payloads not)."""
-    rng = np.random.default_rng(4242)
+    rng = np.random.default_rng(4242 + k)
     special = np.array([0.0, -0.0, 5e-324, -2.2e-308, 1e-300, -1e300, 1.7e308, np.inf, -np.inf, np.nan,
                         1.0, -1.0, 2.0 ** -53, 2.0 ** 52 + 1])
 
     def draw(shape, p_special):
-        v = gen.g_k(rng, 4, shape)
+        v = gen.g_k(rng, k, shape)
         m = rng.random(v.shape) < p_special
         return np.where(m, rng.choice(special, v.shape), v)
 

@@ -179,6 +179,18 @@ def test_horner_qd_step_bodies(sass):
     assert sorted(fp64_blocks(body)) == sorted([(2 * 193, 2 * 10, 2 * 6), (2 * 156, 2 * 7, 2 * 3)])
 
 
+def test_horner_td_step_bodies(sass):
+    """horner_kernel<3, BF>: the full step body 2 x (DADD 87, DMUL 6, DFMA 3)
+    and the double-point body 2 x (td_mul_bf_d + add) = 2 x (DADD 23 + 57,
+    DMUL 5, DFMA 2), each one basic block without FP64 compares."""
+    hits = [f for f in sass if f.startswith("_ZN2mw13horner_kernelILi3ELi1EEEv")]
+    assert len(hits) == 1, hits
+    body = sass[hits[0]]
+    _, _, _, _, dsetp = mix(body)
+    assert dsetp == 0
+    assert sorted(fp64_blocks(body)) == sorted([(2 * 87, 2 * 6, 2 * 3), (2 * 80, 2 * 5, 2 * 2)])
+
+
 @pytest.mark.parametrize("k", [2, 3, 4])
 def test_gemm_every_tile_slot_mac_mix(sass, k):
     """gemm_kernel<K, BF>, every tile slot the per-call choice can pick:
