@@ -17,9 +17,9 @@
 // product with the operations removed that +0 low words determine (QD 63
 // instead of 106 FP64 instructions, TD 30 instead of 39; mw_eft.cuh; the DD
 // product has none to remove) -- bit-identical for finite values; a
-// thread whose result has a non-finite component (overflow, or a NaN / inf
-// in the inputs) re-runs its points through the full product, so the result
-// is the reference's in every case.  The choice is per thread from the
+// CTA in which some such thread ends with a non-finite component (overflow,
+// or a NaN / inf in the inputs) re-runs through the full product, so the
+// result is the reference's in every case.  The choice is per thread from the
 // point's own words: no flag, no pre-pass, nothing stored between calls.
 #include "common.cuh"
 
